@@ -1,0 +1,151 @@
+/* rlhf_engine.h — C-ABI of the B200 RLHF PPO step engine.
+ *
+ * Drop-in boundary.  The reference (arXiv 2312.11819 artifact, /root/reference)
+ * is a C++ simulator whose executor slot is
+ *     SimReport simulate(const PlacementPlan&, const PipelineSpec&, const CostModel&,
+ *                        const ClusterTopology&, const SimOptions&)
+ *     (/root/reference/proj/include/rlhfsim/simulator.hpp:46-47)
+ * with per-task cost  stage_compute_time(...)  (costmodel.hpp:63-64) and per-
+ * collective cost  collective_time(...)  (costmodel.hpp:55-56).  This ABI
+ * replaces that slot with real execution: rlhf_engine_step() runs one PPO
+ * iteration of the task DAG (workload.cpp:109-175) on the local GPU and fills
+ * an rlhf_step_report whose fields are SimReport's (simulator.hpp:30-44),
+ * measured with CUDA events instead of the analytic clock.
+ *
+ * Conventions: plain C types, caller-owned host buffers, int status
+ * (0 ok; 2 config, 3 infeasible, 5 device error — the reference's exit codes,
+ * errors.hpp:8-22, plus 5).  No exceptions cross the ABI.  rlhf_last_error()
+ * returns the message of the calling thread's last failure.
+ */
+#ifndef RLHF_ENGINE_H
+#define RLHF_ENGINE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "rlhf_init.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RLHF_OK 0
+#define RLHF_ERR_CONFIG 2
+#define RLHF_ERR_INFEASIBLE 3
+#define RLHF_ERR_DEVICE 5
+
+/* PPO hyper-parameters + shapes of one RLHF step (DeepSpeed-Chat step-3
+ * conventions).  Ref shares the Actor's arch, Reward the
+ * Critic's arch. */
+typedef struct rlhf_ppo_config {
+  rlhf_arch actor;        /* scalar_head forced to 0 */
+  rlhf_arch critic;       /* scalar_head forced to 1 */
+  int batch;              /* samples of this rank's shard */
+  int prompt_len;
+  int gen_len;
+  uint64_t seed;          /* model seeds = rlhf_model_seed(seed, role) */
+  uint64_t prompt_seed;   /* prompts: rlhf_prompt_token(prompt_seed, b + sample_offset, t, V) */
+  int sample_offset;      /* global index of this rank's first sample */
+  float kl_ctl;           /* 0.1 */
+  float clip_reward;      /* 5.0 */
+  float gamma;            /* 1.0 */
+  float lam;              /* 0.95 */
+  float cliprange;        /* 0.2 */
+  float cliprange_value;  /* 0.2 */
+  float lr_actor;         /* 1e-5 */
+  float lr_critic;        /* 5e-6 */
+  float beta1, beta2, adam_eps, weight_decay; /* 0.9, 0.95, 1e-8, 0 */
+  float loss_denominator; /* global B*R (DP mean); 0 -> local batch*gen_len */
+} rlhf_ppo_config;
+
+/* Fill cfg with the defaults above for the given arch pair and shapes. */
+void rlhf_ppo_config_default(rlhf_ppo_config* cfg, const rlhf_arch* actor, const rlhf_arch* critic,
+                             int batch, int prompt_len, int gen_len);
+
+/* Resolve a named shape ("tiny", "opt-125m", "opt-350m", "opt-1.3b") into an
+ * arch with max_pos = max_pos.  Returns 0 or RLHF_ERR_CONFIG. */
+int rlhf_arch_by_name(const char* name, int max_pos, int scalar_head, rlhf_arch* out);
+
+/* ---- placement / stage DAG queries (pure host logic, no GPU) -------------- */
+
+/* Stage DAG of one iteration, flattened: for task i, kind/model/mb/rollout/
+ * epoch and deps[dep_off[i] .. dep_off[i+1]).  Mirrors task_graph()
+ * (workload.cpp:109-175).  Arrays sized by the caller: call once with
+ * max_tasks = 0 to get the counts in *n_tasks / *n_deps. */
+int rlhf_task_graph(int structure /*0 ACShare, 1 ACNonShare*/, int batch, int micro_batches,
+                    int rollout_nums, int ppo_epochs, int shadows, int max_tasks, int max_deps,
+                    int* n_tasks, int* n_deps, int* kind, int* model, int* mb, int* rollout,
+                    int* epoch, int* dep_off, int* deps);
+
+/* Placement of the four (or six) models on an n-device B200 box.
+ * strategy: "colocated" | "interleaving1" | "interleaving2" | "disaggregated".
+ * out_mask[m] = bitmask of devices hosting ModelName m (Actor, Critic, Ref,
+ * Reward, ShadowActor, ShadowCritic); out_role[d] = DeviceRole of device d.
+ * Returns the plan encoding (PlacementPlan::encoding) in enc (NUL-terminated). */
+int rlhf_plan(const char* strategy, int n_devices, int zero_level, double inference_ratio,
+              int tp_gen, uint32_t out_mask[6], int* out_role, char* enc, int enc_len);
+
+/* Communication schedule the plan induces (derive_comm_schedule): per op
+ * kind (CollectiveKind), attach (0 Before, 1 After), anchor task, payload. */
+int rlhf_comm_schedule(const char* strategy, int n_devices, int batch, int prompt_len, int gen_len,
+                       int micro_batches, int max_ops, int* n_ops, int* kind, int* attach,
+                       int* anchor, double* payload, uint32_t* group_mask);
+
+/* ---- engine --------------------------------------------------------------- */
+
+typedef struct rlhf_engine rlhf_engine;
+
+/* Roles this rank executes in a placement (bit i = ModelName i), and the
+ * collective wiring.  world_size == 1 needs no NCCL id. */
+typedef struct rlhf_engine_options {
+  int device;                 /* CUDA ordinal */
+  int rank, world_size;
+  const char* strategy;       /* colocated | interleaving1 | interleaving2 | disaggregated */
+  const uint8_t* nccl_id;     /* 128 bytes from rlhf_nccl_unique_id (rank 0), NULL at world 1 */
+  int use_cuda_graph;         /* capture the decode step in a CUDA graph */
+} rlhf_engine_options;
+
+int rlhf_nccl_unique_id(uint8_t out[128]);
+
+int rlhf_engine_create(const rlhf_ppo_config* cfg, const rlhf_engine_options* opt, rlhf_engine** out);
+void rlhf_engine_destroy(rlhf_engine* e);
+
+/* Per-stage measured time (CUDA events), SimReport vocabulary. */
+typedef struct rlhf_step_report {
+  double step_seconds;
+  double throughput_samples_per_sec;   /* global batch * rollouts / step_seconds */
+  double stage_seconds[4];             /* Stage: generation, forward, training, sync */
+  double decode_seconds;               /* generation minus prefill */
+  double prefill_seconds;
+  double comm_bytes_total;
+  double actor_loss, critic_loss;
+  double mean_score, mean_kl;
+  int gpu_launches;                    /* kernels this rank launched in the step */
+} rlhf_step_report;
+
+/* One PPO iteration (generation -> forward x4 -> GAE -> train -> sync).
+ * prompts_host: [batch, prompt_len] int32 for this rank's shard, or NULL to use
+ * the seeded synthetic prompts.  stream: cudaStream_t (NULL = engine stream). */
+int rlhf_engine_step(rlhf_engine* e, const int32_t* prompts_host, rlhf_step_report* rep);
+
+/* Copy a named engine tensor to host (parity tests).  Names: "tokens" int32
+ * [B,S]; "logp_old", "logp_ref", "values", "rewards", "advantages", "returns"
+ * fp32 [B,R]; "score" [B]; "actor_grad", "critic_grad", "actor_master",
+ * "critic_master" fp32 flat; "actor_params", "critic_params", "ref_params",
+ * "reward_params" bf16 flat.  bytes must equal the tensor size. */
+int rlhf_engine_read(rlhf_engine* e, const char* name, void* host, size_t bytes);
+/* Size in bytes of a named tensor (0 if unknown). */
+size_t rlhf_engine_tensor_bytes(rlhf_engine* e, const char* name);
+
+/* Teacher-forced generation check: feed `tokens_host` [B,S] through the decode
+ * path and return the greedy prediction + top-2 margin at every generated
+ * position ([B,R] each). */
+int rlhf_engine_greedy_check(rlhf_engine* e, const int32_t* tokens_host, int32_t* pred_host,
+                             float* margin_host);
+
+const char* rlhf_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RLHF_ENGINE_H */

@@ -1,0 +1,253 @@
+"""Generate golden vectors for the oracle (tests/golden/c1_golden.npz).
+
+Independent restatement of the PPO step in torch (float64 autograd), used to pin
+the C++ oracle (oracle/ppo_oracle.cpp), whose backward pass is hand-derived.
+Nothing here is shared with the oracle except the INPUT format: the seeded
+weight/prompt generator of include/rlhf_init.h, re-implemented below in numpy.
+
+Forward rounding points (bf16) match the oracle's contract; they are
+straight-through in autograd, so gradients here are exact float64 gradients of
+the rounded forward -- the oracle (which also rounds gradients to bf16 at GEMM
+inputs) must agree within the tolerances in tests/test_oracle_golden.py.
+
+Numerics: DeepSpeed-Chat step 3.  Run:
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+
+torch.set_default_dtype(torch.float64)
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+# ---- rlhf_init.h re-implemented in numpy -----------------------------------
+M64 = (1 << 64) - 1
+T_TOK, T_POS, T_LN1G, T_LN1B, T_WQKV, T_BQKV, T_WO, T_BO, T_LN2G, T_LN2B, T_W1, T_B1, T_W2, T_B2, \
+    T_LNFG, T_LNFB, T_VHEAD = range(17)
+LAYER_T = list(range(T_LN1G, T_B2 + 1))
+
+
+def splitmix(x):
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def uniform(stream, counter):
+    with np.errstate(over="ignore"):
+        z = splitmix(np.uint64(stream) ^ splitmix(np.asarray(counter, np.uint64) + np.uint64(0x632BE59BD9B4E019)))
+    return ((z >> np.uint64(11)).astype(np.float64) + 0.5) * (1.0 / 9007199254740992.0)
+
+
+def normal(stream, n):
+    i = np.arange(n, dtype=np.uint64)
+    u1, u2 = uniform(stream, 2 * i), uniform(stream, 2 * i + np.uint64(1))
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(6.283185307179586 * u2)
+
+
+def to_bf16(x):
+    """float -> bf16 value (float64 holding it), round-to-nearest-even via float32."""
+    f = np.asarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + np.uint64(0x7FFF) + ((u >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)
+    return (u.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+def stream_of(seed, t, l):
+    with np.errstate(over="ignore"):
+        v = np.uint64(seed) * np.uint64(0x100000001B3) + np.uint64(t * 4099) + np.uint64(l * 131) + np.uint64(17)
+    return int(splitmix(v))
+
+
+def init_dist(arch, t):
+    if t == T_TOK:
+        return 0.0, 2.0 / np.sqrt(arch["d"])
+    if t == T_POS:
+        return 0.0, 1.0
+    if t in (T_LN1G, T_LN2G, T_LNFG):
+        return 1.0, 0.05
+    if t == T_VHEAD:
+        return 0.0, 1.0 / np.sqrt(arch["d"])
+    if t in (T_WQKV, T_WO, T_W1):
+        return 0.0, 1.0 / np.sqrt(arch["d"])
+    if t == T_W2:
+        return 0.0, 1.0 / np.sqrt(arch["ff"])
+    return 0.0, 0.02
+
+
+def shape_of(arch, t):
+    V, d, f, mp = arch["V"], arch["d"], arch["ff"], arch["max_pos"]
+    return {T_TOK: (V, d), T_POS: (mp, d), T_WQKV: (3 * d, d), T_BQKV: (3 * d,), T_WO: (d, d),
+            T_W1: (f, d), T_B1: (f,), T_W2: (d, f), T_VHEAD: (d,)}.get(t, (d,))
+
+
+def make_weights(arch, seed, scalar_head):
+    def gen(t, l):
+        shp = shape_of(arch, t)
+        mean, std = init_dist(arch, t)
+        return torch.tensor(to_bf16(mean + std * normal(stream_of(seed, t, l), int(np.prod(shp)))).reshape(shp))
+    w = {"tok": gen(T_TOK, 0), "pos": gen(T_POS, 0), "lnf_g": gen(T_LNFG, 0), "lnf_b": gen(T_LNFB, 0), "layers": []}
+    names = ["ln1_g", "ln1_b", "wqkv", "bqkv", "wo", "bo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2"]
+    for l in range(arch["L"]):
+        w["layers"].append({n: gen(t, l) for n, t in zip(names, LAYER_T)})
+    if scalar_head:
+        w["vhead"] = gen(T_VHEAD, 0)
+    return w
+
+
+def prompt_token(seed, b, t, V):
+    with np.errstate(over="ignore"):
+        z = splitmix(splitmix(np.uint64(seed) ^ np.uint64(0xA5A5A5A5)) + np.uint64(b * 1000003) + np.uint64(t))
+    return int(z % np.uint64(V))
+
+
+# ---- model in torch ----------------------------------------------------------
+class RoundBF16(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        return torch.tensor(to_bf16(x.detach().numpy()))
+
+    @staticmethod
+    def backward(ctx, g):
+        return g
+
+
+rb = RoundBF16.apply
+
+
+def layernorm(x, g, b):
+    mu = x.mean(-1, keepdim=True)
+    var = ((x - mu) ** 2).mean(-1, keepdim=True)
+    return (x - mu) / torch.sqrt(var + 1e-5) * g + b
+
+
+def decoder(w, tok, arch):
+    """tok [B,S] long -> final-LN hidden [B,S,d] (bf16-rounded)."""
+    B, S = tok.shape
+    d, H = arch["d"], arch["H"]
+    hd = d // H
+    x = w["tok"][tok] + w["pos"][:S][None]
+    mask = torch.ones(S, S, dtype=torch.bool).tril()
+    for lw in w["layers"]:
+        h = rb(layernorm(x, lw["ln1_g"], lw["ln1_b"]))
+        qkv = rb(h @ lw["wqkv"].T + lw["bqkv"])
+        q, k, v = qkv.split(d, -1)
+        q = q.view(B, S, H, hd).transpose(1, 2)
+        k = k.view(B, S, H, hd).transpose(1, 2)
+        v = v.view(B, S, H, hd).transpose(1, 2)
+        s = (q @ k.transpose(-1, -2)) * (1.0 / np.sqrt(hd))
+        s = s.masked_fill(~mask, float("-inf"))
+        p = rb(torch.softmax(s, -1))
+        o = rb((p @ v).transpose(1, 2).reshape(B, S, d))
+        x = x + (o @ lw["wo"].T + lw["bo"])
+        h2 = rb(layernorm(x, lw["ln2_g"], lw["ln2_b"]))
+        f = rb(torch.relu(h2 @ lw["w1"].T + lw["b1"]))
+        x = x + (f @ lw["w2"].T + lw["b2"])
+    return rb(layernorm(x, w["lnf_g"], w["lnf_b"]))
+
+
+def params_of(w):
+    ps = [w["tok"], w["pos"]]
+    for lw in w["layers"]:
+        ps += list(lw.values())
+    ps += [w["lnf_g"], w["lnf_b"]]
+    if "vhead" in w:
+        ps.append(w["vhead"])
+    return ps
+
+
+def main():
+    arch = dict(V=512, d=128, L=2, H=2, ff=512, max_pos=64)
+    B, P, R = 4, 16, 16
+    S = P + R
+    seed, prompt_seed = 7, 1000
+    kl_ctl, clip_reward, gamma, lam, clip, clipv = 0.1, 5.0, 1.0, 0.95, 0.2, 0.2
+
+    actor = make_weights(arch, seed * 16 + 0, False)
+    critic = make_weights(arch, seed * 16 + 1, True)
+    ref = make_weights(arch, seed * 16 + 2, False)
+    reward = make_weights(arch, seed * 16 + 3, True)
+
+    tok = torch.zeros(B, S, dtype=torch.long)
+    for b in range(B):
+        for t in range(P):
+            tok[b, t] = prompt_token(prompt_seed, b, t, arch["V"])
+    margins = np.zeros((B, R))
+    with torch.no_grad():  # greedy generation by full recomputation (no KV cache)
+        for step in range(R):
+            t = P - 1 + step
+            hf = decoder(actor, tok[:, : t + 1], arch)
+            z = hf[:, t] @ actor["tok"].T
+            top = torch.topk(z, 2, -1)
+            tok[:, t + 1] = top.indices[:, 0]
+            margins[:, step] = (top.values[:, 0] - top.values[:, 1]).numpy()
+
+    def logprobs(w, hf):
+        z = hf[:, P - 1:S - 1] @ w["tok"].T
+        return torch.log_softmax(z, -1).gather(-1, tok[:, P:, None])[..., 0]
+
+    with torch.no_grad():
+        logp_old = logprobs(actor, decoder(actor, tok, arch))
+        values = decoder(critic, tok, arch)[:, P - 1:S - 1] @ critic["vhead"]
+        logp_ref = logprobs(ref, decoder(ref, tok, arch))
+        score = decoder(reward, tok, arch)[:, S - 1] @ reward["vhead"]
+        rewards = -kl_ctl * (logp_old - logp_ref)
+        rewards[:, -1] += score.clamp(-clip_reward, clip_reward)
+        adv = torch.zeros(B, R)
+        last = torch.zeros(B)
+        for j in reversed(range(R)):
+            nextv = values[:, j + 1] if j < R - 1 else torch.zeros(B)
+            delta = rewards[:, j] + gamma * nextv - values[:, j]
+            last = delta + gamma * lam * last
+            adv[:, j] = last
+        returns = adv + values
+
+    N = B * R
+    for p in params_of(actor):
+        p.requires_grad_(True)
+    logp = logprobs(actor, decoder(actor, tok, arch))
+    ratio = torch.exp(logp - logp_old)
+    actor_loss = torch.sum(torch.max(-adv * ratio, -adv * ratio.clamp(1 - clip, 1 + clip))) / N
+    actor_loss.backward()
+
+    for p in params_of(critic):
+        p.requires_grad_(True)
+    v = decoder(critic, tok, arch)[:, P - 1:S - 1] @ critic["vhead"]
+    vc = torch.max(torch.min(v, values + clipv), values - clipv)
+    critic_loss = 0.5 * torch.sum(torch.max((v - returns) ** 2, (vc - returns) ** 2)) / N
+    critic_loss.backward()
+
+    def grad_summary(w):
+        out = {}
+        names = ["tok", "pos"] + [f"l{l}.{k}" for l in range(arch["L"]) for k in w["layers"][l]] + ["lnf_g", "lnf_b"]
+        if "vhead" in w:
+            names.append("vhead")
+        for name, p in zip(names, params_of(w)):
+            g = p.grad.detach().numpy().ravel()
+            out[name] = (g[:256].astype(np.float32), float(np.linalg.norm(g)), float(g.sum()))
+        return out
+
+    fx = dict(
+        config=np.array([B, P, R, seed, prompt_seed]), arch=np.array([arch[k] for k in ("V", "d", "L", "H", "ff", "max_pos")]),
+        tokens=tok.numpy().astype(np.int32), margins=margins.astype(np.float32),
+        logp_old=logp_old.numpy().astype(np.float32), logp_ref=logp_ref.numpy().astype(np.float32),
+        values=values.numpy().astype(np.float32), score=score.numpy().astype(np.float32),
+        rewards=rewards.numpy().astype(np.float32), advantages=adv.numpy().astype(np.float32),
+        returns=returns.numpy().astype(np.float32), losses=np.array([actor_loss.item(), critic_loss.item()]),
+    )
+    for tag, w in (("actor", actor), ("critic", critic)):
+        for name, (head, norm, tot) in grad_summary(w).items():
+            fx[f"{tag}_grad/{name}/head"] = head
+            fx[f"{tag}_grad/{name}/stats"] = np.array([norm, tot])
+    np.savez_compressed(os.path.join(HERE, "c1_golden.npz"), **fx)
+    print("wrote", os.path.join(HERE, "c1_golden.npz"), "losses", fx["losses"], "min margin", margins.min())
+
+
+if __name__ == "__main__":
+    main()
