@@ -1,0 +1,136 @@
+/* rlhf_kernels.h — per-op C-ABI of the sm_100a kernels (lower boundary).
+ *
+ * The reference prices every stage task with
+ *     double stage_compute_time(TaskKind, const ModelSpec&, const ParallelCfg&,
+ *                               const PipelineSpec&, const ClusterTopology&, const CostModel&)
+ *     (/root/reference/proj/include/rlhfsim/costmodel.hpp:63-64; formula SPEC.md:209:
+ *      Generation = prefill + gen_len x decode, Forward = 2*P*B*(prompt+gen),
+ *      TrainFB = 6*P*B*(prompt+gen))
+ * The engine executes those tasks instead; each entry point below is one piece
+ * of that execution, tagged with the TaskKind it serves.
+ *
+ * Conventions: POD params, raw device pointers, caller-owned
+ * memory (workspaces included), asynchronous on the given stream, int status
+ * (0 ok, 2 bad argument, 5 CUDA error).  No CPU fallback.
+ * Element types: bf16 = uint16 bit pattern (__nv_bfloat16), f32 = float.
+ */
+#ifndef RLHF_KERNELS_H
+#define RLHF_KERNELS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* rlhf_stream_t; /* == cudaStream_t */
+
+/* ---- GEMM (Generation prefill/decode, Forward, TrainFB fwd+bwd) -----------
+ * Per batch z = b*batch_h + h:  C[m,n] = epilogue( alpha * sum_k A[m,k] B[n,k] )
+ *   A logical [M,K]: a_mn_major=0 -> element (m,k) at A + m*lda + k (K contiguous)
+ *                    a_mn_major=1 -> element (m,k) at A + k*lda + m (M contiguous)
+ *   B logical [N,K]: same with ldb / b_mn_major.   (+ h*stride_h + b*stride_b)
+ *   C element (m,n) at C + b*c_stride_b + h*c_stride_h + m*c_rs + n*c_cs.
+ * Epilogue: v = alpha*acc (+ bias[n] or bias[m]); relu; v *= (aux[m,n] > 0);
+ *           accumulate -> v += C_old; store bf16/f32.
+ * causal: 0 none; 1 "QK" skip tiles strictly above the diagonal; 2 "PV"
+ *         reduce k < m0+128 only; 3 "TN" reduce k >= floor(m0/64)*64 only.
+ * split_k > 1: deterministic split-K (fixed-order reduction) needing
+ *   workspace >= rlhf_gemm_workspace_bytes() and zeroed int counters. */
+typedef struct rlhf_gemm_params {
+  int M, N, K;
+  int batch, batch_h;
+  const void* A; int a_mn_major; int64_t lda, a_stride_h, a_stride_b;
+  const void* B; int b_mn_major; int64_t ldb, b_stride_h, b_stride_b;
+  void* C; int c_f32; int64_t c_rs, c_cs, c_stride_h, c_stride_b;
+  float alpha;
+  int accumulate;
+  const void* bias; int bias_f32; int bias_along_m;
+  int relu;
+  const void* aux; int64_t aux_rs, aux_cs; /* bf16 mask source, same batch strides as C */
+  int causal;
+  int split_k;
+  int block_n;        /* 0 = auto; else 32/64/128/256 */
+  void* workspace; size_t workspace_bytes;
+  int* counters; int counters_len;
+} rlhf_gemm_params;
+
+int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t s);
+size_t rlhf_gemm_workspace_bytes(const rlhf_gemm_params* p);
+int rlhf_gemm_block_n(const rlhf_gemm_params* p); /* tile width the dispatcher picks */
+
+/* ---- embedding / norms (all stages) --------------------------------------
+ * x[r] = tok_emb[tokens[b*tok_stride + p]] + pos_emb[p],  r = b*T + i,
+ * p = p0 + i, with p0 = *p0_dev when p0_dev != NULL (decode steps in a graph). */
+int rlhf_embed(const int32_t* tokens, int64_t tok_stride, int B, int T, int p0, const int* p0_dev,
+               const void* tok_emb, const void* pos_emb, int d, float* x, rlhf_stream_t s);
+/* tok_emb grad (+ pos grad) scatter-add of dx [B*T, d] (TrainFB). */
+int rlhf_embed_bwd(const int32_t* tokens, int64_t tok_stride, int B, int T, const float* dx, int d,
+                   float* dtok_emb, float* dpos_emb, rlhf_stream_t s);
+/* y = bf16(LN(x) * g + b), eps 1e-5; mean/rstd optional (saved for backward). */
+int rlhf_layernorm(const float* x, const void* g, const void* b, void* y, float* mean, float* rstd, int M,
+                   int d, rlhf_stream_t s);
+/* dx += LN backward of dy; dg/db partials -> ws [nblk, 2, d] -> reduced into dg, db (+=). */
+int rlhf_layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd, const void* g,
+                       float* dx, float* dg, float* db, int M, int d, float* ws, size_t ws_floats,
+                       rlhf_stream_t s);
+/* out_bf16 = bf16(x) elementwise (n elements). */
+int rlhf_round_bf16(const float* x, void* out, int64_t n, rlhf_stream_t s);
+/* db[n] += sum_m G[m, n] (bf16 G, fp32 sums, fixed order).  ws >= 64*N floats. */
+int rlhf_colsum_bf16(const void* G, int M, int N, float* db, float* ws, rlhf_stream_t s);
+/* Row gather/scatter between [B*S, d] and response rows [B*R, d]: row (b, j) <-> b*S + off + j. */
+int rlhf_gather_rows(const void* src, void* dst, int B, int S, int R, int off, int d, int elem_bytes,
+                     rlhf_stream_t s);
+int rlhf_scatter_rows_f32(const float* src, float* dst, int B, int S, int R, int off, int d, rlhf_stream_t s);
+
+/* ---- attention (Generation prefill, Forward, TrainFB) ---------------------
+ * Row-wise causal softmax of scores [Z, S, S] (f32) -> probs bf16 (zeros above
+ * the diagonal); scores already scaled. */
+int rlhf_attn_softmax(const float* scores, void* probs, int Z, int S, rlhf_stream_t s);
+/* dS = bf16(P * (dP - rowsum(P*dP)) * scale) for the causal lower triangle. */
+int rlhf_attn_softmax_bwd(const void* probs, const float* dP, void* dS, int Z, int S, float scale,
+                          rlhf_stream_t s);
+/* KV cache [B, H, Smax, hd] <- k,v columns of qkv rows [B*T, 3d] at positions p0+i. */
+int rlhf_kv_store(const void* qkv, int B, int T, int p0, const int* p0_dev, int H, int hd, int Smax,
+                  void* kcache, void* vcache, rlhf_stream_t s);
+/* Decode attention: one query per sample at position p (= *pos_dev), keys 0..p. */
+int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax, const void* kcache, const void* vcache,
+                     const int* pos_dev, void* out, rlhf_stream_t s);
+
+/* ---- heads, experience, PPO (Generation, Forward, TrainFB) ---------------- */
+/* logp[r] = z[r, y_r] - logsumexp(z[r, :]), y_r = tokens[b*S + P + j] for r = b*R + j; lse saved. */
+int rlhf_logprob(const float* logits, int rows, int V, const int32_t* tokens, int S, int P, int R,
+                 float* logp, float* lse, rlhf_stream_t s);
+/* dz[r, v] = bf16(g[r] * (1[v == y_r] - exp(z[r,v] - lse[r]))) */
+int rlhf_logprob_bwd(const float* logits, const float* lse, const float* g, int rows, int V,
+                     const int32_t* tokens, int S, int P, int R, void* dz, rlhf_stream_t s);
+/* Greedy pick over logits rows [B, V]: tokens[b*S + *pos_dev + 1] = argmax (ties -> lowest id);
+ * margin (optional, [B]) = top1 - top2.  ws >= B * 64 * 4 floats. */
+int rlhf_argmax_tokens(const float* logits, int B, int V, int32_t* tokens, int S, const int* pos_dev,
+                       float* margin, float* ws, rlhf_stream_t s);
+/* out[b*R + j] = hf[(b*S + off + j)] . w  (bf16 hf rows, bf16 w, fp32 out) */
+int rlhf_scalar_head(const void* hf, const void* w, int B, int S, int R, int off, int d, float* out,
+                     rlhf_stream_t s);
+/* dhf rows += g * w ; dw += sum g * hf  (fp32, fixed order).  ws >= 64*d floats. */
+int rlhf_scalar_head_bwd(const void* hf, const void* w, const float* g, int B, int S, int R, int off, int d,
+                         float* dhf, float* dw, float* ws, rlhf_stream_t s);
+/* Experience buffer: rewards = -kl*(logp-logp_ref) (+clip(score) at the last
+ * token); GAE(gamma, lam) -> advantages, returns.  One warp per sample. */
+int rlhf_gae(const float* logp, const float* logp_ref, const float* values, const float* score, int B, int R,
+             float kl_ctl, float clip_reward, float gamma, float lam, float* rewards, float* adv, float* ret,
+             rlhf_stream_t s);
+/* PPO clipped policy loss: g = dL/dlogp; loss_sum[0] += sum(max(pg1, pg2)). */
+int rlhf_ppo_actor_loss(const float* logp, const float* logp_old, const float* adv, int n, float clip, float denom,
+                        float* g, float* loss_sum, rlhf_stream_t s);
+/* Clipped value loss: g = dL/dv; loss_sum[0] += sum(max(l1, l2)) (x0.5/denom on host). */
+int rlhf_ppo_critic_loss(const float* v, const float* v_old, const float* ret, int n, float clip, float denom,
+                         float* g, float* loss_sum, rlhf_stream_t s);
+/* Fused AdamW over a flat fp32 master: m, v updated; bf16 copy written. */
+int rlhf_adamw(float* master, float* m, float* v, const float* grad, void* w_bf16, int64_t n, float lr,
+               float beta1, float beta2, float eps, float weight_decay, int step, rlhf_stream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RLHF_KERNELS_H */

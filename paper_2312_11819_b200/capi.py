@@ -91,6 +91,8 @@ def lib() -> C.CDLL:
 def _declare(L: C.CDLL) -> None:
     i, p, vp = C.c_int, C.POINTER, C.c_void_p
     L.rlhf_last_error.restype = C.c_char_p
+    if not hasattr(L, "rlhf_engine_create"):
+        return
     L.rlhf_task_graph.argtypes = [i] * 8 + [p(i)] * 9
     L.rlhf_plan.argtypes = [C.c_char_p, i, i, C.c_double, i, p(C.c_uint32), p(i), C.c_char_p, i]
     L.rlhf_comm_schedule.argtypes = [C.c_char_p, i, i, i, i, i, i, p(i), p(i), p(i), p(i), p(C.c_double),

@@ -1,0 +1,284 @@
+// heads.cu — output heads and the experience-buffer / PPO math of one step:
+// LM log-softmax gather (fwd + bwd), greedy argmax sampler, scalar value/reward
+// head (fwd + bwd), reward shaping + GAE, clipped actor / value losses.
+// Numerics: DeepSpeed-Chat step 3 conventions; reference
+// structure: experience-buffer barrier /root/reference/proj/src/workload.cpp:153-163.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cfloat>
+
+#include "rlhf_kernels.h"
+
+namespace rlhf {
+
+__device__ __forceinline__ float hb2f(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+__device__ __forceinline__ uint16_t hf2b(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
+
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, Op op, T* sh) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x / 32, nw = blockDim.x / 32;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[w] = v;
+  __syncthreads();
+  T r = sh[0];
+  for (int k = 1; k < nw; ++k) r = op(r, sh[k]);
+  return r;
+}
+
+struct MaxOp { __device__ float operator()(float a, float b) const { return fmaxf(a, b); } };
+struct SumOp { __device__ float operator()(float a, float b) const { return a + b; } };
+
+// One CTA per logits row r = b*R + j; target y = tokens[b*S + P + j].
+__global__ void logprob_kernel(const float* __restrict__ z, int V, const int32_t* __restrict__ tok, int S, int P, int R,
+                               float* __restrict__ logp, float* __restrict__ lse_out) {
+  __shared__ float sh[32];
+  const int r = blockIdx.x;
+  const float* zr = z + static_cast<int64_t>(r) * V;
+  float mx = -FLT_MAX;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) mx = fmaxf(mx, zr[v]);
+  mx = block_reduce(mx, MaxOp(), sh);
+  float s = 0.f;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) s += expf(zr[v] - mx);
+  s = block_reduce(s, SumOp(), sh);
+  if (threadIdx.x == 0) {
+    const float lse = mx + logf(s);
+    const int b = r / R, j = r % R;
+    const int y = tok[static_cast<int64_t>(b) * S + P + j];
+    logp[r] = zr[y] - lse;
+    if (lse_out) lse_out[r] = lse;
+  }
+}
+
+__global__ void logprob_bwd_kernel(const float* __restrict__ z, const float* __restrict__ lse, const float* __restrict__ g,
+                                   int V, const int32_t* __restrict__ tok, int S, int P, int R, uint16_t* __restrict__ dz) {
+  const int r = blockIdx.x;
+  const int b = r / R, j = r % R;
+  const int y = tok[static_cast<int64_t>(b) * S + P + j];
+  const float* zr = z + static_cast<int64_t>(r) * V;
+  uint16_t* o = dz + static_cast<int64_t>(r) * V;
+  const float L = lse[r], gr = g[r];
+  for (int v = threadIdx.x; v < V; v += blockDim.x) o[v] = hf2b(gr * ((v == y ? 1.0f : 0.0f) - expf(zr[v] - L)));
+}
+
+// Greedy argmax per sample (ties -> lowest id) + top-2 margin.  Two phases:
+// 64 CTAs per row scan slices into ws, then one warp per row merges.
+constexpr int kArgSlices = 64;
+
+struct Top2 { float v1; int i1; float v2; };
+
+__device__ __forceinline__ Top2 top2_merge(Top2 a, Top2 b) {
+  Top2 r;
+  if (b.v1 > a.v1 || (b.v1 == a.v1 && b.i1 < a.i1)) {
+    r.v1 = b.v1; r.i1 = b.i1; r.v2 = fmaxf(a.v1, b.v2);
+  } else {
+    r.v1 = a.v1; r.i1 = a.i1; r.v2 = fmaxf(a.v2, b.v1);
+  }
+  return r;
+}
+
+__global__ void argmax_slice_kernel(const float* __restrict__ z, int V, float* __restrict__ ws) {
+  const int b = blockIdx.y, sl = blockIdx.x;
+  const int per = (V + kArgSlices - 1) / kArgSlices;
+  const int v0 = sl * per, v1 = min(V, v0 + per);
+  Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
+  for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) t = top2_merge(t, Top2{z[static_cast<int64_t>(b) * V + v], v, -FLT_MAX});
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Top2 u{__shfl_xor_sync(0xffffffffu, t.v1, o), __shfl_xor_sync(0xffffffffu, t.i1, o), __shfl_xor_sync(0xffffffffu, t.v2, o)};
+    t = top2_merge(t, u);
+  }
+  __shared__ Top2 sh[8];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < blockDim.x / 32; ++w) t = top2_merge(t, sh[w]);
+    float* o = ws + (static_cast<int64_t>(b) * kArgSlices + sl) * 4;
+    o[0] = t.v1; o[1] = __int_as_float(t.i1); o[2] = t.v2;
+  }
+}
+
+__global__ void argmax_merge_kernel(const float* __restrict__ ws, int B, int32_t* __restrict__ tok, int S,
+                                    const int* __restrict__ pos_dev, float* __restrict__ margin) {
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x;
+  Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
+  for (int s = lane; s < kArgSlices; s += 32) {
+    const float* o = ws + (static_cast<int64_t>(b) * kArgSlices + s) * 4;
+    t = top2_merge(t, Top2{o[0], __float_as_int(o[1]), o[2]});
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Top2 u{__shfl_xor_sync(0xffffffffu, t.v1, o), __shfl_xor_sync(0xffffffffu, t.i1, o), __shfl_xor_sync(0xffffffffu, t.v2, o)};
+    t = top2_merge(t, u);
+  }
+  if (lane == 0) {
+    tok[static_cast<int64_t>(b) * S + *pos_dev + 1] = t.i1;
+    if (margin) margin[b] = t.v1 - t.v2;
+  }
+}
+
+// out[b*R + j] = hf[b*S + off + j] . w   (warp per row)
+__global__ void scalar_head_kernel(const uint16_t* __restrict__ hf, const uint16_t* __restrict__ w, int S, int R, int off,
+                                   int d, float* __restrict__ out, int rows) {
+  const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int b = r / R, j = r % R;
+  const uint16_t* h = hf + (static_cast<int64_t>(b) * S + off + j) * d;
+  float s = 0.f;
+  for (int e = lane; e < d; e += 32) s += hb2f(h[e]) * hb2f(w[e]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[r] = s;
+}
+
+// dhf[row] += g * w ; per-chunk partials of dw (fixed order)
+constexpr int kHeadChunks = 64;
+__global__ void scalar_head_bwd_kernel(const uint16_t* __restrict__ hf, const uint16_t* __restrict__ w,
+                                       const float* __restrict__ g, int S, int R, int off, int d, float* __restrict__ dhf,
+                                       float* __restrict__ ws, int rows) {
+  const int chunk = blockIdx.y;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d) return;
+  const int per = (rows + kHeadChunks - 1) / kHeadChunks;
+  const int r0 = chunk * per, r1 = min(rows, r0 + per);
+  const float we = hb2f(w[e]);
+  float acc = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    const int b = r / R, j = r % R;
+    const int64_t row = static_cast<int64_t>(b) * S + off + j;
+    dhf[row * d + e] += g[r] * we;
+    acc += g[r] * hb2f(hf[row * d + e]);
+  }
+  ws[static_cast<int64_t>(chunk) * d + e] = acc;
+}
+
+__global__ void sum_chunks_kernel(const float* __restrict__ ws, int chunks, int n, float* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  float s = 0.f;
+  for (int c = 0; c < chunks; ++c) s += ws[static_cast<int64_t>(c) * n + e];
+  out[e] += s;
+}
+
+// One thread per sample: reverse scan over the response (R sequential steps).
+__global__ void gae_kernel(const float* __restrict__ logp, const float* __restrict__ logp_ref, const float* __restrict__ val,
+                           const float* __restrict__ score, int B, int R, float kl, float clip_r, float gamma, float lam,
+                           float* __restrict__ rew, float* __restrict__ adv, float* __restrict__ ret) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int64_t o = static_cast<int64_t>(b) * R;
+  for (int j = 0; j < R; ++j) rew[o + j] = -kl * (logp[o + j] - logp_ref[o + j]);
+  rew[o + R - 1] += fminf(fmaxf(score[b], -clip_r), clip_r);
+  float last = 0.f;
+  for (int j = R - 1; j >= 0; --j) {
+    const float nextv = j < R - 1 ? val[o + j + 1] : 0.0f;
+    const float delta = rew[o + j] + gamma * nextv - val[o + j];
+    last = delta + gamma * lam * last;
+    adv[o + j] = last;
+  }
+  for (int j = 0; j < R; ++j) ret[o + j] = adv[o + j] + val[o + j];
+}
+
+__global__ void actor_loss_kernel(const float* __restrict__ lp, const float* __restrict__ lpo, const float* __restrict__ A,
+                                  int n, float clip, float denom, float* __restrict__ g, float* __restrict__ loss) {
+  __shared__ float sh[32];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  float l = 0.f;
+  if (k < n) {
+    const float ratio = expf(lp[k] - lpo[k]);
+    const float a = A[k];
+    const float cl = fminf(fmaxf(ratio, 1.0f - clip), 1.0f + clip);
+    const float pg1 = -a * ratio, pg2 = -a * cl;
+    l = fmaxf(pg1, pg2);
+    const bool inside = ratio >= 1.0f - clip && ratio <= 1.0f + clip;
+    const float d1 = -a * ratio / denom, d2 = inside ? -a * ratio / denom : 0.0f;
+    g[k] = pg1 > pg2 ? d1 : (pg1 < pg2 ? d2 : 0.5f * (d1 + d2));
+  }
+  l = block_reduce(l, SumOp(), sh);
+  if (threadIdx.x == 0) atomicAdd(loss, l);
+}
+
+__global__ void critic_loss_kernel(const float* __restrict__ v, const float* __restrict__ vo, const float* __restrict__ ret,
+                                   int n, float clip, float denom, float* __restrict__ g, float* __restrict__ loss) {
+  __shared__ float sh[32];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  float l = 0.f;
+  if (k < n) {
+    const float x = v[k], o = vo[k], R = ret[k];
+    const float vc = fminf(fmaxf(x, o - clip), o + clip);
+    const float l1 = (x - R) * (x - R), l2 = (vc - R) * (vc - R);
+    l = fmaxf(l1, l2);
+    const bool inside = x >= o - clip && x <= o + clip;
+    const float d1 = (x - R) / denom, d2 = inside ? (vc - R) / denom : 0.0f;
+    g[k] = l1 > l2 ? d1 : (l1 < l2 ? d2 : 0.5f * (d1 + d2));
+  }
+  l = block_reduce(l, SumOp(), sh);
+  if (threadIdx.x == 0) atomicAdd(loss, l);
+}
+
+}  // namespace rlhf
+
+using namespace rlhf;
+
+static inline cudaStream_t HS(rlhf_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline int HST() { return cudaGetLastError() == cudaSuccess ? 0 : 5; }
+
+extern "C" int rlhf_logprob(const float* logits, int rows, int V, const int32_t* tokens, int S, int P, int R, float* logp,
+                            float* lse, rlhf_stream_t s) {
+  logprob_kernel<<<rows, 512, 0, HS(s)>>>(logits, V, tokens, S, P, R, logp, lse);
+  return HST();
+}
+
+extern "C" int rlhf_logprob_bwd(const float* logits, const float* lse, const float* g, int rows, int V,
+                                const int32_t* tokens, int S, int P, int R, void* dz, rlhf_stream_t s) {
+  logprob_bwd_kernel<<<rows, 512, 0, HS(s)>>>(logits, lse, g, V, tokens, S, P, R, static_cast<uint16_t*>(dz));
+  return HST();
+}
+
+extern "C" int rlhf_argmax_tokens(const float* logits, int B, int V, int32_t* tokens, int S, const int* pos_dev,
+                                  float* margin, float* ws, rlhf_stream_t s) {
+  argmax_slice_kernel<<<dim3(kArgSlices, B), 256, 0, HS(s)>>>(logits, V, ws);
+  argmax_merge_kernel<<<B, 32, 0, HS(s)>>>(ws, B, tokens, S, pos_dev, margin);
+  return HST();
+}
+
+extern "C" int rlhf_scalar_head(const void* hf, const void* w, int B, int S, int R, int off, int d, float* out,
+                                rlhf_stream_t s) {
+  const int rows = B * R;
+  scalar_head_kernel<<<(rows + 7) / 8, 256, 0, HS(s)>>>(static_cast<const uint16_t*>(hf), static_cast<const uint16_t*>(w), S,
+                                                        R, off, d, out, rows);
+  return HST();
+}
+
+extern "C" int rlhf_scalar_head_bwd(const void* hf, const void* w, const float* g, int B, int S, int R, int off, int d,
+                                    float* dhf, float* dw, float* ws, rlhf_stream_t s) {
+  const int rows = B * R;
+  scalar_head_bwd_kernel<<<dim3((d + 255) / 256, kHeadChunks), 256, 0, HS(s)>>>(
+      static_cast<const uint16_t*>(hf), static_cast<const uint16_t*>(w), g, S, R, off, d, dhf, ws, rows);
+  sum_chunks_kernel<<<(d + 255) / 256, 256, 0, HS(s)>>>(ws, kHeadChunks, d, dw);
+  return HST();
+}
+
+extern "C" int rlhf_gae(const float* logp, const float* logp_ref, const float* values, const float* score, int B, int R,
+                        float kl_ctl, float clip_reward, float gamma, float lam, float* rewards, float* adv, float* ret,
+                        rlhf_stream_t s) {
+  gae_kernel<<<(B + 127) / 128, 128, 0, HS(s)>>>(logp, logp_ref, values, score, B, R, kl_ctl, clip_reward, gamma, lam,
+                                                 rewards, adv, ret);
+  return HST();
+}
+
+extern "C" int rlhf_ppo_actor_loss(const float* logp, const float* logp_old, const float* adv, int n, float clip,
+                                   float denom, float* g, float* loss_sum, rlhf_stream_t s) {
+  actor_loss_kernel<<<(n + 255) / 256, 256, 0, HS(s)>>>(logp, logp_old, adv, n, clip, denom, g, loss_sum);
+  return HST();
+}
+
+extern "C" int rlhf_ppo_critic_loss(const float* v, const float* v_old, const float* ret, int n, float clip, float denom,
+                                    float* g, float* loss_sum, rlhf_stream_t s) {
+  critic_loss_kernel<<<(n + 255) / 256, 256, 0, HS(s)>>>(v, v_old, ret, n, clip, denom, g, loss_sum);
+  return HST();
+}

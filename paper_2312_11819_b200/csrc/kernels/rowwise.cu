@@ -1,0 +1,297 @@
+// rowwise.cu — HBM-bound row / element kernels of the PPO step: embedding
+// (fwd + scatter-add bwd), LayerNorm (fwd + bwd), bf16 rounding, bias-gradient
+// column sums, response-row gather/scatter, fused AdamW.
+// All follow the rounding contract in DESIGN.md §3 (mirrored by oracle/ppo_oracle.cpp).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "rlhf_kernels.h"
+
+namespace rlhf {
+
+__device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+__device__ __forceinline__ uint16_t f2bf(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+static inline int cuda_status() { return cudaGetLastError() == cudaSuccess ? 0 : 5; }
+static inline cudaStream_t S(rlhf_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// x[r] = E[tok] + Pm[p]; one thread per (row, 4 columns).
+__global__ void embed_kernel(const int32_t* __restrict__ tokens, int64_t tok_stride, int T, int p0,
+                             const int* __restrict__ p0_dev, const uint16_t* __restrict__ E,
+                             const uint16_t* __restrict__ Pm, int d, float* __restrict__ x, int rows) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int qd = d / 4;
+  if (idx >= static_cast<int64_t>(rows) * qd) return;
+  const int r = static_cast<int>(idx / qd), c = static_cast<int>(idx % qd) * 4;
+  const int b = r / T, i = r % T;
+  const int p = (p0_dev ? *p0_dev : p0) + i;
+  const int id = tokens[b * tok_stride + p];
+  const uint2 e = *reinterpret_cast<const uint2*>(E + static_cast<int64_t>(id) * d + c);
+  const uint2 q = *reinterpret_cast<const uint2*>(Pm + static_cast<int64_t>(p) * d + c);
+  float4 o;
+  o.x = bf2f(e.x & 0xFFFFu) + bf2f(q.x & 0xFFFFu);
+  o.y = bf2f(e.x >> 16) + bf2f(q.x >> 16);
+  o.z = bf2f(e.y & 0xFFFFu) + bf2f(q.y & 0xFFFFu);
+  o.w = bf2f(e.y >> 16) + bf2f(q.y >> 16);
+  *reinterpret_cast<float4*>(x + static_cast<int64_t>(r) * d + c) = o;
+}
+
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ tokens, int64_t tok_stride, int T,
+                                 const float* __restrict__ dx, int d, float* __restrict__ dE, float* __restrict__ dP,
+                                 int rows) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(rows) * d) return;
+  const int r = static_cast<int>(idx / d), c = static_cast<int>(idx % d);
+  const int b = r / T, i = r % T;
+  const int id = tokens[b * tok_stride + i];
+  const float g = dx[idx];
+  atomicAdd(dE + static_cast<int64_t>(id) * d + c, g);
+  atomicAdd(dP + static_cast<int64_t>(i) * d + c, g);
+}
+
+// One warp per row.  Three passes over the row (re-reads hit L1).
+__global__ void layernorm_kernel(const float* __restrict__ x, const uint16_t* __restrict__ g,
+                                 const uint16_t* __restrict__ bta, uint16_t* __restrict__ y, float* __restrict__ mean,
+                                 float* __restrict__ rstd, int M, int d) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * d);
+  const int q = d / 4;
+  float s = 0.f;
+  for (int c = lane; c < q; c += 32) {
+    const float4 v = xr[c];
+    s += (v.x + v.y) + (v.z + v.w);
+  }
+  const float mu = warp_sum(s) / d;
+  float vs = 0.f;
+  for (int c = lane; c < q; c += 32) {
+    const float4 v = xr[c];
+    vs += (v.x - mu) * (v.x - mu) + (v.y - mu) * (v.y - mu) + (v.z - mu) * (v.z - mu) + (v.w - mu) * (v.w - mu);
+  }
+  const float rs = 1.0f / sqrtf(warp_sum(vs) / d + 1e-5f);
+  uint2* yr = reinterpret_cast<uint2*>(y + static_cast<int64_t>(row) * d);
+  const uint2* g2 = reinterpret_cast<const uint2*>(g);
+  const uint2* b2 = reinterpret_cast<const uint2*>(bta);
+  for (int c = lane; c < q; c += 32) {
+    const float4 v = xr[c];
+    const uint2 gg = g2[c], bb = b2[c];
+    const float o0 = (v.x - mu) * rs * bf2f(gg.x & 0xFFFFu) + bf2f(bb.x & 0xFFFFu);
+    const float o1 = (v.y - mu) * rs * bf2f(gg.x >> 16) + bf2f(bb.x >> 16);
+    const float o2 = (v.z - mu) * rs * bf2f(gg.y & 0xFFFFu) + bf2f(bb.y & 0xFFFFu);
+    const float o3 = (v.w - mu) * rs * bf2f(gg.y >> 16) + bf2f(bb.y >> 16);
+    yr[c] = make_uint2(f2bf(o0) | (static_cast<uint32_t>(f2bf(o1)) << 16), f2bf(o2) | (static_cast<uint32_t>(f2bf(o3)) << 16));
+  }
+  if (lane == 0) {
+    if (mean) mean[row] = mu;
+    if (rstd) rstd[row] = rs;
+  }
+}
+
+constexpr int kLnBwdRows = 32;  // rows per block (8 warps x 4 rows)
+
+// dx += rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)); per-block dg/db partials -> ws.
+__global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+                                     const float* __restrict__ mean, const float* __restrict__ rstd,
+                                     const uint16_t* __restrict__ g, float* __restrict__ dx, float* __restrict__ ws,
+                                     int M, int d) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * kLnBwdRows;
+  for (int rr = warp; rr < kLnBwdRows; rr += 8) {
+    const int row = r0 + rr;
+    if (row >= M) break;
+    const float* dr = dy + static_cast<int64_t>(row) * d;
+    const float* xr = x + static_cast<int64_t>(row) * d;
+    const float mu = mean[row], rs = rstd[row];
+    float a = 0.f, c = 0.f;
+    for (int j = lane; j < d; j += 32) {
+      const float xh = (xr[j] - mu) * rs;
+      const float t = dr[j] * bf2f(g[j]);
+      a += t;
+      c += t * xh;
+    }
+    a = warp_sum(a) / d;
+    c = warp_sum(c) / d;
+    float* o = dx + static_cast<int64_t>(row) * d;
+    for (int j = lane; j < d; j += 32) {
+      const float xh = (xr[j] - mu) * rs;
+      o[j] += rs * (dr[j] * bf2f(g[j]) - a - xh * c);
+    }
+  }
+  // column partials of this block (fixed row order -> deterministic)
+  const int r1 = min(M, r0 + kLnBwdRows);
+  float* wg = ws + static_cast<int64_t>(blockIdx.x) * 2 * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float sg = 0.f, sb = 0.f;
+    for (int row = r0; row < r1; ++row) {
+      const float t = dy[static_cast<int64_t>(row) * d + j];
+      sg += t * (x[static_cast<int64_t>(row) * d + j] - mean[row]) * rstd[row];
+      sb += t;
+    }
+    wg[j] = sg;
+    wg[d + j] = sb;
+  }
+}
+
+// out[j] += sum_{blk} ws[blk][j]  (fixed order).  ws laid out [nblk][ncol]; stride = ncol.
+__global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblk, int ncol, int64_t blk_stride,
+                                       float* __restrict__ out0, float* __restrict__ out1, int split) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncol) return;
+  float s = 0.f;
+  for (int k = 0; k < nblk; ++k) s += ws[k * blk_stride + j];
+  if (j < split) out0[j] += s;
+  else out1[j - split] += s;
+}
+
+__global__ void round_bf16_kernel(const float* __restrict__ x, uint16_t* __restrict__ y, int64_t n) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (i + 3 < n) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    *reinterpret_cast<uint2*>(y + i) =
+        make_uint2(f2bf(v.x) | (static_cast<uint32_t>(f2bf(v.y)) << 16), f2bf(v.z) | (static_cast<uint32_t>(f2bf(v.w)) << 16));
+  } else {
+    for (int64_t k = i; k < n; ++k) y[k] = f2bf(x[k]);
+  }
+}
+
+constexpr int kColsumChunks = 64;
+
+__global__ void colsum_bf16_kernel(const uint16_t* __restrict__ G, int M, int N, float* __restrict__ ws) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y;
+  if (col >= N) return;
+  const int per = (M + kColsumChunks - 1) / kColsumChunks;
+  const int r0 = chunk * per, r1 = min(M, r0 + per);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += bf2f(G[static_cast<int64_t>(r) * N + col]);
+  ws[static_cast<int64_t>(chunk) * N + col] = s;
+}
+
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int S, int R, int off,
+                                   int row_bytes) {
+  const int r = blockIdx.x;  // response row b*R + j
+  const int b = r / R, j = r % R;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + (static_cast<int64_t>(b) * S + off + j) * row_bytes);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + static_cast<int64_t>(r) * row_bytes);
+  for (int c = threadIdx.x; c < row_bytes / 16; c += blockDim.x) d4[c] = s4[c];
+}
+
+__global__ void scatter_rows_kernel(const float* __restrict__ src, float* __restrict__ dst, int S, int R, int off, int d) {
+  const int r = blockIdx.x;
+  const int b = r / R, j = r % R;
+  const float4* s4 = reinterpret_cast<const float4*>(src + static_cast<int64_t>(r) * d);
+  float4* d4 = reinterpret_cast<float4*>(dst + (static_cast<int64_t>(b) * S + off + j) * d);
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) d4[c] = s4[c];
+}
+
+__global__ void adamw_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
+                             const float* __restrict__ g, uint16_t* __restrict__ wb, int64_t n, float lr, float b1,
+                             float b2, float eps, float wd, float bc1, float bc2) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i * 4 >= n) return;
+  float4 W = reinterpret_cast<float4*>(w)[i], Mm = reinterpret_cast<float4*>(m)[i], Vv = reinterpret_cast<float4*>(v)[i];
+  const float4 G = reinterpret_cast<const float4*>(g)[i];
+  float* Wp = &W.x;
+  float* Mp = &Mm.x;
+  float* Vp = &Vv.x;
+  const float* Gp = &G.x;
+  uint16_t o[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    Mp[k] = b1 * Mp[k] + (1.0f - b1) * Gp[k];
+    Vp[k] = b2 * Vp[k] + (1.0f - b2) * Gp[k] * Gp[k];
+    const float upd = (Mp[k] / bc1) / (sqrtf(Vp[k] / bc2) + eps);
+    Wp[k] = Wp[k] - lr * (upd + wd * Wp[k]);
+    o[k] = f2bf(Wp[k]);
+  }
+  reinterpret_cast<float4*>(w)[i] = W;
+  reinterpret_cast<float4*>(m)[i] = Mm;
+  reinterpret_cast<float4*>(v)[i] = Vv;
+  reinterpret_cast<uint2*>(wb)[i] = make_uint2(o[0] | (static_cast<uint32_t>(o[1]) << 16), o[2] | (static_cast<uint32_t>(o[3]) << 16));
+}
+
+}  // namespace rlhf
+
+using namespace rlhf;
+
+extern "C" int rlhf_embed(const int32_t* tokens, int64_t tok_stride, int B, int T, int p0, const int* p0_dev,
+                          const void* tok_emb, const void* pos_emb, int d, float* x, rlhf_stream_t s) {
+  if (d % 4) return 2;
+  const int rows = B * T;
+  const int64_t n = static_cast<int64_t>(rows) * (d / 4);
+  embed_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, S(s)>>>(
+      tokens, tok_stride, T, p0, p0_dev, static_cast<const uint16_t*>(tok_emb), static_cast<const uint16_t*>(pos_emb), d, x, rows);
+  return cuda_status();
+}
+
+extern "C" int rlhf_embed_bwd(const int32_t* tokens, int64_t tok_stride, int B, int T, const float* dx, int d,
+                              float* dtok, float* dpos, rlhf_stream_t s) {
+  const int rows = B * T;
+  const int64_t n = static_cast<int64_t>(rows) * d;
+  embed_bwd_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, S(s)>>>(tokens, tok_stride, T, dx, d, dtok, dpos, rows);
+  return cuda_status();
+}
+
+extern "C" int rlhf_layernorm(const float* x, const void* g, const void* b, void* y, float* mean, float* rstd, int M,
+                              int d, rlhf_stream_t s) {
+  if (d % 4) return 2;
+  layernorm_kernel<<<(M + 7) / 8, 256, 0, S(s)>>>(x, static_cast<const uint16_t*>(g), static_cast<const uint16_t*>(b),
+                                                  static_cast<uint16_t*>(y), mean, rstd, M, d);
+  return cuda_status();
+}
+
+extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd, const void* g,
+                                  float* dx, float* dg, float* db, int M, int d, float* ws, size_t ws_floats,
+                                  rlhf_stream_t s) {
+  const int nblk = (M + kLnBwdRows - 1) / kLnBwdRows;
+  if (ws_floats < static_cast<size_t>(nblk) * 2 * d) return 2;
+  layernorm_bwd_kernel<<<nblk, 256, 0, S(s)>>>(dy, x, mean, rstd, static_cast<const uint16_t*>(g), dx, ws, M, d);
+  reduce_partials_kernel<<<(2 * d + 255) / 256, 256, 0, S(s)>>>(ws, nblk, 2 * d, 2 * d, dg, db, d);
+  return cuda_status();
+}
+
+extern "C" int rlhf_round_bf16(const float* x, void* out, int64_t n, rlhf_stream_t s) {
+  const int64_t q = (n + 3) / 4;
+  round_bf16_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, S(s)>>>(x, static_cast<uint16_t*>(out), n);
+  return cuda_status();
+}
+
+extern "C" int rlhf_colsum_bf16(const void* G, int M, int N, float* db, float* ws, rlhf_stream_t s) {
+  dim3 grid((N + 255) / 256, kColsumChunks);
+  colsum_bf16_kernel<<<grid, 256, 0, S(s)>>>(static_cast<const uint16_t*>(G), M, N, ws);
+  reduce_partials_kernel<<<(N + 255) / 256, 256, 0, S(s)>>>(ws, kColsumChunks, N, N, db, db, N);
+  return cuda_status();
+}
+
+extern "C" int rlhf_gather_rows(const void* src, void* dst, int B, int S_, int R, int off, int d, int elem_bytes,
+                                rlhf_stream_t s) {
+  const int row_bytes = d * elem_bytes;
+  if (row_bytes % 16) return 2;
+  gather_rows_kernel<<<B * R, 128, 0, S(s)>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), S_, R, off,
+                                               row_bytes);
+  return cuda_status();
+}
+
+extern "C" int rlhf_scatter_rows_f32(const float* src, float* dst, int B, int S_, int R, int off, int d, rlhf_stream_t s) {
+  if (d % 4) return 2;
+  scatter_rows_kernel<<<B * R, 128, 0, S(s)>>>(src, dst, S_, R, off, d);
+  return cuda_status();
+}
+
+extern "C" int rlhf_adamw(float* master, float* m, float* v, const float* grad, void* w_bf16, int64_t n, float lr,
+                          float beta1, float beta2, float eps, float weight_decay, int step, rlhf_stream_t s) {
+  if (n % 4) return 2;
+  const float bc1 = 1.0f - powf(beta1, static_cast<float>(step));
+  const float bc2 = 1.0f - powf(beta2, static_cast<float>(step));
+  const int64_t q = n / 4;
+  adamw_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, S(s)>>>(master, m, v, grad, static_cast<uint16_t*>(w_bf16), n,
+                                                                          lr, beta1, beta2, eps, weight_decay, bc1, bc2);
+  return cuda_status();
+}

@@ -1,0 +1,92 @@
+"""Thin torch-tensor wrappers over the per-op C-ABI (include/rlhf_kernels.h).
+
+Used by the GPU numerics tests and for ad-hoc kernel timing.  The engine itself
+(csrc/host/engine.cpp) calls the same entry points from C++.  Every call goes to
+the sm_100a library; there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from .capi import lib
+
+
+class GemmParams(C.Structure):
+    _fields_ = [("M", C.c_int), ("N", C.c_int), ("K", C.c_int), ("batch", C.c_int), ("batch_h", C.c_int),
+                ("A", C.c_void_p), ("a_mn_major", C.c_int), ("lda", C.c_int64), ("a_stride_h", C.c_int64),
+                ("a_stride_b", C.c_int64),
+                ("B", C.c_void_p), ("b_mn_major", C.c_int), ("ldb", C.c_int64), ("b_stride_h", C.c_int64),
+                ("b_stride_b", C.c_int64),
+                ("C", C.c_void_p), ("c_f32", C.c_int), ("c_rs", C.c_int64), ("c_cs", C.c_int64),
+                ("c_stride_h", C.c_int64), ("c_stride_b", C.c_int64),
+                ("alpha", C.c_float), ("accumulate", C.c_int),
+                ("bias", C.c_void_p), ("bias_f32", C.c_int), ("bias_along_m", C.c_int),
+                ("relu", C.c_int),
+                ("aux", C.c_void_p), ("aux_rs", C.c_int64), ("aux_cs", C.c_int64),
+                ("causal", C.c_int), ("split_k", C.c_int), ("block_n", C.c_int),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+                ("counters", C.c_void_p), ("counters_len", C.c_int)]
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _declare_gemm():
+    L = lib()
+    L.rlhf_gemm.argtypes = [C.POINTER(GemmParams), C.c_void_p]
+    L.rlhf_gemm_workspace_bytes.argtypes = [C.POINTER(GemmParams)]
+    L.rlhf_gemm_workspace_bytes.restype = C.c_size_t
+    return L
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = False, out: torch.Tensor | None = None,
+         out_f32: bool = True, alpha: float = 1.0, accumulate: bool = False, bias: torch.Tensor | None = None,
+         bias_along_m: bool = False, relu: bool = False, aux: torch.Tensor | None = None, split_k: int = 1,
+         block_n: int = 0, swap_out: bool = False) -> torch.Tensor:
+    """2-D GEMM: C[M,N] = A[M,K] . B[N,K]^T with the C-ABI's operand conventions.
+
+    a_mn: `a` is stored [K, M] (M contiguous); b_mn: `b` is stored [K, N].
+    swap_out: write C transposed (element (m,n) at n*M + m) into `out` [N, M].
+    """
+    L = _declare_gemm()
+    M = a.shape[1] if a_mn else a.shape[0]
+    K = a.shape[0] if a_mn else a.shape[1]
+    N = b.shape[1] if b_mn else b.shape[0]
+    if out is None:
+        shape = (N, M) if swap_out else (M, N)
+        out = torch.zeros(shape, device=a.device, dtype=torch.float32 if out_f32 else torch.bfloat16)
+    p = GemmParams()
+    p.M, p.N, p.K, p.batch, p.batch_h = M, N, K, 1, 1
+    p.A, p.a_mn_major, p.lda = a.data_ptr(), int(a_mn), a.stride(0)
+    p.B, p.b_mn_major, p.ldb = b.data_ptr(), int(b_mn), b.stride(0)
+    p.C, p.c_f32 = out.data_ptr(), int(out.dtype == torch.float32)
+    p.c_rs, p.c_cs = (1, M) if swap_out else (out.stride(0), 1)
+    p.alpha, p.accumulate = alpha, int(accumulate)
+    if bias is not None:
+        p.bias, p.bias_f32, p.bias_along_m = bias.data_ptr(), int(bias.dtype == torch.float32), int(bias_along_m)
+    p.relu = int(relu)
+    if aux is not None:
+        p.aux, p.aux_rs, p.aux_cs = aux.data_ptr(), p.c_rs, p.c_cs
+    p.split_k, p.block_n = split_k, block_n
+    keep = []
+    if split_k > 1:
+        ws_bytes = L.rlhf_gemm_workspace_bytes(C.byref(p))
+        ws = torch.empty(ws_bytes // 4 + 1, device=a.device, dtype=torch.float32)
+        cnt = torch.zeros(65536, device=a.device, dtype=torch.int32)
+        keep += [ws, cnt]
+        p.workspace, p.workspace_bytes = ws.data_ptr(), ws_bytes
+        p.counters, p.counters_len = cnt.data_ptr(), cnt.numel()
+    st = L.rlhf_gemm(C.byref(p), _stream())
+    if st != 0:
+        raise RuntimeError(f"rlhf_gemm failed with status {st}")
+    return out
+
+
+def gemm_batched(params: GemmParams) -> None:
+    L = _declare_gemm()
+    st = L.rlhf_gemm(C.byref(params), _stream())
+    if st != 0:
+        raise RuntimeError(f"rlhf_gemm failed with status {st}")
