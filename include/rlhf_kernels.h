@@ -33,7 +33,8 @@ typedef struct CUstream_st* rlhf_stream_t; /* == cudaStream_t */
  *   B logical [N,K]: same with ldb / b_mn_major.   (+ h*stride_h + b*stride_b)
  *   C element (m,n) at C + b*c_stride_b + h*c_stride_h + m*c_rs + n*c_cs.
  * Epilogue: v = alpha*acc (+ bias[n] or bias[m]); relu; v *= (aux[m,n] > 0);
- *           accumulate -> v += C_old; store bf16/f32.
+ *           v += residual[m,n] (f32, C's strides; may alias C); accumulate -> v += C_old;
+ *           store bf16/f32.
  * causal: 0 none; 1 "QK" skip tiles strictly above the diagonal; 2 "PV"
  *         reduce k < m0+128 only; 3 "TN" reduce k >= floor(m0/64)*64 only.
  * split_k > 1: deterministic split-K (fixed-order reduction) needing
@@ -49,6 +50,7 @@ typedef struct rlhf_gemm_params {
   const void* bias; int bias_f32; int bias_along_m;
   int relu;
   const void* aux; int64_t aux_rs, aux_cs; /* bf16 mask source, same batch strides as C */
+  const float* residual;                    /* f32, same strides as C */
   int causal;
   int split_k;
   int block_n;        /* 0 = auto; else 32/64/128/256 */
@@ -106,7 +108,7 @@ int rlhf_logprob(const float* logits, int rows, int V, const int32_t* tokens, in
 int rlhf_logprob_bwd(const float* logits, const float* lse, const float* g, int rows, int V,
                      const int32_t* tokens, int S, int P, int R, void* dz, rlhf_stream_t s);
 /* Greedy pick over logits rows [B, V]: tokens[b*S + *pos_dev + 1] = argmax (ties -> lowest id);
- * margin (optional, [B]) = top1 - top2.  ws >= B * 64 * 4 floats. */
+ * margin (optional, [B,S] like tokens) = top1 - top2.  ws >= B * 64 * 4 floats. */
 int rlhf_argmax_tokens(const float* logits, int B, int V, int32_t* tokens, int S, const int* pos_dev,
                        float* margin, float* ws, rlhf_stream_t s);
 /* out[b*R + j] = hf[(b*S + off + j)] . w  (bf16 hf rows, bf16 w, fp32 out) */
@@ -126,6 +128,8 @@ int rlhf_ppo_actor_loss(const float* logp, const float* logp_old, const float* a
 /* Clipped value loss: g = dL/dv; loss_sum[0] += sum(max(l1, l2)) (x0.5/denom on host). */
 int rlhf_ppo_critic_loss(const float* v, const float* v_old, const float* ret, int n, float clip, float denom,
                          float* g, float* loss_sum, rlhf_stream_t s);
+/* *p += v on the device (decode position counter inside the CUDA graph). */
+int rlhf_add_int(int* p, int v, rlhf_stream_t s);
 /* Fused AdamW over a flat fp32 master: m, v updated; bf16 copy written. */
 int rlhf_adamw(float* master, float* m, float* v, const float* grad, void* w_bf16, int64_t n, float lr,
                float beta1, float beta2, float eps, float weight_decay, int step, rlhf_stream_t s);

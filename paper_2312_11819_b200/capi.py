@@ -83,6 +83,8 @@ def lib() -> C.CDLL:
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"{LIB_PATH} missing: run paper_2312_11819_b200.build.build() first "
                                "(there is no CPU fallback)")
+        # torch first: its libnccl.so.2 is the one the engine dlopens (nccl_dyn.hpp)
+        import torch  # noqa: F401
         _lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
         _declare(_lib)
     return _lib

@@ -1,0 +1,137 @@
+// engine.hpp — the executor that replaces the reference simulator's analytic
+// clock (simulate(), /root/reference/proj/include/rlhfsim/simulator.hpp:46-47)
+// with real execution of the PPO iteration on one GPU per process.
+//
+// Per rank: the models this rank hosts under its placement (colocated: all
+// four; interleaving: a subset), their bf16 weights (+ fp32 master / Adam state
+// for trainable ones), one activation arena sized for the largest model, the
+// Actor's KV cache, and an NCCL communicator per device group.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "flexrlhf/placement.hpp"
+#include "rlhf_engine.h"
+#include "rlhf_kernels.h"
+
+namespace flexrlhf {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf();
+  void alloc(size_t n);
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// One decoder (OPT family) resident on this device.
+struct Decoder {
+  rlhf_arch a{};
+  uint64_t seed = 0;
+  bool trainable = false;
+  int64_t n = 0;  // flat parameter count (rlhf_param_total)
+  DevBuf w;       // bf16 flat
+  DevBuf master, m, v, grad;  // fp32 flat (trainable only)
+  int adam_step = 0;
+  const uint16_t* T(int t, int l = 0) const { return w.as<uint16_t>() + rlhf_tensor_offset(&a, t, l); }
+  float* G(int t, int l = 0) const { return grad.as<float>() + rlhf_tensor_offset(&a, t, l); }
+};
+
+// Activation arena shared by every model on the rank (they run one at a time).
+struct Arena {
+  int B = 0, S = 0, R = 0, d = 0, ff = 0, H = 0, V = 0, L = 0;  // capacities
+  int64_t T = 0, Z = 0;
+  std::vector<DevBuf*> owned;
+  float *xres = nullptr, *mean = nullptr, *rstd = nullptr;  // [(2L+1)][T*d], [(2L+1)][T]
+  uint16_t *h1 = nullptr, *qkv = nullptr, *P = nullptr, *o = nullptr, *h2 = nullptr, *f = nullptr, *hf = nullptr;
+  float* scores = nullptr;
+  uint16_t* dS = nullptr;
+  uint16_t* hf_resp = nullptr;
+  float *logits = nullptr, *lse = nullptr, *dhf_resp = nullptr;
+  uint16_t* dz = nullptr;
+  float *dres = nullptr, *dhf = nullptr, *dh = nullptr;
+  uint16_t *g = nullptr, *dpre = nullptr, *dov = nullptr, *dqkv = nullptr;
+  float* ws = nullptr;
+  size_t ws_floats = 0;
+  float* gemm_ws = nullptr;
+  size_t gemm_ws_bytes = 0;
+  int* counters = nullptr;
+  int counters_len = 0;
+  ~Arena();
+};
+
+struct KVCache {
+  DevBuf k, v;  // [L][B][H][Smax][hd] bf16
+  int L = 0, B = 0, H = 0, Smax = 0, hd = 0;
+  uint16_t* Kc(int l) const { return k.as<uint16_t>() + static_cast<int64_t>(l) * B * H * Smax * hd; }
+  uint16_t* Vc(int l) const { return v.as<uint16_t>() + static_cast<int64_t>(l) * B * H * Smax * hd; }
+};
+
+class Engine {
+ public:
+  Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt);
+  ~Engine();
+  void step(const int32_t* prompts_host, rlhf_step_report* rep);
+  size_t tensor_bytes(const std::string& name) const;
+  void read(const std::string& name, void* host, size_t bytes);
+  void greedy_check(const int32_t* tokens_host, int32_t* pred_host, float* margin_host);
+
+ private:
+  // ---- building blocks (engine_model.cpp) ----
+  void init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool trainable);
+  void forward(const Decoder& m, const int32_t* tokens, int B, int tok_stride, int T, bool save, KVCache* kv);
+  void attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd);
+  void attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_t* dov, uint16_t* dqkv, int B, int T, int H, int hd);
+  void backward(Decoder& m, const int32_t* tokens, int B, int S);
+  void lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits);
+  void generate(const Decoder& m, int B, bool teacher_forced);
+  void decode_step(const Decoder& m, int B);
+  void train_actor();
+  void train_critic();
+  void adam(Decoder& m, float lr);
+  void allreduce_grads(Decoder& m, ncclComm_t comm);
+
+  // GEMM helpers (all go through rlhf_gemm)
+  void linear(const uint16_t* X, int M, int K, const uint16_t* W, int N, const uint16_t* bias, void* Y, bool y_f32,
+              bool relu, const float* residual);
+  void linear_decode(const uint16_t* W, int N_out, int K, const uint16_t* X, int Bg, const uint16_t* bias, void* Y,
+                     bool y_f32, bool relu, const float* residual);
+  void gemm(rlhf_gemm_params& p);
+  void kcheck(int status, const char* what);
+  void event(cudaEvent_t e) { cudaEventRecord(e, stream_); }
+
+  rlhf_ppo_config cfg_;
+  rlhf_engine_options opt_;
+  std::string strategy_;
+  int B_, P_, R_, S_;
+  cudaStream_t stream_ = nullptr;
+  ncclComm_t world_ = nullptr;
+  int launches_ = 0;
+  bool hosts_[6] = {false, false, false, false, false, false};
+
+  Decoder actor_, critic_, ref_, reward_;
+  Arena ar_;
+  KVCache kv_;
+  // per-step buffers
+  DevBuf tokens_, pred_, margin_, pos_;
+  DevBuf logp_old_, logp_ref_, values_, score_, rewards_, adv_, ret_, logp_new_, values_new_, gbuf_, loss_;
+  DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_hf_, dec_logits_, argmax_ws_;
+  cudaGraphExec_t decode_graph_ = nullptr;
+  int graph_launches_ = 0;
+  bool graph_for_pred_ = false;
+  double last_losses_[2] = {0, 0};
+  cudaEvent_t ev_[8];
+};
+
+}  // namespace flexrlhf

@@ -1,0 +1,391 @@
+// engine_model.cpp — per-model execution on one device: weight init, the
+// teacher-forced forward (Forward / TrainFB tasks), the backward pass, the
+// LM-head logprobs and greedy generation (Generation task: prefill + CUDA-graph
+// decode loop).  Every launch goes through the C-ABI of include/rlhf_kernels.h.
+// Rounding points follow DESIGN.md §3 and are mirrored by oracle/ppo_oracle.cpp.
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "engine.hpp"
+#include "flexrlhf/errors.hpp"
+
+namespace flexrlhf {
+
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+
+void DevBuf::alloc(size_t n) {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = n;
+  if (n == 0) return;
+  if (cudaMalloc(&p, n) != cudaSuccess) throw DeviceError("cudaMalloc of " + std::to_string(n) + " bytes failed");
+  cudaMemset(p, 0, n);
+}
+
+Arena::~Arena() {
+  for (DevBuf* b : owned) delete b;
+}
+
+void Engine::kcheck(int status, const char* what) {
+  if (status != 0) {
+    cudaError_t e = cudaGetLastError();
+    throw DeviceError(std::string(what) + " failed (status " + std::to_string(status) + ", " + cudaGetErrorString(e) + ")");
+  }
+}
+
+#define K(call, n)                \
+  do {                            \
+    kcheck((call), #call);        \
+    launches_ += (n);             \
+  } while (0)
+
+void Engine::gemm(rlhf_gemm_params& p) {
+  if (p.split_k > 1) {
+    p.workspace = ar_.gemm_ws;
+    p.workspace_bytes = ar_.gemm_ws_bytes;
+    p.counters = ar_.counters;
+    p.counters_len = ar_.counters_len;
+    if (rlhf_gemm_workspace_bytes(&p) > ar_.gemm_ws_bytes) p.split_k = 1;
+  }
+  K(rlhf_gemm(&p, stream_), 1);
+}
+
+// Y[M,N] = X[M,K] W[N,K]^T (+bias) (relu) (+residual), token-major output.
+void Engine::linear(const uint16_t* X, int M, int Kd, const uint16_t* W, int N, const uint16_t* bias, void* Y,
+                    bool y_f32, bool relu, const float* residual) {
+  rlhf_gemm_params p{};
+  p.M = M; p.N = N; p.K = Kd; p.batch = 1; p.batch_h = 1;
+  p.A = X; p.lda = Kd;
+  p.B = W; p.ldb = Kd;
+  p.C = Y; p.c_f32 = y_f32; p.c_rs = N; p.c_cs = 1;
+  p.alpha = 1.0f;
+  p.bias = bias;
+  p.relu = relu;
+  p.residual = residual;
+  gemm(p);
+}
+
+// Decode: Y[Bg, N_out] via swap-AB (weights fill the MMA M dimension), split-K
+// sized so the grid covers ~2 waves of the 148 SMs.
+void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t* X, int Bg, const uint16_t* bias,
+                           void* Y, bool y_f32, bool relu, const float* residual) {
+  rlhf_gemm_params p{};
+  p.M = N_out; p.N = Bg; p.K = Kd; p.batch = 1; p.batch_h = 1;
+  p.A = W; p.lda = Kd;
+  p.B = X; p.ldb = Kd;
+  p.C = Y; p.c_f32 = y_f32; p.c_rs = 1; p.c_cs = N_out;
+  p.alpha = 1.0f;
+  p.bias = bias; p.bias_along_m = 1;
+  p.relu = relu;
+  p.residual = residual;
+  const int tiles = (N_out + 127) / 128 * ((Bg + 127) / 128 > 0 ? 1 : 1);
+  const int kb = (Kd + 63) / 64;
+  int split = (296 + tiles - 1) / tiles;
+  split = std::max(1, std::min(split, kb));
+  // equalise k-blocks per split so no split is empty
+  const int per = (kb + split - 1) / split;
+  split = (kb + per - 1) / per;
+  p.split_k = split;
+  gemm(p);
+}
+
+void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool trainable) {
+  m.a = a;
+  m.seed = seed;
+  m.trainable = trainable;
+  m.n = rlhf_param_total(&a);
+  std::vector<uint16_t> host(static_cast<size_t>(m.n), 0);
+  struct Piece { int t, l; int64_t i0, i1; };
+  std::vector<Piece> pieces;
+  const int64_t chunk = 1 << 18;
+  for (int t = 0; t < RLHF_T_COUNT; ++t) {
+    const bool per_layer = t >= RLHF_LAYER_FIRST && t <= RLHF_LAYER_LAST;
+    for (int l = 0; l < (per_layer ? a.n_layers : 1); ++l) {
+      const int64_t ne = rlhf_tensor_numel(&a, t);
+      for (int64_t i = 0; i < ne; i += chunk) pieces.push_back({t, l, i, std::min(ne, i + chunk)});
+    }
+  }
+  const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (unsigned w = 0; w < nth; ++w)
+    th.emplace_back([&, w] {
+      for (size_t i = w; i < pieces.size(); i += nth) {
+        const Piece& pc = pieces[i];
+        rlhf_init_tensor_range(&a, seed, pc.t, pc.l, pc.i0, pc.i1,
+                               host.data() + rlhf_tensor_offset(&a, pc.t, pc.l) + pc.i0);
+      }
+    });
+  for (auto& t : th) t.join();
+  m.w.alloc(static_cast<size_t>(m.n) * 2);
+  if (cudaMemcpy(m.w.p, host.data(), host.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess)
+    throw DeviceError("weight upload failed");
+  if (trainable) {
+    std::vector<float> f(host.size());
+    for (size_t i = 0; i < host.size(); ++i) f[i] = rlhf_bf16_to_f32(host[i]);
+    m.master.alloc(f.size() * 4);
+    cudaMemcpy(m.master.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice);
+    m.m.alloc(f.size() * 4);
+    m.v.alloc(f.size() * 4);
+    m.grad.alloc(f.size() * 4);
+  }
+}
+
+// Teacher-forced forward over positions [0, T) of B sequences (row r = b*T + i).
+// save: keep every layer's activations for backward (TrainFB); kv: store K/V
+// (Generation prefill).  Result: final-LN hidden states in ar_.hf (bf16).
+void Engine::forward(const Decoder& m, const int32_t* tokens, int B, int tok_stride, int T, bool save, KVCache* kv) {
+  const rlhf_arch& a = m.a;
+  const int d = a.d_model, H = a.n_heads, hd = d / H, ff = a.d_ff, L = a.n_layers;
+  const int rows = B * T;
+  const int64_t Td = static_cast<int64_t>(rows) * d;
+  auto X = [&](int k) { return ar_.xres + (save ? static_cast<int64_t>(k) * ar_.T * ar_.d : 0); };
+  auto MEAN = [&](int k) { return save ? ar_.mean + static_cast<int64_t>(k) * ar_.T : nullptr; };
+  auto RSTD = [&](int k) { return save ? ar_.rstd + static_cast<int64_t>(k) * ar_.T : nullptr; };
+  auto slot = [&](uint16_t* base, int64_t per, int l) { return base + (save ? static_cast<int64_t>(l) * per : 0); };
+  (void)Td;
+  K(rlhf_embed(tokens, tok_stride, B, T, 0, nullptr, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, X(0), stream_), 1);
+  for (int l = 0; l < L; ++l) {
+    uint16_t* h1 = slot(ar_.h1, ar_.T * ar_.d, l);
+    uint16_t* qkv = slot(ar_.qkv, ar_.T * 3 * ar_.d, l);
+    uint16_t* P = slot(ar_.P, ar_.Z * ar_.S * ar_.S, l);
+    uint16_t* o = slot(ar_.o, ar_.T * ar_.d, l);
+    uint16_t* h2 = slot(ar_.h2, ar_.T * ar_.d, l);
+    uint16_t* f = slot(ar_.f, ar_.T * ar_.ff, l);
+    float* xin = X(2 * l);
+    float* xmid = X(2 * l + 1);
+    float* xout = X(2 * l + 2);
+    K(rlhf_layernorm(xin, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h1, MEAN(2 * l), RSTD(2 * l), rows, d, stream_), 1);
+    linear(h1, rows, d, m.T(RLHF_T_WQKV, l), 3 * d, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr);
+    if (kv) K(rlhf_kv_store(qkv, B, T, 0, nullptr, H, hd, kv->Smax, kv->Kc(l), kv->Vc(l), stream_), 1);
+    attention_fwd(qkv, P, o, B, T, H, hd);
+    linear(o, rows, d, m.T(RLHF_T_WO, l), d, m.T(RLHF_T_BO, l), xmid, true, false, xin);
+    K(rlhf_layernorm(xmid, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h2, MEAN(2 * l + 1), RSTD(2 * l + 1), rows, d,
+                     stream_), 1);
+    linear(h2, rows, d, m.T(RLHF_T_W1, l), ff, m.T(RLHF_T_B1, l), f, false, true, nullptr);
+    linear(f, rows, ff, m.T(RLHF_T_W2, l), d, m.T(RLHF_T_B2, l), xout, true, false, xmid);
+  }
+  K(rlhf_layernorm(X(2 * L), m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), ar_.hf, MEAN(2 * L), RSTD(2 * L), rows, d, stream_), 1);
+}
+
+// S = softmax(Q K^T / sqrt(hd)) (causal), O = P V — batched over (b, h) straight
+// out of the packed qkv rows; P kept (bf16) for backward.
+void Engine::attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd) {
+  const int d = H * hd;
+  const int64_t TT = static_cast<int64_t>(T) * T;
+  rlhf_gemm_params s{};
+  s.M = T; s.N = T; s.K = hd; s.batch = B * H; s.batch_h = H;
+  s.A = qkv; s.lda = 3 * d; s.a_stride_h = hd; s.a_stride_b = static_cast<int64_t>(T) * 3 * d;
+  s.B = qkv + d; s.ldb = 3 * d; s.b_stride_h = hd; s.b_stride_b = static_cast<int64_t>(T) * 3 * d;
+  s.C = ar_.scores; s.c_f32 = 1; s.c_rs = T; s.c_cs = 1; s.c_stride_h = TT; s.c_stride_b = H * TT;
+  s.alpha = 1.0f / std::sqrt(static_cast<float>(hd));
+  s.causal = 1;
+  gemm(s);
+  K(rlhf_attn_softmax(ar_.scores, P, B * H, T, stream_), 1);
+  rlhf_gemm_params pv{};
+  pv.M = T; pv.N = hd; pv.K = T; pv.batch = B * H; pv.batch_h = H;
+  pv.A = P; pv.lda = T; pv.a_stride_h = TT; pv.a_stride_b = H * TT;
+  pv.B = qkv + 2 * d; pv.b_mn_major = 1; pv.ldb = 3 * d; pv.b_stride_h = hd; pv.b_stride_b = static_cast<int64_t>(T) * 3 * d;
+  pv.C = o; pv.c_f32 = 0; pv.c_rs = d; pv.c_cs = 1; pv.c_stride_h = hd; pv.c_stride_b = static_cast<int64_t>(T) * d;
+  pv.alpha = 1.0f;
+  pv.causal = 2;
+  gemm(pv);
+}
+
+void Engine::attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_t* dov, uint16_t* dqkv, int B, int T, int H,
+                           int hd) {
+  const int d = H * hd;
+  const int64_t TT = static_cast<int64_t>(T) * T;
+  const int64_t qb = static_cast<int64_t>(T) * 3 * d, ob = static_cast<int64_t>(T) * d;
+  // dP = dO V^T (fp32, causal tiles)
+  rlhf_gemm_params dp{};
+  dp.M = T; dp.N = T; dp.K = hd; dp.batch = B * H; dp.batch_h = H;
+  dp.A = dov; dp.lda = d; dp.a_stride_h = hd; dp.a_stride_b = ob;
+  dp.B = qkv + 2 * d; dp.ldb = 3 * d; dp.b_stride_h = hd; dp.b_stride_b = qb;
+  dp.C = ar_.scores; dp.c_f32 = 1; dp.c_rs = T; dp.c_cs = 1; dp.c_stride_h = TT; dp.c_stride_b = H * TT;
+  dp.alpha = 1.0f; dp.causal = 1;
+  gemm(dp);
+  K(rlhf_attn_softmax_bwd(P, ar_.scores, ar_.dS, B * H, T, 1.0f / std::sqrt(static_cast<float>(hd)), stream_), 1);
+  // dQ = dS K
+  rlhf_gemm_params dq{};
+  dq.M = T; dq.N = hd; dq.K = T; dq.batch = B * H; dq.batch_h = H;
+  dq.A = ar_.dS; dq.lda = T; dq.a_stride_h = TT; dq.a_stride_b = H * TT;
+  dq.B = qkv + d; dq.b_mn_major = 1; dq.ldb = 3 * d; dq.b_stride_h = hd; dq.b_stride_b = qb;
+  dq.C = dqkv; dq.c_rs = 3 * d; dq.c_cs = 1; dq.c_stride_h = hd; dq.c_stride_b = qb;
+  dq.alpha = 1.0f; dq.causal = 2;
+  gemm(dq);
+  // dK = dS^T Q
+  rlhf_gemm_params dk{};
+  dk.M = T; dk.N = hd; dk.K = T; dk.batch = B * H; dk.batch_h = H;
+  dk.A = ar_.dS; dk.a_mn_major = 1; dk.lda = T; dk.a_stride_h = TT; dk.a_stride_b = H * TT;
+  dk.B = qkv; dk.b_mn_major = 1; dk.ldb = 3 * d; dk.b_stride_h = hd; dk.b_stride_b = qb;
+  dk.C = dqkv + d; dk.c_rs = 3 * d; dk.c_cs = 1; dk.c_stride_h = hd; dk.c_stride_b = qb;
+  dk.alpha = 1.0f; dk.causal = 3;
+  gemm(dk);
+  // dV = P^T dO
+  rlhf_gemm_params dv{};
+  dv.M = T; dv.N = hd; dv.K = T; dv.batch = B * H; dv.batch_h = H;
+  dv.A = P; dv.a_mn_major = 1; dv.lda = T; dv.a_stride_h = TT; dv.a_stride_b = H * TT;
+  dv.B = dov; dv.b_mn_major = 1; dv.ldb = d; dv.b_stride_h = hd; dv.b_stride_b = ob;
+  dv.C = dqkv + 2 * d; dv.c_rs = 3 * d; dv.c_cs = 1; dv.c_stride_h = hd; dv.c_stride_b = qb;
+  dv.alpha = 1.0f; dv.causal = 3;
+  gemm(dv);
+}
+
+// dL/dhf is in ar_.dhf (fp32 [B*S, d]); accumulates every parameter gradient of m.
+void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
+  const rlhf_arch& a = m.a;
+  const int d = a.d_model, H = a.n_heads, hd = d / H, ff = a.d_ff, L = a.n_layers;
+  const int rows = B * S;
+  auto X = [&](int k) { return ar_.xres + static_cast<int64_t>(k) * ar_.T * ar_.d; };
+  auto MEAN = [&](int k) { return ar_.mean + static_cast<int64_t>(k) * ar_.T; };
+  auto RSTD = [&](int k) { return ar_.rstd + static_cast<int64_t>(k) * ar_.T; };
+  cudaMemsetAsync(ar_.dres, 0, static_cast<size_t>(rows) * d * 4, stream_);
+  K(rlhf_layernorm_bwd(ar_.dhf, X(2 * L), MEAN(2 * L), RSTD(2 * L), m.T(RLHF_T_LNF_G), ar_.dres, m.G(RLHF_T_LNF_G),
+                       m.G(RLHF_T_LNF_B), rows, d, ar_.ws, ar_.ws_floats, stream_), 2);
+  // dW[N_out, K_in] += dY[T, N_out]^T X[T, K_in]
+  auto wgrad = [&](const uint16_t* dY, int N_out, const uint16_t* Xin, int K_in, float* dW) {
+    rlhf_gemm_params p{};
+    p.M = N_out; p.N = K_in; p.K = rows; p.batch = 1; p.batch_h = 1;
+    p.A = dY; p.a_mn_major = 1; p.lda = N_out;
+    p.B = Xin; p.b_mn_major = 1; p.ldb = K_in;
+    p.C = dW; p.c_f32 = 1; p.c_rs = K_in; p.c_cs = 1;
+    p.alpha = 1.0f; p.accumulate = 1;
+    gemm(p);
+  };
+  // dX[T, K_in] = dY[T, N_out] W[N_out, K_in]
+  auto dgrad = [&](const uint16_t* dY, int N_out, const uint16_t* W, int K_in, void* dX, bool f32, const uint16_t* mask) {
+    rlhf_gemm_params p{};
+    p.M = rows; p.N = K_in; p.K = N_out; p.batch = 1; p.batch_h = 1;
+    p.A = dY; p.lda = N_out;
+    p.B = W; p.b_mn_major = 1; p.ldb = K_in;
+    p.C = dX; p.c_f32 = f32; p.c_rs = K_in; p.c_cs = 1;
+    p.alpha = 1.0f;
+    p.aux = mask; p.aux_rs = K_in; p.aux_cs = 1;
+    gemm(p);
+  };
+  for (int l = L - 1; l >= 0; --l) {
+    const int64_t Tn = ar_.T;
+    const uint16_t* h1 = ar_.h1 + l * Tn * ar_.d;
+    const uint16_t* qkv = ar_.qkv + l * Tn * 3 * ar_.d;
+    const uint16_t* P = ar_.P + l * ar_.Z * ar_.S * ar_.S;
+    const uint16_t* o = ar_.o + l * Tn * ar_.d;
+    const uint16_t* h2 = ar_.h2 + l * Tn * ar_.d;
+    const uint16_t* f = ar_.f + l * Tn * ar_.ff;
+    // FFN: x_out = x_mid + relu(h2 W1^T + b1) W2^T + b2
+    K(rlhf_round_bf16(ar_.dres, ar_.g, static_cast<int64_t>(rows) * d, stream_), 1);
+    K(rlhf_colsum_bf16(ar_.g, rows, d, m.G(RLHF_T_B2, l), ar_.ws, stream_), 2);
+    wgrad(ar_.g, d, f, ff, m.G(RLHF_T_W2, l));
+    dgrad(ar_.g, d, m.T(RLHF_T_W2, l), ff, ar_.dpre, false, f);
+    K(rlhf_colsum_bf16(ar_.dpre, rows, ff, m.G(RLHF_T_B1, l), ar_.ws, stream_), 2);
+    wgrad(ar_.dpre, ff, h2, d, m.G(RLHF_T_W1, l));
+    dgrad(ar_.dpre, ff, m.T(RLHF_T_W1, l), d, ar_.dh, true, nullptr);
+    K(rlhf_layernorm_bwd(ar_.dh, X(2 * l + 1), MEAN(2 * l + 1), RSTD(2 * l + 1), m.T(RLHF_T_LN2_G, l), ar_.dres,
+                         m.G(RLHF_T_LN2_G, l), m.G(RLHF_T_LN2_B, l), rows, d, ar_.ws, ar_.ws_floats, stream_), 2);
+    // attention block: x_mid = x_in + attn(h1) Wo^T + bo
+    K(rlhf_round_bf16(ar_.dres, ar_.g, static_cast<int64_t>(rows) * d, stream_), 1);
+    K(rlhf_colsum_bf16(ar_.g, rows, d, m.G(RLHF_T_BO, l), ar_.ws, stream_), 2);
+    wgrad(ar_.g, d, o, d, m.G(RLHF_T_WO, l));
+    dgrad(ar_.g, d, m.T(RLHF_T_WO, l), d, ar_.dov, false, nullptr);
+    attention_bwd(qkv, P, ar_.dov, ar_.dqkv, B, S, H, hd);
+    K(rlhf_colsum_bf16(ar_.dqkv, rows, 3 * d, m.G(RLHF_T_BQKV, l), ar_.ws, stream_), 2);
+    wgrad(ar_.dqkv, 3 * d, h1, d, m.G(RLHF_T_WQKV, l));
+    dgrad(ar_.dqkv, 3 * d, m.T(RLHF_T_WQKV, l), d, ar_.dh, true, nullptr);
+    K(rlhf_layernorm_bwd(ar_.dh, X(2 * l), MEAN(2 * l), RSTD(2 * l), m.T(RLHF_T_LN1_G, l), ar_.dres, m.G(RLHF_T_LN1_G, l),
+                         m.G(RLHF_T_LN1_B, l), rows, d, ar_.ws, ar_.ws_floats, stream_), 2);
+  }
+  K(rlhf_embed_bwd(tokens, S, B, S, ar_.dres, d, m.G(RLHF_T_TOK_EMB), m.G(RLHF_T_POS_EMB), stream_), 1);
+}
+
+// Per-token logprobs of the response tokens under m (tied LM head); logits and
+// lse stay in the arena for the backward when keep_logits.
+void Engine::lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits) {
+  const int d = m.a.d_model, V = m.a.vocab;
+  (void)keep_logits;
+  K(rlhf_gather_rows(ar_.hf, ar_.hf_resp, B, S_, R_, P_ - 1, d, 2, stream_), 1);
+  linear(ar_.hf_resp, B * R_, d, m.T(RLHF_T_TOK_EMB), V, nullptr, ar_.logits, true, false, nullptr);
+  K(rlhf_logprob(ar_.logits, B * R_, V, tokens, S_, P_, R_, logp, ar_.lse, stream_), 1);
+}
+
+// One decode step at position *pos: embed -> L x (LN, qkv, KV store, attention,
+// o-proj, LN, FFN) -> final LN -> LM head -> greedy argmax -> pos += 1.
+void Engine::decode_step(const Decoder& m, int B) {
+  const rlhf_arch& a = m.a;
+  const int d = a.d_model, H = a.n_heads, hd = d / H, ff = a.d_ff, V = a.vocab;
+  int* pos = pos_.as<int>();
+  float* x = dec_x_.as<float>();
+  uint16_t* h = dec_h_.as<uint16_t>();
+  uint16_t* qkv = dec_qkv_.as<uint16_t>();
+  uint16_t* o = dec_o_.as<uint16_t>();
+  uint16_t* f = dec_f_.as<uint16_t>();
+  const int32_t* tok = tokens_.as<int32_t>();
+  K(rlhf_embed(tok, S_, B, 1, 0, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x, stream_), 1);
+  for (int l = 0; l < a.n_layers; ++l) {
+    K(rlhf_layernorm(x, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h, nullptr, nullptr, B, d, stream_), 1);
+    linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr);
+    K(rlhf_kv_store(qkv, B, 1, 0, pos, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), stream_), 1);
+    K(rlhf_attn_decode(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o, stream_), 1);
+    linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, m.T(RLHF_T_BO, l), x, true, false, x);
+    K(rlhf_layernorm(x, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h, nullptr, nullptr, B, d, stream_), 1);
+    linear_decode(m.T(RLHF_T_W1, l), ff, d, h, B, m.T(RLHF_T_B1, l), f, false, true, nullptr);
+    linear_decode(m.T(RLHF_T_W2, l), d, ff, f, B, m.T(RLHF_T_B2, l), x, true, false, x);
+  }
+  K(rlhf_layernorm(x, m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), dec_hf_.as<uint16_t>(), nullptr, nullptr, B, d, stream_), 1);
+  linear_decode(m.T(RLHF_T_TOK_EMB), V, d, dec_hf_.as<uint16_t>(), B, nullptr, dec_logits_.as<float>(), true, false, nullptr);
+  int32_t* dst = graph_for_pred_ ? pred_.as<int32_t>() : tokens_.as<int32_t>();
+  K(rlhf_argmax_tokens(dec_logits_.as<float>(), B, V, dst, S_, pos, margin_.as<float>(), argmax_ws_.as<float>(), stream_), 2);
+  K(rlhf_add_int(pos, 1, stream_), 1);
+}
+
+// Greedy generation of R tokens for the B prompts already in tokens_[:, :P].
+// teacher_forced: tokens_ already holds full sequences; predictions go to pred_.
+void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
+  const int d = m.a.d_model, V = m.a.vocab;
+  // prefill: forward over the prompt, K/V stored for every prompt position
+  forward(m, tokens_.as<int32_t>(), B, S_, P_, false, &kv_);
+  K(rlhf_gather_rows(ar_.hf, dec_hf_.p, B, P_, 1, P_ - 1, d, 2, stream_), 1);
+  linear_decode(m.T(RLHF_T_TOK_EMB), V, d, dec_hf_.as<uint16_t>(), B, nullptr, dec_logits_.as<float>(), true, false, nullptr);
+  const int start = P_ - 1;
+  cudaMemcpyAsync(pos_.p, &start, sizeof(int), cudaMemcpyHostToDevice, stream_);
+  int32_t* dst = teacher_forced ? pred_.as<int32_t>() : tokens_.as<int32_t>();
+  K(rlhf_argmax_tokens(dec_logits_.as<float>(), B, V, dst, S_, pos_.as<int>(), margin_.as<float>(), argmax_ws_.as<float>(),
+                       stream_), 2);
+  K(rlhf_add_int(pos_.as<int>(), 1, stream_), 1);
+  cudaEventRecord(ev_[1], stream_);  // prefill done
+  if (R_ <= 1) return;
+  const bool use_graph = opt_.use_cuda_graph != 0;
+  if (use_graph) {
+    if (!decode_graph_ || graph_for_pred_ != teacher_forced) {
+      if (decode_graph_) cudaGraphExecDestroy(decode_graph_);
+      decode_graph_ = nullptr;
+      graph_for_pred_ = teacher_forced;
+      cudaGraph_t g;
+      const int before = launches_;
+      if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        throw DeviceError("decode graph capture begin failed");
+      decode_step(m, B);
+      if (cudaStreamEndCapture(stream_, &g) != cudaSuccess) throw DeviceError("decode graph capture failed");
+      if (cudaGraphInstantiate(&decode_graph_, g, 0) != cudaSuccess) throw DeviceError("decode graph instantiate failed");
+      cudaGraphDestroy(g);
+      graph_launches_ = launches_ - before;
+      launches_ = before;
+    }
+    for (int s = 1; s < R_; ++s) {
+      if (cudaGraphLaunch(decode_graph_, stream_) != cudaSuccess) throw DeviceError("decode graph launch failed");
+      launches_ += graph_launches_;
+    }
+  } else {
+    graph_for_pred_ = teacher_forced;
+    for (int s = 1; s < R_; ++s) decode_step(m, B);
+  }
+}
+
+void Engine::adam(Decoder& m, float lr) {
+  m.adam_step += 1;
+  K(rlhf_adamw(m.master.as<float>(), m.m.as<float>(), m.v.as<float>(), m.grad.as<float>(), m.w.p, m.n, lr, cfg_.beta1,
+               cfg_.beta2, cfg_.adam_eps, cfg_.weight_decay, m.adam_step, stream_), 1);
+}
+
+}  // namespace flexrlhf

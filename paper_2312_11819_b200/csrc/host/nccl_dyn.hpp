@@ -1,0 +1,65 @@
+// nccl_dyn.hpp — NCCL entry points resolved at runtime.
+//
+// The engine library does not link NCCL: torch already brings its own
+// libnccl.so.2 (2.28.x) into the process, and a second copy (the system 2.27.x)
+// loaded first would shadow it by SONAME.  We dlopen("libnccl.so.2") lazily,
+// which returns the copy the process already holds, and use nccl.h for types.
+#pragma once
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+namespace flexrlhf {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+inline const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    auto get = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      if (!fn && err.empty()) err = std::string("libnccl.so.2 lacks ") + name;
+    };
+    get(api.GetUniqueId, "ncclGetUniqueId");
+    get(api.CommInitRank, "ncclCommInitRank");
+    get(api.CommDestroy, "ncclCommDestroy");
+    get(api.CommSplit, "ncclCommSplit");
+    get(api.AllReduce, "ncclAllReduce");
+    get(api.AllGather, "ncclAllGather");
+    get(api.Broadcast, "ncclBroadcast");
+    get(api.Send, "ncclSend");
+    get(api.Recv, "ncclRecv");
+    get(api.GroupStart, "ncclGroupStart");
+    get(api.GroupEnd, "ncclGroupEnd");
+    get(api.GetErrorString, "ncclGetErrorString");
+  });
+  if (!err.empty()) throw std::runtime_error(err);
+  return api;
+}
+
+}  // namespace flexrlhf

@@ -50,6 +50,7 @@ struct GemmArgs {
   int relu;
   const uint16_t* aux;
   int64_t aux_rs, aux_cs;
+  const float* residual;
   int causal;
   float* ws;
   int* counters;
@@ -82,6 +83,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& e, int b, int h, 
       const uint16_t a = e.aux[b * e.c_sb + h * e.c_sh + static_cast<int64_t>(m) * e.aux_rs + static_cast<int64_t>(n) * e.aux_cs];
       if ((a & 0x8000u) || a == 0) x = 0.0f;
     }
+    if (e.residual && n < e.N) x += e.residual[cbase + static_cast<int64_t>(n) * e.c_cs];
     v[j] = x;
   }
   const bool full = n_base + 32 <= e.N;
@@ -429,6 +431,7 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
   a.aux = static_cast<const uint16_t*>(p->aux);
   a.aux_rs = p->aux_rs;
   a.aux_cs = p->aux_cs;
+  a.residual = p->residual;
   a.causal = p->causal;
   if (splits > 1) {
     if (!p->workspace || p->workspace_bytes < rlhf_gemm_workspace_bytes(p)) return 2;

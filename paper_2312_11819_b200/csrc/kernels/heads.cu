@@ -116,7 +116,7 @@ __global__ void argmax_merge_kernel(const float* __restrict__ ws, int B, int32_t
   }
   if (lane == 0) {
     tok[static_cast<int64_t>(b) * S + *pos_dev + 1] = t.i1;
-    if (margin) margin[b] = t.v1 - t.v2;
+    if (margin) margin[static_cast<int64_t>(b) * S + *pos_dev + 1] = t.v1 - t.v2;
   }
 }
 

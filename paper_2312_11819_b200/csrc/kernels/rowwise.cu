@@ -217,9 +217,16 @@ __global__ void adamw_kernel(float* __restrict__ w, float* __restrict__ m, float
   reinterpret_cast<uint2*>(wb)[i] = make_uint2(o[0] | (static_cast<uint32_t>(o[1]) << 16), o[2] | (static_cast<uint32_t>(o[3]) << 16));
 }
 
+__global__ void add_int_kernel(int* p, int v) { *p += v; }
+
 }  // namespace rlhf
 
 using namespace rlhf;
+
+extern "C" int rlhf_add_int(int* p, int v, rlhf_stream_t s) {
+  add_int_kernel<<<1, 1, 0, S(s)>>>(p, v);
+  return cuda_status();
+}
 
 extern "C" int rlhf_embed(const int32_t* tokens, int64_t tok_stride, int B, int T, int p0, const int* p0_dev,
                           const void* tok_emb, const void* pos_emb, int d, float* x, rlhf_stream_t s) {

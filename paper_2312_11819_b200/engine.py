@@ -1,0 +1,95 @@
+"""Python handle on the C++ PPO-step engine (rlhf_engine_* in include/rlhf_engine.h).
+
+    eng = Engine(make_config("tiny", "tiny", 4, 16, 16))
+    rep = eng.step()                # one PPO iteration on cuda:<device>
+    logp = eng.read("logp_old")     # any named engine tensor, as numpy
+
+The reference's executor slot is ``simulate(plan, pipeline, cost, topo, opts)``
+(/root/reference/proj/include/rlhfsim/simulator.hpp:46-47); ``Engine.step`` is
+its executed counterpart and returns the same report fields (SimReport,
+simulator.hpp:30-44) measured with CUDA events.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from .capi import EngineOptions, PPOConfig, StepReport, check, lib
+
+STAGES = ("generation", "forward", "training", "sync")
+
+_DTYPES = {"tokens": np.int32, "pred": np.int32, "actor_params": np.uint16, "critic_params": np.uint16,
+           "ref_params": np.uint16, "reward_params": np.uint16}
+
+
+class Engine:
+    def __init__(self, cfg: PPOConfig, device: int = 0, rank: int = 0, world_size: int = 1,
+                 strategy: str = "colocated", nccl_id: bytes | None = None, cuda_graph: bool = True):
+        L = lib()
+        self._cfg = cfg
+        self._keep = []
+        idp = None
+        if nccl_id is not None:
+            buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            self._keep.append(buf)
+            idp = C.cast(buf, C.POINTER(C.c_uint8))
+        opt = EngineOptions(device, rank, world_size, strategy.encode(), idp, int(cuda_graph))
+        h = C.c_void_p()
+        check(L.rlhf_engine_create(C.byref(cfg), C.byref(opt), C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().rlhf_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def step(self, prompts: np.ndarray | None = None) -> dict:
+        rep = StepReport()
+        p = None
+        if prompts is not None:
+            prompts = np.ascontiguousarray(prompts, dtype=np.int32)
+            p = prompts.ctypes.data_as(C.POINTER(C.c_int32))
+        check(lib().rlhf_engine_step(self._h, p, C.byref(rep)))
+        return {"step_seconds": rep.step_seconds, "throughput_samples_per_sec": rep.throughput_samples_per_sec,
+                "per_stage_seconds": dict(zip(STAGES, list(rep.stage_seconds))),
+                "decode_seconds": rep.decode_seconds, "prefill_seconds": rep.prefill_seconds,
+                "comm_bytes_total": rep.comm_bytes_total, "actor_loss": rep.actor_loss,
+                "critic_loss": rep.critic_loss, "gpu_launches": rep.gpu_launches}
+
+    def read(self, name: str) -> np.ndarray:
+        L = lib()
+        nbytes = L.rlhf_engine_tensor_bytes(self._h, name.encode())
+        if nbytes == 0:
+            raise KeyError(name)
+        dt = _DTYPES.get(name, np.float32)
+        out = np.empty(nbytes // np.dtype(dt).itemsize, dtype=dt)
+        check(L.rlhf_engine_read(self._h, name.encode(), out.ctypes.data_as(C.c_void_p), nbytes))
+        B, R, S = self._cfg.batch, self._cfg.gen_len, self._cfg.prompt_len + self._cfg.gen_len
+        if out.size == B * R:
+            return out.reshape(B, R)
+        if out.size == B * S:
+            return out.reshape(B, S)
+        return out
+
+    def greedy_check(self, tokens: np.ndarray):
+        B, R = self._cfg.batch, self._cfg.gen_len
+        tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+        pred = np.zeros((B, R), np.int32)
+        margin = np.zeros((B, R), np.float32)
+        check(lib().rlhf_engine_greedy_check(self._h, tokens.ctypes.data_as(C.POINTER(C.c_int32)),
+                                             pred.ctypes.data_as(C.POINTER(C.c_int32)),
+                                             margin.ctypes.data_as(C.POINTER(C.c_float))))
+        return pred, margin
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().rlhf_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

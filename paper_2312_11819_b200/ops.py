@@ -25,7 +25,7 @@ class GemmParams(C.Structure):
                 ("bias", C.c_void_p), ("bias_f32", C.c_int), ("bias_along_m", C.c_int),
                 ("relu", C.c_int),
                 ("aux", C.c_void_p), ("aux_rs", C.c_int64), ("aux_cs", C.c_int64),
-                ("causal", C.c_int), ("split_k", C.c_int), ("block_n", C.c_int),
+                ("residual", C.c_void_p), ("causal", C.c_int), ("split_k", C.c_int), ("block_n", C.c_int),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("counters", C.c_void_p), ("counters_len", C.c_int)]
 
@@ -44,7 +44,8 @@ def _declare_gemm():
 
 def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = False, out: torch.Tensor | None = None,
          out_f32: bool = True, alpha: float = 1.0, accumulate: bool = False, bias: torch.Tensor | None = None,
-         bias_along_m: bool = False, relu: bool = False, aux: torch.Tensor | None = None, split_k: int = 1,
+         bias_along_m: bool = False, relu: bool = False, aux: torch.Tensor | None = None,
+         residual: torch.Tensor | None = None, split_k: int = 1,
          block_n: int = 0, swap_out: bool = False) -> torch.Tensor:
     """2-D GEMM: C[M,N] = A[M,K] . B[N,K]^T with the C-ABI's operand conventions.
 
@@ -70,6 +71,8 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = F
     p.relu = int(relu)
     if aux is not None:
         p.aux, p.aux_rs, p.aux_cs = aux.data_ptr(), p.c_rs, p.c_cs
+    if residual is not None:
+        p.residual = residual.data_ptr()
     p.split_k, p.block_n = split_k, block_n
     keep = []
     if split_k > 1:
