@@ -143,6 +143,9 @@ size_t rlhf_engine_tensor_bytes(rlhf_engine* e, const char* name);
 int rlhf_engine_greedy_check(rlhf_engine* e, const int32_t* tokens_host, int32_t* pred_host,
                              float* margin_host);
 
+/* The engine's CUDA stream (cudaStream_t) — callers time steps with events on it. */
+void* rlhf_engine_stream(rlhf_engine* e);
+
 const char* rlhf_last_error(void);
 
 #ifdef __cplusplus

@@ -107,6 +107,8 @@ def _declare(L: C.CDLL) -> None:
     L.rlhf_engine_read.argtypes = [vp, C.c_char_p, vp, C.c_size_t]
     L.rlhf_engine_tensor_bytes.argtypes = [vp, C.c_char_p]
     L.rlhf_engine_tensor_bytes.restype = C.c_size_t
+    L.rlhf_engine_stream.argtypes = [vp]
+    L.rlhf_engine_stream.restype = vp
     L.rlhf_engine_greedy_check.argtypes = [vp, p(C.c_int32), p(C.c_int32), p(C.c_float)]
 
 
@@ -153,3 +155,21 @@ def named_slices(a: Arch):
     if a.scalar_head:
         out.append(("vhead", tensor_offset(a, 16), a.d_model))
     return out
+
+
+def prompt_tokens(seed: int, batch: int, prompt_len: int, vocab: int, sample_offset: int = 0):
+    """rlhf_prompt_token() of include/rlhf_init.h, vectorised: uniform iid ids in [0, vocab)."""
+    import numpy as np
+
+    def splitmix(x):
+        with np.errstate(over="ignore"):
+            x = x + np.uint64(0x9E3779B97F4A7C15)
+            x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            return x ^ (x >> np.uint64(31))
+
+    b = np.arange(sample_offset, sample_offset + batch, dtype=np.uint64)[:, None]
+    t = np.arange(prompt_len, dtype=np.uint64)[None, :]
+    with np.errstate(over="ignore"):
+        z = splitmix(splitmix(np.uint64(seed) ^ np.uint64(0xA5A5A5A5)) + b * np.uint64(1000003) + t)
+    return (z % np.uint64(vocab)).astype(np.int32)

@@ -242,9 +242,9 @@ void Engine::step(const int32_t* prompts_host, rlhf_step_report* rep) {
       tok[static_cast<size_t>(b) * S_ + t] =
           prompts_host ? prompts_host[static_cast<size_t>(b) * P_ + t]
                        : rlhf_prompt_token(cfg_.prompt_seed, b + cfg_.sample_offset, t, cfg_.actor.vocab);
-  cudaEventRecord(ev_[0], stream_);
   CK(cudaMemcpyAsync(tokens_.p, tok.data(), tok.size() * 4, cudaMemcpyHostToDevice, stream_));
   cudaMemsetAsync(loss_.p, 0, 16, stream_);
+  cudaEventRecord(ev_[0], stream_);  // device-resident inputs from here on
 
   // ---- Generation: Actor.generate(Query) (workload.cpp:148) ----------------
   generate(actor_, B_, false);
@@ -395,6 +395,8 @@ extern "C" int rlhf_engine_step(rlhf_engine* e, const int32_t* prompts_host, rlh
     return flexrlhf::capi_status(ex);
   }
 }
+
+extern "C" void* rlhf_engine_stream(rlhf_engine* e) { return e->impl->stream(); }
 
 extern "C" size_t rlhf_engine_tensor_bytes(rlhf_engine* e, const char* name) { return e->impl->tensor_bytes(name); }
 

@@ -86,6 +86,7 @@ class Engine {
   size_t tensor_bytes(const std::string& name) const;
   void read(const std::string& name, void* host, size_t bytes);
   void greedy_check(const int32_t* tokens_host, int32_t* pred_host, float* margin_host);
+  cudaStream_t stream() const { return stream_; }
 
  private:
   // ---- building blocks (engine_model.cpp) ----

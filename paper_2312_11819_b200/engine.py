@@ -58,6 +58,11 @@ class Engine:
                 "comm_bytes_total": rep.comm_bytes_total, "actor_loss": rep.actor_loss,
                 "critic_loss": rep.critic_loss, "gpu_launches": rep.gpu_launches}
 
+    @property
+    def stream_handle(self) -> int:
+        """cudaStream_t the engine launches on (for CUDA-event timing)."""
+        return lib().rlhf_engine_stream(self._h)
+
     def read(self, name: str) -> np.ndarray:
         L = lib()
         nbytes = L.rlhf_engine_tensor_bytes(self._h, name.encode())

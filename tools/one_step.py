@@ -1,0 +1,24 @@
+"""Profiling driver: build the c2 (or c1) engine and run one PPO step.
+
+    python tools/one_step.py [--workload c2] [--steps 1] [--no-graph]
+Used under `ncu` to collect per-kernel launch lists (profiles/).
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2312_11819_b200.capi import make_config  # noqa: E402
+from paper_2312_11819_b200.engine import Engine  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="c2")
+ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--no-graph", action="store_true")
+a = ap.parse_args()
+cfg = make_config("opt-125m", "opt-125m", 32, 256, 256) if a.workload == "c2" else make_config("tiny", "tiny", 4, 16, 16)
+eng = Engine(cfg, cuda_graph=not a.no_graph)
+for _ in range(a.steps):
+    rep = eng.step()
+print(rep)
