@@ -3,6 +3,7 @@
 // LM-head logprobs and greedy generation (Generation task: prefill + CUDA-graph
 // decode loop).  Every launch goes through the C-ABI of include/rlhf_kernels.h.
 // Rounding points follow DESIGN.md §3 and are mirrored by oracle/ppo_oracle.cpp.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <thread>
@@ -81,12 +82,13 @@ void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t*
   p.bias = bias; p.bias_along_m = 1;
   p.relu = relu;
   p.residual = residual;
-  const int tiles = (N_out + 127) / 128 * ((Bg + 127) / 128 > 0 ? 1 : 1);
+  // Split-K keeps ~2 CTAs per SM busy streaming weights; at most 8 splits of
+  // >= 2 k-blocks each so the fixed-order partial reduction stays short.
+  const int tiles = (N_out + 127) / 128;
   const int kb = (Kd + 63) / 64;
-  int split = (296 + tiles - 1) / tiles;
-  split = std::max(1, std::min(split, kb));
-  // equalise k-blocks per split so no split is empty
-  const int per = (kb + split - 1) / split;
+  int split = (2 * 148 + tiles - 1) / tiles;
+  split = std::max(1, std::min({split, 8, kb / 2}));
+  const int per = (kb + split - 1) / split;  // equalise k-blocks per split
   split = (kb + per - 1) / per;
   p.split_k = split;
   gemm(p);

@@ -90,7 +90,6 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
   __shared__ float q[HD];
   __shared__ float sc[kDecMaxCtx];
   __shared__ float red[kDecThreads / 32];
-  __shared__ float part[kDecThreads / HD][HD];
   const int bh = blockIdx.x, b = bh / H, h = bh % H;
   const int d = H * HD;
   const int ctx = *pos_dev + 1;
@@ -138,17 +137,30 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
 #pragma unroll
   for (int w = 0; w < kDecThreads / 32; ++w) sum += red[w];
   const float inv = 1.0f / sum;
-  // O[e] = sum_j bf16(p_j) V[j][e]
-  constexpr int G = kDecThreads / HD;
-  const int e = threadIdx.x % HD, grp = threadIdx.x / HD;
-  float acc = 0.f;
-  for (int j = grp; j < ctx; j += G) acc += bf2f_a(f2bf_a(sc[j] * inv)) * bf2f_a(V[static_cast<int64_t>(j) * HD + e]);
-  part[grp][e] = acc;
-  __syncthreads();
-  if (grp == 0) {
-    float o = 0.f;
+  // O[e] = sum_j bf16(p_j) V[j][e]: thread = (16-byte dim chunk c, key group g);
+  // a warp reads whole contiguous V rows (coalesced 16B vectors).
+  constexpr int CH = HD / 8;              // 16-byte chunks per row
+  constexpr int G = kDecThreads / CH;     // key groups
+  const int c = threadIdx.x % CH, grp = threadIdx.x / CH;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int j = grp; j < ctx; j += G) {
+    const float pj = bf2f_a(f2bf_a(sc[j] * inv));
+    const uint4 u = *reinterpret_cast<const uint4*>(V + static_cast<int64_t>(j) * HD + c * 8);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int g2 = 0; g2 < G; ++g2) o += part[g2][e];
+    for (int t = 0; t < 4; ++t) {
+      acc[2 * t] += pj * bf2f_a(static_cast<uint16_t>(w[t] & 0xFFFFu));
+      acc[2 * t + 1] += pj * bf2f_a(static_cast<uint16_t>(w[t] >> 16));
+    }
+  }
+  float* part = sc;  // scores no longer needed: reuse as [G][HD] partials
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < 8; ++t) part[grp * HD + c * 8 + t] = acc[t];
+  __syncthreads();
+  for (int e = threadIdx.x; e < HD; e += kDecThreads) {
+    float o = 0.f;
+    for (int g2 = 0; g2 < G; ++g2) o += part[g2 * HD + e];
     out[static_cast<int64_t>(b) * d + h * HD + e] = f2bf_a(o);
   }
 }

@@ -32,7 +32,8 @@ struct TileCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int RAW_STAGES = (196 * 1024) / STAGE_BYTES;
+  // narrow tiles serve decode (few k-blocks per CTA): 4 stages -> 2-3 CTAs/SM
+  static constexpr int RAW_STAGES = BN <= 64 ? 4 : (196 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = RAW_STAGES > 8 ? 8 : RAW_STAGES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
@@ -148,7 +149,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& e, int b, int h, 
 }
 
 template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmArgs e) {
   using Cfg = TileCfg<BN>;

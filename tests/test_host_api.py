@@ -1,0 +1,179 @@
+"""Host-side API (no GPU): the stage DAG, placements and comm schedules through the
+engine's C-ABI, pinned against the COMPILED REFERENCE (oracle/_ref built from
+/root/reference/proj/src/{topology,workload}.cpp) and against the SPEC.md
+examples; plus the C-ABI export check for every header declaration.
+"""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2312_11819_b200 import capi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "librlhfsim_ref.so")
+
+TASK_KINDS = ["Generation", "Forward", "TrainFB", "Collective", "ParamSync", "Barrier"]
+MODELS = ["Actor", "Critic", "Ref", "Reward", "ShadowActor", "ShadowCritic"]
+
+
+def _graph(fn, *args):
+    n, nd = C.c_int(), C.c_int()
+    null = [None] * 9
+    st = fn(*args, 0, 0, C.byref(n), C.byref(nd), *null)
+    if st != 0:
+        return st, None
+    arrs = [(C.c_int * max(1, n.value))() for _ in range(5)] + [(C.c_int * (n.value + 1))(), (C.c_int * max(1, nd.value))()]
+    st = fn(*args, n.value, nd.value, C.byref(n), C.byref(nd), *arrs)
+    assert st == 0
+    kind, model, mb, ro, ep, off, deps = arrs
+    return 0, [(TASK_KINDS[kind[i]], MODELS[model[i]], mb[i], ro[i], ep[i], tuple(deps[off[i]:off[i + 1]]))
+               for i in range(n.value)]
+
+
+@pytest.fixture(scope="module")
+def L():
+    return capi.lib()
+
+
+@pytest.fixture(scope="module")
+def REF():
+    if not os.path.exists(REF_SO):
+        if not os.path.isdir("/root/reference/proj"):
+            pytest.skip("compiled reference unavailable (no /root/reference here)")
+        subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"])
+    r = C.CDLL(REF_SO)
+    r.ref_last_error.restype = C.c_char_p
+    return r
+
+
+def mine(L, structure, batch, mb, ro, ep, shadows):
+    return _graph(L.rlhf_task_graph, structure, batch, mb, ro, ep, shadows)
+
+
+def ref(R, structure, batch, mb, ro, ep, shadows):
+    d = C.c_double
+    return _graph(R.ref_task_graph, structure, batch, mb, ro, ep, shadows, d(1e8), d(1e8), d(1e8), d(1e8))
+
+
+# Known-answer table, SURVEY.md §4 (measured on the compiled reference)
+@pytest.mark.parametrize("structure,batch,mb,ro,ep,shadows,count", [
+    (1, 4, 1, 1, 1, 0, 7), (1, 4, 4, 1, 1, 2, 31), (1, 4, 4, 1, 1, 0, 28), (0, 4, 1, 1, 1, 0, 5),
+    (0, 4, 4, 1, 1, 2, 22), (1, 4, 1, 2, 2, 0, 14)])
+def test_task_graph_known_answers(L, structure, batch, mb, ro, ep, shadows, count):
+    st, g = mine(L, structure, batch, mb, ro, ep, shadows)
+    assert st == 0 and len(g) == count
+
+
+@pytest.mark.parametrize("structure", [0, 1])
+@pytest.mark.parametrize("mb", [1, 2, 4])
+@pytest.mark.parametrize("ro,ep", [(1, 1), (2, 1), (1, 3), (2, 2)])
+@pytest.mark.parametrize("shadows", [0, 2])
+def test_task_graph_identical_to_compiled_reference(L, REF, structure, mb, ro, ep, shadows):
+    assert mine(L, structure, 8, mb, ro, ep, shadows) == ref(REF, structure, 8, mb, ro, ep, shadows)
+
+
+@pytest.mark.parametrize("args", [(1, 0, 1, 1, 1, 0),   # batch 0
+                                  (1, 6, 4, 1, 1, 0),   # batch not divisible by micro_batches
+                                  (1, 4, 1, 0, 1, 0),   # rollout_nums 0
+                                  (1, 4, 1, 1, 1, 1)])  # shadows requested without shadow entries
+def test_task_graph_config_errors_match_reference(L, REF, args):
+    st_m, _ = mine(L, *args)
+    st_r, _ = ref(REF, *args)
+    assert st_m == st_r == 2
+
+
+def test_experience_buffer_barrier(L):
+    _, g = mine(L, 1, 8, 2, 1, 2, 0)
+    fwds = {i for i, t in enumerate(g) if t[0] == "Forward"}
+    ep0 = [t for t in g if t[0] == "TrainFB" and t[4] == 0]
+    assert all(set(t[5]) == fwds for t in ep0)  # every epoch-0 TrainFB waits for every Forward
+
+
+def plan(L, strategy, n, zero=0, ratio=0.5, tp_gen=1):
+    masks = (C.c_uint32 * 6)()
+    roles = (C.c_int * n)()
+    enc = C.create_string_buffer(1024)
+    st = L.rlhf_plan(strategy.encode(), n, zero, ratio, tp_gen, masks, roles, enc, 1024)
+    if st:
+        return st, None, None, None
+    devs = {MODELS[m]: [d for d in range(n) if masks[m] >> d & 1] for m in range(6) if masks[m]}
+    return 0, devs, [roles[d] for d in range(n)], enc.value.decode()
+
+
+def test_colocated_plan(L):
+    st, devs, roles, enc = plan(L, "colocated", 8)
+    assert st == 0 and all(v == list(range(8)) for v in devs.values()) and set(devs) == set(MODELS[:4])
+    assert roles == [2] * 8 and enc.startswith("colocated")
+
+
+def test_interleaving1_plan_spec_example(L):
+    # [1,1,.5,.5] on 8 devices -> Ref 0-3, Reward 4-7, Actor/Critic 0-7
+    _, devs, _, _ = plan(L, "interleaving1", 8)
+    assert devs["Ref"] == [0, 1, 2, 3] and devs["Reward"] == [4, 5, 6, 7]
+    assert devs["Actor"] == devs["Critic"] == list(range(8))
+
+
+def test_interleaving2_plan_is_actor_ref_vs_critic_reward(L):
+    _, devs, _, _ = plan(L, "interleaving2", 8)
+    assert devs["Actor"] == devs["Ref"] == [0, 1, 2, 3]
+    assert devs["Critic"] == devs["Reward"] == [4, 5, 6, 7]
+
+
+def test_interleaving_needs_two_devices(L):
+    assert plan(L, "interleaving1", 1)[0] == 2
+
+
+def test_disaggregated_plan_partitions_roles(L):
+    _, devs, roles, _ = plan(L, "disaggregated", 8, zero=0, ratio=0.5, tp_gen=4)
+    assert devs["Actor"] == devs["Critic"] == [0, 1, 2, 3]
+    for m in ("ShadowActor", "ShadowCritic", "Ref", "Reward"):
+        assert devs[m] == [4, 5, 6, 7]
+    assert roles == [0, 0, 0, 0, 1, 1, 1, 1]
+    assert plan(L, "disaggregated", 8, ratio=1.0)[0] == 2       # no training devices
+    assert plan(L, "disaggregated", 8, tp_gen=16)[0] == 2       # tp_gen exceeds node width
+
+
+def schedule(L, strategy, n, batch=32, P=256, R=256, mb=1):
+    cnt = C.c_int()
+    st = L.rlhf_comm_schedule(strategy.encode(), n, batch, P, R, mb, 0, C.byref(cnt), None, None, None, None, None)
+    assert st == 0
+    k = cnt.value
+    kind, att, anc = (C.c_int * max(1, k))(), (C.c_int * max(1, k))(), (C.c_int * max(1, k))()
+    pay, grp = (C.c_double * max(1, k))(), (C.c_uint32 * max(1, k))()
+    assert L.rlhf_comm_schedule(strategy.encode(), n, batch, P, R, mb, k, C.byref(cnt), kind, att, anc, pay, grp) == 0
+    names = ["AllGather", "ReduceScatter", "AllReduce", "AlltoAll", "Broadcast", "P2P"]
+    return [(names[kind[i]], att[i], anc[i], pay[i], grp[i]) for i in range(k)]
+
+
+def test_comm_schedule_shapes(L):
+    # SPEC.md:329-331
+    assert schedule(L, "colocated", 8) == []
+    s = schedule(L, "interleaving1", 8)
+    assert [o[0] for o in s] == ["AllGather", "AlltoAll"] and s[0][1] == 0 and s[1][1] == 1
+    assert s[0][3] == 32 * 512 * 8.0  # (Query, Response) records: B x S x 8 B
+    d = schedule(L, "disaggregated", 8, mb=4)
+    assert sum(o[0] == "Broadcast" for o in d) == 2      # ParamSync Actor + Critic
+    assert sum(o[0] == "P2P" for o in d) == 3 * 4         # 2 P2P phases + 1 Send per micro-batch
+
+
+def test_topology_group_min_bandwidth_matches_reference(REF):
+    d = C.c_double
+    kinds = (C.c_char_p * 2)(b"A100", b"V100")
+    for groups, nodes, dpn, grp, exp in [(1, [2], [8], [0, 1, 2, 3], 600e9), (1, [2], [8], [6, 7, 8, 9], 100e9),
+                                        (2, [1, 2], [8, 4], [7, 8], 25e9)]:
+        out, nd, nn = d(), C.c_int(), C.c_int()
+        st = REF.ref_topology_query(groups, (C.c_int * 2)(*(nodes + [0])[:2]), (C.c_int * 2)(*(dpn + [0])[:2]), kinds, d(600e9), d(100e9),
+                                    d(25e9), len(grp), (C.c_int * len(grp))(*grp), C.byref(out), C.byref(nd), C.byref(nn))
+        assert st == 0 and out.value == exp
+
+
+def test_library_exports_every_declared_symbol(L):
+    for h in ("rlhf_engine.h", "rlhf_kernels.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        names = set(re.findall(r"^\s*(?:int|void|size_t|const char\*|void\*)\s+\**(rlhf_\w+)\s*\(", src, re.M))
+        assert names, h
+        for n in names:
+            assert hasattr(L, n), f"{n} declared in {h} but not exported"
