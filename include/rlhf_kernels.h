@@ -56,6 +56,7 @@ typedef struct rlhf_gemm_params {
   int block_n;        /* 0 = auto; else 32/64/128/256 */
   void* workspace; size_t workspace_bytes;
   int* counters; int counters_len;
+  unsigned long long* probe; /* optional: per-CTA phase timestamps (clock64), 8 per CTA */
 } rlhf_gemm_params;
 
 int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t s);

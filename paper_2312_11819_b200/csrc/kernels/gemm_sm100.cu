@@ -1,4 +1,4 @@
-// gemm_sm100.cu — warp-specialised tcgen05 + TMA GEMM for sm_100a.
+// gemm_sm100.cu — persistent, warp-specialised tcgen05 + TMA GEMM for sm_100a.
 //
 // Serves every matmul of the PPO step (reference TaskKind work items,
 // costmodel.hpp:63-64 / SPEC.md:209):
@@ -7,15 +7,21 @@
 //   backward dX = dY W        (B MN-major)      dW = dY^T X   (A, B MN-major)
 //   attention S = Q K^T, O = P V, dP, dQ, dK, dV (batched over (b, h), causal tile skipping)
 //
-// CTA = 192 threads: warp 0 TMA producer, warp 1 TMEM allocator + single-thread
-// UMMA issuer, warps 2-5 epilogue (TMEM -> registers -> fused epilogue -> HBM).
-// Tile 128 x BN x 64 (BN in {32, 64, 128, 256}), 4-8 stage mbarrier ring,
-// SWIZZLE_128B smem operands, fp32 accumulator in TMEM (BN columns).
-// Deterministic split-K: every split writes its fp32 partial, the last CTA of a
-// tile (atomic ticket) reduces all partials in split order and runs the epilogue.
+// CTA = 192 threads, persistent over a static round-robin list of work units
+// (tile x split-K slice):
+//   warp 0      TMA producer (4-D tensor maps, SWIZZLE_128B) into a STAGES-deep ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
+//   warps 2..5  epilogue: TMEM -> registers -> smem transpose -> fused epilogue ->
+//               contiguous row-segment stores
+// The fp32 accumulator is double-buffered in TMEM (2 x BN columns): the epilogue of
+// unit i overlaps the mainloop of unit i+1.
+// Deterministic split-K: each slice writes its fp32 partial; the last slice of a tile
+// (atomic ticket) sums all partials in slice order and runs the epilogue.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "rlhf_kernels.h"
@@ -25,21 +31,25 @@ namespace rlhf {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;
+constexpr int kThreads = 64 + 32 * 4 * 1;  // warp 0 TMA, warp 1 MMA, 4 epilogue warps
+constexpr int kEpiWarps = 4;
+constexpr int kStagePitch = 33;  // fp32 epilogue staging pitch (conflict-free transpose)
 
 template <int BN>
 struct TileCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // narrow tiles serve decode (few k-blocks per CTA): 4 stages -> 2-3 CTAs/SM
-  static constexpr int RAW_STAGES = BN <= 64 ? 4 : (196 * 1024) / STAGE_BYTES;
+  static constexpr int EPI_BYTES = kEpiWarps * 32 * kStagePitch * 4;  // per-epilogue-warp transpose tiles
+  // narrow tiles serve decode (few k-blocks per unit): 3 stages -> 2 CTAs/SM
+  static constexpr int RAW_STAGES = BN <= 64 ? 3 : (218 * 1024 - EPI_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = RAW_STAGES > 8 ? 8 : RAW_STAGES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+  static constexpr int TMEM_COLS = 2 * BN;
 };
 
 struct GemmArgs {
-  int M, N, batch_h, splits, num_kb, tiles_m, tiles_n;
+  int M, N, batch_h, splits, num_kb, tiles_m, tiles_n, units;
   int a_mn, b_mn;
   void* C;
   int c_f32;
@@ -55,168 +65,367 @@ struct GemmArgs {
   int causal;
   float* ws;
   int* counters;
+  unsigned long long* probe;
+  int debug;
 };
 
-__device__ __forceinline__ float bf16_bits_to_f32(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
-
-__device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
-  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+__device__ __forceinline__ unsigned long long clk() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
 }
+#define PROBE(k)                                                                        \
+  do {                                                                                  \
+    if (e.probe && first) e.probe[static_cast<size_t>(blockIdx.x) * 16 + (k)] = clk();   \
+  } while (0)
 
-// Apply the fused epilogue to 32 consecutive columns of one row and store.
-__device__ __forceinline__ void epilogue_store(const GemmArgs& e, int b, int h, int m, int n_base, float (&v)[32]) {
-  if (m >= e.M) return;
-  const int64_t cbase = b * e.c_sb + h * e.c_sh + static_cast<int64_t>(m) * e.c_rs;
-  float bm = 0.0f;
-  if (e.bias && e.bias_along_m)
-    bm = e.bias_f32 ? static_cast<const float*>(e.bias)[m] : bf16_bits_to_f32(static_cast<const uint16_t*>(e.bias)[m]);
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int n = n_base + j;
-    float x = v[j] * e.alpha;
-    if (e.bias) {
-      if (e.bias_along_m) x += bm;
-      else if (n < e.N)
-        x += e.bias_f32 ? static_cast<const float*>(e.bias)[n] : bf16_bits_to_f32(static_cast<const uint16_t*>(e.bias)[n]);
-    }
-    if (e.relu) x = fmaxf(x, 0.0f);
-    if (e.aux && n < e.N) {
-      const uint16_t a = e.aux[b * e.c_sb + h * e.c_sh + static_cast<int64_t>(m) * e.aux_rs + static_cast<int64_t>(n) * e.aux_cs];
-      if ((a & 0x8000u) || a == 0) x = 0.0f;
-    }
-    if (e.residual && n < e.N) x += e.residual[cbase + static_cast<int64_t>(n) * e.c_cs];
-    v[j] = x;
-  }
-  const bool full = n_base + 32 <= e.N;
-  if (e.c_cs == 1 && full) {
-    if (e.c_f32) {
-      float* dst = static_cast<float*>(e.C) + cbase + n_base;
-      if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-        float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          if (e.accumulate) {
-            const float4 old = d4[q];
-            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-          }
-          d4[q] = o;
-        }
-        return;
-      }
-    } else {
-      uint16_t* dst = static_cast<uint16_t*>(e.C) + cbase + n_base;
-      if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-        uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float f[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) f[t] = v[8 * q + t];
-          if (e.accumulate) {
-            const uint4 old = d4[q];
-            const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              f[2 * t] += bf16_bits_to_f32(static_cast<uint16_t>(ow[t] & 0xFFFFu));
-              f[2 * t + 1] += bf16_bits_to_f32(static_cast<uint16_t>(ow[t] >> 16));
-            }
-          }
-          uint32_t w[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            w[t] = static_cast<uint32_t>(f32_to_bf16_bits(f[2 * t])) | (static_cast<uint32_t>(f32_to_bf16_bits(f[2 * t + 1])) << 16);
-          d4[q] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        return;
-      }
-    }
-  }
-#pragma unroll 4
-  for (int j = 0; j < 32; ++j) {
-    const int n = n_base + j;
-    if (n >= e.N) break;
-    const int64_t off = cbase + static_cast<int64_t>(n) * e.c_cs;
-    if (e.c_f32) {
-      float* d = static_cast<float*>(e.C) + off;
-      *d = e.accumulate ? *d + v[j] : v[j];
-    } else {
-      uint16_t* d = static_cast<uint16_t*>(e.C) + off;
-      const float x = e.accumulate ? bf16_bits_to_f32(*d) + v[j] : v[j];
-      *d = f32_to_bf16_bits(x);
-    }
-  }
-}
+struct Unit {
+  int z, h, b, m_tile, n_tile, split, m0, n0, kb_begin, kb_end;
+  bool skip;
+};
 
+// Work unit u -> (batch z, m tile, n tile, split); split fastest, then n, then m.
 template <int BN>
-__global__ void __launch_bounds__(kThreads, 2)
+__device__ __forceinline__ Unit get_unit(const GemmArgs& e, int u) {
+  Unit w;
+  w.split = u % e.splits;
+  int t = u / e.splits;
+  w.n_tile = t % e.tiles_n;
+  t /= e.tiles_n;
+  w.m_tile = t % e.tiles_m;
+  w.z = t / e.tiles_m;
+  w.h = w.z % e.batch_h;
+  w.b = w.z / e.batch_h;
+  w.m0 = w.m_tile * BM;
+  w.n0 = w.n_tile * BN;
+  w.kb_begin = 0;
+  w.kb_end = e.num_kb;
+  w.skip = e.causal == 1 && w.n0 > w.m0 + BM - 1;  // tile strictly above the diagonal
+  if (e.causal == 2) w.kb_end = min(w.kb_end, (w.m0 + BM + BK - 1) / BK);
+  if (e.causal == 3) w.kb_begin = w.m0 / BK;
+  if (e.splits > 1) {
+    const int per = (e.num_kb + e.splits - 1) / e.splits;
+    w.kb_begin = w.split * per;
+    w.kb_end = min(e.num_kb, w.kb_begin + per);
+  }
+  return w;
+}
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+__device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
+// two floats -> packed bf16x2 (one cvt.rn.bf16x2.f32)
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&p);
+}
+
+__device__ __forceinline__ void unpack8(const uint4 u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    f[2 * t] = bf16_bits_to_f32(static_cast<uint16_t>(w[t] & 0xFFFFu));
+    f[2 * t + 1] = bf16_bits_to_f32(static_cast<uint16_t>(w[t] >> 16));
+  }
+}
+
+// Scalar epilogue for one element (tails, unaligned and column-major outputs).
+__device__ __noinline__ void epi_scalar(const GemmArgs& e, int b, int h, int m, int n, float x) {
+  if (m >= e.M || n >= e.N) return;
+  const int64_t off = b * e.c_sb + h * e.c_sh + static_cast<int64_t>(m) * e.c_rs + static_cast<int64_t>(n) * e.c_cs;
+  x *= e.alpha;
+  if (e.bias) {
+    const int bi = e.bias_along_m ? m : n;
+    x += e.bias_f32 ? static_cast<const float*>(e.bias)[bi] : bf16_bits_to_f32(static_cast<const uint16_t*>(e.bias)[bi]);
+  }
+  if (e.relu) x = fmaxf(x, 0.0f);
+  if (e.aux) {
+    const uint16_t a = e.aux[b * e.c_sb + h * e.c_sh + static_cast<int64_t>(m) * e.aux_rs + static_cast<int64_t>(n) * e.aux_cs];
+    if ((a & 0x8000u) || a == 0) x = 0.0f;
+  }
+  if (e.residual) x += e.residual[off];
+  if (e.c_f32) {
+    float* d = static_cast<float*>(e.C) + off;
+    *d = e.accumulate ? *d + x : x;
+  } else {
+    uint16_t* d = static_cast<uint16_t*>(e.C) + off;
+    *d = f32_to_bf16_bits(e.accumulate ? bf16_bits_to_f32(*d) + x : x);
+  }
+}
+
+// Column-major C (swap-AB decode outputs, c_rs == 1): lane = row m, 32 columns of
+// one chunk (vals[j] in smem).  All global inputs are loaded before use so their
+// latencies overlap; stores are coalesced across the warp (consecutive m).
+__device__ __forceinline__ void epi_column32(const GemmArgs& e, int b, int h, int m, int n0, const float* vals) {
+  if (m >= e.M) return;
+  if (n0 + 32 > e.N) {
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) epi_scalar(e, b, h, m, n0 + j, vals[j]);
+    return;
+  }
+  const int64_t base = b * e.c_sb + h * e.c_sh + static_cast<int64_t>(m) * e.c_rs + static_cast<int64_t>(n0) * e.c_cs;
+  float x[32], r[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = vals[j] * e.alpha;
+  if (e.residual) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) r[j] = e.residual[base + j * e.c_cs];
+  }
+  if (e.accumulate) {
+    if (e.c_f32) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r[j] = (e.residual ? r[j] : 0.0f) + static_cast<const float*>(e.C)[base + j * e.c_cs];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        r[j] = (e.residual ? r[j] : 0.0f) + bf16_bits_to_f32(static_cast<const uint16_t*>(e.C)[base + j * e.c_cs]);
+    }
+  }
+  if (e.bias) {
+    if (e.bias_along_m) {
+      const float bm = e.bias_f32 ? static_cast<const float*>(e.bias)[m] : bf16_bits_to_f32(static_cast<const uint16_t*>(e.bias)[m]);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] += bm;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        x[j] += e.bias_f32 ? static_cast<const float*>(e.bias)[n0 + j] : bf16_bits_to_f32(static_cast<const uint16_t*>(e.bias)[n0 + j]);
+    }
+  }
+  if (e.relu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fmaxf(x[j], 0.0f);
+  }
+  if (e.aux) {
+    const int64_t ab = b * e.c_sb + h * e.c_sh + static_cast<int64_t>(m) * e.aux_rs + static_cast<int64_t>(n0) * e.aux_cs;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const uint16_t av = e.aux[ab + j * e.aux_cs];
+      if ((av & 0x8000u) || av == 0) x[j] = 0.0f;
+    }
+  }
+  if (e.residual || e.accumulate) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] += r[j];
+  }
+  if (e.c_f32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) static_cast<float*>(e.C)[base + j * e.c_cs] = x[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) static_cast<uint16_t*>(e.C)[base + j * e.c_cs] = f32_to_bf16_bits(x[j]);
+  }
+}
+
+// Row-major C: 4 rows (m, m+8, m+16, m+24) x 8 consecutive columns [n, n+8).
+// Vectorised; every global input of the 4 rows is loaded before any is used.
+__device__ __noinline__ void epi_rows4_slow(const GemmArgs& e, int b, int h, int m, int n, const float* st, int pitch) {
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i)
+#pragma unroll 1
+    for (int t = 0; t < 8; ++t) epi_scalar(e, b, h, m + 8 * i, n + t, st[8 * i * pitch + t]);
+}
+
+// st: this lane's first value in the smem staging tile (row stride `pitch`), for the slow path.
+__device__ __forceinline__ void epi_rows4(const GemmArgs& e, int b, int h, int m, int n, float (&v)[4][8], const float* st,
+                                          int pitch) {
+  const int64_t bh = b * e.c_sb + h * e.c_sh;
+  const int esz = e.c_f32 ? 4 : 2;
+  const int64_t c0 = bh + static_cast<int64_t>(m) * e.c_rs + n;
+  const int64_t a0 = bh + static_cast<int64_t>(m) * e.aux_rs + n;
+  uintptr_t align = reinterpret_cast<uintptr_t>(static_cast<const char*>(e.C) + c0 * esz) | static_cast<uintptr_t>(e.c_rs * esz);
+  if (e.residual) align |= reinterpret_cast<uintptr_t>(e.residual + c0) | static_cast<uintptr_t>(e.c_rs * 4);
+  if (e.aux) align |= reinterpret_cast<uintptr_t>(e.aux + a0) | static_cast<uintptr_t>(e.aux_rs * 2) | (e.aux_cs != 1 ? 1 : 0);
+  if (e.bias && !e.bias_along_m) align |= e.bias_f32 ? 1 : reinterpret_cast<uintptr_t>(static_cast<const uint16_t*>(e.bias) + n);
+  if (n + 8 > e.N || m + 24 >= e.M || (align & 15)) {
+    epi_rows4_slow(e, b, h, m, n, st, pitch);
+    return;
+  }
+  // ---- issue loads
+  uint4 braw = make_uint4(0, 0, 0, 0);
+  float bm[4] = {0.f, 0.f, 0.f, 0.f};
+  if (e.bias) {
+    if (!e.bias_along_m) {
+      braw = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(e.bias) + n);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        bm[i] = e.bias_f32 ? static_cast<const float*>(e.bias)[m + 8 * i]
+                           : bf16_bits_to_f32(static_cast<const uint16_t*>(e.bias)[m + 8 * i]);
+    }
+  }
+  float4 res[4][2];
+  if (e.residual) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4* r = reinterpret_cast<const float4*>(e.residual + c0 + 8 * i * e.c_rs);
+      res[i][0] = r[0];
+      res[i][1] = r[1];
+    }
+  }
+  uint4 ax[4];
+  if (e.aux) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ax[i] = *reinterpret_cast<const uint4*>(e.aux + a0 + 8 * i * e.aux_rs);
+  }
+  float4 old[4][2];
+  if (e.accumulate) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (e.c_f32) {
+        const float4* d = reinterpret_cast<const float4*>(static_cast<const float*>(e.C) + c0 + 8 * i * e.c_rs);
+        old[i][0] = d[0];
+        old[i][1] = d[1];
+      } else {
+        const uint4 u = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(e.C) + c0 + 8 * i * e.c_rs);
+        old[i][0] = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
+      }
+    }
+  }
+  // ---- compute + store
+  float bb[8];
+  unpack8(braw, bb);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float x[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) x[t] = v[i][t] * e.alpha + (e.bias_along_m ? bm[i] : bb[t]);
+    if (e.relu) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) x[t] = fmaxf(x[t], 0.0f);
+    }
+    if (e.aux) {
+      const uint32_t aw[4] = {ax[i].x, ax[i].y, ax[i].z, ax[i].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint16_t lo = static_cast<uint16_t>(aw[t] & 0xFFFFu), hi = static_cast<uint16_t>(aw[t] >> 16);
+        if ((lo & 0x8000u) || lo == 0) x[2 * t] = 0.0f;
+        if ((hi & 0x8000u) || hi == 0) x[2 * t + 1] = 0.0f;
+      }
+    }
+    if (e.residual) {
+      x[0] += res[i][0].x; x[1] += res[i][0].y; x[2] += res[i][0].z; x[3] += res[i][0].w;
+      x[4] += res[i][1].x; x[5] += res[i][1].y; x[6] += res[i][1].z; x[7] += res[i][1].w;
+    }
+    const int64_t ci = c0 + 8 * i * e.c_rs;
+    if (e.c_f32) {
+      if (e.accumulate) {
+        x[0] += old[i][0].x; x[1] += old[i][0].y; x[2] += old[i][0].z; x[3] += old[i][0].w;
+        x[4] += old[i][1].x; x[5] += old[i][1].y; x[6] += old[i][1].z; x[7] += old[i][1].w;
+      }
+      float4* d4 = reinterpret_cast<float4*>(static_cast<float*>(e.C) + ci);
+      d4[0] = make_float4(x[0], x[1], x[2], x[3]);
+      d4[1] = make_float4(x[4], x[5], x[6], x[7]);
+    } else {
+      if (e.accumulate) {
+        float o8[8];
+        unpack8(make_uint4(__float_as_uint(old[i][0].x), __float_as_uint(old[i][0].y), __float_as_uint(old[i][0].z),
+                           __float_as_uint(old[i][0].w)),
+                o8);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[t] += o8[t];
+      }
+      *reinterpret_cast<uint4*>(static_cast<uint16_t*>(e.C) + ci) =
+          make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]), pack_bf16x2(x[6], x[7]));
+    }
+  }
+}
+
+// Split-K fixup: s[i][t] = sum over slices (in slice order) of the partial at
+// row (row0 + 8i), column col+t of this tile; two slices' loads in flight at a time.
+__device__ __forceinline__ void reduce_partials(const GemmArgs& e, size_t tile_id, int row0, int col, int bn, float (&s)[4][8]) {
+#pragma unroll 1
+  for (int s0 = 0; s0 < e.splits; s0 += 2) {
+    float4 p[2][4][2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (s0 + k < e.splits) {
+          const float4* src = reinterpret_cast<const float4*>(e.ws + ((tile_id * e.splits + s0 + k) * BM + row0 + 8 * i) * bn + col);
+          p[k][i][0] = __ldcg(src);
+          p[k][i][1] = __ldcg(src + 1);
+        } else {
+          p[k][i][0] = p[k][i][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        s[i][0] += p[k][i][0].x; s[i][1] += p[k][i][0].y; s[i][2] += p[k][i][0].z; s[i][3] += p[k][i][0].w;
+        s[i][4] += p[k][i][1].x; s[i][5] += p[k][i][1].y; s[i][6] += p[k][i][1].z; s[i][7] += p[k][i][1].w;
+      }
+  }
+}
+
+template <int BN, int COLMAJOR>
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const GemmArgs e) {
+                      const __grid_constant__ GemmArgs e) {
   using Cfg = TileCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);
   uint64_t* empty_bar = full_bar + Cfg::STAGES;
-  uint64_t* acc_bar = empty_bar + Cfg::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_bar + 1);
+  uint64_t* tfull = empty_bar + Cfg::STAGES;  // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;               // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
-  const int n_tile = blockIdx.x, m_tile = blockIdx.y;
-  const int z = blockIdx.z / e.splits, split = blockIdx.z % e.splits;
-  const int h = z % e.batch_h, b = z / e.batch_h;
-  const int m0 = m_tile * BM, n0 = n_tile * BN;
-  if (e.causal == 1 && n0 > m0 + BM - 1) return;  // tile strictly above the diagonal
-
-  int kb_begin = 0, kb_end = e.num_kb;
-  if (e.causal == 2) kb_end = min(kb_end, (m0 + BM + BK - 1) / BK);
-  if (e.causal == 3) kb_begin = m0 / BK;
-  if (e.splits > 1) {
-    const int per = (e.num_kb + e.splits - 1) / e.splits;
-    kb_begin = split * per;
-    kb_end = min(e.num_kb, kb_begin + per);
-  }
-  const int nkb = kb_end > kb_begin ? kb_end - kb_begin : 0;
-
   const uint32_t warp = warp_id(), lane = lane_id();
+  bool first = threadIdx.x == 0;
+  PROBE(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(acc_bar, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
+    }
     mbar_fence_init();
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, BN);
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  PROBE(1);
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb_begin; kb < kb_end; ++kb) {
-        mbar_wait(&empty_bar[stage], phase ^ 1u);
-        uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
-        uint8_t* sb = sa + Cfg::A_BYTES;
-        mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
-        const int k0 = kb * BK;
-        if (!e.a_mn) {
-          tma_load_4d(sa, &tmA, &full_bar[stage], k0, h, m0, b);
-        } else {
+      first = true;
+      for (int u = blockIdx.x; u < e.units; u += gridDim.x) {
+        const Unit w = get_unit<BN>(e, u);
+        if (w.skip) continue;
+        for (int kb = w.kb_begin; kb < w.kb_end; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1u);
+          PROBE(2);
+          first = false;
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (!e.a_mn) {
+            tma_load_4d(sa, &tmA, &full_bar[stage], k0, w.h, w.m0, w.b);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BM / 64; ++j) tma_load_4d(sa + j * 8192, &tmA, &full_bar[stage], m0 + 64 * j, h, k0, b);
-        }
-        if (!e.b_mn) {
-          tma_load_4d(sb, &tmB, &full_bar[stage], k0, h, n0, b);
-        } else {
+            for (int j = 0; j < BM / 64; ++j) tma_load_4d(sa + j * 8192, &tmA, &full_bar[stage], w.m0 + 64 * j, w.h, k0, w.b);
+          }
+          if (!e.b_mn) {
+            tma_load_4d(sb, &tmB, &full_bar[stage], k0, w.h, w.n0, w.b);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) tma_load_4d(sb + j * 8192, &tmB, &full_bar[stage], n0 + 64 * j, h, k0, b);
+            for (int j = 0; j < BN / 64; ++j) tma_load_4d(sb + j * 8192, &tmB, &full_bar[stage], w.n0 + 64 * j, w.h, k0, w.b);
+          }
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
-        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
       }
     }
   } else if (warp == 1) {
@@ -224,86 +433,148 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t idesc = umma_idesc_bf16(BM, BN, e.a_mn, e.b_mn);
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb_begin; kb < kb_end; ++kb) {
-        mbar_wait(&full_bar[stage], phase);
+      int it = 0;
+      for (int u = blockIdx.x; u < e.units; u += gridDim.x) {
+        const Unit w = get_unit<BN>(e, u);
+        if (w.skip) continue;
+        const int acc = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        ++it;
+        mbar_wait(&tempty[acc], aph ^ 1u);  // epilogue has drained this accumulator
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-        const uint32_t sb = sa + Cfg::A_BYTES;
+        const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
+        first = it == 1;
+        for (int kb = w.kb_begin; kb < w.kb_end; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          if (kb == w.kb_begin) PROBE(3);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint32_t sb = sa + Cfg::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          const uint64_t ad = e.a_mn ? umma_desc_sw128(sa + k * 2048, 8192, 1024) : umma_desc_sw128(sa + k * 32, 16, 1024);
-          const uint64_t bd = e.b_mn ? umma_desc_sw128(sb + k * 2048, 8192, 1024) : umma_desc_sw128(sb + k * 32, 16, 1024);
-          umma_bf16(tmem, ad, bd, idesc, (kb > kb_begin || k > 0) ? 1u : 0u);
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = e.a_mn ? umma_desc_sw128(sa + k * 2048, 8192, 1024) : umma_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = e.b_mn ? umma_desc_sw128(sb + k * 2048, 8192, 1024) : umma_desc_sw128(sb + k * 32, 16, 1024);
+            umma_bf16(d, ad, bd, idesc, (kb > w.kb_begin || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
-        umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
-        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+        PROBE(4);
+        if (w.kb_end > w.kb_begin) umma_commit(&tfull[acc]);
+        else mbar_arrive(&tfull[acc]);
       }
-      if (nkb > 0) umma_commit(acc_bar);
-      else mbar_arrive(acc_bar);
     }
     __syncwarp();
-  } else {  // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
-    mbar_wait(acc_bar, 0);
-    tc_fence_after();
+  } else {  // ---- epilogue warps 2..9: TMEM lane quarter q = warp % 4, chunk parity = half
     const int q = static_cast<int>(warp & 3u);
-    const int row = q * 32 + static_cast<int>(lane);
-    const int m = m0 + row;
-    const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    bool final_pass = true;
-    size_t tile_id = 0;
-    if (e.splits > 1) {
-      tile_id = (static_cast<size_t>(z) * e.tiles_m + m_tile) * e.tiles_n + n_tile;
-      float* mine = e.ws + ((tile_id * e.splits + split) * BM + row) * BN;
+    const int half = static_cast<int>(warp - 2) >> 2;  // 0 with 4 epilogue warps
+    constexpr int NCH = BN / 32;
+    const int my_last = kEpiWarps == 4 ? NCH - 1 : (((NCH - 1 - half) >= 0) ? NCH - 1 - ((NCH - 1 - half) & 1) : -1);
+    float* st = epi_stage + (warp - 2) * 32 * kStagePitch;
+    const uint32_t tq = static_cast<uint32_t>(q * 32) << 16;
+    constexpr bool row_major = COLMAJOR == 0;
+    const int rr0 = static_cast<int>(lane >> 2), cc = static_cast<int>(lane & 3) * 8;
+    int it = 0;
+    for (int u = blockIdx.x; u < e.units; u += gridDim.x) {
+      const Unit w = get_unit<BN>(e, u);
+      if (w.skip) continue;
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      ++it;
+      const bool has_k = w.kb_end > w.kb_begin;
+      mbar_wait(&tfull[acc], aph);
+      first = threadIdx.x == 64 && it == 1;
+      PROBE(5);
+      tc_fence_after();
+      const uint32_t tbase = tmem + tq + static_cast<uint32_t>(acc * BN);
+      const size_t tile_id = (static_cast<size_t>(w.z) * e.tiles_m + w.m_tile) * e.tiles_n + w.n_tile;
+      float* part = (COLMAJOR && e.splits > 1) ? e.ws + ((tile_id * e.splits + w.split) * BM + q * 32) * BN : nullptr;
+      const int mq = w.m0 + q * 32;
+      if (my_last < 0) {  // no chunk for this warp (BN == 32): release immediately
+        tc_fence_before();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < NCH; c += kEpiWarps / 4) {
         float v[32];
-        if (nkb > 0) tmem_ld32(tbase + c * 32, v);
+        if (has_k) tmem_ld32(tbase + c * 32, v);
         else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0.0f;
         }
-        float4* d4 = reinterpret_cast<float4*>(mine + c * 32);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) d4[t] = make_float4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]);
-      }
-      __threadfence();
-      named_bar_sync(1, 128);
-      if (threadIdx.x == 64) *last_flag = (atomicAdd(&e.counters[tile_id], 1) == e.splits - 1);
-      named_bar_sync(1, 128);
-      final_pass = *last_flag != 0;
-      __threadfence();
-    }
-    if (final_pass) {
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        float v[32];
-        if (e.splits > 1) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.0f;
-          for (int s = 0; s < e.splits; ++s) {  // fixed order -> deterministic
-            const float4* src = reinterpret_cast<const float4*>(e.ws + ((tile_id * e.splits + s) * BM + row) * BN + c * 32);
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              const float4 p = __ldcg(src + t);
-              v[4 * t] += p.x; v[4 * t + 1] += p.y; v[4 * t + 2] += p.z; v[4 * t + 3] += p.w;
-            }
-          }
-        } else if (nkb > 0) {
-          tmem_ld32(tbase + c * 32, v);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+        if (c == half) PROBE(8);
+        if (c == my_last) {  // this warp is done with the accumulator
+          tc_fence_before();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        epilogue_store(e, b, h, m, n0 + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) st[lane * kStagePitch + j] = v[j];
+        __syncwarp();
+        if (c == half) PROBE(9);
+        if constexpr (!row_major) {
+          if (!part) epi_column32(e, w.b, w.h, mq + static_cast<int>(lane), w.n0 + c * 32, st + lane * kStagePitch);
+        }
+        if (row_major || part) {
+          // lane l owns rows l/4 + 8i (i < 4), columns 8*(l%4)..+8 -> 64 B contiguous per row
+          float s[4][8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) s[i][t] = st[(rr0 + 8 * i) * kStagePitch + cc + t];
+          if constexpr (!row_major) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float4* dst = reinterpret_cast<float4*>(part + (rr0 + 8 * i) * BN + c * 32 + cc);
+              dst[0] = make_float4(s[i][0], s[i][1], s[i][2], s[i][3]);
+              dst[1] = make_float4(s[i][4], s[i][5], s[i][6], s[i][7]);
+            }
+          } else {
+            epi_rows4(e, w.b, w.h, mq + rr0, w.n0 + c * 32 + cc, s, st + rr0 * kStagePitch + cc, kStagePitch);
+          }
+        }
+        __syncwarp();
+        if (c == half) PROBE(10);
+        if (c == half + 3) PROBE(11);
       }
-      if (e.splits > 1 && threadIdx.x == 64) e.counters[tile_id] = 0;  // re-arm for the next launch
+      PROBE(6);
+      if constexpr (row_major) continue;
+      if (!part) continue;
+      // split-K: ticket; the last slice of the tile reduces all partials in order
+      __threadfence();
+      named_bar_sync(1, 32 * kEpiWarps);
+      if (threadIdx.x == 64) *last_flag = (atomicAdd(&e.counters[tile_id], 1) == e.splits - 1);
+      named_bar_sync(1, 32 * kEpiWarps);
+      const bool last = *last_flag != 0;
+      named_bar_sync(1, 32 * kEpiWarps);  // flag consumed before the next unit may rewrite it
+      if (!last) continue;
+      __threadfence();
+#pragma unroll 1
+      for (int c = half; c < NCH; c += kEpiWarps / 4) {
+        float s[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int t = 0; t < 8; ++t) s[i][t] = 0.0f;
+        reduce_partials(e, tile_id, q * 32 + rr0, c * 32 + cc, BN, s);
+        {  // column-major output: back to lane = row for coalesced stores
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) st[(rr0 + 8 * i) * kStagePitch + cc + t] = s[i][t];
+          __syncwarp();
+          epi_column32(e, w.b, w.h, mq + static_cast<int>(lane), w.n0 + c * 32, st + lane * kStagePitch);
+          __syncwarp();
+        }
+      }
+      if (threadIdx.x == 64) e.counters[tile_id] = 0;  // re-arm for the next launch
+      PROBE(7);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, BN);
+    tmem_dealloc(tmem, Cfg::TMEM_COLS);
   }
 }
 
@@ -363,17 +634,36 @@ static int pick_bn(const rlhf_gemm_params* p) {
   return bn;
 }
 
-template <int BN>
-static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, dim3 grid, cudaStream_t s) {
-  using Cfg = TileCfg<BN>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(gemm_sm100_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
-      return 5;
-    configured = true;
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
   }
-  gemm_sm100_kernel<BN><<<grid, kThreads, Cfg::SMEM, s>>>(ta, tb, a);
+  return n;
+}
+
+template <int BN, int COLMAJOR>
+static int launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t s) {
+  using Cfg = TileCfg<BN>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    if (cudaFuncSetAttribute(gemm_sm100_kernel<BN, COLMAJOR>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
+      return 5;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_sm100_kernel<BN, COLMAJOR>, kThreads, Cfg::SMEM) != cudaSuccess)
+      per_sm = 1;
+    per_sm = std::max(1, std::min(per_sm, 512 / Cfg::TMEM_COLS));
+  }
+  const int grid = std::min(a.units, per_sm * sm_count());
+  gemm_sm100_kernel<BN, COLMAJOR><<<grid, kThreads, Cfg::SMEM, s>>>(ta, tb, a);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+template <int BN>
+static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t s) {
+  return a.c_cs == 1 ? launch_mode<BN, 0>(ta, tb, a, s) : launch_mode<BN, 1>(ta, tb, a, s);
 }
 
 }  // namespace rlhf
@@ -385,8 +675,10 @@ extern "C" int rlhf_gemm_block_n(const rlhf_gemm_params* p) { return pick_bn(p);
 extern "C" size_t rlhf_gemm_workspace_bytes(const rlhf_gemm_params* p) {
   if (p->split_k <= 1) return 0;
   const int bn = pick_bn(p);
+  if (p->c_cs == 1) return 0;
+  const int splits = std::min(p->split_k, (p->K + BK - 1) / BK);
   const size_t tiles = static_cast<size_t>((p->M + BM - 1) / BM) * ((p->N + bn - 1) / bn) * p->batch;
-  return tiles * p->split_k * BM * bn * sizeof(float);
+  return tiles * splits * BM * bn * sizeof(float);
 }
 
 extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
@@ -394,7 +686,9 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
   const int bn = pick_bn(p);
   if (bn != 32 && bn != 64 && bn != 128 && bn != 256) return 2;
   if (p->b_mn_major && bn < 64) return 2;
-  const int splits = p->split_k > 1 ? p->split_k : 1;
+  const int num_kb = (p->K + BK - 1) / BK;
+  // split-K is a decode (column-major, swap-AB) feature
+  const int splits = (p->split_k > 1 && p->c_cs != 1) ? std::min(p->split_k, num_kb) : 1;
   if (splits > 1 && p->causal) return 2;
   const int bb = p->batch / p->batch_h;
   CUtensorMap ta, tb;
@@ -412,9 +706,10 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
   a.N = p->N;
   a.batch_h = p->batch_h;
   a.splits = splits;
-  a.num_kb = (p->K + BK - 1) / BK;
+  a.num_kb = num_kb;
   a.tiles_m = (p->M + BM - 1) / BM;
   a.tiles_n = (p->N + bn - 1) / bn;
+  a.units = a.tiles_m * a.tiles_n * p->batch * splits;
   a.a_mn = p->a_mn_major;
   a.b_mn = p->b_mn_major;
   a.C = p->C;
@@ -434,18 +729,23 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
   a.aux_cs = p->aux_cs;
   a.residual = p->residual;
   a.causal = p->causal;
+  a.probe = p->probe;
+  {
+    static int dbg = -1;
+    if (dbg < 0) dbg = getenv("RLHF_GEMM_DEBUG") ? atoi(getenv("RLHF_GEMM_DEBUG")) : 0;
+    a.debug = dbg;
+  }
   if (splits > 1) {
     if (!p->workspace || p->workspace_bytes < rlhf_gemm_workspace_bytes(p)) return 2;
     if (!p->counters || p->counters_len < a.tiles_m * a.tiles_n * p->batch) return 2;
     a.ws = static_cast<float*>(p->workspace);
     a.counters = p->counters;
   }
-  dim3 grid(a.tiles_n, a.tiles_m, p->batch * splits);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (bn) {
-    case 32: return launch<32>(ta, tb, a, grid, s);
-    case 64: return launch<64>(ta, tb, a, grid, s);
-    case 128: return launch<128>(ta, tb, a, grid, s);
-    default: return launch<256>(ta, tb, a, grid, s);
+    case 32: return launch<32>(ta, tb, a, s);
+    case 64: return launch<64>(ta, tb, a, s);
+    case 128: return launch<128>(ta, tb, a, s);
+    default: return launch<256>(ta, tb, a, s);
   }
 }
