@@ -60,6 +60,26 @@ typedef struct rlhf_gemm_params {
 } rlhf_gemm_params;
 
 int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t s);
+
+/* ---- decode GEMM (Generation): Y^T[N, M] = W[M, K] . X[N, K]^T, N <= 64 -----
+ * swap-AB tcgen05; each 128-row weight tile is a thread-block cluster of `splits`
+ * (1/2/4/8) CTAs over K, reduced through distributed shared memory in fixed order.
+ * Y element (n, m) at Y + n*ldy + m; epilogue bias[m] (bf16), relu, + residual
+ * (f32, same layout as Y, may alias Y).  pdl: launch as a programmatic dependent
+ * (weights are prefetched before waiting on the previous kernel). */
+typedef struct rlhf_gemm_decode_params {
+  int M, N, K;
+  const void* W; int64_t ldw;
+  const void* X; int64_t ldx;
+  void* Y; int y_f32; int64_t ldy;
+  const void* bias;
+  int relu;
+  const float* residual;
+  int splits;
+  int pdl;
+  unsigned long long* probe; /* optional: per-CTA phase timestamps (clock64), 16 per CTA */
+} rlhf_gemm_decode_params;
+int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t s);
 size_t rlhf_gemm_workspace_bytes(const rlhf_gemm_params* p);
 int rlhf_gemm_block_n(const rlhf_gemm_params* p); /* tile width the dispatcher picks */
 
@@ -129,6 +149,10 @@ int rlhf_ppo_actor_loss(const float* logp, const float* logp_old, const float* a
 /* Clipped value loss: g = dL/dv; loss_sum[0] += sum(max(l1, l2)) (x0.5/denom on host). */
 int rlhf_ppo_critic_loss(const float* v, const float* v_old, const float* ret, int n, float clip, float denom,
                          float* g, float* loss_sum, rlhf_stream_t s);
+/* Programmatic dependent launch for the decode-step kernels issued by this host
+ * thread (embed, layernorm, kv_store, attn_decode, argmax, add_int; decode GEMM
+ * takes its own flag).  Used while recording the decode CUDA graph. */
+void rlhf_set_pdl(int on);
 /* *p += v on the device (decode position counter inside the CUDA graph). */
 int rlhf_add_int(int* p, int v, rlhf_stream_t s);
 /* Fused AdamW over a flat fp32 master: m, v updated; bf16 copy written. */

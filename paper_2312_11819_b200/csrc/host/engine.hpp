@@ -119,6 +119,7 @@ class Engine {
   cudaStream_t stream_ = nullptr;
   ncclComm_t world_ = nullptr;
   int launches_ = 0;
+  int pdl_ = 0;  // launch decode kernels as programmatic dependents
   bool hosts_[6] = {false, false, false, false, false, false};
 
   Decoder actor_, critic_, ref_, reward_;

@@ -69,29 +69,39 @@ void Engine::linear(const uint16_t* X, int M, int Kd, const uint16_t* W, int N, 
   gemm(p);
 }
 
-// Decode: Y[Bg, N_out] via swap-AB (weights fill the MMA M dimension), split-K
-// sized so the grid covers ~2 waves of the 148 SMs.
+// Decode: Y[Bg, N_out] via the swap-AB decode GEMM (weights fill the MMA M
+// dimension); K split over a thread-block cluster so ~2 CTAs per SM stream weights.
 void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t* X, int Bg, const uint16_t* bias,
                            void* Y, bool y_f32, bool relu, const float* residual) {
-  rlhf_gemm_params p{};
-  p.M = N_out; p.N = Bg; p.K = Kd; p.batch = 1; p.batch_h = 1;
-  p.A = W; p.lda = Kd;
-  p.B = X; p.ldb = Kd;
-  p.C = Y; p.c_f32 = y_f32; p.c_rs = 1; p.c_cs = N_out;
-  p.alpha = 1.0f;
-  p.bias = bias; p.bias_along_m = 1;
+  rlhf_gemm_decode_params p{};
+  p.M = N_out; p.N = Bg; p.K = Kd;
+  p.W = W; p.ldw = Kd;
+  p.X = X; p.ldx = Kd;
+  p.Y = Y; p.y_f32 = y_f32; p.ldy = N_out;
+  p.bias = bias;
   p.relu = relu;
   p.residual = residual;
-  // Split-K keeps ~2 CTAs per SM busy streaming weights; at most 8 splits of
-  // >= 2 k-blocks each so the fixed-order partial reduction stays short.
   const int tiles = (N_out + 127) / 128;
   const int kb = (Kd + 63) / 64;
-  int split = (2 * 148 + tiles - 1) / tiles;
-  split = std::max(1, std::min({split, 8, kb / 2}));
-  const int per = (kb + split - 1) / split;  // equalise k-blocks per split
-  split = (kb + per - 1) / per;
-  p.split_k = split;
-  gemm(p);
+  if (tiles >= 148) {  // LM head: enough 128-row tiles already -> persistent GEMM, column-major out
+    rlhf_gemm_params q{};
+    q.M = N_out; q.N = Bg; q.K = Kd; q.batch = 1; q.batch_h = 1;
+    q.A = W; q.lda = Kd;
+    q.B = X; q.ldb = Kd;
+    q.C = Y; q.c_f32 = y_f32; q.c_rs = 1; q.c_cs = N_out;
+    q.alpha = 1.0f;
+    q.bias = bias; q.bias_along_m = 1;
+    q.relu = relu;
+    q.residual = residual;
+    gemm(q);
+    return;
+  }
+  // K slices of one 128-row tile form a cluster; keep >= 2 k-blocks per slice
+  int split = 1;
+  while (split < 8 && tiles * split * 2 <= 2 * 148 && kb / (split * 2) >= 2) split *= 2;
+  p.splits = split;
+  p.pdl = pdl_;
+  K(rlhf_gemm_decode(&p, stream_), 1);
 }
 
 void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool trainable) {
@@ -367,7 +377,11 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
       const int before = launches_;
       if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         throw DeviceError("decode graph capture begin failed");
+      pdl_ = opt_.use_cuda_graph > 1 ? 0 : 1;  // programmatic dependent launches inside the graph
+      rlhf_set_pdl(pdl_);
       decode_step(m, B);
+      rlhf_set_pdl(0);
+      pdl_ = 0;
       if (cudaStreamEndCapture(stream_, &g) != cudaSuccess) throw DeviceError("decode graph capture failed");
       if (cudaGraphInstantiate(&decode_graph_, g, 0) != cudaSuccess) throw DeviceError("decode graph instantiate failed");
       cudaGraphDestroy(g);

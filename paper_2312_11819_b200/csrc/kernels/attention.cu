@@ -7,6 +7,7 @@
 
 #include <cfloat>
 
+#include "launch_util.cuh"
 #include "rlhf_kernels.h"
 
 namespace rlhf {
@@ -62,6 +63,7 @@ __global__ void attn_softmax_bwd_kernel(const uint16_t* __restrict__ P, const fl
 // cache[b][h][p][e] <- qkv[(b*T + i)][d + h*hd + e] (k) / [2d + ...] (v)
 __global__ void kv_store_kernel(const uint16_t* __restrict__ qkv, int T, int p0, const int* __restrict__ p0_dev, int H,
                                 int hd, int Smax, uint16_t* __restrict__ kc, uint16_t* __restrict__ vc, int rows) {
+  pdl_entry();
   const int d = H * hd;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // unit: 8 elements
   const int per_row = d / 8;
@@ -90,6 +92,7 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
   __shared__ float q[HD];
   __shared__ float sc[kDecMaxCtx];
   __shared__ float red[kDecThreads / 32];
+  pdl_entry();
   const int bh = blockIdx.x, b = bh / H, h = bh % H;
   const int d = H * HD;
   const int ctx = *pos_dev + 1;
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
   constexpr int G = kDecThreads / CH;     // key groups
   const int c = threadIdx.x % CH, grp = threadIdx.x / CH;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
   for (int j = grp; j < ctx; j += G) {
     const float pj = bf2f_a(f2bf_a(sc[j] * inv));
     const uint4 u = *reinterpret_cast<const uint4*>(V + static_cast<int64_t>(j) * HD + c * 8);
@@ -191,10 +195,9 @@ extern "C" int rlhf_kv_store(const void* qkv, int B, int T, int p0, const int* p
   if (hd % 8) return 2;
   const int rows = B * T;
   const int64_t n = static_cast<int64_t>(rows) * (H * hd / 8);
-  kv_store_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, AS(s)>>>(
-      static_cast<const uint16_t*>(qkv), T, p0, p0_dev, H, hd, Smax, static_cast<uint16_t*>(kcache),
-      static_cast<uint16_t*>(vcache), rows);
-  return AST();
+  return launch_k(kv_store_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, AS(s),
+                  static_cast<const uint16_t*>(qkv), T, p0, p0_dev, H, hd, Smax, static_cast<uint16_t*>(kcache),
+                  static_cast<uint16_t*>(vcache), rows);
 }
 
 extern "C" int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax, const void* kcache, const void* vcache,
@@ -205,9 +208,8 @@ extern "C" int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax,
   const auto* v = static_cast<const uint16_t*>(vcache);
   auto* o = static_cast<uint16_t*>(out);
   switch (hd) {
-    case 64: attn_decode_kernel<64><<<B * H, kDecThreads, 0, AS(s)>>>(q, H, Smax, k, v, pos_dev, o); break;
-    case 128: attn_decode_kernel<128><<<B * H, kDecThreads, 0, AS(s)>>>(q, H, Smax, k, v, pos_dev, o); break;
+    case 64: return launch_k(attn_decode_kernel<64>, dim3(B * H), dim3(kDecThreads), 0, AS(s), q, H, Smax, k, v, pos_dev, o);
+    case 128: return launch_k(attn_decode_kernel<128>, dim3(B * H), dim3(kDecThreads), 0, AS(s), q, H, Smax, k, v, pos_dev, o);
     default: return 2;
   }
-  return AST();
 }

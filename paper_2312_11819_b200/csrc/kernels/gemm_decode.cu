@@ -1,0 +1,321 @@
+// gemm_decode.cu — HBM-bound decode GEMM: Y^T[Bg, N] = W[N, K] . X[Bg, K]^T (swap-AB).
+//
+// Generation-stage workhorse (reference: stage_compute_time(Generation) decode term,
+// SPEC.md:209 "gen_len x max(compute, bytes_infer_per_param*P/tp / hbm)").
+//  * weights fill the 128-row tcgen05 M dimension, the (<= 64) batch is N;
+//  * one 128-row weight tile = one thread-block CLUSTER of `splits` CTAs (1,2,4,8),
+//    each CTA streams a K-slice through TMA into smem and accumulates in TMEM;
+//  * partials are reduced across the cluster through distributed shared memory
+//    (mapa + ld.shared::cluster) in fixed slice order: deterministic, no global
+//    workspace, no atomics;
+//  * programmatic dependent launch: the weight TMA loads are issued before
+//    griddepcontrol.wait (they do not depend on the previous kernel), so their
+//    latency overlaps the previous kernel's tail.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
+#include "rlhf_kernels.h"
+#include "sm100_common.cuh"
+
+namespace rlhf {
+
+namespace dec {
+constexpr int BM = 128, BK = 64, kThreads = 128;
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int MAX_KB = BN <= 32 ? 8 : 6;
+  static constexpr int PART_PITCH = BN + 4;  // 16 B aligned rows for v4 DSMEM reads
+  static constexpr int PART_BYTES = BM * PART_PITCH * 4;
+  static constexpr int SMEM = MAX_KB * STAGE_BYTES + PART_BYTES + 1024 + 256;
+  static int smem_for(int kb_per) { return kb_per * STAGE_BYTES + PART_BYTES + 1024 + 256; }
+};
+
+struct Args {
+  int M, N, K, splits, kb_per;
+  void* Y;
+  int y_f32;
+  int64_t ldy;  // Y element (n, m) at Y + n*ldy + m
+  const uint16_t* bias;  // [M] bf16 or null
+  int relu;
+  const float* residual;  // same layout as Y (may alias), or null
+  unsigned long long* probe;
+};
+__device__ __forceinline__ unsigned long long dclk() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+#define DPROBE(k) do { if (e.probe && threadIdx.x == 0) e.probe[blockIdx.x * 16 + (k)] = dclk(); } while (0)
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t local_saddr, uint32_t rank) {
+  uint32_t remote;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_saddr), "r"(rank));
+  return remote;
+}
+// non-volatile: independent DSMEM loads may be issued back to back (ordering is
+// provided by the cluster barriers around the reduction)
+__device__ __forceinline__ float ld_cluster_f32(uint32_t remote) {
+  float v;
+  asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote));
+  return v;
+}
+__device__ __forceinline__ float4 ld_cluster_v4(uint32_t remote) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(remote));
+  return v;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+__device__ __forceinline__ float b2f(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                       const __grid_constant__ Args e) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* part = reinterpret_cast<float*>(smem + e.kb_per * C::STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + e.kb_per * C::STAGE_BYTES + C::PART_BYTES);
+  uint64_t* acc_bar = full_bar + e.kb_per;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_bar + 1);
+
+  const int split = static_cast<int>(cluster_rank());
+  const int tile = blockIdx.x / e.splits;
+  const int m0 = tile * BM;
+  const int num_kb = (e.K + BK - 1) / BK;
+  const int kb0 = split * e.kb_per;
+  const int kb1 = min(num_kb, kb0 + e.kb_per);
+  const int nkb = kb1 > kb0 ? kb1 - kb0 : 0;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  DPROBE(0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < e.kb_per; ++s) mbar_init(&full_bar[s], 1);
+    mbar_init(acc_bar, 1);
+    mbar_fence_init();
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmX);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  DPROBE(1);
+  pdl_trigger();  // the next kernel may start its (independent) prologue
+
+  if (threadIdx.x == 0) {
+    // weights do not depend on the previous kernel: stream them first
+    for (int j = 0; j < nkb; ++j) {
+      uint8_t* sa = smem + j * C::STAGE_BYTES;
+      mbar_arrive_expect_tx(&full_bar[j], C::STAGE_BYTES);
+      tma_load_4d(sa, &tmW, &full_bar[j], (kb0 + j) * BK, 0, m0, 0);
+    }
+    DPROBE(2);
+    pdl_wait();  // activations X are produced by the previous kernel
+    DPROBE(3);
+    for (int j = 0; j < nkb; ++j) {
+      uint8_t* sb = smem + j * C::STAGE_BYTES + C::A_BYTES;
+      tma_load_4d(sb, &tmX, &full_bar[j], (kb0 + j) * BK, 0, 0, 0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    const uint32_t idesc = umma_idesc_bf16(BM, BN, 0, 0);
+    for (int j = 0; j < nkb; ++j) {
+      mbar_wait(&full_bar[j], 0);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + j * C::STAGE_BYTES);
+      const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k)
+        umma_bf16(tmem, umma_desc_sw128(sa + k * 32, 16, 1024), umma_desc_sw128(sb + k * 32, 16, 1024), idesc,
+                  (j > 0 || k > 0) ? 1u : 0u);
+    }
+    if (nkb > 0) umma_commit(acc_bar);
+    else mbar_arrive(acc_bar);
+  }
+  pdl_wait();  // residual (and Y when aliased) come from earlier kernels
+
+  // ---- partial accumulator -> own smem (row = TMEM lane)
+  mbar_wait(acc_bar, 0);
+  DPROBE(4);
+  tc_fence_after();
+  {
+    const int row = static_cast<int>(warp) * 32 + static_cast<int>(lane);
+    const uint32_t tb = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      if (nkb > 0) tmem_ld32(tb + c * 32, v);
+      else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) part[row * C::PART_PITCH + c * 32 + j] = v[j];
+    }
+  }
+  tc_fence_before();
+  DPROBE(5);
+  cluster_sync_all();  // every slice's partial is visible cluster-wide
+  DPROBE(6);
+
+  // ---- this CTA reduces rows [split*rows_per, +rows_per) over all slices, in slice
+  // order.  Work unit = (row r, 4 consecutive columns): one 16 B DSMEM load per
+  // slice, issued unconditionally (ranks >= splits alias this CTA, masked below).
+  const int rows_per = BM / e.splits;
+  const uint32_t part_s = smem_u32(part);
+  uint32_t peer[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) peer[s] = map_rank(part_s, static_cast<uint32_t>(s < e.splits ? s : split));
+  const int units = rows_per * (BN / 4);
+#pragma unroll 1
+  for (int u = threadIdx.x; u < units; u += kThreads) {
+    const int r = split * rows_per + u % rows_per;  // consecutive threads -> consecutive m (coalesced Y)
+    const int c4 = (u / rows_per) * 4;
+    const int m = m0 + r;
+    const bool mok = m < e.M;
+    const uint32_t off = static_cast<uint32_t>((r * C::PART_PITCH + c4) * 4);
+    float4 v[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[s] = ld_cluster_v4(peer[s] + off);
+    float res[4] = {0.f, 0.f, 0.f, 0.f};
+    if (e.residual && mok) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (c4 + t < e.N) res[t] = e.residual[static_cast<int64_t>(c4 + t) * e.ldy + m];
+    }
+    const float bm = (e.bias && mok) ? b2f(e.bias[m]) : 0.0f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {  // fixed slice order
+      if (s < e.splits) {
+        acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w;
+      }
+    }
+    const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int n = c4 + t;
+      if (!mok || n >= e.N) continue;
+      float x = a4[t] + bm;
+      if (e.relu) x = fmaxf(x, 0.0f);
+      x += res[t];
+      const int64_t o = static_cast<int64_t>(n) * e.ldy + m;
+      if (e.y_f32) static_cast<float*>(e.Y)[o] = x;
+      else static_cast<uint16_t*>(e.Y)[o] = __bfloat16_as_ushort(__float2bfloat16_rn(x));
+    }
+  }
+  DPROBE(7);
+  cluster_sync_all();  // peers may still be reading this CTA's partial
+  DPROBE(8);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, BN);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int map2d(CUtensorMap* m, const void* ptr, int64_t K, int64_t rows, int64_t ld, int box_rows) {
+  auto fn = encode();
+  if (!fn || (reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 2) % 16) return 2;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(K), 1, static_cast<cuuint64_t>(rows), 1};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld * rows * 2), static_cast<cuuint64_t>(ld * 2),
+                           static_cast<cuuint64_t>(ld * rows * 2)};
+  cuuint32_t box[4] = {64u, 1u, static_cast<cuuint32_t>(box_rows), 1u};
+  cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? 0
+             : 5;
+}
+
+template <int BN>
+int launch(const CUtensorMap& tw, const CUtensorMap& tx, const Args& a, int tiles, int pdl, cudaStream_t s) {
+  using C = Cfg<BN>;
+  static bool init = false;
+  if (!init) {
+    if (cudaFuncSetAttribute(gemm_decode_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
+      return 5;
+    init = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(tiles * a.splits);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::smem_for(a.kb_per);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = a.splits;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, gemm_decode_kernel<BN>, tw, tx, a) == cudaSuccess ? 0 : 5;
+}
+
+}  // namespace dec
+}  // namespace rlhf
+
+using namespace rlhf;
+
+extern "C" int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t stream) {
+  const int bn = p->N <= 32 ? 32 : 64;
+  if (p->N < 1 || p->N > 64 || p->M < 1 || p->K < 1 || p->K % 8) return 2;
+  const int num_kb = (p->K + dec::BK - 1) / dec::BK;
+  const int max_kb = bn == 32 ? dec::Cfg<32>::MAX_KB : dec::Cfg<64>::MAX_KB;
+  int splits = p->splits;
+  if (splits != 1 && splits != 2 && splits != 4 && splits != 8) return 2;
+  while ((num_kb + splits - 1) / splits > max_kb && splits < 8) splits *= 2;  // every slice must fit in smem
+  const int kb_per = (num_kb + splits - 1) / splits;
+  if (kb_per > max_kb) return 2;
+  CUtensorMap tw, tx;
+  if (dec::map2d(&tw, p->W, p->K, p->M, p->ldw, dec::BM)) return 2;
+  if (dec::map2d(&tx, p->X, p->K, p->N, p->ldx, bn)) return 2;
+  dec::Args a{};
+  a.M = p->M;
+  a.N = p->N;
+  a.K = p->K;
+  a.splits = splits;
+  a.kb_per = kb_per;
+  a.Y = p->Y;
+  a.y_f32 = p->y_f32;
+  a.ldy = p->ldy;
+  a.bias = static_cast<const uint16_t*>(p->bias);
+  a.relu = p->relu;
+  a.residual = p->residual;
+  a.probe = p->probe;
+  const int tiles = (p->M + dec::BM - 1) / dec::BM;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return bn == 32 ? dec::launch<32>(tw, tx, a, tiles, p->pdl, s) : dec::launch<64>(tw, tx, a, tiles, p->pdl, s);
+}

@@ -8,6 +8,7 @@
 
 #include <cfloat>
 
+#include "launch_util.cuh"
 #include "rlhf_kernels.h"
 
 namespace rlhf {
@@ -80,6 +81,7 @@ __device__ __forceinline__ Top2 top2_merge(Top2 a, Top2 b) {
 }
 
 __global__ void argmax_slice_kernel(const float* __restrict__ z, int V, float* __restrict__ ws) {
+  pdl_entry();
   const int b = blockIdx.y, sl = blockIdx.x;
   const int per = (V + kArgSlices - 1) / kArgSlices;
   const int v0 = sl * per, v1 = min(V, v0 + per);
@@ -102,6 +104,7 @@ __global__ void argmax_slice_kernel(const float* __restrict__ z, int V, float* _
 
 __global__ void argmax_merge_kernel(const float* __restrict__ ws, int B, int32_t* __restrict__ tok, int S,
                                     const int* __restrict__ pos_dev, float* __restrict__ margin) {
+  pdl_entry();
   const int b = blockIdx.x;
   const int lane = threadIdx.x;
   Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
@@ -241,9 +244,9 @@ extern "C" int rlhf_logprob_bwd(const float* logits, const float* lse, const flo
 
 extern "C" int rlhf_argmax_tokens(const float* logits, int B, int V, int32_t* tokens, int S, const int* pos_dev,
                                   float* margin, float* ws, rlhf_stream_t s) {
-  argmax_slice_kernel<<<dim3(kArgSlices, B), 256, 0, HS(s)>>>(logits, V, ws);
-  argmax_merge_kernel<<<B, 32, 0, HS(s)>>>(ws, B, tokens, S, pos_dev, margin);
-  return HST();
+  const int st = launch_k(argmax_slice_kernel, dim3(kArgSlices, B), dim3(256), 0, HS(s), logits, V, ws);
+  if (st) return st;
+  return launch_k(argmax_merge_kernel, dim3(B), dim3(32), 0, HS(s), ws, B, tokens, S, pos_dev, margin);
 }
 
 extern "C" int rlhf_scalar_head(const void* hf, const void* w, int B, int S, int R, int off, int d, float* out,

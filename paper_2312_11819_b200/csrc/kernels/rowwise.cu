@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "launch_util.cuh"
 #include "rlhf_kernels.h"
 
 namespace rlhf {
@@ -25,6 +26,7 @@ static inline cudaStream_t S(rlhf_stream_t s) { return reinterpret_cast<cudaStre
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, int64_t tok_stride, int T, int p0,
                              const int* __restrict__ p0_dev, const uint16_t* __restrict__ E,
                              const uint16_t* __restrict__ Pm, int d, float* __restrict__ x, int rows) {
+  pdl_entry();
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int qd = d / 4;
   if (idx >= static_cast<int64_t>(rows) * qd) return;
@@ -55,37 +57,52 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tokens, int64_t tok
   atomicAdd(dP + static_cast<int64_t>(i) * d + c, g);
 }
 
-// One warp per row.  Three passes over the row (re-reads hit L1).
+// One warp per row, row held in registers (d <= 4096): a single round trip to
+// memory for x, gamma and beta, then two register passes (mean, variance).
+template <int VPL>  // float4 vectors per lane
 __global__ void layernorm_kernel(const float* __restrict__ x, const uint16_t* __restrict__ g,
                                  const uint16_t* __restrict__ bta, uint16_t* __restrict__ y, float* __restrict__ mean,
                                  float* __restrict__ rstd, int M, int d) {
+  pdl_entry();
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
   const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * d);
-  const int q = d / 4;
-  float s = 0.f;
-  for (int c = lane; c < q; c += 32) {
-    const float4 v = xr[c];
-    s += (v.x + v.y) + (v.z + v.w);
-  }
-  const float mu = warp_sum(s) / d;
-  float vs = 0.f;
-  for (int c = lane; c < q; c += 32) {
-    const float4 v = xr[c];
-    vs += (v.x - mu) * (v.x - mu) + (v.y - mu) * (v.y - mu) + (v.z - mu) * (v.z - mu) + (v.w - mu) * (v.w - mu);
-  }
-  const float rs = 1.0f / sqrtf(warp_sum(vs) / d + 1e-5f);
-  uint2* yr = reinterpret_cast<uint2*>(y + static_cast<int64_t>(row) * d);
   const uint2* g2 = reinterpret_cast<const uint2*>(g);
   const uint2* b2 = reinterpret_cast<const uint2*>(bta);
-  for (int c = lane; c < q; c += 32) {
-    const float4 v = xr[c];
-    const uint2 gg = g2[c], bb = b2[c];
-    const float o0 = (v.x - mu) * rs * bf2f(gg.x & 0xFFFFu) + bf2f(bb.x & 0xFFFFu);
-    const float o1 = (v.y - mu) * rs * bf2f(gg.x >> 16) + bf2f(bb.x >> 16);
-    const float o2 = (v.z - mu) * rs * bf2f(gg.y & 0xFFFFu) + bf2f(bb.y & 0xFFFFu);
-    const float o3 = (v.w - mu) * rs * bf2f(gg.y >> 16) + bf2f(bb.y >> 16);
+  const int q = d / 4;
+  float4 v[VPL];
+  uint2 gg[VPL], bb[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c = lane + 32 * k;
+    if (c < q) {
+      v[k] = xr[c];
+      gg[k] = g2[c];
+      bb[k] = b2[c];
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k)
+    if (lane + 32 * k < q) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  const float mu = warp_sum(s) / d;
+  float vs = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k)
+    if (lane + 32 * k < q)
+      vs += (v[k].x - mu) * (v[k].x - mu) + (v[k].y - mu) * (v[k].y - mu) + (v[k].z - mu) * (v[k].z - mu) +
+            (v[k].w - mu) * (v[k].w - mu);
+  const float rs = 1.0f / sqrtf(warp_sum(vs) / d + 1e-5f);
+  uint2* yr = reinterpret_cast<uint2*>(y + static_cast<int64_t>(row) * d);
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c = lane + 32 * k;
+    if (c >= q) continue;
+    const float o0 = (v[k].x - mu) * rs * bf2f(gg[k].x & 0xFFFFu) + bf2f(bb[k].x & 0xFFFFu);
+    const float o1 = (v[k].y - mu) * rs * bf2f(gg[k].x >> 16) + bf2f(bb[k].x >> 16);
+    const float o2 = (v[k].z - mu) * rs * bf2f(gg[k].y & 0xFFFFu) + bf2f(bb[k].y & 0xFFFFu);
+    const float o3 = (v[k].w - mu) * rs * bf2f(gg[k].y >> 16) + bf2f(bb[k].y >> 16);
     yr[c] = make_uint2(f2bf(o0) | (static_cast<uint32_t>(f2bf(o1)) << 16), f2bf(o2) | (static_cast<uint32_t>(f2bf(o3)) << 16));
   }
   if (lane == 0) {
@@ -217,15 +234,19 @@ __global__ void adamw_kernel(float* __restrict__ w, float* __restrict__ m, float
   reinterpret_cast<uint2*>(wb)[i] = make_uint2(o[0] | (static_cast<uint32_t>(o[1]) << 16), o[2] | (static_cast<uint32_t>(o[3]) << 16));
 }
 
-__global__ void add_int_kernel(int* p, int v) { *p += v; }
+__global__ void add_int_kernel(int* p, int v) {
+  pdl_entry();
+  *p += v;
+}
 
 }  // namespace rlhf
 
 using namespace rlhf;
 
+extern "C" void rlhf_set_pdl(int on) { g_pdl = on; }
+
 extern "C" int rlhf_add_int(int* p, int v, rlhf_stream_t s) {
-  add_int_kernel<<<1, 1, 0, S(s)>>>(p, v);
-  return cuda_status();
+  return launch_k(add_int_kernel, dim3(1), dim3(1), 0, S(s), p, v);
 }
 
 extern "C" int rlhf_embed(const int32_t* tokens, int64_t tok_stride, int B, int T, int p0, const int* p0_dev,
@@ -233,9 +254,8 @@ extern "C" int rlhf_embed(const int32_t* tokens, int64_t tok_stride, int B, int 
   if (d % 4) return 2;
   const int rows = B * T;
   const int64_t n = static_cast<int64_t>(rows) * (d / 4);
-  embed_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, S(s)>>>(
-      tokens, tok_stride, T, p0, p0_dev, static_cast<const uint16_t*>(tok_emb), static_cast<const uint16_t*>(pos_emb), d, x, rows);
-  return cuda_status();
+  return launch_k(embed_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, S(s), tokens, tok_stride, T, p0,
+                  p0_dev, static_cast<const uint16_t*>(tok_emb), static_cast<const uint16_t*>(pos_emb), d, x, rows);
 }
 
 extern "C" int rlhf_embed_bwd(const int32_t* tokens, int64_t tok_stride, int B, int T, const float* dx, int d,
@@ -249,9 +269,14 @@ extern "C" int rlhf_embed_bwd(const int32_t* tokens, int64_t tok_stride, int B, 
 extern "C" int rlhf_layernorm(const float* x, const void* g, const void* b, void* y, float* mean, float* rstd, int M,
                               int d, rlhf_stream_t s) {
   if (d % 4) return 2;
-  layernorm_kernel<<<(M + 7) / 8, 256, 0, S(s)>>>(x, static_cast<const uint16_t*>(g), static_cast<const uint16_t*>(b),
-                                                  static_cast<uint16_t*>(y), mean, rstd, M, d);
-  return cuda_status();
+  const dim3 grid((M + 7) / 8), blk(256);
+  const auto* gp = static_cast<const uint16_t*>(g);
+  const auto* bp = static_cast<const uint16_t*>(b);
+  auto* yp = static_cast<uint16_t*>(y);
+  if (d <= 1024) return launch_k(layernorm_kernel<8>, grid, blk, 0, S(s), x, gp, bp, yp, mean, rstd, M, d);
+  if (d <= 2048) return launch_k(layernorm_kernel<16>, grid, blk, 0, S(s), x, gp, bp, yp, mean, rstd, M, d);
+  if (d <= 4096) return launch_k(layernorm_kernel<32>, grid, blk, 0, S(s), x, gp, bp, yp, mean, rstd, M, d);
+  return 2;
 }
 
 extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd, const void* g,

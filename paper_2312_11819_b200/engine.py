@@ -25,7 +25,7 @@ _DTYPES = {"tokens": np.int32, "pred": np.int32, "actor_params": np.uint16, "cri
 
 class Engine:
     def __init__(self, cfg: PPOConfig, device: int = 0, rank: int = 0, world_size: int = 1,
-                 strategy: str = "colocated", nccl_id: bytes | None = None, cuda_graph: bool = True):
+                 strategy: str = "colocated", nccl_id: bytes | None = None, cuda_graph: int = 1):
         L = lib()
         self._cfg = cfg
         self._keep = []

@@ -127,3 +127,27 @@ def test_gemm_batched_attention_causal():
     expO = (P.float() @ v).transpose(1, 2).reshape(B * S, d)
     torch.cuda.synchronize()
     assert (O.float() - expO).abs().max().item() < 2e-2
+
+
+@pytest.mark.parametrize("M,K", [(2304, 768), (768, 3072), (3072, 768), (50272, 768), (384, 128)])
+@pytest.mark.parametrize("N", [4, 16, 32, 64])
+@pytest.mark.parametrize("splits", [1, 2, 4, 8])
+def test_gemm_decode_cluster_split(M, K, N, splits):
+    from paper_2312_11819_b200 import ops
+    W = torch.randn(M, K, device="cuda").bfloat16()
+    X = torch.randn(N, K, device="cuda").bfloat16()
+    bias = torch.randn(M, device="cuda").bfloat16()
+    res = torch.randn(N, M, device="cuda")
+    out = res.clone()
+    ops.gemm_decode(W, X, out=out, bias=bias, residual=out, splits=splits)
+    exp = res + (X.float() @ W.float().t() + bias.float())
+    torch.cuda.synchronize()
+    close(out, exp, 1e-4)
+    out2 = res.clone()
+    ops.gemm_decode(W, X, out=out2, bias=bias, residual=out2, splits=splits)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)  # deterministic
+    yb = ops.gemm_decode(W, X, bias=bias, relu=True, splits=splits, out_f32=False)
+    expb = torch.relu(X.float() @ W.float().t() + bias.float())
+    torch.cuda.synchronize()
+    assert (yb.float() - expb).abs().max().item() <= 0.02 * expb.abs().max().item()

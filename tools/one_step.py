@@ -16,9 +16,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c2")
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--no-graph", action="store_true")
+ap.add_argument("--graph-mode", type=int, default=1, help="1: graph + PDL, 2: graph without PDL")
 a = ap.parse_args()
 cfg = make_config("opt-125m", "opt-125m", 32, 256, 256) if a.workload == "c2" else make_config("tiny", "tiny", 4, 16, 16)
-eng = Engine(cfg, cuda_graph=not a.no_graph)
+eng = Engine(cfg, cuda_graph=0 if a.no_graph else a.graph_mode)
 for _ in range(a.steps):
     rep = eng.step()
-print(rep)
+    print({k: (round(v * 1e3, 2) if isinstance(v, float) else v) for k, v in rep.items() if k != "per_stage_seconds"})
