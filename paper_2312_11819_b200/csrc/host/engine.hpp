@@ -98,10 +98,16 @@ class Engine {
   void lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits);
   void generate(const Decoder& m, int B, bool teacher_forced);
   void decode_step(const Decoder& m, int B);
-  void train_actor();
-  void train_critic();
+  void train_actor(Decoder& m, int B, ncclComm_t comm);
+  void train_critic(Decoder& m, int B, ncclComm_t comm);
   void adam(Decoder& m, float lr);
   void allreduce_grads(Decoder& m, ncclComm_t comm);
+  void p2p(const std::vector<std::pair<const void*, size_t>>& sends, const std::vector<std::pair<void*, size_t>>& recvs);
+  void score_logp(const Decoder& m, const int32_t* tok, int B, float* logp);
+  void score_values(const Decoder& m, const int32_t* tok, int B, float* values);
+  void score_reward(const Decoder& m, const int32_t* tok, int B, float* score);
+  void gae(int B);
+  void place_prompts(const int32_t* dev_prompts, int row0);
 
   // GEMM helpers (all go through rlhf_gemm)
   void linear(const uint16_t* X, int M, int K, const uint16_t* W, int N, const uint16_t* bias, void* Y, bool y_f32,
@@ -115,24 +121,32 @@ class Engine {
   rlhf_ppo_config cfg_;
   rlhf_engine_options opt_;
   std::string strategy_;
-  int B_, P_, R_, S_;
+  int P_, R_, S_;
+  int rank_ = 0, world_n_ = 1, partner_ = -1;
+  int Bg_ = 0;     // samples of this rank's shard (prompts it owns)
+  int Bcap_ = 0;   // experience rows this rank may hold (Bg or 2*Bg)
+  int gen_B_ = 0;  // sequences this rank generates
+  PlacementPlan plan_;
+  StrategyTag tag_ = StrategyTag::Colocated;
   cudaStream_t stream_ = nullptr;
-  ncclComm_t world_ = nullptr;
+  ncclComm_t world_ = nullptr, actor_comm_ = nullptr, critic_comm_ = nullptr;
+  double comm_bytes_ = 0;
+  std::vector<int> sample_ids_;
   int launches_ = 0;
   int pdl_ = 0;  // launch decode kernels as programmatic dependents
   bool hosts_[6] = {false, false, false, false, false, false};
 
-  Decoder actor_, critic_, ref_, reward_;
+  Decoder actor_, critic_, ref_, reward_, shadow_actor_, shadow_critic_;
+  Decoder* generator_ = nullptr;
   Arena ar_;
   KVCache kv_;
   // per-step buffers
-  DevBuf tokens_, pred_, margin_, pos_;
-  DevBuf logp_old_, logp_ref_, values_, score_, rewards_, adv_, ret_, logp_new_, values_new_, gbuf_, loss_;
+  DevBuf tokens_, tok2_, pred_, margin_, pos_, prompt_stage_;
+  DevBuf logp_old_, logp_ref_, values_, score_, rewards_, adv_, ret_, logp_new_, values_new_, gbuf_, loss_, out2_, score2_;
   DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_hf_, dec_logits_, argmax_ws_;
   cudaGraphExec_t decode_graph_ = nullptr;
   int graph_launches_ = 0;
   bool graph_for_pred_ = false;
-  double last_losses_[2] = {0, 0};
   cudaEvent_t ev_[8];
 };
 

@@ -19,8 +19,9 @@ from .capi import EngineOptions, PPOConfig, StepReport, check, lib
 
 STAGES = ("generation", "forward", "training", "sync")
 
-_DTYPES = {"tokens": np.int32, "pred": np.int32, "actor_params": np.uint16, "critic_params": np.uint16,
-           "ref_params": np.uint16, "reward_params": np.uint16}
+_DTYPES = {"tokens": np.int32, "pred": np.int32, "sample_ids": np.int32, "actor_params": np.uint16,
+           "critic_params": np.uint16, "ref_params": np.uint16, "reward_params": np.uint16,
+           "shadow_actor_params": np.uint16, "shadow_critic_params": np.uint16}
 
 
 class Engine:
@@ -71,11 +72,14 @@ class Engine:
         dt = _DTYPES.get(name, np.float32)
         out = np.empty(nbytes // np.dtype(dt).itemsize, dtype=dt)
         check(L.rlhf_engine_read(self._h, name.encode(), out.ctypes.data_as(C.c_void_p), nbytes))
-        B, R, S = self._cfg.batch, self._cfg.gen_len, self._cfg.prompt_len + self._cfg.gen_len
-        if out.size == B * R:
-            return out.reshape(B, R)
-        if out.size == B * S:
-            return out.reshape(B, S)
+        R, S = self._cfg.gen_len, self._cfg.prompt_len + self._cfg.gen_len
+        rows = L.rlhf_engine_tensor_bytes(self._h, b"sample_ids") // 4  # experience rows held by this rank
+        if name in ("sample_ids", "score"):
+            return out
+        if out.size == rows * R and "params" not in name and "grad" not in name and "master" not in name:
+            return out.reshape(rows, R)
+        if out.size == rows * S and name in ("tokens", "pred", "margin"):
+            return out.reshape(rows, S)
         return out
 
     def greedy_check(self, tokens: np.ndarray):
