@@ -78,6 +78,10 @@ typedef struct rlhf_gemm_decode_params {
   int splits;
   int pdl;
   unsigned long long* probe; /* optional: per-CTA phase timestamps (clock64), 16 per CTA */
+  /* fused LayerNorm prologue (X may be NULL): X = bf16(LN(ln_x) * ln_g + ln_b), ln_x f32 [N, K], K <= 2048 */
+  const float* ln_x; const void* ln_g; const void* ln_b;
+  /* fused KV-cache store (Y = packed qkv [N, 3*kv_d] bf16): k/v -> cache[n][h][*pos][e] */
+  void* kcache; void* vcache; const int* pos; int kv_d, kv_hd, kv_H, kv_Smax;
 } rlhf_gemm_decode_params;
 int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t s);
 size_t rlhf_gemm_workspace_bytes(const rlhf_gemm_params* p);

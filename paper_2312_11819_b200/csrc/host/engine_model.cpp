@@ -72,8 +72,21 @@ void Engine::linear(const uint16_t* X, int M, int Kd, const uint16_t* W, int N, 
 // Decode: Y[Bg, N_out] via the swap-AB decode GEMM (weights fill the MMA M
 // dimension); K split over a thread-block cluster so ~2 CTAs per SM stream weights.
 void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t* X, int Bg, const uint16_t* bias,
-                           void* Y, bool y_f32, bool relu, const float* residual) {
+                           void* Y, bool y_f32, bool relu, const float* residual, const float* ln_x,
+                           const uint16_t* ln_g, const uint16_t* ln_b, int kv_layer) {
   rlhf_gemm_decode_params p{};
+  p.ln_x = ln_x;
+  p.ln_g = ln_g;
+  p.ln_b = ln_b;
+  if (kv_layer >= 0) {
+    p.kcache = kv_.Kc(kv_layer);
+    p.vcache = kv_.Vc(kv_layer);
+    p.pos = pos_.as<int>();
+    p.kv_d = N_out / 3;
+    p.kv_hd = kv_.hd;
+    p.kv_H = kv_.H;
+    p.kv_Smax = kv_.Smax;
+  }
   p.M = N_out; p.N = Bg; p.K = Kd;
   p.W = W; p.ldw = Kd;
   p.X = X; p.ldx = Kd;
@@ -83,7 +96,7 @@ void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t*
   p.residual = residual;
   const int tiles = (N_out + 127) / 128;
   const int kb = (Kd + 63) / 64;
-  if (tiles >= 148) {  // LM head: enough 128-row tiles already -> persistent GEMM, column-major out
+  if (tiles >= 148 && !ln_x && kv_layer < 0) {  // LM head: enough 128-row tiles -> persistent GEMM, column-major out
     rlhf_gemm_params q{};
     q.M = N_out; q.N = Bg; q.K = Kd; q.batch = 1; q.batch_h = 1;
     q.A = W; q.lda = Kd;
@@ -334,10 +347,12 @@ void Engine::decode_step(const Decoder& m, int B) {
   uint16_t* f = dec_f_.as<uint16_t>();
   const int32_t* tok = tokens_.as<int32_t>();
   K(rlhf_embed(tok, S_, B, 1, 0, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x, stream_), 1);
+  // per layer 7 launches: LN1, [QKV GEMM + KV-cache store], attention,
+  // [O-proj + residual], LN2, [FFN-up + ReLU], [FFN-down + residual]
   for (int l = 0; l < a.n_layers; ++l) {
     K(rlhf_layernorm(x, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h, nullptr, nullptr, B, d, stream_), 1);
-    linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr);
-    K(rlhf_kv_store(qkv, B, 1, 0, pos, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), stream_), 1);
+    linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr, nullptr, nullptr,
+                  nullptr, l);
     K(rlhf_attn_decode(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o, stream_), 1);
     linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, m.T(RLHF_T_BO, l), x, true, false, x);
     K(rlhf_layernorm(x, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h, nullptr, nullptr, B, d, stream_), 1);

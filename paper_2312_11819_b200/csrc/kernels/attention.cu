@@ -26,38 +26,91 @@ __device__ __forceinline__ float wsum(float v) {
   return v;
 }
 
-// One warp per score row i of matrix z: valid keys j <= i.
+// One warp per score row i: the causal prefix j <= i is read once into registers
+// (float4), max / sum / normalise from registers, bf16 probabilities written for
+// the whole row (zeros above the diagonal).  CH = float4 chunks per lane.
+template <int CH>
 __global__ void attn_softmax_kernel(const float* __restrict__ sc, uint16_t* __restrict__ P, int Z, int S) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row >= static_cast<int64_t>(Z) * S) return;
   const int i = static_cast<int>(row % S);
-  const float* s = sc + row * S;
-  uint16_t* p = P + row * S;
+  const float4* s4 = reinterpret_cast<const float4*>(sc + row * S);
+  float4 v[CH];
   float mx = -FLT_MAX;
-  for (int j = lane; j <= i; j += 32) mx = fmaxf(mx, s[j]);
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int j0 = (lane + 32 * k) * 4;
+    v[k] = j0 <= i ? s4[lane + 32 * k] : make_float4(-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX);
+    if (j0 + 1 > i) v[k].y = -FLT_MAX;
+    if (j0 + 2 > i) v[k].z = -FLT_MAX;
+    if (j0 + 3 > i) v[k].w = -FLT_MAX;
+    mx = fmaxf(mx, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
+  }
   mx = wmax(mx);
   float sum = 0.f;
-  for (int j = lane; j <= i; j += 32) sum += expf(s[j] - mx);
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int j0 = (lane + 32 * k) * 4;
+    v[k].x = j0 <= i ? expf(v[k].x - mx) : 0.f;
+    v[k].y = j0 + 1 <= i ? expf(v[k].y - mx) : 0.f;
+    v[k].z = j0 + 2 <= i ? expf(v[k].z - mx) : 0.f;
+    v[k].w = j0 + 3 <= i ? expf(v[k].w - mx) : 0.f;
+    sum += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
   sum = wsum(sum);
   const float inv = 1.0f / sum;
-  for (int j = lane; j < S; j += 32) p[j] = j <= i ? f2bf_a(expf(s[j] - mx) * inv) : static_cast<uint16_t>(0);
+  uint2* p2 = reinterpret_cast<uint2*>(P + row * S);
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = lane + 32 * k;
+    if (c * 4 >= S) break;
+    p2[c] = make_uint2(f2bf_a(v[k].x * inv) | (static_cast<uint32_t>(f2bf_a(v[k].y * inv)) << 16),
+                       f2bf_a(v[k].z * inv) | (static_cast<uint32_t>(f2bf_a(v[k].w * inv)) << 16));
+  }
 }
 
 // dS_ij = bf16(P_ij (dP_ij - D_i) scale), D_i = sum_j P_ij dP_ij (j <= i); zero above the diagonal.
+template <int CH>
 __global__ void attn_softmax_bwd_kernel(const uint16_t* __restrict__ P, const float* __restrict__ dP,
                                         uint16_t* __restrict__ dS, int Z, int S, float scale) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row >= static_cast<int64_t>(Z) * S) return;
   const int i = static_cast<int>(row % S);
-  const uint16_t* p = P + row * S;
-  const float* g = dP + row * S;
-  uint16_t* o = dS + row * S;
+  const uint2* p2 = reinterpret_cast<const uint2*>(P + row * S);
+  const float4* g4 = reinterpret_cast<const float4*>(dP + row * S);
+  float pv[CH][4], gv[CH][4];
   float D = 0.f;
-  for (int j = lane; j <= i; j += 32) D += bf2f_a(p[j]) * g[j];
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = lane + 32 * k;
+    const int j0 = c * 4;
+    if (j0 <= i) {
+      const uint2 u = p2[c];
+      const float4 g = g4[c];
+      pv[k][0] = bf2f_a(static_cast<uint16_t>(u.x & 0xFFFFu)); pv[k][1] = bf2f_a(static_cast<uint16_t>(u.x >> 16));
+      pv[k][2] = bf2f_a(static_cast<uint16_t>(u.y & 0xFFFFu)); pv[k][3] = bf2f_a(static_cast<uint16_t>(u.y >> 16));
+      gv[k][0] = g.x; gv[k][1] = g.y; gv[k][2] = g.z; gv[k][3] = g.w;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) pv[k][t] = gv[k][t] = 0.f;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (j0 + t <= i) D += pv[k][t] * gv[k][t];
+  }
   D = wsum(D);
-  for (int j = lane; j < S; j += 32) o[j] = j <= i ? f2bf_a(bf2f_a(p[j]) * (g[j] - D) * scale) : static_cast<uint16_t>(0);
+  uint2* o2 = reinterpret_cast<uint2*>(dS + row * S);
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = lane + 32 * k;
+    if (c * 4 >= S) break;
+    uint16_t h[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) h[t] = c * 4 + t <= i ? f2bf_a(pv[k][t] * (gv[k][t] - D) * scale) : static_cast<uint16_t>(0);
+    o2[c] = make_uint2(h[0] | (static_cast<uint32_t>(h[1]) << 16), h[2] | (static_cast<uint32_t>(h[3]) << 16));
+  }
 }
 
 // cache[b][h][p][e] <- qkv[(b*T + i)][d + h*hd + e] (k) / [2d + ...] (v)
@@ -178,15 +231,27 @@ static inline int AST() { return cudaGetLastError() == cudaSuccess ? 0 : 5; }
 
 extern "C" int rlhf_attn_softmax(const float* scores, void* probs, int Z, int S, rlhf_stream_t s) {
   const int64_t rows = static_cast<int64_t>(Z) * S;
-  attn_softmax_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, AS(s)>>>(scores, static_cast<uint16_t*>(probs), Z, S);
+  if (S % 4) return 2;
+  const unsigned g = static_cast<unsigned>((rows + 7) / 8);
+  auto* p = static_cast<uint16_t*>(probs);
+  if (S <= 128) attn_softmax_kernel<1><<<g, 256, 0, AS(s)>>>(scores, p, Z, S);
+  else if (S <= 512) attn_softmax_kernel<4><<<g, 256, 0, AS(s)>>>(scores, p, Z, S);
+  else if (S <= 1536) attn_softmax_kernel<12><<<g, 256, 0, AS(s)>>>(scores, p, Z, S);
+  else return 2;
   return AST();
 }
 
 extern "C" int rlhf_attn_softmax_bwd(const void* probs, const float* dP, void* dS, int Z, int S, float scale,
                                      rlhf_stream_t s) {
   const int64_t rows = static_cast<int64_t>(Z) * S;
-  attn_softmax_bwd_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, AS(s)>>>(
-      static_cast<const uint16_t*>(probs), dP, static_cast<uint16_t*>(dS), Z, S, scale);
+  if (S % 4) return 2;
+  const unsigned g = static_cast<unsigned>((rows + 7) / 8);
+  const auto* p = static_cast<const uint16_t*>(probs);
+  auto* o = static_cast<uint16_t*>(dS);
+  if (S <= 128) attn_softmax_bwd_kernel<1><<<g, 256, 0, AS(s)>>>(p, dP, o, Z, S, scale);
+  else if (S <= 512) attn_softmax_bwd_kernel<4><<<g, 256, 0, AS(s)>>>(p, dP, o, Z, S, scale);
+  else if (S <= 1536) attn_softmax_bwd_kernel<12><<<g, 256, 0, AS(s)>>>(p, dP, o, Z, S, scale);
+  else return 2;
   return AST();
 }
 

@@ -46,6 +46,15 @@ struct Args {
   int relu;
   const float* residual;  // same layout as Y (may alias), or null
   unsigned long long* probe;
+  // fused LayerNorm prologue: X = bf16(LN(ln_x) * ln_g + ln_b), ln_x fp32 [N, K]
+  const float* ln_x;
+  const uint16_t* ln_g;
+  const uint16_t* ln_b;
+  // fused KV-cache store of the k / v column blocks of a packed qkv output
+  uint16_t* kc;
+  uint16_t* vc;
+  const int* pos;
+  int kv_d, kv_hd, kv_H, kv_Smax;
 };
 __device__ __forceinline__ unsigned long long dclk() {
   unsigned long long c;
@@ -120,21 +129,78 @@ __global__ void __launch_bounds__(kThreads, 1)
   DPROBE(1);
   pdl_trigger();  // the next kernel may start its (independent) prologue
 
+  const bool ln = e.ln_x != nullptr;
   if (threadIdx.x == 0) {
     // weights do not depend on the previous kernel: stream them first
     for (int j = 0; j < nkb; ++j) {
       uint8_t* sa = smem + j * C::STAGE_BYTES;
-      mbar_arrive_expect_tx(&full_bar[j], C::STAGE_BYTES);
+      mbar_arrive_expect_tx(&full_bar[j], ln ? C::A_BYTES : C::STAGE_BYTES);
       tma_load_4d(sa, &tmW, &full_bar[j], (kb0 + j) * BK, 0, m0, 0);
     }
     DPROBE(2);
-    pdl_wait();  // activations X are produced by the previous kernel
-    DPROBE(3);
-    for (int j = 0; j < nkb; ++j) {
-      uint8_t* sb = smem + j * C::STAGE_BYTES + C::A_BYTES;
-      tma_load_4d(sb, &tmX, &full_bar[j], (kb0 + j) * BK, 0, 0, 0);
+    if (!ln) {
+      pdl_wait();  // activations X are produced by the previous kernel
+      DPROBE(3);
+      for (int j = 0; j < nkb; ++j) {
+        uint8_t* sb = smem + j * C::STAGE_BYTES + C::A_BYTES;
+        tma_load_4d(sb, &tmX, &full_bar[j], (kb0 + j) * BK, 0, 0, 0);
+      }
     }
-  } else if (warp == 1 && lane == 0) {
+  }
+  if (ln) {
+    // LayerNorm of every batch row (full K for the statistics), written for this
+    // CTA's K-slice straight into the SWIZZLE_128B K-major B tiles:
+    //   byte(n, kk) = n*128 + ((kk/8) ^ (n%8))*16 + (kk%8)*2   within a 64-wide k block
+    pdl_wait();
+    const int K4 = e.K / 4;
+    for (int n = static_cast<int>(warp); n < e.N; n += kThreads / 32) {
+      const float4* xr = reinterpret_cast<const float4*>(e.ln_x + static_cast<int64_t>(n) * e.K);
+      float4 v[16];
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = static_cast<int>(lane) + 32 * i;
+        v[i] = c < K4 ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const float mu = sum / e.K;
+      float vs = 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = static_cast<int>(lane) + 32 * i;
+        if (c < K4)
+          vs += (v[i].x - mu) * (v[i].x - mu) + (v[i].y - mu) * (v[i].y - mu) + (v[i].z - mu) * (v[i].z - mu) +
+                (v[i].w - mu) * (v[i].w - mu);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) vs += __shfl_xor_sync(0xffffffffu, vs, o);
+      const float rs = 1.0f / sqrtf(vs / e.K + 1e-5f);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = static_cast<int>(lane) + 32 * i;
+        const int k = 4 * c;
+        if (c >= K4 || k < kb0 * BK || k >= kb1 * BK) continue;
+        const uint2 gg = *reinterpret_cast<const uint2*>(e.ln_g + k);
+        const uint2 bb = *reinterpret_cast<const uint2*>(e.ln_b + k);
+        const float y0 = (v[i].x - mu) * rs * b2f(static_cast<uint16_t>(gg.x & 0xFFFFu)) + b2f(static_cast<uint16_t>(bb.x & 0xFFFFu));
+        const float y1 = (v[i].y - mu) * rs * b2f(static_cast<uint16_t>(gg.x >> 16)) + b2f(static_cast<uint16_t>(bb.x >> 16));
+        const float y2 = (v[i].z - mu) * rs * b2f(static_cast<uint16_t>(gg.y & 0xFFFFu)) + b2f(static_cast<uint16_t>(bb.y & 0xFFFFu));
+        const float y3 = (v[i].w - mu) * rs * b2f(static_cast<uint16_t>(gg.y >> 16)) + b2f(static_cast<uint16_t>(bb.y >> 16));
+        const int j = k / BK - kb0, kk = k % BK;
+        uint8_t* dst = smem + j * C::STAGE_BYTES + C::A_BYTES + n * 128 + (((kk >> 3) ^ (n & 7)) << 4) + (kk & 7) * 2;
+        const uint32_t w0 = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y0))) |
+                            (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y1))) << 16);
+        const uint32_t w1 = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y2))) |
+                            (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y3))) << 16);
+        *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> visible to tcgen05.mma
+    __syncthreads();
+  }
+  if (warp == 1 && lane == 0) {
     const uint32_t idesc = umma_idesc_bf16(BM, BN, 0, 0);
     for (int j = 0; j < nkb; ++j) {
       mbar_wait(&full_bar[j], 0);
@@ -217,8 +283,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (e.relu) x = fmaxf(x, 0.0f);
       x += res[t];
       const int64_t o = static_cast<int64_t>(n) * e.ldy + m;
-      if (e.y_f32) static_cast<float*>(e.Y)[o] = x;
-      else static_cast<uint16_t*>(e.Y)[o] = __bfloat16_as_ushort(__float2bfloat16_rn(x));
+      if (e.y_f32) {
+        static_cast<float*>(e.Y)[o] = x;
+      } else {
+        const uint16_t hb = __bfloat16_as_ushort(__float2bfloat16_rn(x));
+        static_cast<uint16_t*>(e.Y)[o] = hb;
+        if (e.kc && m >= e.kv_d) {  // k / v columns of qkv -> KV cache [n][h][pos][e]
+          const int mm = m - e.kv_d, which = mm / e.kv_d, within = mm % e.kv_d;
+          const int h = within / e.kv_hd, ee = within % e.kv_hd;
+          const int64_t dst = ((static_cast<int64_t>(n) * e.kv_H + h) * e.kv_Smax + *e.pos) * e.kv_hd + ee;
+          (which == 0 ? e.kc : e.vc)[dst] = hb;
+        }
+      }
     }
   }
   DPROBE(7);
@@ -301,7 +377,7 @@ extern "C" int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t 
   if (kb_per > max_kb) return 2;
   CUtensorMap tw, tx;
   if (dec::map2d(&tw, p->W, p->K, p->M, p->ldw, dec::BM)) return 2;
-  if (dec::map2d(&tx, p->X, p->K, p->N, p->ldx, bn)) return 2;
+  if (dec::map2d(&tx, p->X ? p->X : p->W, p->K, p->X ? p->N : p->M, p->X ? p->ldx : p->ldw, bn)) return 2;
   dec::Args a{};
   a.M = p->M;
   a.N = p->N;
@@ -315,6 +391,18 @@ extern "C" int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t 
   a.relu = p->relu;
   a.residual = p->residual;
   a.probe = p->probe;
+  a.ln_x = p->ln_x;
+  a.ln_g = static_cast<const uint16_t*>(p->ln_g);
+  a.ln_b = static_cast<const uint16_t*>(p->ln_b);
+  a.kc = static_cast<uint16_t*>(p->kcache);
+  a.vc = static_cast<uint16_t*>(p->vcache);
+  a.pos = p->pos;
+  a.kv_d = p->kv_d;
+  a.kv_hd = p->kv_hd;
+  a.kv_H = p->kv_H;
+  a.kv_Smax = p->kv_Smax;
+  if (a.ln_x && (p->K > 2048 || p->K % 4 || p->N > 64)) return 2;
+  if (a.kc && (p->y_f32 || !p->pos || p->M != 3 * p->kv_d)) return 2;
   const int tiles = (p->M + dec::BM - 1) / dec::BM;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return bn == 32 ? dec::launch<32>(tw, tx, a, tiles, p->pdl, s) : dec::launch<64>(tw, tx, a, tiles, p->pdl, s);

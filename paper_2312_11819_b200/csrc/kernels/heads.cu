@@ -32,20 +32,48 @@ __device__ __forceinline__ T block_reduce(T v, Op op, T* sh) {
 struct MaxOp { __device__ float operator()(float a, float b) const { return fmaxf(a, b); } };
 struct SumOp { __device__ float operator()(float a, float b) const { return a + b; } };
 
-// One CTA per logits row r = b*R + j; target y = tokens[b*S + P + j].
+// One CTA per logits row r = b*R + j; target y = tokens[b*S + P + j].  Single
+// pass: online (max, sum-exp) per thread over float4 loads, then block merge.
 __global__ void logprob_kernel(const float* __restrict__ z, int V, const int32_t* __restrict__ tok, int S, int P, int R,
                                float* __restrict__ logp, float* __restrict__ lse_out) {
-  __shared__ float sh[32];
+  __shared__ float shm[32], shs[32];
   const int r = blockIdx.x;
   const float* zr = z + static_cast<int64_t>(r) * V;
-  float mx = -FLT_MAX;
-  for (int v = threadIdx.x; v < V; v += blockDim.x) mx = fmaxf(mx, zr[v]);
-  mx = block_reduce(mx, MaxOp(), sh);
-  float s = 0.f;
-  for (int v = threadIdx.x; v < V; v += blockDim.x) s += expf(zr[v] - mx);
-  s = block_reduce(s, SumOp(), sh);
+  float m = -FLT_MAX, s = 0.f;
+  auto add = [&](float x) {
+    if (x > m) {
+      s = s * expf(m - x) + 1.0f;
+      m = x;
+    } else {
+      s += expf(x - m);
+    }
+  };
+  const int V4 = V / 4;
+  const float4* z4 = reinterpret_cast<const float4*>(zr);
+  for (int v = threadIdx.x; v < V4; v += blockDim.x) {
+    const float4 q = z4[v];
+    add(q.x); add(q.y); add(q.z); add(q.w);
+  }
+  for (int v = V4 * 4 + threadIdx.x; v < V; v += blockDim.x) add(zr[v]);
+  // warp merge
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mm = fmaxf(m, m2);
+    s = s * expf(m - mm) + s2 * expf(m2 - mm);
+    m = mm;
+  }
+  const int w = threadIdx.x / 32, nw = blockDim.x / 32;
+  if ((threadIdx.x & 31) == 0) { shm[w] = m; shs[w] = s; }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const float lse = mx + logf(s);
+    float M = shm[0], Ssum = shs[0];
+    for (int k = 1; k < nw; ++k) {
+      const float mm = fmaxf(M, shm[k]);
+      Ssum = Ssum * expf(M - mm) + shs[k] * expf(shm[k] - mm);
+      M = mm;
+    }
+    const float lse = M + logf(Ssum);
     const int b = r / R, j = r % R;
     const int y = tok[static_cast<int64_t>(b) * S + P + j];
     logp[r] = zr[y] - lse;
@@ -61,7 +89,19 @@ __global__ void logprob_bwd_kernel(const float* __restrict__ z, const float* __r
   const float* zr = z + static_cast<int64_t>(r) * V;
   uint16_t* o = dz + static_cast<int64_t>(r) * V;
   const float L = lse[r], gr = g[r];
-  for (int v = threadIdx.x; v < V; v += blockDim.x) o[v] = hf2b(gr * ((v == y ? 1.0f : 0.0f) - expf(zr[v] - L)));
+  const int V4 = V / 4;
+  const float4* z4 = reinterpret_cast<const float4*>(zr);
+  uint2* o4 = reinterpret_cast<uint2*>(o);
+  for (int v = threadIdx.x; v < V4; v += blockDim.x) {
+    const float4 q = z4[v];
+    const int b0 = 4 * v;
+    const uint16_t h0 = hf2b(gr * ((b0 == y ? 1.0f : 0.0f) - expf(q.x - L)));
+    const uint16_t h1 = hf2b(gr * ((b0 + 1 == y ? 1.0f : 0.0f) - expf(q.y - L)));
+    const uint16_t h2 = hf2b(gr * ((b0 + 2 == y ? 1.0f : 0.0f) - expf(q.z - L)));
+    const uint16_t h3 = hf2b(gr * ((b0 + 3 == y ? 1.0f : 0.0f) - expf(q.w - L)));
+    o4[v] = make_uint2(h0 | (static_cast<uint32_t>(h1) << 16), h2 | (static_cast<uint32_t>(h3) << 16));
+  }
+  for (int v = V4 * 4 + threadIdx.x; v < V; v += blockDim.x) o[v] = hf2b(gr * ((v == y ? 1.0f : 0.0f) - expf(zr[v] - L)));
 }
 
 // Greedy argmax per sample (ties -> lowest id) + top-2 margin.  Two phases:

@@ -111,48 +111,72 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const uint16_t* __
   }
 }
 
-constexpr int kLnBwdRows = 32;  // rows per block (8 warps x 4 rows)
+constexpr int kLnBwdRows = 64;  // rows per block (8 warps x 8 rows)
 
-// dx += rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)); per-block dg/db partials -> ws.
+// dx += rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)).  Each warp keeps its
+// rows' dgamma/dbeta column partials in registers (lane owns columns lane+32k),
+// the block reduces its 8 warps in smem in fixed order -> ws[blk][2][d].
+template <int CPL>  // columns per lane (d <= 32*CPL)
 __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
                                      const float* __restrict__ mean, const float* __restrict__ rstd,
                                      const uint16_t* __restrict__ g, float* __restrict__ dx, float* __restrict__ ws,
                                      int M, int d) {
+  extern __shared__ float red[];  // [8 warps][2][d]
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int r0 = blockIdx.x * kLnBwdRows;
+  float gg[CPL], pg[CPL], pb[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    const int j = lane + 32 * k;
+    gg[k] = j < d ? bf2f(g[j]) : 0.f;
+    pg[k] = pb[k] = 0.f;
+  }
   for (int rr = warp; rr < kLnBwdRows; rr += 8) {
     const int row = r0 + rr;
     if (row >= M) break;
     const float* dr = dy + static_cast<int64_t>(row) * d;
     const float* xr = x + static_cast<int64_t>(row) * d;
     const float mu = mean[row], rs = rstd[row];
+    float dyv[CPL], xh[CPL];
     float a = 0.f, c = 0.f;
-    for (int j = lane; j < d; j += 32) {
-      const float xh = (xr[j] - mu) * rs;
-      const float t = dr[j] * bf2f(g[j]);
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int j = lane + 32 * k;
+      dyv[k] = j < d ? dr[j] : 0.f;
+      xh[k] = j < d ? (xr[j] - mu) * rs : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const float t = dyv[k] * gg[k];
       a += t;
-      c += t * xh;
+      c += t * xh[k];
+      pg[k] += dyv[k] * xh[k];
+      pb[k] += dyv[k];
     }
     a = warp_sum(a) / d;
     c = warp_sum(c) / d;
     float* o = dx + static_cast<int64_t>(row) * d;
-    for (int j = lane; j < d; j += 32) {
-      const float xh = (xr[j] - mu) * rs;
-      o[j] += rs * (dr[j] * bf2f(g[j]) - a - xh * c);
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int j = lane + 32 * k;
+      if (j < d) o[j] += rs * (dyv[k] * gg[k] - a - xh[k] * c);
     }
   }
-  // column partials of this block (fixed row order -> deterministic)
-  const int r1 = min(M, r0 + kLnBwdRows);
-  float* wg = ws + static_cast<int64_t>(blockIdx.x) * 2 * d;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    float sg = 0.f, sb = 0.f;
-    for (int row = r0; row < r1; ++row) {
-      const float t = dy[static_cast<int64_t>(row) * d + j];
-      sg += t * (x[static_cast<int64_t>(row) * d + j] - mean[row]) * rstd[row];
-      sb += t;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    const int j = lane + 32 * k;
+    if (j < d) {
+      red[(warp * 2) * d + j] = pg[k];
+      red[(warp * 2 + 1) * d + j] = pb[k];
     }
-    wg[j] = sg;
-    wg[d + j] = sb;
+  }
+  __syncthreads();
+  float* wg = ws + static_cast<int64_t>(blockIdx.x) * 2 * d;
+  for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
+    const int which = j / d, col = j % d;
+    float acc = 0.f;
+    for (int w = 0; w < 8; ++w) acc += red[(w * 2 + which) * d + col];  // fixed warp order
+    wg[j] = acc;
   }
 }
 
@@ -180,15 +204,41 @@ __global__ void round_bf16_kernel(const float* __restrict__ x, uint16_t* __restr
 
 constexpr int kColsumChunks = 64;
 
+// Partial column sums of a bf16 [M, N] matrix: block = 32 column groups of 8
+// (16 B loads, a warp reads 512 contiguous bytes of a row) x 8 row lanes; rows of
+// chunk blockIdx.y; fixed-order smem reduction of the 8 row lanes -> ws[chunk][N].
 __global__ void colsum_bf16_kernel(const uint16_t* __restrict__ G, int M, int N, float* __restrict__ ws) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  const int chunk = blockIdx.y;
-  if (col >= N) return;
+  __shared__ float red[8][256];
+  const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int col0 = blockIdx.x * 256 + cg * 8;
   const int per = (M + kColsumChunks - 1) / kColsumChunks;
-  const int r0 = chunk * per, r1 = min(M, r0 + per);
-  float s = 0.f;
-  for (int r = r0; r < r1; ++r) s += bf2f(G[static_cast<int64_t>(r) * N + col]);
-  ws[static_cast<int64_t>(chunk) * N + col] = s;
+  const int r0 = blockIdx.y * per, r1 = min(M, r0 + per);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (col0 + 8 <= N) {
+    for (int r = r0 + rl; r < r1; r += 8) {
+      const uint4 u = *reinterpret_cast<const uint4*>(G + static_cast<int64_t>(r) * N + col0);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        acc[2 * t] += bf2f(static_cast<uint16_t>(w[t] & 0xFFFFu));
+        acc[2 * t + 1] += bf2f(static_cast<uint16_t>(w[t] >> 16));
+      }
+    }
+  } else {
+    for (int r = r0 + rl; r < r1; r += 8)
+      for (int t = 0; t < 8; ++t)
+        if (col0 + t < N) acc[t] += bf2f(G[static_cast<int64_t>(r) * N + col0 + t]);
+  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t) red[rl][cg * 8 + t] = acc[t];
+  __syncthreads();
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < N) {
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum += red[k][threadIdx.x];
+    ws[static_cast<int64_t>(blockIdx.y) * N + c] = sum;
+  }
 }
 
 __global__ void gather_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int S, int R, int off,
@@ -284,7 +334,17 @@ extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* 
                                   rlhf_stream_t s) {
   const int nblk = (M + kLnBwdRows - 1) / kLnBwdRows;
   if (ws_floats < static_cast<size_t>(nblk) * 2 * d) return 2;
-  layernorm_bwd_kernel<<<nblk, 256, 0, S(s)>>>(dy, x, mean, rstd, static_cast<const uint16_t*>(g), dx, ws, M, d);
+  const size_t sm = static_cast<size_t>(16) * d * 4;
+  const auto* gp = static_cast<const uint16_t*>(g);
+  if (d <= 1024) {
+    cudaFuncSetAttribute(layernorm_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024 * 4);
+    layernorm_bwd_kernel<32><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
+  } else if (d <= 2048) {
+    cudaFuncSetAttribute(layernorm_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4);
+    layernorm_bwd_kernel<64><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
+  } else {
+    return 2;
+  }
   reduce_partials_kernel<<<(2 * d + 255) / 256, 256, 0, S(s)>>>(ws, nblk, 2 * d, 2 * d, dg, db, d);
   return cuda_status();
 }
@@ -296,6 +356,7 @@ extern "C" int rlhf_round_bf16(const float* x, void* out, int64_t n, rlhf_stream
 }
 
 extern "C" int rlhf_colsum_bf16(const void* G, int M, int N, float* db, float* ws, rlhf_stream_t s) {
+  if (N % 8) return 2;
   dim3 grid((N + 255) / 256, kColsumChunks);
   colsum_bf16_kernel<<<grid, 256, 0, S(s)>>>(static_cast<const uint16_t*>(G), M, N, ws);
   reduce_partials_kernel<<<(N + 255) / 256, 256, 0, S(s)>>>(ws, kColsumChunks, N, N, db, db, N);

@@ -99,22 +99,27 @@ class GemmDecodeParams(C.Structure):
     _fields_ = [("M", C.c_int), ("N", C.c_int), ("K", C.c_int), ("W", C.c_void_p), ("ldw", C.c_int64),
                 ("X", C.c_void_p), ("ldx", C.c_int64), ("Y", C.c_void_p), ("y_f32", C.c_int), ("ldy", C.c_int64),
                 ("bias", C.c_void_p), ("relu", C.c_int), ("residual", C.c_void_p), ("splits", C.c_int),
-                ("pdl", C.c_int), ("probe", C.c_void_p)]
+                ("pdl", C.c_int), ("probe", C.c_void_p), ("ln_x", C.c_void_p), ("ln_g", C.c_void_p),
+                ("ln_b", C.c_void_p), ("kcache", C.c_void_p), ("vcache", C.c_void_p), ("pos", C.c_void_p),
+                ("kv_d", C.c_int), ("kv_hd", C.c_int), ("kv_H", C.c_int), ("kv_Smax", C.c_int)]
 
 
 def gemm_decode(W: torch.Tensor, X: torch.Tensor, *, out: torch.Tensor | None = None, bias=None, relu=False,
-                residual=None, splits: int = 1, out_f32: bool = True, probe=None) -> torch.Tensor:
+                residual=None, splits: int = 1, out_f32: bool = True, probe=None, ln=None) -> torch.Tensor:
     """Y[N, M] = X[N, K] . W[M, K]^T (+bias[M]) (relu) (+residual) via rlhf_gemm_decode."""
     L = lib()
     L.rlhf_gemm_decode.argtypes = [C.POINTER(GemmDecodeParams), C.c_void_p]
     M, K = W.shape
-    N = X.shape[0]
+    N = X.shape[0] if X is not None else ln[0].shape[0]
     if out is None:
         out = torch.zeros(N, M, device=W.device, dtype=torch.float32 if out_f32 else torch.bfloat16)
-    p = GemmDecodeParams(M, N, K, W.data_ptr(), W.stride(0), X.data_ptr(), X.stride(0), out.data_ptr(),
+    p = GemmDecodeParams(M, N, K, W.data_ptr(), W.stride(0), X.data_ptr() if X is not None else None,
+                         X.stride(0) if X is not None else K, out.data_ptr(),
                          int(out.dtype == torch.float32), out.stride(0), bias.data_ptr() if bias is not None else None,
                          int(relu), residual.data_ptr() if residual is not None else None, splits, 0,
                          probe.data_ptr() if probe is not None else None)
+    if ln is not None:  # (x fp32 [N, K], gamma bf16 [K], beta bf16 [K])
+        p.ln_x, p.ln_g, p.ln_b = ln[0].data_ptr(), ln[1].data_ptr(), ln[2].data_ptr()
     st = L.rlhf_gemm_decode(C.byref(p), _stream())
     if st != 0:
         raise RuntimeError(f"rlhf_gemm_decode failed with status {st}")

@@ -151,3 +151,18 @@ def test_gemm_decode_cluster_split(M, K, N, splits):
     expb = torch.relu(X.float() @ W.float().t() + bias.float())
     torch.cuda.synchronize()
     assert (yb.float() - expb).abs().max().item() <= 0.02 * expb.abs().max().item()
+
+
+@pytest.mark.parametrize("M,K,N,splits", [(2304, 768, 32, 4), (3072, 768, 32, 4), (384, 128, 4, 1), (6144, 2048, 16, 2)])
+def test_gemm_decode_fused_layernorm(M, K, N, splits):
+    """X = bf16(LN(x)) computed inside the decode GEMM == separate LN kernel + GEMM."""
+    from paper_2312_11819_b200 import ops
+    W = torch.randn(M, K, device="cuda").bfloat16()
+    x = torch.randn(N, K, device="cuda") * 3 + 1
+    g = (1 + 0.1 * torch.randn(K, device="cuda")).bfloat16()
+    b = (0.1 * torch.randn(K, device="cuda")).bfloat16()
+    h = torch.nn.functional.layer_norm(x, (K,), g.float(), b.float(), eps=1e-5).bfloat16()
+    out = ops.gemm_decode(W, None, ln=(x, g, b), splits=splits)
+    exp = h.float() @ W.float().t()
+    torch.cuda.synchronize()
+    close(out, exp, 2e-2)  # bf16 rounding of h may flip between the two LN evaluations
