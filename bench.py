@@ -39,6 +39,11 @@ WORKLOADS = {
                name="c2: OPT-125m-shaped Actor/Ref + Critic/Reward, batch 32/GPU, prompt 256 + response 256"),
     "c1": dict(actor="tiny", critic="tiny", batch=4, prompt=16, gen=16,
                name="c1: tiny decoder x4, batch 4/GPU, prompt 16 + response 16"),
+    # c3 / c5 shapes (B=64 over 8 GPUs in the paper's setting; per-GPU 16 here)
+    "c3": dict(actor="opt-1.3b", critic="opt-350m", batch=16, prompt=256, gen=256,
+               name="c3: OPT-1.3B Actor/Ref + OPT-350m-shaped Critic/Reward, batch 16/GPU, prompt 256 + response 256"),
+    "c5-r1024": dict(actor="opt-1.3b", critic="opt-350m", batch=16, prompt=256, gen=1024,
+                     name="c5: OPT-1.3B/350m, batch 16/GPU, prompt 256 + response 1024"),
 }
 
 

@@ -33,12 +33,12 @@ struct Cfg {
   static constexpr int MAX_KB = BN <= 32 ? 8 : 6;
   static constexpr int PART_PITCH = BN + 4;  // 16 B aligned rows for v4 DSMEM reads
   static constexpr int PART_BYTES = BM * PART_PITCH * 4;
-  static constexpr int SMEM = MAX_KB * STAGE_BYTES + PART_BYTES + 1024 + 256;
-  static int smem_for(int kb_per) { return kb_per * STAGE_BYTES + PART_BYTES + 1024 + 256; }
+  static constexpr int SMEM = MAX_KB * STAGE_BYTES + PART_BYTES + 1024 + 512;
+  static int smem_for(int stages) { return stages * STAGE_BYTES + PART_BYTES + 1024 + 512; }
 };
 
 struct Args {
-  int M, N, K, splits, kb_per;
+  int M, N, K, splits, kb_per, stages;
   void* Y;
   int y_f32;
   int64_t ldy;  // Y element (n, m) at Y + n*ldy + m
@@ -100,9 +100,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* part = reinterpret_cast<float*>(smem + e.kb_per * C::STAGE_BYTES);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + e.kb_per * C::STAGE_BYTES + C::PART_BYTES);
-  uint64_t* acc_bar = full_bar + e.kb_per;
+  float* part = reinterpret_cast<float*>(smem + e.stages * C::STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + e.stages * C::STAGE_BYTES + C::PART_BYTES);
+  uint64_t* empty_bar = full_bar + e.stages;
+  uint64_t* acc_bar = empty_bar + e.stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_bar + 1);
 
   const int split = static_cast<int>(cluster_rank());
@@ -115,7 +116,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_id(), lane = lane_id();
   DPROBE(0);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < e.kb_per; ++s) mbar_init(&full_bar[s], 1);
+    for (int s = 0; s < e.stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
     mbar_init(acc_bar, 1);
     mbar_fence_init();
     tma_prefetch(&tmW);
@@ -131,8 +135,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const bool ln = e.ln_x != nullptr;
   if (threadIdx.x == 0) {
-    // weights do not depend on the previous kernel: stream them first
-    for (int j = 0; j < nkb; ++j) {
+    // weights do not depend on the previous kernel: fill the ring with them first
+    const int first = min(nkb, e.stages);
+    for (int j = 0; j < first; ++j) {
       uint8_t* sa = smem + j * C::STAGE_BYTES;
       mbar_arrive_expect_tx(&full_bar[j], ln ? C::A_BYTES : C::STAGE_BYTES);
       tma_load_4d(sa, &tmW, &full_bar[j], (kb0 + j) * BK, 0, m0, 0);
@@ -141,9 +146,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!ln) {
       pdl_wait();  // activations X are produced by the previous kernel
       DPROBE(3);
-      for (int j = 0; j < nkb; ++j) {
+      for (int j = 0; j < first; ++j) {
         uint8_t* sb = smem + j * C::STAGE_BYTES + C::A_BYTES;
         tma_load_4d(sb, &tmX, &full_bar[j], (kb0 + j) * BK, 0, 0, 0);
+      }
+      for (int j = first; j < nkb; ++j) {  // ring reuse once the MMA released a slot
+        const int st = j % e.stages;
+        mbar_wait(&empty_bar[st], ((j / e.stages) - 1) & 1);
+        uint8_t* sa = smem + st * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full_bar[st], C::STAGE_BYTES);
+        tma_load_4d(sa, &tmW, &full_bar[st], (kb0 + j) * BK, 0, m0, 0);
+        tma_load_4d(sa + C::A_BYTES, &tmX, &full_bar[st], (kb0 + j) * BK, 0, 0, 0);
       }
     }
   }
@@ -203,14 +216,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1 && lane == 0) {
     const uint32_t idesc = umma_idesc_bf16(BM, BN, 0, 0);
     for (int j = 0; j < nkb; ++j) {
-      mbar_wait(&full_bar[j], 0);
+      const int st = j % e.stages;
+      mbar_wait(&full_bar[st], (j / e.stages) & 1);
       tc_fence_after();
-      const uint32_t sa = smem_u32(smem + j * C::STAGE_BYTES);
+      const uint32_t sa = smem_u32(smem + st * C::STAGE_BYTES);
       const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
       for (int k = 0; k < BK / 16; ++k)
         umma_bf16(tmem, umma_desc_sw128(sa + k * 32, 16, 1024), umma_desc_sw128(sb + k * 32, 16, 1024), idesc,
                   (j > 0 || k > 0) ? 1u : 0u);
+      umma_commit(&empty_bar[st]);
     }
     if (nkb > 0) umma_commit(acc_bar);
     else mbar_arrive(acc_bar);
@@ -346,7 +361,7 @@ int launch(const CUtensorMap& tw, const CUtensorMap& tx, const Args& a, int tile
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles * a.splits);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::smem_for(a.kb_per);
+  cfg.dynamicSmemBytes = C::smem_for(a.stages);
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -370,11 +385,11 @@ extern "C" int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t 
   if (p->N < 1 || p->N > 64 || p->M < 1 || p->K < 1 || p->K % 8) return 2;
   const int num_kb = (p->K + dec::BK - 1) / dec::BK;
   const int max_kb = bn == 32 ? dec::Cfg<32>::MAX_KB : dec::Cfg<64>::MAX_KB;
-  int splits = p->splits;
+  const int splits = p->splits;
   if (splits != 1 && splits != 2 && splits != 4 && splits != 8) return 2;
-  while ((num_kb + splits - 1) / splits > max_kb && splits < 8) splits *= 2;  // every slice must fit in smem
   const int kb_per = (num_kb + splits - 1) / splits;
-  if (kb_per > max_kb) return 2;
+  const int stages = std::min(kb_per, max_kb);  // smem ring (weights stream through it)
+  if (p->ln_x && kb_per > stages) return 2;    // fused LN writes every B tile up front
   CUtensorMap tw, tx;
   if (dec::map2d(&tw, p->W, p->K, p->M, p->ldw, dec::BM)) return 2;
   if (dec::map2d(&tx, p->X ? p->X : p->W, p->K, p->X ? p->N : p->M, p->X ? p->ldx : p->ldw, bn)) return 2;
@@ -384,6 +399,7 @@ extern "C" int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t 
   a.K = p->K;
   a.splits = splits;
   a.kb_per = kb_per;
+  a.stages = stages;
   a.Y = p->Y;
   a.y_f32 = p->y_f32;
   a.ldy = p->ldy;
