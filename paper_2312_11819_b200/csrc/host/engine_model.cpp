@@ -5,6 +5,7 @@
 // Rounding points follow DESIGN.md §3 and are mirrored by oracle/ppo_oracle.cpp.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -346,18 +347,28 @@ void Engine::decode_step(const Decoder& m, int B) {
   uint16_t* o = dec_o_.as<uint16_t>();
   uint16_t* f = dec_f_.as<uint16_t>();
   const int32_t* tok = tokens_.as<int32_t>();
+  // RLHF_DECODE_SKIP (debug timing only, results become wrong): bit 0 LN, 1 attention,
+  // 2 qkv GEMM, 3 o-proj, 4 FFN GEMMs, 5 LM head + argmax
+  static const int skip = [] { const char* e = getenv("RLHF_DECODE_SKIP"); return e ? atoi(e) : 0; }();
   K(rlhf_embed(tok, S_, B, 1, 0, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x, stream_), 1);
   // per layer 7 launches: LN1, [QKV GEMM + KV-cache store], attention,
   // [O-proj + residual], LN2, [FFN-up + ReLU], [FFN-down + residual]
   for (int l = 0; l < a.n_layers; ++l) {
-    K(rlhf_layernorm(x, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h, nullptr, nullptr, B, d, stream_), 1);
-    linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr, nullptr, nullptr,
-                  nullptr, l);
-    K(rlhf_attn_decode(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o, stream_), 1);
-    linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, m.T(RLHF_T_BO, l), x, true, false, x);
-    K(rlhf_layernorm(x, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h, nullptr, nullptr, B, d, stream_), 1);
-    linear_decode(m.T(RLHF_T_W1, l), ff, d, h, B, m.T(RLHF_T_B1, l), f, false, true, nullptr);
-    linear_decode(m.T(RLHF_T_W2, l), d, ff, f, B, m.T(RLHF_T_B2, l), x, true, false, x);
+    if (!(skip & 1)) K(rlhf_layernorm(x, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h, nullptr, nullptr, B, d, stream_), 1);
+    if (!(skip & 4))
+      linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr, nullptr, nullptr,
+                    nullptr, l);
+    if (!(skip & 2)) K(rlhf_attn_decode(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o, stream_), 1);
+    if (!(skip & 8)) linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, m.T(RLHF_T_BO, l), x, true, false, x);
+    if (!(skip & 1)) K(rlhf_layernorm(x, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h, nullptr, nullptr, B, d, stream_), 1);
+    if (!(skip & 16)) {
+      linear_decode(m.T(RLHF_T_W1, l), ff, d, h, B, m.T(RLHF_T_B1, l), f, false, true, nullptr);
+      linear_decode(m.T(RLHF_T_W2, l), d, ff, f, B, m.T(RLHF_T_B2, l), x, true, false, x);
+    }
+  }
+  if (skip & 32) {
+    K(rlhf_add_int(pos, 1, stream_), 1);
+    return;
   }
   K(rlhf_layernorm(x, m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), dec_hf_.as<uint16_t>(), nullptr, nullptr, B, d, stream_), 1);
   linear_decode(m.T(RLHF_T_TOK_EMB), V, d, dec_hf_.as<uint16_t>(), B, nullptr, dec_logits_.as<float>(), true, false, nullptr);

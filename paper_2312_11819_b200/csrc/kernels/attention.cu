@@ -8,6 +8,7 @@
 #include <cfloat>
 
 #include "launch_util.cuh"
+#include "sm100_common.cuh"
 #include "rlhf_kernels.h"
 
 namespace rlhf {
@@ -134,51 +135,117 @@ __global__ void kv_store_kernel(const uint16_t* __restrict__ qkv, int T, int p0,
 constexpr int kDecThreads = 256;
 constexpr int kDecMaxCtx = 4096;
 
-// One CTA per (sample, head): scores (thread per key, 16B loads), block softmax,
-// bf16-rounded probabilities, then P.V with (dim, key-group) thread split.
+// One CTA per (sample, head).  The key and value rows [0, ctx) of the head are
+// streamed into shared memory with bulk async copies (cp.async.bulk, mbarrier
+// completion) in chunks of C positions; for ctx <= C both are in flight from the
+// first instruction, so the CTA pays one HBM latency instead of one per loop
+// trip.  Scores: LPR lanes per key row (16 B each, conflict-free rows), block
+// softmax, bf16-rounded probabilities, then P.V with a (dim chunk, key group)
+// thread split over the staged value rows.
+template <int HD>
+struct DecCfg {
+  static constexpr int C = HD == 64 ? 256 : 128;  // positions per staged chunk (K + V = 64 KB)
+  static constexpr int LPR = HD / 8;              // lanes per key row
+  static constexpr int RPW = 32 / LPR;            // key rows per warp pass
+  static constexpr size_t smem(int Smax) {
+    return static_cast<size_t>(2) * C * HD * 2 + static_cast<size_t>((Smax + 3) / 4 * 4) * 4 + HD * 4;
+  }
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int HD>
+__device__ __forceinline__ void dec_issue(uint16_t* dst, const uint16_t* src, int chunk, int ctx, uint64_t* bar) {
+  constexpr int C = DecCfg<HD>::C;
+  const int rows = min(C, ctx - chunk * C);
+  mbar_arrive_expect_tx(bar, static_cast<uint32_t>(rows * HD * 2));
+  for (int r0 = 0; r0 < rows; r0 += 64)
+    bulk_g2s(dst + r0 * HD, src + static_cast<int64_t>(chunk * C + r0) * HD, static_cast<uint32_t>(min(64, rows - r0) * HD * 2),
+             bar);
+}
+
 template <int HD>
 __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t* __restrict__ qkv, int H, int Smax,
                                                                   const uint16_t* __restrict__ kc,
                                                                   const uint16_t* __restrict__ vc,
                                                                   const int* __restrict__ pos_dev,
                                                                   uint16_t* __restrict__ out) {
-  __shared__ float q[HD];
-  __shared__ float sc[kDecMaxCtx];
-  __shared__ float red[kDecThreads / 32];
+  using Cf = DecCfg<HD>;
+  constexpr int C = Cf::C, LPR = Cf::LPR, RPW = Cf::RPW, NW = kDecThreads / 32;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint16_t* Ks = reinterpret_cast<uint16_t*>(dsm);
+  uint16_t* Vs = Ks + C * HD;
+  float* sc = reinterpret_cast<float*>(Vs + C * HD);
+  float* q = sc + (Smax + 3) / 4 * 4;
+  __shared__ float red[NW];
+  __shared__ uint64_t bars[2];
   pdl_entry();
   const int bh = blockIdx.x, b = bh / H, h = bh % H;
   const int d = H * HD;
   const int ctx = *pos_dev + 1;
+  const int nch = (ctx + C - 1) / C;
+  const uint16_t* K = kc + static_cast<int64_t>(bh) * Smax * HD;
+  const uint16_t* V = vc + static_cast<int64_t>(bh) * Smax * HD;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+    dec_issue<HD>(Ks, K, 0, ctx, &bars[0]);
+    dec_issue<HD>(Vs, V, 0, ctx, &bars[1]);
+  }
   const float scale = rsqrtf(static_cast<float>(HD));
   const uint16_t* qsrc = qkv + static_cast<int64_t>(b) * 3 * d + h * HD;
   for (int e = threadIdx.x; e < HD; e += kDecThreads) q[e] = bf2f_a(qsrc[e]);
   __syncthreads();
-  const uint16_t* K = kc + static_cast<int64_t>(bh) * Smax * HD;
-  const uint16_t* V = vc + static_cast<int64_t>(bh) * Smax * HD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane % LPR, rsub = lane / LPR;
+  float qr[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) qr[t] = q[sub * 8 + t];
   float mx = -FLT_MAX;
-  for (int j = threadIdx.x; j < ctx; j += kDecThreads) {
-    const uint4* kr = reinterpret_cast<const uint4*>(K + static_cast<int64_t>(j) * HD);
-    float s = 0.f;
+  for (int c = 0; c < nch; ++c) {
+    mbar_wait(&bars[0], c & 1);
+    const int rows = min(C, ctx - c * C);
+    for (int r0 = warp * RPW; r0 < rows; r0 += NW * RPW) {  // warp-uniform trip count
+      const int r = r0 + rsub;
+      float s = 0.f;
+      if (r < rows) {
+        const uint4 u = *reinterpret_cast<const uint4*>(Ks + r * HD + sub * 8);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int c = 0; c < HD / 8; ++c) {
-      const uint4 u = kr[c];
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        for (int t = 0; t < 4; ++t) {
+          s += qr[2 * t] * bf2f_a(static_cast<uint16_t>(w[t] & 0xFFFFu));
+          s += qr[2 * t + 1] * bf2f_a(static_cast<uint16_t>(w[t] >> 16));
+        }
+      }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        s += q[c * 8 + 2 * t] * bf2f_a(static_cast<uint16_t>(w[t] & 0xFFFFu));
-        s += q[c * 8 + 2 * t + 1] * bf2f_a(static_cast<uint16_t>(w[t] >> 16));
+      for (int o = LPR / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (sub == 0 && r < rows) {
+        s *= scale;
+        sc[c * C + r] = s;
+        mx = fmaxf(mx, s);
       }
     }
-    s *= scale;
-    sc[j] = s;
-    mx = fmaxf(mx, s);
+    if (c + 1 < nch) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_proxy_async_smem();
+        dec_issue<HD>(Ks, K, c + 1, ctx, &bars[0]);
+      }
+    }
   }
   mx = wmax(mx);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = mx;
+  if (lane == 0) red[warp] = mx;
   __syncthreads();
   mx = red[0];
 #pragma unroll
-  for (int w = 1; w < kDecThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+  for (int w = 1; w < NW; ++w) mx = fmaxf(mx, red[w]);
   __syncthreads();
   float sum = 0.f;
   for (int j = threadIdx.x; j < ctx; j += kDecThreads) {
@@ -187,33 +254,43 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
     sum += e;
   }
   sum = wsum(sum);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = sum;
+  if (lane == 0) red[warp] = sum;
   __syncthreads();
   sum = 0.f;
 #pragma unroll
-  for (int w = 0; w < kDecThreads / 32; ++w) sum += red[w];
+  for (int w = 0; w < NW; ++w) sum += red[w];
   const float inv = 1.0f / sum;
-  // O[e] = sum_j bf16(p_j) V[j][e]: thread = (16-byte dim chunk c, key group g);
-  // a warp reads whole contiguous V rows (coalesced 16B vectors).
-  constexpr int CH = HD / 8;              // 16-byte chunks per row
-  constexpr int G = kDecThreads / CH;     // key groups
-  const int c = threadIdx.x % CH, grp = threadIdx.x / CH;
+  // O[e] = sum_j bf16(p_j) V[j][e]: thread = (16-byte dim chunk cc, key group grp)
+  constexpr int CH = HD / 8;
+  constexpr int G = kDecThreads / CH;
+  const int cc = threadIdx.x % CH, grp = threadIdx.x / CH;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int c = 0; c < nch; ++c) {
+    mbar_wait(&bars[1], c & 1);
+    const int rows = min(C, ctx - c * C);
 #pragma unroll 4
-  for (int j = grp; j < ctx; j += G) {
-    const float pj = bf2f_a(f2bf_a(sc[j] * inv));
-    const uint4 u = *reinterpret_cast<const uint4*>(V + static_cast<int64_t>(j) * HD + c * 8);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    for (int r = grp; r < rows; r += G) {
+      const float pj = bf2f_a(f2bf_a(sc[c * C + r] * inv));
+      const uint4 u = *reinterpret_cast<const uint4*>(Vs + r * HD + cc * 8);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      acc[2 * t] += pj * bf2f_a(static_cast<uint16_t>(w[t] & 0xFFFFu));
-      acc[2 * t + 1] += pj * bf2f_a(static_cast<uint16_t>(w[t] >> 16));
+      for (int t = 0; t < 4; ++t) {
+        acc[2 * t] += pj * bf2f_a(static_cast<uint16_t>(w[t] & 0xFFFFu));
+        acc[2 * t + 1] += pj * bf2f_a(static_cast<uint16_t>(w[t] >> 16));
+      }
+    }
+    if (c + 1 < nch) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_proxy_async_smem();
+        dec_issue<HD>(Vs, V, c + 1, ctx, &bars[1]);
+      }
     }
   }
-  float* part = sc;  // scores no longer needed: reuse as [G][HD] partials
+  float* part = reinterpret_cast<float*>(Ks);  // [G][HD] partials (key rows no longer needed)
   __syncthreads();
 #pragma unroll
-  for (int t = 0; t < 8; ++t) part[grp * HD + c * 8 + t] = acc[t];
+  for (int t = 0; t < 8; ++t) part[grp * HD + cc * 8 + t] = acc[t];
   __syncthreads();
   for (int e = threadIdx.x; e < HD; e += kDecThreads) {
     float o = 0.f;
@@ -265,6 +342,20 @@ extern "C" int rlhf_kv_store(const void* qkv, int B, int T, int p0, const int* p
                   static_cast<uint16_t*>(vcache), rows);
 }
 
+template <int HD>
+static int launch_dec(int grid, cudaStream_t st, const uint16_t* q, int H, int Smax, const uint16_t* k, const uint16_t* v,
+                      const int* pos_dev, uint16_t* o) {
+  const size_t smem = DecCfg<HD>::smem(Smax);
+  static size_t configured = 0;  // per-HD opt-in to > 48 KB dynamic shared memory
+  if (smem > configured) {
+    if (cudaFuncSetAttribute(attn_decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+      return 5;
+    configured = smem;
+  }
+  return launch_k(attn_decode_kernel<HD>, dim3(grid), dim3(kDecThreads), smem, st, q, H, Smax, k, v, pos_dev, o);
+}
+
 extern "C" int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax, const void* kcache, const void* vcache,
                                 const int* pos_dev, void* out, rlhf_stream_t s) {
   if (Smax > kDecMaxCtx) return 2;
@@ -273,8 +364,8 @@ extern "C" int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax,
   const auto* v = static_cast<const uint16_t*>(vcache);
   auto* o = static_cast<uint16_t*>(out);
   switch (hd) {
-    case 64: return launch_k(attn_decode_kernel<64>, dim3(B * H), dim3(kDecThreads), 0, AS(s), q, H, Smax, k, v, pos_dev, o);
-    case 128: return launch_k(attn_decode_kernel<128>, dim3(B * H), dim3(kDecThreads), 0, AS(s), q, H, Smax, k, v, pos_dev, o);
+    case 64: return launch_dec<64>(B * H, AS(s), q, H, Smax, k, v, pos_dev, o);
+    case 128: return launch_dec<128>(B * H, AS(s), q, H, Smax, k, v, pos_dev, o);
     default: return 2;
   }
 }

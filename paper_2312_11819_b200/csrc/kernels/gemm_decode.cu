@@ -31,8 +31,7 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int MAX_KB = BN <= 32 ? 8 : 6;
-  static constexpr int PART_PITCH = BN + 4;  // 16 B aligned rows for v4 DSMEM reads
-  static constexpr int PART_BYTES = BM * PART_PITCH * 4;
+  static constexpr int PART_BYTES = BM * BN * 4;  // receive buffer: [slice][row of this CTA][BN] fp32
   static constexpr int SMEM = MAX_KB * STAGE_BYTES + PART_BYTES + 1024 + 512;
   static int smem_for(int stages) { return stages * STAGE_BYTES + PART_BYTES + 1024 + 512; }
 };
@@ -88,6 +87,15 @@ __device__ __forceinline__ float4 ld_cluster_v4(uint32_t remote) {
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(remote));
   return v;
 }
+// async 16 B store into a peer CTA's shared memory, completing bytes on the peer's mbarrier
+__device__ __forceinline__ void st_async_v4(uint32_t remote_addr, float a, float b, float c, float d, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(remote_addr),
+               "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)), "r"(__float_as_uint(d)),
+               "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -104,7 +112,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + e.stages * C::STAGE_BYTES + C::PART_BYTES);
   uint64_t* empty_bar = full_bar + e.stages;
   uint64_t* acc_bar = empty_bar + e.stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_bar + 1);
+  uint64_t* recv_bar = acc_bar + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
+  const int rows_per = BM / e.splits;
 
   const int split = static_cast<int>(cluster_rank());
   const int tile = blockIdx.x / e.splits;
@@ -121,6 +131,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(acc_bar, 1);
+    mbar_init(recv_bar, 1);
+    // every slice pushes its rows_per x BN fp32 rows of this CTA's share here
+    mbar_arrive_expect_tx(recv_bar, static_cast<uint32_t>(e.splits * rows_per * BN * 4));
     mbar_fence_init();
     tma_prefetch(&tmW);
     tma_prefetch(&tmX);
@@ -160,6 +173,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  // peers' receive barriers are initialised before anyone pushes partials
+  cluster_arrive_relaxed();
+  cluster_wait();
   if (ln) {
     // LayerNorm of every batch row (full K for the statistics), written for this
     // CTA's K-slice straight into the SWIZZLE_128B K-major B tiles:
@@ -232,13 +248,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   pdl_wait();  // residual (and Y when aliased) come from earlier kernels
 
-  // ---- partial accumulator -> own smem (row = TMEM lane)
+  // ---- partial accumulator rows -> the owning CTA's receive buffer (st.async, DSMEM)
   mbar_wait(acc_bar, 0);
   DPROBE(4);
   tc_fence_after();
   {
     const int row = static_cast<int>(warp) * 32 + static_cast<int>(lane);
     const uint32_t tb = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const int owner = row / rows_per, rl = row % rows_per;
+    const uint32_t dst = map_rank(smem_u32(part) + static_cast<uint32_t>(((split * rows_per + rl) * BN) * 4),
+                                  static_cast<uint32_t>(owner));
+    const uint32_t rbar = map_rank(smem_u32(recv_bar), static_cast<uint32_t>(owner));
 #pragma unroll
     for (int c = 0; c < BN / 32; ++c) {
       float v[32];
@@ -248,33 +268,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 32; ++j) v[j] = 0.0f;
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) part[row * C::PART_PITCH + c * 32 + j] = v[j];
+      for (int q = 0; q < 8; ++q)
+        st_async_v4(dst + static_cast<uint32_t>((c * 32 + 4 * q) * 4), v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3],
+                    rbar);
     }
   }
   tc_fence_before();
   DPROBE(5);
-  cluster_sync_all();  // every slice's partial is visible cluster-wide
+  mbar_wait(recv_bar, 0);  // all slices' rows of this CTA's share have landed
   DPROBE(6);
 
-  // ---- this CTA reduces rows [split*rows_per, +rows_per) over all slices, in slice
-  // order.  Work unit = (row r, 4 consecutive columns): one 16 B DSMEM load per
-  // slice, issued unconditionally (ranks >= splits alias this CTA, masked below).
-  const int rows_per = BM / e.splits;
-  const uint32_t part_s = smem_u32(part);
-  uint32_t peer[8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) peer[s] = map_rank(part_s, static_cast<uint32_t>(s < e.splits ? s : split));
+  // ---- reduce rows [split*rows_per, +rows_per) over the slices in slice order.
+  // Work unit = (row r, 4 consecutive columns); consecutive threads -> consecutive m.
   const int units = rows_per * (BN / 4);
 #pragma unroll 1
   for (int u = threadIdx.x; u < units; u += kThreads) {
-    const int r = split * rows_per + u % rows_per;  // consecutive threads -> consecutive m (coalesced Y)
+    const int rl = u % rows_per;
+    const int r = split * rows_per + rl;
     const int c4 = (u / rows_per) * 4;
     const int m = m0 + r;
     const bool mok = m < e.M;
-    const uint32_t off = static_cast<uint32_t>((r * C::PART_PITCH + c4) * 4);
-    float4 v[8];
-#pragma unroll
-    for (int s = 0; s < 8; ++s) v[s] = ld_cluster_v4(peer[s] + off);
     float res[4] = {0.f, 0.f, 0.f, 0.f};
     if (e.residual && mok) {
 #pragma unroll
@@ -283,11 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const float bm = (e.bias && mok) ? b2f(e.bias[m]) : 0.0f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {  // fixed slice order
-      if (s < e.splits) {
-        acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w;
-      }
+#pragma unroll 8
+    for (int s2 = 0; s2 < e.splits; ++s2) {  // fixed slice order
+      const float4 v = *reinterpret_cast<const float4*>(part + (s2 * rows_per + rl) * BN + c4);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
     const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
@@ -313,7 +325,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   DPROBE(7);
-  cluster_sync_all();  // peers may still be reading this CTA's partial
   DPROBE(8);
   if (warp == 1) {
     tc_fence_after();

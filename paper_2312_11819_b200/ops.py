@@ -124,3 +124,21 @@ def gemm_decode(W: torch.Tensor, X: torch.Tensor, *, out: torch.Tensor | None = 
     if st != 0:
         raise RuntimeError(f"rlhf_gemm_decode failed with status {st}")
     return out
+
+
+def attn_decode(qkv: torch.Tensor, kcache: torch.Tensor, vcache: torch.Tensor, pos: torch.Tensor) -> torch.Tensor:
+    """Decode attention of one new token per sample (rlhf_attn_decode).
+
+    qkv [B, 3*d] bf16 (q in columns [0, d)); kcache / vcache [B, H, Smax, hd] bf16;
+    pos int32[1] on the device: keys [0, pos] are attended.  Returns [B, d] bf16.
+    """
+    L = lib()
+    L.rlhf_attn_decode.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]
+    B, H, Smax, hd = kcache.shape
+    out = torch.empty(B, H * hd, device=qkv.device, dtype=torch.bfloat16)
+    rc = L.rlhf_attn_decode(qkv.data_ptr(), B, H, hd, Smax, kcache.data_ptr(), vcache.data_ptr(), pos.data_ptr(),
+                            out.data_ptr(), _stream())
+    if rc:
+        raise RuntimeError(f"rlhf_attn_decode failed ({rc})")
+    return out
