@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdlib>
 
 #include "launch_util.cuh"
 #include "sm100_common.cuh"
@@ -136,19 +137,21 @@ constexpr int kDecThreads = 256;
 constexpr int kDecMaxCtx = 4096;
 
 // One CTA per (sample, head).  The key and value rows [0, ctx) of the head are
-// streamed into shared memory with bulk async copies (cp.async.bulk, mbarrier
-// completion) in chunks of C positions; for ctx <= C both are in flight from the
-// first instruction, so the CTA pays one HBM latency instead of one per loop
-// trip.  Scores: LPR lanes per key row (16 B each, conflict-free rows), block
-// softmax, bf16-rounded probabilities, then P.V with a (dim chunk, key group)
-// thread split over the staged value rows.
-template <int HD>
+// streamed into shared memory with bulk async copies (cp.async.bulk, one
+// mbarrier per 64-row block) through two rings of NS blocks each: the first NS
+// key blocks and NS value blocks are in flight from the first instruction, and
+// every consumed block's slot is refilled NS blocks ahead, so the CTA never
+// waits for more than the HBM stream.  Scores: LPR lanes per key row (16 B
+// each, conflict-free rows), block softmax, bf16-rounded probabilities, then
+// P.V with a (dim chunk, key group) thread split over the staged value rows.
+template <int HD, int NS_ = (HD == 64 ? 4 : 2)>
 struct DecCfg {
-  static constexpr int C = HD == 64 ? 256 : 128;  // positions per staged chunk (K + V = 64 KB)
-  static constexpr int LPR = HD / 8;              // lanes per key row
-  static constexpr int RPW = 32 / LPR;            // key rows per warp pass
+  static constexpr int RB = 64;                     // rows per block (one bulk copy, one mbarrier)
+  static constexpr int NS = NS_;                    // ring slots per K / V (default: K + V = 64 KB)
+  static constexpr int LPR = HD / 8;                // lanes per key row
+  static constexpr int RPW = 32 / LPR;              // key rows per warp pass
   static constexpr size_t smem(int Smax) {
-    return static_cast<size_t>(2) * C * HD * 2 + static_cast<size_t>((Smax + 3) / 4 * 4) * 4 + HD * 4;
+    return static_cast<size_t>(2) * NS * RB * HD * 2 + static_cast<size_t>((Smax + 3) / 4 * 4) * 4 + HD * 4;
   }
 };
 
@@ -160,44 +163,51 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-template <int HD>
-__device__ __forceinline__ void dec_issue(uint16_t* dst, const uint16_t* src, int chunk, int ctx, uint64_t* bar) {
-  constexpr int C = DecCfg<HD>::C;
-  const int rows = min(C, ctx - chunk * C);
-  mbar_arrive_expect_tx(bar, static_cast<uint32_t>(rows * HD * 2));
-  for (int r0 = 0; r0 < rows; r0 += 64)
-    bulk_g2s(dst + r0 * HD, src + static_cast<int64_t>(chunk * C + r0) * HD, static_cast<uint32_t>(min(64, rows - r0) * HD * 2),
-             bar);
+// block blk (rows [64 blk, +64) clipped to ctx) of src -> ring slot blk % NS
+template <int HD, int NS>
+__device__ __forceinline__ void dec_issue(uint16_t* ring, const uint16_t* src, int blk, int ctx, uint64_t* bars) {
+  using Cf = DecCfg<HD, NS>;
+  const int rows = min(Cf::RB, ctx - blk * Cf::RB);
+  if (rows <= 0) return;
+  const int slot = blk % Cf::NS;
+  mbar_arrive_expect_tx(&bars[slot], static_cast<uint32_t>(rows * HD * 2));
+  bulk_g2s(ring + slot * Cf::RB * HD, src + static_cast<int64_t>(blk) * Cf::RB * HD, static_cast<uint32_t>(rows * HD * 2),
+           &bars[slot]);
 }
 
-template <int HD>
+template <int HD, int NS_>
 __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t* __restrict__ qkv, int H, int Smax,
                                                                   const uint16_t* __restrict__ kc,
                                                                   const uint16_t* __restrict__ vc,
                                                                   const int* __restrict__ pos_dev,
                                                                   uint16_t* __restrict__ out) {
-  using Cf = DecCfg<HD>;
-  constexpr int C = Cf::C, LPR = Cf::LPR, RPW = Cf::RPW, NW = kDecThreads / 32;
+  using Cf = DecCfg<HD, NS_>;
+  constexpr int RB = Cf::RB, NS = Cf::NS, LPR = Cf::LPR, RPW = Cf::RPW, NW = kDecThreads / 32;
   extern __shared__ __align__(128) uint8_t dsm[];
   uint16_t* Ks = reinterpret_cast<uint16_t*>(dsm);
-  uint16_t* Vs = Ks + C * HD;
-  float* sc = reinterpret_cast<float*>(Vs + C * HD);
+  uint16_t* Vs = Ks + NS * RB * HD;
+  float* sc = reinterpret_cast<float*>(Vs + NS * RB * HD);
   float* q = sc + (Smax + 3) / 4 * 4;
   __shared__ float red[NW];
-  __shared__ uint64_t bars[2];
+  __shared__ uint64_t kbar[NS], vbar[NS];
   pdl_entry();
   const int bh = blockIdx.x, b = bh / H, h = bh % H;
   const int d = H * HD;
   const int ctx = *pos_dev + 1;
-  const int nch = (ctx + C - 1) / C;
+  const int nblk = (ctx + RB - 1) / RB;
   const uint16_t* K = kc + static_cast<int64_t>(bh) * Smax * HD;
   const uint16_t* V = vc + static_cast<int64_t>(bh) * Smax * HD;
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kbar[i], 1);
+      mbar_init(&vbar[i], 1);
+    }
     mbar_fence_init();
-    dec_issue<HD>(Ks, K, 0, ctx, &bars[0]);
-    dec_issue<HD>(Vs, V, 0, ctx, &bars[1]);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) dec_issue<HD, NS>(Ks, K, i, ctx, kbar);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) dec_issue<HD, NS>(Vs, V, i, ctx, vbar);
   }
   const float scale = rsqrtf(static_cast<float>(HD));
   const uint16_t* qsrc = qkv + static_cast<int64_t>(b) * 3 * d + h * HD;
@@ -209,14 +219,16 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
 #pragma unroll
   for (int t = 0; t < 8; ++t) qr[t] = q[sub * 8 + t];
   float mx = -FLT_MAX;
-  for (int c = 0; c < nch; ++c) {
-    mbar_wait(&bars[0], c & 1);
-    const int rows = min(C, ctx - c * C);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int slot = blk % NS;
+    mbar_wait(&kbar[slot], (blk / NS) & 1);
+    const int rows = min(RB, ctx - blk * RB);
+    const uint16_t* Kb = Ks + slot * RB * HD;
     for (int r0 = warp * RPW; r0 < rows; r0 += NW * RPW) {  // warp-uniform trip count
       const int r = r0 + rsub;
       float s = 0.f;
       if (r < rows) {
-        const uint4 u = *reinterpret_cast<const uint4*>(Ks + r * HD + sub * 8);
+        const uint4 u = *reinterpret_cast<const uint4*>(Kb + r * HD + sub * 8);
         const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -228,15 +240,15 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
       for (int o = LPR / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (sub == 0 && r < rows) {
         s *= scale;
-        sc[c * C + r] = s;
+        sc[blk * RB + r] = s;
         mx = fmaxf(mx, s);
       }
     }
-    if (c + 1 < nch) {
-      __syncthreads();
+    if (blk + NS < nblk) {
+      __syncthreads();  // every warp is done with this slot
       if (threadIdx.x == 0) {
         fence_proxy_async_smem();
-        dec_issue<HD>(Ks, K, c + 1, ctx, &bars[0]);
+        dec_issue<HD, NS>(Ks, K, blk + NS, ctx, kbar);
       }
     }
   }
@@ -265,13 +277,16 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
   constexpr int G = kDecThreads / CH;
   const int cc = threadIdx.x % CH, grp = threadIdx.x / CH;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int c = 0; c < nch; ++c) {
-    mbar_wait(&bars[1], c & 1);
-    const int rows = min(C, ctx - c * C);
-#pragma unroll 4
-    for (int r = grp; r < rows; r += G) {
-      const float pj = bf2f_a(f2bf_a(sc[c * C + r] * inv));
-      const uint4 u = *reinterpret_cast<const uint4*>(Vs + r * HD + cc * 8);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int slot = blk % NS;
+    mbar_wait(&vbar[slot], (blk / NS) & 1);
+    const int rows = min(RB, ctx - blk * RB);
+    const uint16_t* Vb = Vs + slot * RB * HD;
+#pragma unroll
+    for (int r = grp; r < RB; r += G) {
+      if (r >= rows) break;
+      const float pj = bf2f_a(f2bf_a(sc[blk * RB + r] * inv));
+      const uint4 u = *reinterpret_cast<const uint4*>(Vb + r * HD + cc * 8);
       const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -279,15 +294,15 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
         acc[2 * t + 1] += pj * bf2f_a(static_cast<uint16_t>(w[t] >> 16));
       }
     }
-    if (c + 1 < nch) {
+    if (blk + NS < nblk) {
       __syncthreads();
       if (threadIdx.x == 0) {
         fence_proxy_async_smem();
-        dec_issue<HD>(Vs, V, c + 1, ctx, &bars[1]);
+        dec_issue<HD, NS>(Vs, V, blk + NS, ctx, vbar);
       }
     }
   }
-  float* part = reinterpret_cast<float*>(Ks);  // [G][HD] partials (key rows no longer needed)
+  float* part = reinterpret_cast<float*>(Ks);  // [G][HD] partials (key ring no longer needed)
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < 8; ++t) part[grp * HD + cc * 8 + t] = acc[t];
@@ -342,18 +357,32 @@ extern "C" int rlhf_kv_store(const void* qkv, int B, int T, int p0, const int* p
                   static_cast<uint16_t*>(vcache), rows);
 }
 
-template <int HD>
-static int launch_dec(int grid, cudaStream_t st, const uint16_t* q, int H, int Smax, const uint16_t* k, const uint16_t* v,
-                      const int* pos_dev, uint16_t* o) {
-  const size_t smem = DecCfg<HD>::smem(Smax);
-  static size_t configured = 0;  // per-HD opt-in to > 48 KB dynamic shared memory
+template <int HD, int NS>
+static int launch_dec_ns(int grid, cudaStream_t st, const uint16_t* q, int H, int Smax, const uint16_t* k,
+                         const uint16_t* v, const int* pos_dev, uint16_t* o) {
+  const size_t smem = DecCfg<HD, NS>::smem(Smax);
+  static size_t configured = 0;  // per-instantiation opt-in to > 48 KB dynamic shared memory
   if (smem > configured) {
-    if (cudaFuncSetAttribute(attn_decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(attn_decode_kernel<HD, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess)
       return 5;
     configured = smem;
   }
-  return launch_k(attn_decode_kernel<HD>, dim3(grid), dim3(kDecThreads), smem, st, q, H, Smax, k, v, pos_dev, o);
+  return launch_k(attn_decode_kernel<HD, NS>, dim3(grid), dim3(kDecThreads), smem, st, q, H, Smax, k, v, pos_dev, o);
+}
+
+template <int HD>
+static int launch_dec(int grid, cudaStream_t st, const uint16_t* q, int H, int Smax, const uint16_t* k, const uint16_t* v,
+                      const int* pos_dev, uint16_t* o) {
+  // RLHF_ATTN_NS: ring depth override (timing experiments only)
+  static const int ns = [] { const char* e = getenv("RLHF_ATTN_NS"); return e ? atoi(e) : 0; }();
+  switch (ns) {
+    case 1: return launch_dec_ns<HD, 1>(grid, st, q, H, Smax, k, v, pos_dev, o);
+    case 2: return launch_dec_ns<HD, 2>(grid, st, q, H, Smax, k, v, pos_dev, o);
+    case 4: return launch_dec_ns<HD, 4>(grid, st, q, H, Smax, k, v, pos_dev, o);
+    case 8: return launch_dec_ns<HD, 8>(grid, st, q, H, Smax, k, v, pos_dev, o);
+    default: return launch_dec_ns<HD, DecCfg<HD>::NS>(grid, st, q, H, Smax, k, v, pos_dev, o);
+  }
 }
 
 extern "C" int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax, const void* kcache, const void* vcache,
