@@ -85,6 +85,35 @@ typedef struct rlhf_gemm_decode_params {
 } rlhf_gemm_decode_params;
 int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t s);
 size_t rlhf_gemm_workspace_bytes(const rlhf_gemm_params* p);
+
+/* ---- persistent greedy decode loop (Generation stage) ----------------------
+ * Runs `steps` greedy decode steps of one decoder in ONE cooperative kernel
+ * (one CTA per SM, grid barriers between phases, weight tiles prefetched by a
+ * producer warp across phases).  Step semantics equal `steps` calls of the
+ * per-kernel decode step: embed tokens[b*tok_stride + *pos] at position *pos,
+ * L layers (K/V of *pos appended to the cache), final LN, tied LM head, greedy
+ * argmax (ties -> lowest id) written to tokens (or pred when non-NULL, inputs
+ * then keep coming from tokens: teacher forcing) at *pos + 1 with the top-2
+ * margin, *pos += 1.  Requires B <= 64, d % 64 == 0, d_ff % 64 == 0,
+ * head dim in {32, 64, 128}.  KV cache [L][kv_B][H][Smax][hd] bf16.
+ * Replaces the decode loop of the reference's Generation stage cost term
+ * (/root/reference/proj/include/rlhfsim/costmodel.hpp:63-64). */
+typedef struct rlhf_decode_loop_params {
+  const struct rlhf_arch* arch;
+  const void* weights;  /* bf16 flat parameters, rlhf_tensor_offset layout */
+  int B;
+  int32_t* tokens; int64_t tok_stride;
+  int32_t* pred;   /* NULL: free-running generation */
+  float* margin;   /* optional, same indexing as tokens */
+  int* pos;        /* device position counter */
+  int steps;
+  void* kcache; void* vcache; int kv_B; int Smax;
+  void* workspace; size_t workspace_bytes;
+  int sms;         /* CTAs (0: every SM) */
+  unsigned long long* probe; /* optional: globaltimer per (phase of step 1, CTA): [P][2][G] */
+} rlhf_decode_loop_params;
+size_t rlhf_decode_loop_workspace_bytes(const rlhf_decode_loop_params* p);
+int rlhf_decode_loop(const rlhf_decode_loop_params* p, rlhf_stream_t s);
 int rlhf_gemm_block_n(const rlhf_gemm_params* p); /* tile width the dispatcher picks */
 
 /* ---- embedding / norms (all stages) --------------------------------------

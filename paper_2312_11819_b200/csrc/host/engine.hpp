@@ -144,6 +144,7 @@ class Engine {
   // per-step buffers
   DevBuf tokens_, tok2_, pred_, margin_, pos_, prompt_stage_;
   DevBuf logp_old_, logp_ref_, values_, score_, rewards_, adv_, ret_, logp_new_, values_new_, gbuf_, loss_, out2_, score2_;
+  DevBuf loop_ws_;  // persistent decode loop workspace
   DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_hf_, dec_logits_, argmax_ws_;
   cudaGraphExec_t decode_graph_ = nullptr;
   int graph_launches_ = 0;

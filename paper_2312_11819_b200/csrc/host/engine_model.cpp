@@ -4,6 +4,8 @@
 // decode loop).  Every launch goes through the C-ABI of include/rlhf_kernels.h.
 // Rounding points follow DESIGN.md §3 and are mirrored by oracle/ppo_oracle.cpp.
 #include <algorithm>
+#include <cstdio>
+#include <vector>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -393,6 +395,68 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   K(rlhf_add_int(pos_.as<int>(), 1, stream_), 1);
   cudaEventRecord(ev_[1], stream_);  // prefill done
   if (R_ <= 1) return;
+  if (opt_.use_cuda_graph == 1) {
+    // persistent decode loop: all R-1 steps in one cooperative kernel
+    rlhf_decode_loop_params lp{};
+    lp.arch = &m.a;
+    lp.weights = m.w.p;
+    lp.B = B;
+    lp.tokens = tokens_.as<int32_t>();
+    lp.tok_stride = S_;
+    lp.pred = teacher_forced ? pred_.as<int32_t>() : nullptr;
+    lp.margin = margin_.as<float>();
+    lp.pos = pos_.as<int>();
+    lp.steps = R_ - 1;
+    lp.kcache = kv_.k.p;
+    lp.vcache = kv_.v.p;
+    lp.kv_B = kv_.B;
+    lp.Smax = kv_.Smax;
+    const size_t need = rlhf_decode_loop_workspace_bytes(&lp);
+    if (need > 0) {
+      if (loop_ws_.bytes < need) loop_ws_.alloc(need);
+      lp.workspace = loop_ws_.p;
+      lp.workspace_bytes = loop_ws_.bytes;
+      // RLHF_LOOP_PROBE=1 (debug): per-phase timestamps of decode step 1 -> stderr summary
+      static const bool probe = getenv("RLHF_LOOP_PROBE") != nullptr;
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt_.device);
+      const int P = 8 * m.a.n_layers + 2;
+      DevBuf pb;
+      if (probe && R_ > 2) {
+        pb.alloc(static_cast<size_t>(P) * 2 * sms * 8);
+        lp.probe = pb.as<unsigned long long>();
+      }
+      K(rlhf_decode_loop(&lp, stream_), 1);
+      if (lp.probe) {
+        std::vector<unsigned long long> h(static_cast<size_t>(P) * 2 * sms);
+        cudaStreamSynchronize(stream_);
+        cudaMemcpy(h.data(), pb.p, h.size() * 8, cudaMemcpyDeviceToHost);
+        auto med = [&](int row) {
+          std::vector<unsigned long long> v(h.begin() + static_cast<size_t>(row) * sms,
+                                            h.begin() + static_cast<size_t>(row + 1) * sms);
+          std::sort(v.begin(), v.end());
+          return std::make_pair(v[v.size() / 2], v.back());
+        };
+        const char* names[8] = {"qkv", "att", "wo", "resln2", "w1", "relu", "w2", "resln1"};
+        unsigned long long prev = med(2 * (P - 1) + 1).first;  // previous phase exit (approx: last of step)
+        prev = 0;
+        double tot = 0;
+        for (int q = 0; q < P; ++q) {
+          const auto work = med(2 * q), exitb = med(2 * q + 1);
+          if (q > 0) {
+            const double ph = (work.second - prev) * 1e-3, bar = (exitb.first - work.second) * 1e-3;
+            tot += (exitb.first - prev) * 1e-3;
+            if (q < 8 || q >= P - 2)
+              fprintf(stderr, "[loop probe] phase %2d %-7s work(max) %7.2f us  barrier %6.2f us\n", q,
+                      q >= P - 2 ? (q == P - 2 ? "lm" : "argmax") : names[q % 8], ph, bar);
+          }
+          prev = exitb.first;
+        }
+        fprintf(stderr, "[loop probe] step total (phases 1..%d) %.2f us\n", P - 1, tot);
+      }
+      return;
+    }
+  }
   const bool use_graph = opt_.use_cuda_graph != 0;
   if (use_graph) {
     if (!decode_graph_ || graph_for_pred_ != teacher_forced) {
@@ -403,7 +467,7 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
       const int before = launches_;
       if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         throw DeviceError("decode graph capture begin failed");
-      pdl_ = opt_.use_cuda_graph > 1 ? 0 : 1;  // programmatic dependent launches inside the graph
+      pdl_ = opt_.use_cuda_graph == 2 ? 0 : 1;  // programmatic dependent launches inside the graph
       rlhf_set_pdl(pdl_);
       decode_step(m, B);
       rlhf_set_pdl(0);

@@ -1,0 +1,847 @@
+// decode_loop.cu — the Generation stage's greedy decode loop as ONE persistent
+// kernel (all R-1 decode steps of all layers in a single launch).
+//
+// Why: at B = 32 / GPU the decode step is latency-bound.  As separate kernels
+// (even PDL-chained inside a CUDA graph) every launch pays ~5 us of fixed cost
+// (grid ramp, first HBM round trip, drain), and a step of an L-layer decoder is
+// ~7L launches.  Here one CTA per SM runs the whole loop; phases are separated
+// by a grid-wide barrier (~1 us) and, crucially, the weight stream never stops:
+// a producer warp walks this CTA's whole schedule of weight tiles ahead of the
+// math, so weight HBM traffic overlaps barriers, attention and LayerNorms.
+//
+// Warp roles (384 threads, 1 CTA / SM, cooperative launch):
+//   warp 0      weight producer: TMA of 128x64 weight tiles into a ring (prefetch
+//               runs ahead across phases / layers / steps, gated only by the ring)
+//   warp 1      TMEM owner + single-thread tcgen05.mma issuer (swap-AB: weight
+//               rows = M 128, batch = N (32 | 64), fp32 accumulators, 2 buffers)
+//   warp 2      activation producer: TMA of the (N x 64) activation tile, issued
+//               once the grid barrier that publishes the activations has passed
+//   warps 4-11  compute: GEMM epilogues (TMEM -> split-K partials / LM top-2),
+//               attention, residual + LayerNorm, FFN activation, argmax + embed
+//
+// Phases of one step (L layers), each followed by a grid barrier:
+//   per layer: QKV-GEMM | ATT | WO-GEMM | RES+LN2 | W1-GEMM | RELU | W2-GEMM | RES+LN1'
+//   then:      LM-GEMM (per-tile top-2 epilogue, logits never stored) | ARGMAX+EMBED+LN1
+// Split-K partials go to an fp32 workspace [split][b][m] and are reduced by the
+// consuming phase in fixed split order (deterministic, no atomics).
+//
+// Numerics follow the per-kernel decode path: bf16 GEMM operands,
+// fp32 accumulation, qkv / h / o / f rounded to bf16, fp32 residual stream,
+// probabilities normalised then rounded to bf16, greedy ties -> lowest token id.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstdio>
+#include <mutex>
+
+#include "rlhf_init.h"
+#include "rlhf_kernels.h"
+#include "sm100_common.cuh"
+
+namespace rlhf {
+namespace dl {
+
+constexpr int BM = 128, BK = 64;
+constexpr int kWarps = 12, kThreads = kWarps * 32;
+constexpr int kCT = 256;                 // compute threads (warps 4..11)
+constexpr int kWT = BM * BK * 2;         // weight tile bytes
+constexpr int kRB = 64;                  // KV rows per bulk block
+constexpr int kKVRing = 32768;           // bytes per K / V ring
+constexpr uint32_t kBarC = 1, kBarE = 2;  // named barriers: compute warps, epilogue warps
+
+enum { M_QKV = 0, M_WO, M_W1, M_W2, M_LM, M_XH, M_XO, M_XF, NMAP };
+struct Maps {
+  CUtensorMap m[NMAP];
+};
+
+struct Args {
+  int d, H, ff, V, L, B, S;
+  int64_t per_layer;
+  const uint16_t *tok_emb, *pos_emb, *ln1_g, *ln1_b, *bqkv, *bo, *ln2_g, *ln2_b, *b1, *b2, *lnf_g, *lnf_b;
+  int32_t* tokens;
+  int32_t* pred;
+  float* margin;
+  int* pos;
+  int steps;
+  uint16_t *kc, *vc;
+  int kvB, Smax;
+  unsigned* gbar;
+  float* x;
+  uint16_t *hbuf, *obuf, *fbuf;
+  float* part;
+  int G, ws, xs;
+  int S_[5], kbper_[5];
+  unsigned long long* probe;
+};
+
+struct Shape {
+  int M, KB, kbper, S, T, U;
+};
+
+__device__ __forceinline__ Shape shape_of(const Args& a, int j) {
+  Shape s;
+  s.M = j == M_QKV ? 3 * a.d : (j == M_W1 ? a.ff : (j == M_LM ? a.V : a.d));
+  s.KB = (j == M_W2 ? a.ff : a.d) / BK;
+  s.kbper = a.kbper_[j];
+  s.S = a.S_[j];
+  s.T = (s.M + BM - 1) / BM;
+  s.U = s.T * s.S;
+  return s;
+}
+
+// phase q of a step (P = 8L + 2 phases): GEMM map id or -1, and the layer
+__device__ __forceinline__ int gemm_of(int q, int L, int& layer) {
+  layer = 0;
+  if (q == 8 * L) return M_LM;
+  if (q > 8 * L) return -1;
+  layer = q / 8;
+  switch (q % 8) {
+    case 0: return M_QKV;
+    case 2: return M_WO;
+    case 4: return M_W1;
+    case 6: return M_W2;
+    default: return -1;
+  }
+}
+__device__ __forceinline__ int xmap_of(int j) { return j == M_WO ? M_XO : (j == M_W2 ? M_XF : M_XH); }
+
+__device__ __forceinline__ float b2f(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+__device__ __forceinline__ uint16_t f2b(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
+__device__ __forceinline__ float rbf(float f) { return b2f(f2b(f)); }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct Top2 {
+  float v1;
+  int i1;
+  float v2;
+};
+__device__ __forceinline__ Top2 top2_merge(Top2 a, Top2 b) {
+  Top2 r;
+  if (b.v1 > a.v1 || (b.v1 == a.v1 && b.i1 < a.i1)) {
+    r.v1 = b.v1; r.i1 = b.i1; r.v2 = fmaxf(a.v1, b.v2);
+  } else {
+    r.v1 = a.v1; r.i1 = a.i1; r.v2 = fmaxf(a.v2, b.v1);
+  }
+  return r;
+}
+__device__ __forceinline__ Top2 top2_warp(Top2 t) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Top2 u{__shfl_xor_sync(0xffffffffu, t.v1, o), __shfl_xor_sync(0xffffffffu, t.i1, o),
+           __shfl_xor_sync(0xffffffffu, t.v2, o)};
+    t = top2_merge(t, u);
+  }
+  return t;
+}
+
+// block-wide (compute warps) sum; red = 8 floats of smem
+__device__ __forceinline__ float csum(float v, float* red, int cw, int lane) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[cw] = v;
+  named_bar_sync(kBarC, kCT);
+  float s = 0.f;
+#pragma unroll
+  for (int w = 0; w < kCT / 32; ++w) s += red[w];
+  named_bar_sync(kBarC, kCT);
+  return s;
+}
+__device__ __forceinline__ float cmax(float v, float* red, int cw, int lane) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) red[cw] = v;
+  named_bar_sync(kBarC, kCT);
+  float s = red[0];
+#pragma unroll
+  for (int w = 1; w < kCT / 32; ++w) s = fmaxf(s, red[w]);
+  named_bar_sync(kBarC, kCT);
+  return s;
+}
+
+// residual row b of width d: x += bias + sum_s part[s][b][:]; y = bf16(LN(x) * g + beta)
+template <int MAXV>
+__device__ __forceinline__ void res_ln_row(const Args& a, int b, int S, const uint16_t* bias, const uint16_t* g,
+                                           const uint16_t* beta, float* red, int ctid, int cw, int lane, bool add) {
+  const int d = a.d;
+  float xv[MAXV];
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const int c = ctid + k * kCT;
+    xv[k] = 0.f;
+    if (c < d) {
+      float xn = __ldcg(a.x + static_cast<int64_t>(b) * d + c);
+      if (add) {
+        float s = 0.f;
+        for (int sp = 0; sp < S; ++sp) s += __ldcg(a.part + (static_cast<int64_t>(sp) * a.B + b) * d + c);
+        xn = (s + b2f(bias[c])) + xn;
+        a.x[static_cast<int64_t>(b) * d + c] = xn;
+      }
+      xv[k] = xn;
+      sum += xn;
+    }
+  }
+  const float mu = csum(sum, red, cw, lane) / d;
+  float vs = 0.f;
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k)
+    if (ctid + k * kCT < d) vs += (xv[k] - mu) * (xv[k] - mu);
+  const float rs = 1.0f / sqrtf(csum(vs, red, cw, lane) / d + 1e-5f);
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const int c = ctid + k * kCT;
+    if (c < d) a.hbuf[static_cast<int64_t>(b) * d + c] = f2b((xv[k] - mu) * rs * b2f(g[c]) + b2f(beta[c]));
+  }
+}
+
+template <int BN, int HD>
+__global__ void __launch_bounds__(kThreads, 1)
+    decode_loop_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args a) {
+  constexpr int XT = BN * BK * 2;  // activation tile bytes
+  constexpr int NEPI = BN / 32 * 4;  // epilogue warps
+  constexpr int NSK = kKVRing / (kRB * HD * 2);
+  constexpr int LPR = HD / 8, RPW = 32 / LPR;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* wring = smem;
+  uint8_t* xring = wring + a.ws * kWT;
+  uint16_t* kring = reinterpret_cast<uint16_t*>(xring + a.xs * XT);
+  uint16_t* vring = kring + kKVRing / 2;
+  float* sc = reinterpret_cast<float*>(vring + kKVRing / 2);
+  float* qn = sc + ((a.Smax + 3) & ~3);  // [3][HD]
+  float* red = qn + 3 * HD;              // 8
+  Top2* t2s = reinterpret_cast<Top2*>(red + 8);  // [8][32]
+  int* itok = reinterpret_cast<int*>(t2s + 8 * 32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(itok + 4 + 7) & ~uintptr_t(7));
+  uint64_t* w_full = bars;
+  uint64_t* w_empty = w_full + a.ws;
+  uint64_t* x_full = w_empty + a.ws;
+  uint64_t* x_empty = x_full + a.xs;
+  uint64_t* acc_full = x_empty + a.xs;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* kbar = acc_empty + 2;
+  uint64_t* vbar = kbar + NSK;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vbar + NSK);
+
+  const int warp = static_cast<int>(warp_id()), lane = static_cast<int>(lane_id());
+  const int cta = blockIdx.x, G = a.G, L = a.L;
+  const int P = 8 * L + 2;
+  const int nphase = 1 + a.steps * P;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.ws; ++i) {
+      mbar_init(&w_full[i], 1);
+      mbar_init(&w_empty[i], 1);
+    }
+    for (int i = 0; i < a.xs; ++i) {
+      mbar_init(&x_full[i], 1);
+      mbar_init(&x_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], NEPI);
+    }
+    for (int i = 0; i < NSK; ++i) {
+      mbar_init(&kbar[i], 1);
+      mbar_init(&vbar[i], 1);
+    }
+    mbar_fence_init();
+    for (int i = 0; i < NMAP; ++i) tma_prefetch(&maps.m[i]);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- weight producer ----------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int gq = 1; gq < nphase; ++gq) {
+        int layer;
+        const int j = gemm_of((gq - 1) % P, L, layer);
+        if (j < 0) continue;
+        const Shape sh = shape_of(a, j);
+        for (int u = cta; u < sh.U; u += G) {
+          const int tile = u / sh.S, split = u % sh.S;
+          const int kb0 = split * sh.kbper, kb1 = min(sh.KB, kb0 + sh.kbper);
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const int st = static_cast<int>(it % a.ws);
+            if (it >= static_cast<uint32_t>(a.ws)) mbar_wait(&w_empty[st], ((it / a.ws) - 1) & 1);
+            mbar_arrive_expect_tx(&w_full[st], kWT);
+            tma_load_4d(wring + st * kWT, &maps.m[j], &w_full[st], kb * BK, 0, tile * BM, layer);
+          }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ---------------- activation producer ----------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int gq = 1; gq < nphase; ++gq) {
+        int layer;
+        const int j = gemm_of((gq - 1) % P, L, layer);
+        if (j < 0) continue;
+        const Shape sh = shape_of(a, j);
+        if (cta >= sh.U) continue;
+        // activations of phase gq are published by grid barrier gq-1
+        while (ld_acquire(a.gbar) < static_cast<unsigned>(gq) * G) {
+        }
+        fence_proxy_async();
+        const CUtensorMap* xm = &maps.m[xmap_of(j)];
+        for (int u = cta; u < sh.U; u += G) {
+          const int split = u % sh.S;
+          const int kb0 = split * sh.kbper, kb1 = min(sh.KB, kb0 + sh.kbper);
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const int st = static_cast<int>(it % a.xs);
+            if (it >= static_cast<uint32_t>(a.xs)) mbar_wait(&x_empty[st], ((it / a.xs) - 1) & 1);
+            mbar_arrive_expect_tx(&x_full[st], XT);
+            tma_load_4d(xring + st * XT, xm, &x_full[st], kb * BK, 0, 0, 0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(BM, BN, 0, 0);
+      uint32_t wit = 0, xit = 0, ucount = 0;
+      for (int gq = 1; gq < nphase; ++gq) {
+        int layer;
+        const int j = gemm_of((gq - 1) % P, L, layer);
+        if (j < 0) continue;
+        const Shape sh = shape_of(a, j);
+        for (int u = cta; u < sh.U; u += G, ++ucount) {
+          const int split = u % sh.S;
+          const int kb0 = split * sh.kbper, kb1 = min(sh.KB, kb0 + sh.kbper);
+          const uint32_t ab = ucount & 1;
+          if (ucount >= 2) mbar_wait(&acc_empty[ab], ((ucount >> 1) - 1) & 1);
+          tc_fence_after();
+          for (int kb = kb0; kb < kb1; ++kb, ++wit, ++xit) {
+            const int ws = static_cast<int>(wit % a.ws), xs = static_cast<int>(xit % a.xs);
+            mbar_wait(&w_full[ws], (wit / a.ws) & 1);
+            mbar_wait(&x_full[xs], (xit / a.xs) & 1);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(wring + ws * kWT), sb = smem_u32(xring + xs * XT);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16(tmem + ab * BN, umma_desc_sw128(sa + k * 32, 16, 1024), umma_desc_sw128(sb + k * 32, 16, 1024),
+                        idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            umma_commit(&w_empty[ws]);
+            umma_commit(&x_empty[xs]);
+          }
+          umma_commit(&acc_full[ab]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- compute warps ----------------
+    const int ctid = static_cast<int>(threadIdx.x) - 128, cw = warp - 4;
+    const int d = a.d, H = a.H, B = a.B;
+    const float scale = rsqrtf(static_cast<float>(HD));
+    int pos = *a.pos;
+    uint32_t ucount = 0, kblk = 0, vblk = 0;
+    for (int gq = 0; gq < nphase; ++gq) {
+      const int q = gq == 0 ? P - 1 : (gq - 1) % P;
+      const int step = gq == 0 ? -1 : (gq - 1) / P;
+      int layer = 0;
+      const int j = gq == 0 ? -1 : gemm_of(q, L, layer);
+      if (j >= 0) {
+        // ======== GEMM epilogue ========
+        const Shape sh = shape_of(a, j);
+        for (int u = cta; u < sh.U; u += G, ++ucount) {
+          const int tile = u / sh.S, split = u % sh.S;
+          const uint32_t ab = ucount & 1;
+          if (cw < NEPI) {  // only the epilogue warps track the accumulator barriers
+            mbar_wait(&acc_full[ab], (ucount >> 1) & 1);
+            tc_fence_after();
+            const int quarter = warp & 3, colbase = (cw / 4) * 32;
+            float v[32];
+            tmem_ld32(tmem + ab * BN + colbase + (static_cast<uint32_t>(quarter * 32) << 16), v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            const int m = tile * BM + quarter * 32 + lane;
+            if (j != M_LM) {
+              if (m < sh.M) {
+                float* dst = a.part + static_cast<int64_t>(split) * B * sh.M + m;
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                  if (colbase + c < B) __stcg(dst + static_cast<int64_t>(colbase + c) * sh.M, v[c]);
+              }
+            } else {
+              Top2 keep{-FLT_MAX, 0x7fffffff, -FLT_MAX};
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                Top2 t{m < sh.M ? v[c] : -FLT_MAX, m < sh.M ? m : 0x7fffffff, -FLT_MAX};
+                t = top2_warp(t);
+                if (lane == c) keep = t;
+              }
+              t2s[cw * 32 + lane] = keep;
+              named_bar_sync(kBarE, NEPI * 32);
+              if (ctid < BN && ctid < B) {
+                const int grp = ctid / 32, cl = ctid % 32;
+                Top2 t = t2s[(grp * 4) * 32 + cl];
+#pragma unroll
+                for (int qq = 1; qq < 4; ++qq) t = top2_merge(t, t2s[(grp * 4 + qq) * 32 + cl]);
+                float* o = a.part + (static_cast<int64_t>(tile) * B + ctid) * 4;
+                __stcg(o, t.v1);
+                __stcg(o + 1, __int_as_float(t.i1));
+                __stcg(o + 2, t.v2);
+              }
+              named_bar_sync(kBarE, NEPI * 32);
+            }
+          }
+        }
+      } else if (gq > 0 && q < 8 * L && q % 8 == 1) {
+        // ======== attention: one (b, h) per unit ========
+        const uint16_t* bq = a.bqkv + layer * a.per_layer;
+        const int S = a.S_[M_QKV];
+        for (int u = cta; u < B * H; u += G) {
+          const int b = u / H, h = u % H;
+          const int64_t head = ((static_cast<int64_t>(layer) * a.kvB + b) * H + h) * a.Smax * HD;
+          const uint16_t* Kg = a.kc + head;
+          const uint16_t* Vg = a.vc + head;
+          const int nold = pos, nblk = (nold + kRB - 1) / kRB;
+          if (ctid == 0) {
+            fence_proxy_async();
+            for (int i = 0; i < NSK && i < nblk; ++i) {
+              const int rows = min(kRB, nold - i * kRB);
+              const uint32_t sk = (kblk + i) % NSK, sv = (vblk + i) % NSK;
+              mbar_arrive_expect_tx(&kbar[sk], rows * HD * 2);
+              bulk_g2s(kring + sk * kRB * HD, Kg + static_cast<int64_t>(i) * kRB * HD, rows * HD * 2, &kbar[sk]);
+              mbar_arrive_expect_tx(&vbar[sv], rows * HD * 2);
+              bulk_g2s(vring + sv * kRB * HD, Vg + static_cast<int64_t>(i) * kRB * HD, rows * HD * 2, &vbar[sv]);
+            }
+          }
+          // q | k | v of this head: reduce the split-K partials, + bias, round to bf16
+          for (int i = ctid; i < 3 * HD; i += kCT) {
+            const int sec = i / HD, e = i % HD;
+            const int col = sec * d + h * HD + e;
+            float s = 0.f;
+            for (int sp = 0; sp < S; ++sp) s += __ldcg(a.part + (static_cast<int64_t>(sp) * B + b) * 3 * d + col);
+            const uint16_t hb = f2b(s + b2f(bq[col]));
+            qn[i] = b2f(hb);
+            if (sec == 1) a.kc[head + static_cast<int64_t>(pos) * HD + e] = hb;
+            if (sec == 2) a.vc[head + static_cast<int64_t>(pos) * HD + e] = hb;
+          }
+          named_bar_sync(kBarC, kCT);
+          // scores of the cached keys (ring) and of the new key
+          const int sub = lane % LPR, rsub = lane / LPR;
+          float qr[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) qr[t] = qn[sub * 8 + t];
+          float mx = -FLT_MAX;
+          for (int i = 0; i < nblk; ++i) {
+            const uint32_t gi = kblk + i, slot = gi % NSK;
+            mbar_wait(&kbar[slot], (gi / NSK) & 1);
+            const int rows = min(kRB, nold - i * kRB);
+            const uint16_t* Kb = kring + slot * kRB * HD;
+            for (int r0 = cw * RPW; r0 < rows; r0 += (kCT / 32) * RPW) {
+              const int r = r0 + rsub;
+              float s = 0.f;
+              if (r < rows) {
+                const uint4 w4 = *reinterpret_cast<const uint4*>(Kb + r * HD + sub * 8);
+                const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  s += qr[2 * t] * b2f(static_cast<uint16_t>(w[t] & 0xFFFFu));
+                  s += qr[2 * t + 1] * b2f(static_cast<uint16_t>(w[t] >> 16));
+                }
+              }
+#pragma unroll
+              for (int o = LPR / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+              if (sub == 0 && r < rows) {
+                s *= scale;
+                sc[i * kRB + r] = s;
+                mx = fmaxf(mx, s);
+              }
+            }
+            if (i + NSK < nblk) {
+              named_bar_sync(kBarC, kCT);
+              if (ctid == 0) {
+                fence_proxy_async();
+                const int rows2 = min(kRB, nold - (i + NSK) * kRB);
+                mbar_arrive_expect_tx(&kbar[slot], rows2 * HD * 2);
+                bulk_g2s(kring + slot * kRB * HD, Kg + static_cast<int64_t>(i + NSK) * kRB * HD, rows2 * HD * 2,
+                         &kbar[slot]);
+              }
+            }
+          }
+          if (cw == 0) {  // the new key (position pos)
+            float s = 0.f;
+            for (int e = lane; e < HD; e += 32) s += qn[e] * qn[HD + e];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            s *= scale;
+            if (lane == 0) sc[nold] = s;
+            mx = fmaxf(mx, s);
+          }
+          mx = cmax(mx, red, cw, lane);
+          float sum = 0.f;
+          for (int jj = ctid; jj <= nold; jj += kCT) {
+            const float e = expf(sc[jj] - mx);
+            sc[jj] = e;
+            sum += e;
+          }
+          sum = csum(sum, red, cw, lane);
+          const float inv = 1.0f / sum;
+          constexpr int CH = HD / 8, GR = kCT / CH;
+          const int cc = ctid % CH, grp = ctid / CH;
+          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          for (int i = 0; i < nblk; ++i) {
+            const uint32_t gi = vblk + i, slot = gi % NSK;
+            mbar_wait(&vbar[slot], (gi / NSK) & 1);
+            const int rows = min(kRB, nold - i * kRB);
+            const uint16_t* Vb = vring + slot * kRB * HD;
+#pragma unroll
+            for (int r = grp; r < kRB; r += GR) {
+              if (r >= rows) break;
+              const float pj = rbf(sc[i * kRB + r] * inv);
+              const uint4 w4 = *reinterpret_cast<const uint4*>(Vb + r * HD + cc * 8);
+              const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                acc[2 * t] += pj * b2f(static_cast<uint16_t>(w[t] & 0xFFFFu));
+                acc[2 * t + 1] += pj * b2f(static_cast<uint16_t>(w[t] >> 16));
+              }
+            }
+            if (i + NSK < nblk) {
+              named_bar_sync(kBarC, kCT);
+              if (ctid == 0) {
+                fence_proxy_async();
+                const int rows2 = min(kRB, nold - (i + NSK) * kRB);
+                mbar_arrive_expect_tx(&vbar[slot], rows2 * HD * 2);
+                bulk_g2s(vring + slot * kRB * HD, Vg + static_cast<int64_t>(i + NSK) * kRB * HD, rows2 * HD * 2,
+                         &vbar[slot]);
+              }
+            }
+          }
+          if (grp == 0) {  // the new value row
+            const float pj = rbf(sc[nold] * inv);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] += pj * qn[2 * HD + cc * 8 + t];
+          }
+          named_bar_sync(kBarC, kCT);  // K ring free: reuse as [GR][HD] partials
+          float* pacc = reinterpret_cast<float*>(kring);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) pacc[grp * HD + cc * 8 + t] = acc[t];
+          named_bar_sync(kBarC, kCT);
+          for (int e = ctid; e < HD; e += kCT) {
+            float o = 0.f;
+            for (int g2 = 0; g2 < GR; ++g2) o += pacc[g2 * HD + e];
+            a.obuf[static_cast<int64_t>(b) * d + h * HD + e] = f2b(o);
+          }
+          kblk += nblk;
+          vblk += nblk;
+          named_bar_sync(kBarC, kCT);
+        }
+      } else if (gq > 0 && q < 8 * L && (q % 8 == 3 || q % 8 == 7)) {
+        // ======== residual + LayerNorm (one CTA per sample row) ========
+        const bool after_wo = q % 8 == 3;
+        const int64_t lo = layer * a.per_layer;
+        const uint16_t* bias = after_wo ? a.bo + lo : a.b2 + lo;
+        const uint16_t *g, *beta;
+        if (after_wo) {
+          g = a.ln2_g + lo;
+          beta = a.ln2_b + lo;
+        } else if (layer + 1 < L) {
+          g = a.ln1_g + lo + a.per_layer;
+          beta = a.ln1_b + lo + a.per_layer;
+        } else {
+          g = a.lnf_g;
+          beta = a.lnf_b;
+        }
+        const int S = a.S_[after_wo ? M_WO : M_W2];
+        for (int b = cta; b < B; b += G) {
+          if (d <= 1024) res_ln_row<4>(a, b, S, bias, g, beta, red, ctid, cw, lane, true);
+          else res_ln_row<16>(a, b, S, bias, g, beta, red, ctid, cw, lane, true);
+        }
+      } else if (gq > 0 && q < 8 * L && q % 8 == 5) {
+        // ======== FFN activation: f = bf16(relu(sum_s part + b1)) ========
+        const uint16_t* b1 = a.b1 + layer * a.per_layer;
+        const int S = a.S_[M_W1], ff = a.ff;
+        const int64_t n = static_cast<int64_t>(B) * ff;
+        for (int64_t i = static_cast<int64_t>(cta) * kCT + ctid; i < n; i += static_cast<int64_t>(G) * kCT) {
+          const int b = static_cast<int>(i / ff), m = static_cast<int>(i % ff);
+          float s = 0.f;
+          for (int sp = 0; sp < S; ++sp) s += __ldcg(a.part + (static_cast<int64_t>(sp) * B + b) * ff + m);
+          a.fbuf[static_cast<int64_t>(b) * ff + m] = f2b(fmaxf(s + b2f(b1[m]), 0.0f));
+        }
+      } else {
+        // ======== greedy argmax of the previous step + embedding + LN1 of layer 0 ========
+        const bool has_prev = gq > 0, has_next = step + 1 < a.steps;
+        for (int b = cta; b < B; b += G) {
+          if (has_prev) {
+            if (cw == 0) {
+              Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
+              const int T = (a.V + BM - 1) / BM;
+              for (int tl = lane; tl < T; tl += 32) {
+                const float* o = a.part + (static_cast<int64_t>(tl) * B + b) * 4;
+                t = top2_merge(t, Top2{__ldcg(o), __float_as_int(__ldcg(o + 1)), __ldcg(o + 2)});
+              }
+              t = top2_warp(t);
+              if (lane == 0) {
+                const int64_t at = static_cast<int64_t>(b) * a.S + pos + 1;
+                (a.pred ? a.pred : a.tokens)[at] = t.i1;
+                if (a.margin) a.margin[at] = t.v1 - t.v2;
+                itok[0] = a.pred ? a.tokens[at] : t.i1;
+              }
+            }
+            named_bar_sync(kBarC, kCT);
+          } else if (ctid == 0) {
+            itok[0] = a.tokens[static_cast<int64_t>(b) * a.S + pos];
+          }
+          if (!has_next) continue;
+          named_bar_sync(kBarC, kCT);
+          const int tok = itok[0];
+          const int p = has_prev ? pos + 1 : pos;
+          for (int c = ctid; c < d; c += kCT)
+            a.x[static_cast<int64_t>(b) * d + c] =
+                b2f(a.tok_emb[static_cast<int64_t>(tok) * d + c]) + b2f(a.pos_emb[static_cast<int64_t>(p) * d + c]);
+          named_bar_sync(kBarC, kCT);
+          if (d <= 1024) res_ln_row<4>(a, b, 0, nullptr, a.ln1_g, a.ln1_b, red, ctid, cw, lane, false);
+          else res_ln_row<16>(a, b, 0, nullptr, a.ln1_g, a.ln1_b, red, ctid, cw, lane, false);
+          named_bar_sync(kBarC, kCT);
+        }
+        if (has_prev) ++pos;
+      }
+      // ======== grid barrier: publish this phase ========
+      if (a.probe && ctid == 0 && step == 1) a.probe[(static_cast<int64_t>(q) * 2) * G + cta] = gtime();
+      fence_proxy_async();
+      named_bar_sync(kBarC, kCT);
+      if (ctid == 0) {
+        __threadfence();
+        atomicAdd(a.gbar, 1u);
+        const unsigned target = static_cast<unsigned>(gq + 1) * G;
+        while (ld_acquire(a.gbar) < target) {
+        }
+        __threadfence();
+      }
+      named_bar_sync(kBarC, kCT);
+      if (a.probe && ctid == 0 && step == 1) a.probe[(static_cast<int64_t>(q) * 2 + 1) * G + cta] = gtime();
+    }
+    if (cta == 0 && ctid == 0) *a.pos = pos;
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 2 * BN);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 4-D view (K, 1, rows, layers) of a K-contiguous bf16 matrix stack; box (64, 1, box_rows, 1)
+int map4(CUtensorMap* m, const void* ptr, int64_t K, int64_t rows, int64_t layers, int64_t layer_stride, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(ptr) & 15) || (K * 2) % 16 || (layer_stride * 2) % 16) return 2;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(K), 1, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(layers)};
+  if (layers <= 1) layer_stride = K * rows;
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(K * 2), static_cast<cuuint64_t>(K * 2),
+                           static_cast<cuuint64_t>(layer_stride * 2)};
+  cuuint32_t box[4] = {64u, 1u, static_cast<cuuint32_t>(box_rows), 1u};
+  cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? 0
+             : 5;
+}
+
+struct Plan {
+  int BN, G, S_[5], kbper_[5], ws, xs;
+  size_t smem, off_x, off_h, off_o, off_f, off_part, total;
+};
+
+static size_t al(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
+
+int plan(const rlhf_decode_loop_params* p, Plan* out) {
+  const rlhf_arch& A = *p->arch;
+  const int d = A.d_model, ff = A.d_ff, V = A.vocab, H = A.n_heads;
+  if (!p->arch || p->B < 1 || p->B > 64 || d % 64 || ff % 64 || H < 1 || d % H) return 2;
+  const int hd = d / H;
+  if (hd != 32 && hd != 64 && hd != 128) return 2;
+  if (d > 4096 || p->Smax < 1) return 2;
+  Plan pl{};
+  pl.BN = p->B <= 32 ? 32 : 64;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  pl.G = p->sms > 0 ? std::min(p->sms, sms) : sms;
+  const int Ms[5] = {3 * d, d, ff, d, V};
+  const int KBs[5] = {d / 64, d / 64, d / 64, ff / 64, d / 64};
+  size_t part = 0;
+  for (int j = 0; j < 5; ++j) {
+    const int T = (Ms[j] + 127) / 128;
+    int kbper = std::max(1, (T * KBs[j] + pl.G - 1) / pl.G);
+    if (j == 4 || kbper > KBs[j]) kbper = KBs[j];
+    pl.kbper_[j] = kbper;
+    pl.S_[j] = (KBs[j] + kbper - 1) / kbper;
+    part = std::max(part, static_cast<size_t>(j == 4 ? 4 : pl.S_[j]) * p->B * (j == 4 ? T : Ms[j]) * 4);
+  }
+  const int XT = pl.BN * 64 * 2;
+  const size_t fixed = 2 * static_cast<size_t>(kKVRing) + ((p->Smax + 3) & ~3) * 4 + 3 * hd * 4 + 32 + 8 * 32 * 12 + 32 +
+                       8 * 64 + 1024 + 256;
+  pl.xs = pl.BN == 32 ? 8 : 4;
+  const size_t budget = 232448 - fixed - static_cast<size_t>(pl.xs) * XT;
+  pl.ws = static_cast<int>(std::min<size_t>(8, budget / kWT));
+  if (pl.ws < 3) return 2;
+  pl.smem = fixed + static_cast<size_t>(pl.xs) * XT + static_cast<size_t>(pl.ws) * kWT;
+  size_t o = 256;  // grid barrier counter
+  pl.off_x = o;
+  o = al(o + static_cast<size_t>(p->B) * d * 4);
+  pl.off_h = o;
+  o = al(o + static_cast<size_t>(pl.BN) * d * 2);
+  pl.off_o = o;
+  o = al(o + static_cast<size_t>(pl.BN) * d * 2);
+  pl.off_f = o;
+  o = al(o + static_cast<size_t>(pl.BN) * ff * 2);
+  pl.off_part = o;
+  o = al(o + part);
+  pl.total = o;
+  *out = pl;
+  return 0;
+}
+
+template <int BN, int HD>
+int launch(const Maps& maps, const Args& a, size_t smem, cudaStream_t s) {
+  static int configured = 0;
+  if (static_cast<int>(smem) > configured) {
+    if (cudaFuncSetAttribute(decode_loop_kernel<BN, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess)
+      return 5;
+    configured = static_cast<int>(smem);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barriers)
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_loop_kernel<BN, HD>, maps, a) == cudaSuccess ? 0 : 5;
+}
+
+}  // namespace dl
+}  // namespace rlhf
+
+using namespace rlhf;
+
+extern "C" size_t rlhf_decode_loop_workspace_bytes(const rlhf_decode_loop_params* p) {
+  dl::Plan pl;
+  return dl::plan(p, &pl) ? 0 : pl.total;
+}
+
+extern "C" int rlhf_decode_loop(const rlhf_decode_loop_params* p, rlhf_stream_t stream) {
+  dl::Plan pl;
+  if (!p || dl::plan(p, &pl)) return 2;
+  if (p->steps < 1) return 0;
+  if (!p->workspace || p->workspace_bytes < pl.total) return 2;
+  const rlhf_arch& A = *p->arch;
+  const int d = A.d_model, ff = A.d_ff, hd = d / A.n_heads, L = A.n_layers;
+  const auto* w = static_cast<const uint16_t*>(p->weights);
+  const int64_t per_layer = rlhf_tensor_offset(&A, RLHF_T_LN1_G, 1) - rlhf_tensor_offset(&A, RLHF_T_LN1_G, 0);
+  auto T = [&](int t) { return w + rlhf_tensor_offset(&A, t, 0); };
+  uint8_t* ws = static_cast<uint8_t*>(p->workspace);
+  dl::Args a{};
+  a.d = d;
+  a.H = A.n_heads;
+  a.ff = ff;
+  a.V = A.vocab;
+  a.L = L;
+  a.B = p->B;
+  a.S = p->tok_stride;
+  a.per_layer = L > 1 ? per_layer : 0;
+  a.tok_emb = T(RLHF_T_TOK_EMB);
+  a.pos_emb = T(RLHF_T_POS_EMB);
+  a.ln1_g = T(RLHF_T_LN1_G);
+  a.ln1_b = T(RLHF_T_LN1_B);
+  a.bqkv = T(RLHF_T_BQKV);
+  a.bo = T(RLHF_T_BO);
+  a.ln2_g = T(RLHF_T_LN2_G);
+  a.ln2_b = T(RLHF_T_LN2_B);
+  a.b1 = T(RLHF_T_B1);
+  a.b2 = T(RLHF_T_B2);
+  a.lnf_g = T(RLHF_T_LNF_G);
+  a.lnf_b = T(RLHF_T_LNF_B);
+  a.tokens = p->tokens;
+  a.pred = p->pred;
+  a.margin = p->margin;
+  a.pos = p->pos;
+  a.steps = p->steps;
+  a.kc = static_cast<uint16_t*>(p->kcache);
+  a.vc = static_cast<uint16_t*>(p->vcache);
+  a.kvB = p->kv_B;
+  a.Smax = p->Smax;
+  a.gbar = reinterpret_cast<unsigned*>(ws);
+  a.x = reinterpret_cast<float*>(ws + pl.off_x);
+  a.hbuf = reinterpret_cast<uint16_t*>(ws + pl.off_h);
+  a.obuf = reinterpret_cast<uint16_t*>(ws + pl.off_o);
+  a.fbuf = reinterpret_cast<uint16_t*>(ws + pl.off_f);
+  a.part = reinterpret_cast<float*>(ws + pl.off_part);
+  a.G = pl.G;
+  a.ws = pl.ws;
+  a.xs = pl.xs;
+  for (int j = 0; j < 5; ++j) {
+    a.S_[j] = pl.S_[j];
+    a.kbper_[j] = pl.kbper_[j];
+  }
+  a.probe = p->probe;
+  const int64_t Lst = L > 1 ? per_layer : 0;
+  dl::Maps maps;
+  int rc = 0;
+  rc |= dl::map4(&maps.m[dl::M_QKV], T(RLHF_T_WQKV), d, 3 * d, L, Lst, dl::BM);
+  rc |= dl::map4(&maps.m[dl::M_WO], T(RLHF_T_WO), d, d, L, Lst, dl::BM);
+  rc |= dl::map4(&maps.m[dl::M_W1], T(RLHF_T_W1), d, ff, L, Lst, dl::BM);
+  rc |= dl::map4(&maps.m[dl::M_W2], T(RLHF_T_W2), ff, d, L, Lst, dl::BM);
+  rc |= dl::map4(&maps.m[dl::M_LM], T(RLHF_T_TOK_EMB), d, A.vocab, 1, 0, dl::BM);
+  rc |= dl::map4(&maps.m[dl::M_XH], a.hbuf, d, pl.BN, 1, 0, pl.BN);
+  rc |= dl::map4(&maps.m[dl::M_XO], a.obuf, d, pl.BN, 1, 0, pl.BN);
+  rc |= dl::map4(&maps.m[dl::M_XF], a.fbuf, ff, pl.BN, 1, 0, pl.BN);
+  if (rc) return 2;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // barrier counter + zero activation rows >= B (MMA N padding)
+  if (cudaMemsetAsync(ws, 0, pl.off_part, s) != cudaSuccess) return 5;
+  if (pl.BN == 32) {
+    if (hd == 32) return dl::launch<32, 32>(maps, a, pl.smem, s);
+    if (hd == 64) return dl::launch<32, 64>(maps, a, pl.smem, s);
+    return dl::launch<32, 128>(maps, a, pl.smem, s);
+  }
+  if (hd == 32) return dl::launch<64, 32>(maps, a, pl.smem, s);
+  if (hd == 64) return dl::launch<64, 64>(maps, a, pl.smem, s);
+  return dl::launch<64, 128>(maps, a, pl.smem, s);
+}
