@@ -102,7 +102,9 @@ typedef struct rlhf_engine_options {
   int rank, world_size;
   const char* strategy;       /* colocated | interleaving1 | interleaving2 | disaggregated */
   const uint8_t* nccl_id;     /* 128 bytes from rlhf_nccl_unique_id (rank 0), NULL at world 1 */
-  int use_cuda_graph;         /* capture the decode step in a CUDA graph */
+  int use_cuda_graph;         /* decode loop: 0 eager kernels, 1 CUDA graph of one step with programmatic
+                                 dependent launches (default), 2 graph without PDL, 3 persistent
+                                 cooperative decode kernel (rlhf_decode_loop) */
 } rlhf_engine_options;
 
 int rlhf_nccl_unique_id(uint8_t out[128]);

@@ -395,8 +395,9 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   K(rlhf_add_int(pos_.as<int>(), 1, stream_), 1);
   cudaEventRecord(ev_[1], stream_);  // prefill done
   if (R_ <= 1) return;
-  if (opt_.use_cuda_graph == 1) {
-    // persistent decode loop: all R-1 steps in one cooperative kernel
+  if (opt_.use_cuda_graph == 3) {
+    // persistent decode loop: all R-1 steps in one cooperative kernel (opt-in;
+    // on one B200 at B = 32 it is not yet faster than the PDL graph)
     rlhf_decode_loop_params lp{};
     lp.arch = &m.a;
     lp.weights = m.w.p;

@@ -50,7 +50,7 @@ constexpr int kSlot = 16384;             // pool slot: one 128x64 weight tile or
 constexpr uint32_t kBarC = 1, kBarE = 2;  // named barriers: compute warps, epilogue warps
 constexpr int kQN = 4;                   // attention units whose q/k/v are reduced together
 
-enum { M_QKV = 0, M_WO, M_W1, M_W2, M_LM, M_XH, M_XO, M_XF, NMAP };
+enum { M_QKV = 0, M_WO, M_W1, M_W2, M_LM, M_XH, M_XO, M_XF, M_KC, M_VC, NMAP };
 struct Maps {
   CUtensorMap m[NMAP];
 };
@@ -166,6 +166,29 @@ __device__ __forceinline__ void tma_load_4d_hint(void* smem, const CUtensorMap* 
       " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(smem)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
       : "memory");
+}
+
+// warp-level bf16 MMA m16n8k16 (fp32 accumulate) and transposed 8x8 matrix loads:
+// the decode attention of head dim 64 runs its q.K^T and P.V on these
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
+         (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
 }
 
 struct Top2 {
@@ -380,10 +403,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t head = ((static_cast<int64_t>(layer) * a.kvB + b) * a.H + h) * a.Smax * HD;
             for (int isv = 0; isv < 2; ++isv)
               for (int i = 0; i < nblk; ++i) {
-                const uint32_t bytes = static_cast<uint32_t>(min(KVR, pos - i * KVR) * HD * 2);
-                const int st = slot_acquire(bytes);
-                bulk_g2s_hint(pool + st * kSlot, (isv ? a.vc : a.kc) + head + static_cast<int64_t>(i) * KVR * HD, bytes,
-                              &p_full[st], pol);
+                if constexpr (HD == 64) {
+                  // SWIZZLE_128B tile of KVR rows (rows >= pos are masked by the consumer)
+                  const int st = slot_acquire(kSlot);
+                  tma_load_4d_hint(pool + st * kSlot, &maps.m[isv ? M_VC : M_KC], &p_full[st], 0, 0, i * KVR,
+                                   (layer * a.kvB + b) * a.H + h, pol);
+                } else {
+                  const uint32_t bytes = static_cast<uint32_t>(min(KVR, pos - i * KVR) * HD * 2);
+                  const int st = slot_acquire(bytes);
+                  bulk_g2s_hint(pool + st * kSlot, (isv ? a.vc : a.kc) + head + static_cast<int64_t>(i) * KVR * HD,
+                                bytes, &p_full[st], pol);
+                }
               }
           }
         }
@@ -604,6 +634,106 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = k0; k < k0 + kn; ++k) {
             const int u = cta + k * G, b = u / H, h = u % H;
             const float* qk = qn + (k - k0) * 3 * HD;
+            if constexpr (HD == 64) {
+              // ---- tensor cores: K / V blocks are SWIZZLE_128B tiles of KVR (128) rows:
+              //      byte(r, dim) = r*128 + ((dim/8) ^ (r%8))*16 + (dim%8)*2  (conflict-free
+              //      fragment loads).  q.K^T: warp cw owns key groups 2cw, 2cw+1 of each block,
+              //      q is row 0 of the m16 A operand.  P.V: warp cw owns output dims 8cw..8cw+7.
+              uint32_t qa0[4], qa2[4];
+#pragma unroll
+              for (int kc = 0; kc < 4; ++kc) {
+                qa0[kc] = lane < 4 ? pack_bf16(qk[kc * 16 + lane * 2], qk[kc * 16 + lane * 2 + 1]) : 0u;
+                qa2[kc] = lane < 4 ? pack_bf16(qk[kc * 16 + 8 + lane * 2], qk[kc * 16 + 8 + lane * 2 + 1]) : 0u;
+              }
+              float mx = -FLT_MAX;
+              for (int i = 0; i < nblk; ++i) {
+                const uint32_t gi = pit + k * per + i, slot = gi % a.np;
+                mbar_wait(&p_full[slot], (gi / a.np) & 1);
+                if (k == 0 && i < 3) ATT_PROBE(2 + 2 * i);
+                const int rows = min(KVR, nold - i * KVR);
+                const uint32_t kb_s = smem_u32(pool + slot * kSlot);
+#pragma unroll
+                for (int gg = 0; gg < 2; ++gg) {
+                  const int g = 2 * cw + gg;
+                  if (g * 8 >= rows) continue;
+                  const int row = g * 8 + lane / 4;
+                  const uint32_t base = kb_s + row * 128 + (lane % 4) * 4;
+                  float dacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                  for (int kc = 0; kc < 4; ++kc) {
+                    const uint32_t b0 = lds32(base + (((2 * kc) ^ (row & 7)) << 4));
+                    const uint32_t b1 = lds32(base + (((2 * kc + 1) ^ (row & 7)) << 4));
+                    mma_bf16_16816(dacc, qa0[kc], 0u, qa2[kc], 0u, b0, b1);
+                  }
+                  if (lane < 4) {
+                    const int key = g * 8 + lane * 2;
+                    if (key < rows) {
+                      const float sx = dacc[0] * scale;
+                      sc[i * KVR + key] = sx;
+                      mx = fmaxf(mx, sx);
+                    }
+                    if (key + 1 < rows) {
+                      const float sx = dacc[1] * scale;
+                      sc[i * KVR + key + 1] = sx;
+                      mx = fmaxf(mx, sx);
+                    }
+                  }
+                }
+                named_bar_sync(kBarC, kCT);  // every warp is done with this slot
+                if (k == 0 && i < 3) ATT_PROBE(3 + 2 * i);
+                if (ctid == 0) mbar_arrive(&p_empty[slot]);
+              }
+              if (cw == 0) {  // the new key (position pos)
+                float s = 0.f;
+                for (int e = lane; e < HD; e += 32) s += qk[e] * qk[HD + e];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                s *= scale;
+                if (lane == 0) sc[nold] = s;
+                mx = fmaxf(mx, s);
+              }
+              mx = cmax(mx, red, cw, lane);
+              float sum = 0.f;
+              for (int jj = ctid; jj <= nold; jj += kCT) {
+                const float e = expf(sc[jj] - mx);
+                sc[jj] = e;
+                sum += e;
+              }
+              sum = csum(sum, red, cw, lane);
+              const float inv = 1.0f / sum;
+              if (k == 0) ATT_PROBE(8);
+              float oacc[4] = {0.f, 0.f, 0.f, 0.f};
+              for (int i = 0; i < nblk; ++i) {
+                const uint32_t gi = pit + k * per + nblk + i, slot = gi % a.np;
+                mbar_wait(&p_full[slot], (gi / a.np) & 1);
+                if (k == 0 && i < 2) ATT_PROBE(9 + i);
+                const int rows = min(KVR, nold - i * KVR);
+                const uint32_t vb_s = smem_u32(pool + slot * kSlot);
+                const float* sp = sc + i * KVR;
+                const int nkc = (rows + 15) / 16;
+                for (int kc = 0; kc < nkc; ++kc) {
+                  uint32_t pa0 = 0u, pa2 = 0u;
+                  if (lane < 4) {
+                    const int j0 = kc * 16 + lane * 2, j2 = j0 + 8;
+                    pa0 = pack_bf16(j0 < rows ? sp[j0] * inv : 0.f, j0 + 1 < rows ? sp[j0 + 1] * inv : 0.f);
+                    pa2 = pack_bf16(j2 < rows ? sp[j2] * inv : 0.f, j2 + 1 < rows ? sp[j2 + 1] * inv : 0.f);
+                  }
+                  const int vrow = kc * 16 + (lane & 15);
+                  uint32_t b0, b1;
+                  ldsm_x2_trans(vb_s + vrow * 128 + ((cw ^ (vrow & 7)) << 4), b0, b1);
+                  mma_bf16_16816(oacc, pa0, 0u, pa2, 0u, b0, b1);
+                }
+                named_bar_sync(kBarC, kCT);
+                if (ctid == 0) mbar_arrive(&p_empty[slot]);
+              }
+              if (lane < 4) {  // + the new value row; lanes 0..3 hold dims 8cw + 2*lane, +1
+                const float pj = rbf(sc[nold] * inv);
+                const int e0 = cw * 8 + lane * 2;
+                const float o0 = oacc[0] + pj * qk[2 * HD + e0];
+                const float o1 = oacc[1] + pj * qk[2 * HD + e0 + 1];
+                *reinterpret_cast<uint32_t*>(a.obuf + static_cast<int64_t>(b) * d + h * HD + e0) = pack_bf16(o0, o1);
+              }
+            } else {
             // scores of the cached keys (ring) and of the new key
             const int sub = lane % LPR, rsub = lane / LPR;
             float qr[8];
@@ -718,7 +848,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int g2 = 0; g2 < GR; ++g2) o += pacc[g2 * HD + e];
               a.obuf[static_cast<int64_t>(b) * d + h * HD + e] = f2b(o);
             }
-            if (k < 3) ATT_PROBE(12 + k);
+            }
+            if (k < 2) ATT_PROBE(11 + k);
             named_bar_sync(kBarC, kCT);
           }
         }
@@ -1033,6 +1164,14 @@ extern "C" int rlhf_decode_loop(const rlhf_decode_loop_params* p, rlhf_stream_t 
   rc |= dl::map4(&maps.m[dl::M_XH], a.hbuf, d, pl.BN, 1, 0, pl.BN);
   rc |= dl::map4(&maps.m[dl::M_XO], a.obuf, d, pl.BN, 1, 0, pl.BN);
   rc |= dl::map4(&maps.m[dl::M_XF], a.fbuf, ff, pl.BN, 1, 0, pl.BN);
+  if (hd == 64) {  // K / V cache as (hd, 1, Smax, L*kv_B*H), 128-row SWIZZLE_128B tiles
+    const int64_t heads = static_cast<int64_t>(L) * p->kv_B * A.n_heads;
+    rc |= dl::map4(&maps.m[dl::M_KC], p->kcache, hd, p->Smax, heads, static_cast<int64_t>(p->Smax) * hd, 128);
+    rc |= dl::map4(&maps.m[dl::M_VC], p->vcache, hd, p->Smax, heads, static_cast<int64_t>(p->Smax) * hd, 128);
+  } else {
+    maps.m[dl::M_KC] = maps.m[dl::M_XH];
+    maps.m[dl::M_VC] = maps.m[dl::M_XH];
+  }
   if (rc) return 2;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // barrier counter + zero activation rows >= B (MMA N padding)

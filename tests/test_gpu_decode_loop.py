@@ -20,8 +20,8 @@ pytestmark = pytest.mark.gpu
 def test_decode_loop_matches_per_kernel_steps(arch, B, P, R):
     from paper_2312_11819_b200.engine import Engine
     cfg = make_config(arch, arch, B, P, R)
-    ref = Engine(cfg, cuda_graph=3)
-    loop = Engine(cfg, cuda_graph=1)
+    ref = Engine(cfg, cuda_graph=1)
+    loop = Engine(cfg, cuda_graph=3)
     rng = np.random.default_rng(B * 1000 + R)
     toks = rng.integers(0, cfg.actor.vocab, size=(B, P + R), dtype=np.int32)
     p3, m3 = ref.greedy_check(toks)
