@@ -137,6 +137,15 @@ def reference_arm(args, wl, rank):
     return 0
 
 
+def profile_json(name):
+    """Committed ncu-derived numbers (profiles/*.json) for the roofline `traffic` fields."""
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def gemm_roofline(a, B, S, tflops_peak):
     """Live CUDA-event timing of the dominant forward/backward GEMM shape of the workload
     (FFN up-projection, M = B*S tokens), through the C-ABI."""
@@ -157,9 +166,12 @@ def gemm_roofline(a, B, S, tflops_peak):
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 1e3 / iters
     fl = 2.0 * M * N * K
+    tr = profile_json("r1_gemm_traffic.json")
+    traffic = tr["dram_bytes_per_launch"] if tr and tr.get("shape") == [M, N, K] else None
     return {"bound": "tensor", "kernel": "gemm_sm100_kernel (FFN up-proj, forward)", "shape": [M, N, K],
             "achieved": fl / t / 1e12, "peak": tflops_peak, "unit": "TFLOP/s", "frac": fl / t / 1e12 / tflops_peak,
-            "traffic": None, "ms": t * 1e3}
+            "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write, profiles/r1_gemm_traffic.json)",
+            "ms": t * 1e3}
 
 
 def main():
@@ -232,9 +244,14 @@ def main():
     hbm, tf_burst, tf_sus, src = peaks()
     dbytes = decode_bytes_per_step(cfg.actor, B, P, R)
     dec_per_launch = dec_s / (args.steps * max(1, R - 1))
+    tr = profile_json("r1_decode_traffic.json") if args.workload == "c2" else None
     roof_decode = {"bound": "hbm", "kernel": "decode step (CUDA graph: swap-AB tcgen05 GEMMs + decode attention)",
                    "achieved": dbytes / dec_per_launch / 1e9, "peak": hbm, "unit": "GB/s",
-                   "frac": dbytes / dec_per_launch / 1e9 / hbm, "traffic": None,
+                   "frac": dbytes / dec_per_launch / 1e9 / hbm,
+                   # ncu DRAM bytes of one decode step (profiles/r1_decode_traffic.json, measured at ctx
+                   # ~265) scaled by its traffic/algorithmic ratio to this average-context step
+                   "traffic": tr["traffic_over_algorithmic"] * dbytes if tr else None,
+                   "traffic_ratio_measured": tr["traffic_over_algorithmic"] if tr else None,
                    "algorithmic_bytes_per_launch": dbytes, "us_per_launch": dec_per_launch * 1e6,
                    "peak_source": src}
     roof_gemm = gemm_roofline(cfg.actor, B, P + R, tf_burst)
@@ -257,7 +274,7 @@ def main():
                    "l2": "working set (4 models' weights + activations) >> 126 MB L2 every step"},
         "split_seconds_per_step": stage,
         "split_fraction": {k: v / (dev_s / args.steps) for k, v in stage.items()},
-        "e2e": {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": B * S * 4,
+        "e2e": {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": B * P * 4,
                 "d2h_bytes_per_step": 8},
         "gpu_launches": launches,
         "roofline": roof_decode,
