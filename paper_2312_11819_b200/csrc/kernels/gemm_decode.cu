@@ -145,6 +145,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   DPROBE(1);
   pdl_trigger();  // the next kernel may start its (independent) prologue
+  // announce "receive barrier initialised" to the cluster now (non-blocking); the
+  // matching wait sits right before the partial pushes, so a producer thread that
+  // blocks on ring slots (K slices longer than the ring) cannot deadlock the MMA
+  cluster_arrive_relaxed();
 
   const bool ln = e.ln_x != nullptr;
   if (threadIdx.x == 0) {
@@ -173,9 +177,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  // peers' receive barriers are initialised before anyone pushes partials
-  cluster_arrive_relaxed();
-  cluster_wait();
   if (ln) {
     // LayerNorm of every batch row (full K for the statistics), written for this
     // CTA's K-slice straight into the SWIZZLE_128B K-major B tiles:
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait();  // residual (and Y when aliased) come from earlier kernels
 
   // ---- partial accumulator rows -> the owning CTA's receive buffer (st.async, DSMEM)
+  cluster_wait();  // every peer's receive barrier is initialised
   mbar_wait(acc_bar, 0);
   DPROBE(4);
   tc_fence_after();

@@ -153,7 +153,7 @@ def test_gemm_decode_cluster_split(M, K, N, splits):
     assert (yb.float() - expb).abs().max().item() <= 0.02 * expb.abs().max().item()
 
 
-@pytest.mark.parametrize("M,K,N,splits", [(2304, 768, 32, 4), (3072, 768, 32, 4), (384, 128, 4, 1), (6144, 2048, 16, 2)])
+@pytest.mark.parametrize("M,K,N,splits", [(2304, 768, 32, 4), (3072, 768, 32, 4), (384, 128, 4, 1), (6144, 2048, 16, 4)])
 def test_gemm_decode_fused_layernorm(M, K, N, splits):
     """X = bf16(LN(x)) computed inside the decode GEMM == separate LN kernel + GEMM."""
     from paper_2312_11819_b200 import ops
