@@ -578,6 +578,252 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---- CTA-pair (cta_group::2) variant ------------------------------------------
+// Two CTAs of a cluster (one TPC) compute a 256 x 256 tile: each holds its 128 rows
+// of A and 128 of B's 256 rows per k-block (32 KB / stage instead of 48 KB, so 6
+// stages and 1.5x less L2->SM operand traffic per FLOP); the leader issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 256) which reads both CTAs' shared memory
+// and writes each CTA's 128 accumulator lanes into its own TMEM.  Both producers'
+// TMA loads complete on the leader's full barrier; the MMA commit is multicast to
+// both CTAs' empty / accumulator-ready barriers; both CTAs' epilogue warps arrive on
+// the leader's accumulator-drained barrier.  Same K order as the 1-CTA kernel, so
+// results are bit-identical to it.  Row-major C, no split-K.
+namespace pair {
+constexpr int PBM = 2 * BM, PBN = 256;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int BH_BYTES = (PBN / 2) * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
+constexpr int EPI_BYTES = kEpiWarps * 32 * kStagePitch * 4;
+constexpr int RAW_STAGES = (218 * 1024 - EPI_BYTES) / STAGE_BYTES;
+constexpr int STAGES = RAW_STAGES > 8 ? 8 : RAW_STAGES;
+constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+constexpr int TMEM_COLS = 2 * PBN;
+
+__device__ __forceinline__ uint32_t ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair(void* smem, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1,
+                                                 int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.cta_group::2"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  const uint16_t mask = 3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+// pair unit u -> (batch z, 256-row m tile, 256-col n tile)
+__device__ __forceinline__ Unit get_unit(const GemmArgs& e, int u) {
+  Unit w;
+  w.split = 0;
+  int t = u;
+  w.n_tile = t % e.tiles_n;
+  t /= e.tiles_n;
+  w.m_tile = t % e.tiles_m;
+  w.z = t / e.tiles_m;
+  w.h = w.z % e.batch_h;
+  w.b = w.z / e.batch_h;
+  w.m0 = w.m_tile * PBM;
+  w.n0 = w.n_tile * PBN;
+  w.kb_begin = 0;
+  w.kb_end = e.num_kb;
+  w.skip = e.causal == 1 && w.n0 > w.m0 + PBM - 1;
+  if (e.causal == 2) w.kb_end = min(w.kb_end, (w.m0 + PBM + BK - 1) / BK);
+  if (e.causal == 3) w.kb_begin = w.m0 / BK;
+  return w;
+}
+}  // namespace pair
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ GemmArgs e) {
+  using namespace pair;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + EPI_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull = empty_bar + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiWarps);  // both CTAs' epilogue warps (leader's copy is used)
+    }
+    mbar_fence_init();
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's barriers exist before any TMA / commit targets them
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs): this CTA's 128 rows of A and of B
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cid; u < e.units; u += ncl) {
+        const Unit w = pair::get_unit(e, u);
+        if (w.skip) continue;
+        const int ma = w.m0 + static_cast<int>(rank) * BM, nb = w.n0 + static_cast<int>(rank) * (PBN / 2);
+        for (int kb = w.kb_begin; kb < w.kb_end; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1u);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          const uint32_t fb = mapa(smem_u32(&full_bar[stage]), 0);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (!e.a_mn) {
+            tma_load_4d_pair(sa, &tmA, fb, k0, w.h, ma, w.b);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_4d_pair(sa + j * 8192, &tmA, fb, ma + 64 * j, w.h, k0, w.b);
+          }
+          if (!e.b_mn) {
+            tma_load_4d_pair(sb, &tmB, fb, k0, w.h, nb, w.b);
+          } else {
+#pragma unroll
+            for (int j = 0; j < (PBN / 2) / 64; ++j) tma_load_4d_pair(sb + j * 8192, &tmB, fb, nb + 64 * j, w.h, k0, w.b);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---- pair MMA issuer (leader CTA only)
+      const uint32_t idesc = umma_idesc_bf16(PBM, PBN, e.a_mn, e.b_mn);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int u = cid; u < e.units; u += ncl) {
+        const Unit w = pair::get_unit(e, u);
+        if (w.skip) continue;
+        const int acc = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        ++it;
+        mbar_wait(&tempty[acc], aph ^ 1u);  // both CTAs drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem + static_cast<uint32_t>(acc * PBN);
+        for (int kb = w.kb_begin; kb < w.kb_end; ++kb) {
+          mbar_wait(&full_bar[stage], phase);  // both CTAs' halves landed
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = e.a_mn ? umma_desc_sw128(sa + k * 2048, 8192, 1024) : umma_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = e.b_mn ? umma_desc_sw128(sb + k * 2048, 8192, 1024) : umma_desc_sw128(sb + k * 32, 16, 1024);
+            umma_pair(d, ad, bd, idesc, (kb > w.kb_begin || k > 0) ? 1u : 0u);
+          }
+          commit_pair(&empty_bar[stage]);  // frees the slot in BOTH CTAs
+          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+        }
+        if (w.kb_end > w.kb_begin) {
+          commit_pair(&tfull[acc]);
+        } else {  // empty K range: release both CTAs' epilogues directly
+          mbar_arrive(&tfull[acc]);
+          arrive_remote(mapa(smem_u32(&tfull[acc]), 1));
+        }
+      }
+    }
+    __syncwarp();
+  } else {  // ---- epilogue warps (both CTAs): this CTA's 128 rows of the 256 x 256 tile
+    const int q = static_cast<int>(warp & 3u);
+    constexpr int NCH = PBN / 32;
+    float* st = epi_stage + (warp - 2) * 32 * kStagePitch;
+    const uint32_t tq = static_cast<uint32_t>(q * 32) << 16;
+    const int rr0 = static_cast<int>(lane >> 2), cc = static_cast<int>(lane & 3) * 8;
+    int it = 0;
+    for (int u = cid; u < e.units; u += ncl) {
+      const Unit w = pair::get_unit(e, u);
+      if (w.skip) continue;
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      ++it;
+      const bool has_k = w.kb_end > w.kb_begin;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem + tq + static_cast<uint32_t>(acc * PBN);
+      const int mq = w.m0 + static_cast<int>(rank) * BM + q * 32;
+#pragma unroll 1
+      for (int c = 0; c < NCH; ++c) {
+        float v[32];
+        if (has_k) tmem_ld32(tbase + c * 32, v);
+        else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+        }
+        if (c == NCH - 1) {  // this warp is done with the accumulator: tell the leader
+          tc_fence_before();
+          if (lane == 0) arrive_remote(mapa(smem_u32(&tempty[acc]), 0));
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) st[lane * kStagePitch + j] = v[j];
+        __syncwarp();
+        float sv[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int t = 0; t < 8; ++t) sv[i][t] = st[(rr0 + 8 * i) * kStagePitch + cc + t];
+        epi_rows4(e, w.b, w.h, mq + rr0, w.n0 + c * 32 + cc, sv, st + rr0 * kStagePitch + cc, kStagePitch);
+        __syncwarp();
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the leader's MMAs wrote this CTA's TMEM: both done before dealloc
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // ---- host side -----------------------------------------------------------------
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -661,6 +907,39 @@ static int launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
 
+static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t s) {
+  static bool init = false;
+  if (!init) {
+    if (cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM) != cudaSuccess)
+      return 5;
+    init = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  const int pairs = std::min(a.units, sm_count() / 2);
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pair::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_pair_kernel, ta, tb, a) == cudaSuccess ? 0 : 5;
+}
+
+// CTA-pair path: full 256-wide N tiles, row-major C, no split-K, enough 256 x 256 tiles
+// to fill the pairs (RLHF_GEMM_PAIR=0 disables it)
+static bool use_pair(const rlhf_gemm_params* p, int bn, int splits) {
+  static int env = -1;
+  if (env < 0) env = getenv("RLHF_GEMM_PAIR") ? atoi(getenv("RLHF_GEMM_PAIR")) : 1;
+  if (!env || bn != 256 || splits != 1 || p->c_cs != 1) return false;
+  const long tiles = static_cast<long>((p->M + 255) / 256) * ((p->N + 255) / 256) * p->batch;
+  return tiles >= sm_count() / 2;
+}
+
 template <int BN>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t s) {
   return a.c_cs == 1 ? launch_mode<BN, 0>(ta, tb, a, s) : launch_mode<BN, 1>(ta, tb, a, s);
@@ -691,13 +970,15 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
   const int splits = (p->split_k > 1 && p->c_cs != 1) ? std::min(p->split_k, num_kb) : 1;
   if (splits > 1 && p->causal) return 2;
   const int bb = p->batch / p->batch_h;
+  const bool pair_mode = use_pair(p, bn, splits);
   CUtensorMap ta, tb;
   int st;
   // A: K-major -> (K, h, M, b) box (64, 1, 128, 1); MN-major -> (M, h, K, b) box (64, 1, 64, 1)
   if (!p->a_mn_major) st = make_map(&ta, p->A, p->K, p->M, p->lda, p->a_stride_h, p->a_stride_b, p->batch_h, bb, BM);
   else st = make_map(&ta, p->A, p->M, p->K, p->lda, p->a_stride_h, p->a_stride_b, p->batch_h, bb, BK);
   if (st) return st;
-  if (!p->b_mn_major) st = make_map(&tb, p->B, p->K, p->N, p->ldb, p->b_stride_h, p->b_stride_b, p->batch_h, bb, bn);
+  if (!p->b_mn_major)
+    st = make_map(&tb, p->B, p->K, p->N, p->ldb, p->b_stride_h, p->b_stride_b, p->batch_h, bb, pair_mode ? bn / 2 : bn);
   else st = make_map(&tb, p->B, p->N, p->K, p->ldb, p->b_stride_h, p->b_stride_b, p->batch_h, bb, BK);
   if (st) return st;
 
@@ -742,6 +1023,12 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
     a.counters = p->counters;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (pair_mode) {
+    a.tiles_m = (p->M + pair::PBM - 1) / pair::PBM;
+    a.tiles_n = (p->N + pair::PBN - 1) / pair::PBN;
+    a.units = a.tiles_m * a.tiles_n * p->batch;
+    return launch_pair(ta, tb, a, s);
+  }
   switch (bn) {
     case 32: return launch<32>(ta, tb, a, s);
     case 64: return launch<64>(ta, tb, a, s);

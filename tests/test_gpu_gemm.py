@@ -177,3 +177,50 @@ def test_gemm_decode_ring_long_k(M, K, N, splits):
     out = ops.gemm_decode(W, X, splits=splits)
     torch.cuda.synchronize()
     close(out, X.float() @ W.float().t(), 1e-4)
+
+
+# ---- CTA-pair (tcgen05 cta_group::2, 256 x 256 tiles) path: large row-major GEMMs ----
+@pytest.mark.parametrize("M,N,K", [(16384, 3072, 768), (8192, 2304, 768), (5000, 3000, 800), (16384, 768, 3072)])
+def test_gemm_pair_nt(M, N, K):
+    a = torch.randn(M, K, device="cuda").bfloat16()
+    b = torch.randn(N, K, device="cuda").bfloat16()
+    bias = torch.randn(N, device="cuda").bfloat16()
+    out = _ops().gemm(a, b, bias=bias, relu=True, out_f32=False)
+    exp = torch.relu(ref(a, b) + bias.float())
+    torch.cuda.synchronize()
+    assert (out.float() - exp).abs().max().item() <= 0.01 * exp.abs().max().item()
+    out2 = _ops().gemm(a, b)
+    torch.cuda.synchronize()
+    close(out2, ref(a, b), 1e-5 * K ** 0.5 + 1e-5)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, True), (True, True), (True, False)])
+def test_gemm_pair_majors(a_mn, b_mn):
+    M, N, K = 8192, 4096, 1024
+    a = torch.randn(K, M, device="cuda").bfloat16() if a_mn else torch.randn(M, K, device="cuda").bfloat16()
+    b = torch.randn(K, N, device="cuda").bfloat16() if b_mn else torch.randn(N, K, device="cuda").bfloat16()
+    out = _ops().gemm(a, b, a_mn=a_mn, b_mn=b_mn)
+    torch.cuda.synchronize()
+    close(out, ref(a, b, a_mn, b_mn), 1e-5 * K ** 0.5 + 1e-5)
+
+
+def test_gemm_pair_batched_attention_causal():
+    """QK^T over (b, h) with causal 256 x 256 pair-tile skipping (S = 512)."""
+    from paper_2312_11819_b200.ops import GemmParams, gemm_batched
+    B, S, H, hd = 2, 512, 12, 64
+    d = H * hd
+    qkv = torch.randn(B * S, 3 * d, device="cuda").bfloat16()
+    scores = torch.full((B, H, S, S), -7.0, device="cuda")
+    p = GemmParams()
+    p.M, p.N, p.K, p.batch, p.batch_h = S, S, hd, B * H, H
+    p.A, p.a_mn_major, p.lda, p.a_stride_h, p.a_stride_b = qkv.data_ptr(), 0, 3 * d, hd, S * 3 * d
+    p.B, p.b_mn_major, p.ldb, p.b_stride_h, p.b_stride_b = qkv.data_ptr() + 2 * d, 0, 3 * d, hd, S * 3 * d
+    p.C, p.c_f32, p.c_rs, p.c_cs, p.c_stride_h, p.c_stride_b = scores.data_ptr(), 1, S, 1, S * S, H * S * S
+    p.alpha, p.causal = 0.125, 1
+    gemm_batched(p)
+    q = qkv[:, :d].float().view(B, S, H, hd).transpose(1, 2)
+    k = qkv[:, d:2 * d].float().view(B, S, H, hd).transpose(1, 2)
+    exp = (q @ k.transpose(-1, -2)) * 0.125
+    torch.cuda.synchronize()
+    mask = torch.ones(S, S, device="cuda", dtype=torch.bool).tril()
+    assert (scores - exp)[..., mask].abs().max().item() < 1e-3
