@@ -281,6 +281,15 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
     p.B = Xin; p.b_mn_major = 1; p.ldb = K_in;
     p.C = dW; p.c_f32 = 1; p.c_rs = K_in; p.c_cs = 1;
     p.alpha = 1.0f; p.accumulate = 1;
+    // very few output tiles (O-projection: 18), long K (tokens): deterministic split-K
+    // fills the SMs.  Larger weight gradients stay unsplit: they are L2-operand-bandwidth
+    // bound and the partial round trip costs more than the idle SMs (tools/gemm_bench.py).
+    const int bn = rlhf_gemm_block_n(&p);
+    const int tiles = ((N_out + 127) / 128) * ((K_in + bn - 1) / bn);
+    int split = 1;
+    if (tiles * 4 <= 148)
+      while (split < 8 && tiles * split * 2 <= 148 && rows / 64 / (split * 2) >= 8) split *= 2;
+    p.split_k = split;
     gemm(p);
   };
   // dX[T, K_in] = dY[T, N_out] W[N_out, K_in]

@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tbase = tmem + tq + static_cast<uint32_t>(acc * BN);
       const size_t tile_id = (static_cast<size_t>(w.z) * e.tiles_m + w.m_tile) * e.tiles_n + w.n_tile;
-      float* part = (COLMAJOR && e.splits > 1) ? e.ws + ((tile_id * e.splits + w.split) * BM + q * 32) * BN : nullptr;
+      float* part = e.splits > 1 ? e.ws + ((tile_id * e.splits + w.split) * BM + q * 32) * BN : nullptr;
       const int mq = w.m0 + q * 32;
       if (my_last < 0) {  // no chunk for this warp (BN == 32): release immediately
         tc_fence_before();
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int t = 0; t < 8; ++t) s[i][t] = st[(rr0 + 8 * i) * kStagePitch + cc + t];
-          if constexpr (!row_major) {
+          if (part) {  // split-K slice: fp32 partial tile -> workspace
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               float4* dst = reinterpret_cast<float4*>(part + (rr0 + 8 * i) * BN + c * 32 + cc);
@@ -537,7 +537,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c == half + 3) PROBE(11);
       }
       PROBE(6);
-      if constexpr (row_major) continue;
       if (!part) continue;
       // split-K: ticket; the last slice of the tile reduces all partials in order
       __threadfence();
@@ -556,7 +555,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int t = 0; t < 8; ++t) s[i][t] = 0.0f;
         reduce_partials(e, tile_id, q * 32 + rr0, c * 32 + cc, BN, s);
-        {  // column-major output: back to lane = row for coalesced stores
+        if constexpr (row_major) {  // row-segment epilogue straight from the reduced values
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) st[(rr0 + 8 * i) * kStagePitch + cc + t] = s[i][t];
+          __syncwarp();
+          epi_rows4(e, w.b, w.h, mq + rr0, w.n0 + c * 32 + cc, s, st + rr0 * kStagePitch + cc, kStagePitch);
+          __syncwarp();
+        } else {  // column-major output: back to lane = row for coalesced stores
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -594,7 +601,9 @@ constexpr int PBM = 2 * BM, PBN = 256;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int BH_BYTES = (PBN / 2) * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
-constexpr int EPI_BYTES = kEpiWarps * 32 * kStagePitch * 4;
+constexpr int EPI_WARPS = 8;  // two warps per TMEM lane quarter, alternating 32-column chunks
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr int EPI_BYTES = EPI_WARPS * 32 * kStagePitch * 4;
 constexpr int RAW_STAGES = (218 * 1024 - EPI_BYTES) / STAGE_BYTES;
 constexpr int STAGES = RAW_STAGES > 8 ? 8 : RAW_STAGES;
 constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
@@ -662,7 +671,7 @@ __device__ __forceinline__ Unit get_unit(const GemmArgs& e, int u) {
 }
 }  // namespace pair
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(pair::THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmArgs e) {
   using namespace pair;
@@ -686,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * kEpiWarps);  // both CTAs' epilogue warps (leader's copy is used)
+      mbar_init(&tempty[a], 2 * EPI_WARPS);  // both CTAs' epilogue warps (leader's copy is used)
     }
     mbar_fence_init();
     tma_prefetch(&tmA);
@@ -774,6 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {  // ---- epilogue warps (both CTAs): this CTA's 128 rows of the 256 x 256 tile
     const int q = static_cast<int>(warp & 3u);
+    const int half = static_cast<int>(warp - 2) >> 2;
     constexpr int NCH = PBN / 32;
     float* st = epi_stage + (warp - 2) * 32 * kStagePitch;
     const uint32_t tq = static_cast<uint32_t>(q * 32) << 16;
@@ -791,14 +801,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tbase = tmem + tq + static_cast<uint32_t>(acc * PBN);
       const int mq = w.m0 + static_cast<int>(rank) * BM + q * 32;
 #pragma unroll 1
-      for (int c = 0; c < NCH; ++c) {
+      for (int c = half; c < NCH; c += 2) {
         float v[32];
         if (has_k) tmem_ld32(tbase + c * 32, v);
         else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0.0f;
         }
-        if (c == NCH - 1) {  // this warp is done with the accumulator: tell the leader
+        if (c + 2 >= NCH) {  // this warp is done with the accumulator: tell the leader
           tc_fence_before();
           if (lane == 0) arrive_remote(mapa(smem_u32(&tempty[acc]), 0));
         }
@@ -917,7 +927,7 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   cudaLaunchConfig_t cfg{};
   const int pairs = std::min(a.units, sm_count() / 2);
   cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(pair::THREADS);
   cfg.dynamicSmemBytes = pair::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -952,9 +962,8 @@ using namespace rlhf;
 extern "C" int rlhf_gemm_block_n(const rlhf_gemm_params* p) { return pick_bn(p); }
 
 extern "C" size_t rlhf_gemm_workspace_bytes(const rlhf_gemm_params* p) {
-  if (p->split_k <= 1) return 0;
+  if (p->split_k <= 1 || p->causal) return 0;
   const int bn = pick_bn(p);
-  if (p->c_cs == 1) return 0;
   const int splits = std::min(p->split_k, (p->K + BK - 1) / BK);
   const size_t tiles = static_cast<size_t>((p->M + BM - 1) / BM) * ((p->N + bn - 1) / bn) * p->batch;
   return tiles * splits * BM * bn * sizeof(float);
@@ -966,8 +975,8 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
   if (bn != 32 && bn != 64 && bn != 128 && bn != 256) return 2;
   if (p->b_mn_major && bn < 64) return 2;
   const int num_kb = (p->K + BK - 1) / BK;
-  // split-K is a decode (column-major, swap-AB) feature
-  const int splits = (p->split_k > 1 && p->c_cs != 1) ? std::min(p->split_k, num_kb) : 1;
+  // split-K: deterministic (fp32 partials, the last slice of a tile reduces them in order)
+  const int splits = p->split_k > 1 ? std::min(p->split_k, num_kb) : 1;
   if (splits > 1 && p->causal) return 2;
   const int bb = p->batch / p->batch_h;
   const bool pair_mode = use_pair(p, bn, splits);

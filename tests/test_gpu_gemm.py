@@ -224,3 +224,21 @@ def test_gemm_pair_batched_attention_causal():
     torch.cuda.synchronize()
     mask = torch.ones(S, S, device="cuda", dtype=torch.bool).tril()
     assert (scores - exp)[..., mask].abs().max().item() < 1e-3
+
+
+@pytest.mark.parametrize("M,N,K,split", [(768, 768, 16384, 8), (2304, 768, 16384, 2), (304, 520, 4096, 3)])
+def test_gemm_row_major_split_k_accumulate(M, N, K, split):
+    """Weight-gradient shape (few tiles, long K): deterministic row-major split-K into an
+    fp32 accumulator (dW += dY^T X with both operands MN-major)."""
+    from paper_2312_11819_b200.ops import GemmParams, gemm_batched
+    a = torch.randn(K, M, device="cuda").bfloat16()
+    b = torch.randn(K, N, device="cuda").bfloat16()
+    base = torch.randn(M, N, device="cuda")
+    outs = []
+    for _ in range(2):
+        c = base.clone()
+        _ops().gemm(a, b, a_mn=True, b_mn=True, out=c, accumulate=True, split_k=split)
+        outs.append(c)
+    torch.cuda.synchronize()
+    close(outs[0], base + ref(a, b, True, True), 1e-5 * K ** 0.5 + 1e-5)
+    assert torch.equal(outs[0], outs[1])

@@ -16,7 +16,12 @@ SHAPES = [  # c2 (OPT-125m, B=32, S=512): forward, dgrad, wgrad, LM head; decode
     ("fwd W2", 16384, 768, 3072, 0, 0, 1),
     ("fwd qkv", 16384, 2304, 768, 0, 0, 1),
     ("dgrad W1", 16384, 768, 3072, 0, 1, 1),
-    ("wgrad W1", 3072, 768, 16384, 1, 1, 1),
+    ("wgrad W1", 3072, 768, 16384, 1, 1, 2),
+    ("fwd Wo", 16384, 768, 768, 0, 0, 1),
+    ("dgrad qkv", 16384, 768, 2304, 0, 1, 1),
+    ("wgrad qkv", 2304, 768, 16384, 1, 1, 2),
+    ("wgrad W2", 768, 3072, 16384, 1, 1, 2),
+    ("wgrad Wo", 768, 768, 16384, 1, 1, 8),
     ("lm head", 8192, 50272, 768, 0, 0, 1),
     ("dec qkv", 2304, 32, 768, 0, 0, 6),
     ("dec W2", 768, 32, 3072, 0, 0, 8),
