@@ -190,13 +190,20 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
   float* q = sc + (Smax + 3) / 4 * 4;
   __shared__ float red[NW];
   __shared__ uint64_t kbar[NS], vbar[NS];
-  pdl_entry();
+  // Programmatic dependent launch: only the new row `pos` (K/V written by the QKV GEMM's
+  // epilogue) and q depend on the predecessor.  The position counter and the cached rows
+  // [0, pos) were final before the predecessor started (every earlier kernel of the step
+  // chain waited on its own predecessor), so their bulk loads are issued before
+  // griddepcontrol.wait and stream while the QKV GEMM is still running.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int bh = blockIdx.x, b = bh / H, h = bh % H;
   const int d = H * HD;
-  const int ctx = *pos_dev + 1;
+  const int pos = *pos_dev;
+  const int ctx = pos + 1;
   const int nblk = (ctx + RB - 1) / RB;
   const uint16_t* K = kc + static_cast<int64_t>(bh) * Smax * HD;
   const uint16_t* V = vc + static_cast<int64_t>(bh) * Smax * HD;
+  const int npre = min(NS, pos / RB);  // leading blocks made only of cached rows
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
@@ -204,10 +211,17 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
       mbar_init(&vbar[i], 1);
     }
     mbar_fence_init();
-#pragma unroll
-    for (int i = 0; i < NS; ++i) dec_issue<HD, NS>(Ks, K, i, ctx, kbar);
-#pragma unroll
-    for (int i = 0; i < NS; ++i) dec_issue<HD, NS>(Vs, V, i, ctx, vbar);
+    for (int i = 0; i < npre; ++i) {
+      dec_issue<HD, NS>(Ks, K, i, ctx, kbar);
+      dec_issue<HD, NS>(Vs, V, i, ctx, vbar);
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int i = npre; i < NS; ++i) {
+      dec_issue<HD, NS>(Ks, K, i, ctx, kbar);
+      dec_issue<HD, NS>(Vs, V, i, ctx, vbar);
+    }
   }
   const float scale = rsqrtf(static_cast<float>(HD));
   const uint16_t* qsrc = qkv + static_cast<int64_t>(b) * 3 * d + h * HD;
