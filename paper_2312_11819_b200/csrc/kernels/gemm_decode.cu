@@ -145,6 +145,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   DPROBE(1);
   pdl_trigger();  // the next kernel may start its (independent) prologue
+  // the bias does not depend on the predecessor: fetch it now (every unit of this thread
+  // has the same row, since rows_per divides the thread count)
+  const int m_own = m0 + split * rows_per + static_cast<int>(threadIdx.x) % rows_per;
+  const float bias_own = (e.bias && m_own < e.M) ? b2f(e.bias[m_own]) : 0.0f;
   // announce "receive barrier initialised" to the cluster now (non-blocking); the
   // matching wait sits right before the partial pushes, so a producer thread that
   // blocks on ring slots (K slices longer than the ring) cannot deadlock the MMA
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < 4; ++t)
         if (c4 + t < e.N) res[t] = e.residual[static_cast<int64_t>(c4 + t) * e.ldy + m];
     }
-    const float bm = (e.bias && mok) ? b2f(e.bias[m]) : 0.0f;
+    const float bm = bias_own;  // m == m_own
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
     for (int s2 = 0; s2 < e.splits; ++s2) {  // fixed slice order

@@ -19,6 +19,15 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Trigger first, then wait: for kernels whose successor's pre-wait work only touches
+// data that is final before this kernel's predecessor ran (decode LayerNorm -> GEMM
+// weight prefetch).  The step's embed kernel keeps pdl_entry() so that every later
+// kernel of a decode step may assume the previous step has completed.
+__device__ __forceinline__ void pdl_entry_early() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 template <typename... KArgs, typename... Args>
 inline int launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};

@@ -63,7 +63,7 @@ template <int VPL>  // float4 vectors per lane
 __global__ void layernorm_kernel(const float* __restrict__ x, const uint16_t* __restrict__ g,
                                  const uint16_t* __restrict__ bta, uint16_t* __restrict__ y, float* __restrict__ mean,
                                  float* __restrict__ rstd, int M, int d) {
-  pdl_entry();
+  pdl_entry_early();
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
