@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "launch_util.cuh"
 #include "rlhf_kernels.h"
 #include "sm100_common.cuh"
 
@@ -395,6 +396,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   PROBE(1);
+  // programmatic dependent launch (decode LM head inside the step graph): setup above
+  // overlapped the predecessor; operands and outputs are touched only after the wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
@@ -913,8 +918,7 @@ static int launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
     per_sm = std::max(1, std::min(per_sm, 512 / Cfg::TMEM_COLS));
   }
   const int grid = std::min(a.units, per_sm * sm_count());
-  gemm_sm100_kernel<BN, COLMAJOR><<<grid, kThreads, Cfg::SMEM, s>>>(ta, tb, a);
-  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+  return launch_k(gemm_sm100_kernel<BN, COLMAJOR>, dim3(grid), dim3(kThreads), Cfg::SMEM, s, ta, tb, a);
 }
 
 static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t s) {
