@@ -116,7 +116,7 @@ constexpr int kLnBwdRows = 64;  // rows per block (8 warps x 8 rows)
 // dx += rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)).  Each warp keeps its
 // rows' dgamma/dbeta column partials in registers (lane owns columns lane+32k),
 // the block reduces its 8 warps in smem in fixed order -> ws[blk][2][d].
-template <int CPL>  // columns per lane (d <= 32*CPL)
+template <int VPL>  // float4 vectors per lane (d <= 128*VPL)
 __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
                                      const float* __restrict__ mean, const float* __restrict__ rstd,
                                      const uint16_t* __restrict__ g, float* __restrict__ dx, float* __restrict__ ws,
@@ -124,50 +124,67 @@ __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* 
   extern __shared__ float red[];  // [8 warps][2][d]
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int r0 = blockIdx.x * kLnBwdRows;
-  float gg[CPL], pg[CPL], pb[CPL];
+  const int q = d / 4;
+  float4 gg[VPL], pg[VPL], pb[VPL];
 #pragma unroll
-  for (int k = 0; k < CPL; ++k) {
-    const int j = lane + 32 * k;
-    gg[k] = j < d ? bf2f(g[j]) : 0.f;
-    pg[k] = pb[k] = 0.f;
+  for (int k = 0; k < VPL; ++k) {
+    const int c = lane + 32 * k;
+    if (c < q) {
+      const uint2 u = reinterpret_cast<const uint2*>(g)[c];
+      gg[k] = make_float4(bf2f(u.x & 0xFFFFu), bf2f(u.x >> 16), bf2f(u.y & 0xFFFFu), bf2f(u.y >> 16));
+    } else {
+      gg[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    pg[k] = pb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   for (int rr = warp; rr < kLnBwdRows; rr += 8) {
     const int row = r0 + rr;
     if (row >= M) break;
-    const float* dr = dy + static_cast<int64_t>(row) * d;
-    const float* xr = x + static_cast<int64_t>(row) * d;
+    const float4* dr = reinterpret_cast<const float4*>(dy + static_cast<int64_t>(row) * d);
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * d);
+    float4* o = reinterpret_cast<float4*>(dx + static_cast<int64_t>(row) * d);
     const float mu = mean[row], rs = rstd[row];
-    float dyv[CPL], xh[CPL];
-    float a = 0.f, c = 0.f;
+    float4 dyv[VPL], xh[VPL], dxo[VPL];
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-      const int j = lane + 32 * k;
-      dyv[k] = j < d ? dr[j] : 0.f;
-      xh[k] = j < d ? (xr[j] - mu) * rs : 0.f;
+    for (int k = 0; k < VPL; ++k) {  // every load of the row in flight at once
+      const int c = lane + 32 * k;
+      const bool ok = c < q;
+      dyv[k] = ok ? dr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      xh[k] = ok ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      dxo[k] = ok ? o[c] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    float a = 0.f, cs = 0.f;
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-      const float t = dyv[k] * gg[k];
-      a += t;
-      c += t * xh[k];
-      pg[k] += dyv[k] * xh[k];
-      pb[k] += dyv[k];
+    for (int k = 0; k < VPL; ++k) {
+      if (lane + 32 * k >= q) continue;
+      xh[k] = make_float4((xh[k].x - mu) * rs, (xh[k].y - mu) * rs, (xh[k].z - mu) * rs, (xh[k].w - mu) * rs);
+      const float t0 = dyv[k].x * gg[k].x, t1 = dyv[k].y * gg[k].y, t2 = dyv[k].z * gg[k].z, t3 = dyv[k].w * gg[k].w;
+      a += (t0 + t1) + (t2 + t3);
+      cs += (t0 * xh[k].x + t1 * xh[k].y) + (t2 * xh[k].z + t3 * xh[k].w);
+      pg[k].x += dyv[k].x * xh[k].x; pg[k].y += dyv[k].y * xh[k].y;
+      pg[k].z += dyv[k].z * xh[k].z; pg[k].w += dyv[k].w * xh[k].w;
+      pb[k].x += dyv[k].x; pb[k].y += dyv[k].y; pb[k].z += dyv[k].z; pb[k].w += dyv[k].w;
     }
     a = warp_sum(a) / d;
-    c = warp_sum(c) / d;
-    float* o = dx + static_cast<int64_t>(row) * d;
+    cs = warp_sum(cs) / d;
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-      const int j = lane + 32 * k;
-      if (j < d) o[j] += rs * (dyv[k] * gg[k] - a - xh[k] * c);
+    for (int k = 0; k < VPL; ++k) {
+      const int c = lane + 32 * k;
+      if (c >= q) continue;
+      float4 r = dxo[k];
+      r.x += rs * (dyv[k].x * gg[k].x - a - xh[k].x * cs);
+      r.y += rs * (dyv[k].y * gg[k].y - a - xh[k].y * cs);
+      r.z += rs * (dyv[k].z * gg[k].z - a - xh[k].z * cs);
+      r.w += rs * (dyv[k].w * gg[k].w - a - xh[k].w * cs);
+      o[c] = r;
     }
   }
 #pragma unroll
-  for (int k = 0; k < CPL; ++k) {
-    const int j = lane + 32 * k;
-    if (j < d) {
-      red[(warp * 2) * d + j] = pg[k];
-      red[(warp * 2 + 1) * d + j] = pb[k];
+  for (int k = 0; k < VPL; ++k) {
+    const int c = lane + 32 * k;
+    if (c < q) {
+      reinterpret_cast<float4*>(red + (warp * 2) * d)[c] = pg[k];
+      reinterpret_cast<float4*>(red + (warp * 2 + 1) * d)[c] = pb[k];
     }
   }
   __syncthreads();
@@ -180,13 +197,13 @@ __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* 
   }
 }
 
-// out[j] += sum_{blk} ws[blk][j]  (fixed order).  ws laid out [nblk][ncol]; stride = ncol.
 __global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblk, int ncol, int64_t blk_stride,
                                        float* __restrict__ out0, float* __restrict__ out1, int split) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= ncol) return;
   float s = 0.f;
-  for (int k = 0; k < nblk; ++k) s += ws[k * blk_stride + j];
+#pragma unroll 8
+  for (int k = 0; k < nblk; ++k) s += ws[k * blk_stride + j];  // fixed order; loads run ahead
   if (j < split) out0[j] += s;
   else out1[j - split] += s;
 }
@@ -333,19 +350,19 @@ extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* 
                                   float* dx, float* dg, float* db, int M, int d, float* ws, size_t ws_floats,
                                   rlhf_stream_t s) {
   const int nblk = (M + kLnBwdRows - 1) / kLnBwdRows;
-  if (ws_floats < static_cast<size_t>(nblk) * 2 * d) return 2;
+  if (d % 4 || ws_floats < static_cast<size_t>(nblk) * 2 * d) return 2;
   const size_t sm = static_cast<size_t>(16) * d * 4;
   const auto* gp = static_cast<const uint16_t*>(g);
   if (d <= 1024) {
-    cudaFuncSetAttribute(layernorm_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024 * 4);
-    layernorm_bwd_kernel<32><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
+    cudaFuncSetAttribute(layernorm_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024 * 4);
+    layernorm_bwd_kernel<8><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
   } else if (d <= 2048) {
-    cudaFuncSetAttribute(layernorm_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4);
-    layernorm_bwd_kernel<64><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
+    cudaFuncSetAttribute(layernorm_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4);
+    layernorm_bwd_kernel<16><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
   } else {
     return 2;
   }
-  reduce_partials_kernel<<<(2 * d + 255) / 256, 256, 0, S(s)>>>(ws, nblk, 2 * d, 2 * d, dg, db, d);
+  reduce_partials_kernel<<<(2 * d + 63) / 64, 64, 0, S(s)>>>(ws, nblk, 2 * d, 2 * d, dg, db, d);
   return cuda_status();
 }
 
