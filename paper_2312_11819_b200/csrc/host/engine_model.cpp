@@ -114,6 +114,7 @@ void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t*
   }
   // K slices of one 128-row tile form a cluster; keep >= 2 k-blocks per slice
   int split = 1;
+  // up to two CTAs per SM (the kernel then uses a 4-stage ring), >= 2 k-blocks per slice
   while (split < 8 && tiles * split * 2 <= 2 * 148 && kb / (split * 2) >= 2) split *= 2;
   p.splits = split;
   p.pdl = pdl_;

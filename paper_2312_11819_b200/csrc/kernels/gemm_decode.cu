@@ -405,7 +405,14 @@ extern "C" int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t 
   const int splits = p->splits;
   if (splits != 1 && splits != 2 && splits != 4 && splits != 8) return 2;
   const int kb_per = (num_kb + splits - 1) / splits;
-  const int stages = std::min(kb_per, max_kb);  // smem ring (weights stream through it)
+  // smem ring (weights stream through it); a grid larger than the SM count gets a
+  // 4-stage ring so two CTAs fit per SM and every CTA is resident at once
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles_all = (p->M + dec::BM - 1) / dec::BM;
+  const bool big_grid = tiles_all * splits > sms && !p->ln_x;  // (the LN prologue needs every B tile resident)
+  const int stages = std::min(kb_per, big_grid ? std::min(max_kb, 4) : max_kb);
   if (p->ln_x && kb_per > stages) return 2;    // fused LN writes every B tile up front
   CUtensorMap tw, tx;
   if (dec::map2d(&tw, p->W, p->K, p->M, p->ldw, dec::BM)) return 2;

@@ -18,7 +18,9 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--no-graph", action="store_true")
 ap.add_argument("--graph-mode", type=int, default=1, help="1: graph + PDL, 2: graph without PDL")
 a = ap.parse_args()
-cfg = make_config("opt-125m", "opt-125m", 32, 256, 256) if a.workload == "c2" else make_config("tiny", "tiny", 4, 16, 16)
+cfg = {"c2": lambda: make_config("opt-125m", "opt-125m", 32, 256, 256),
+       "c3": lambda: make_config("opt-1.3b", "opt-350m", 16, 256, 256),
+       "c1": lambda: make_config("tiny", "tiny", 4, 16, 16)}[a.workload]()
 eng = Engine(cfg, cuda_graph=0 if a.no_graph else a.graph_mode)
 for _ in range(a.steps):
     rep = eng.step()
