@@ -116,6 +116,8 @@ void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t*
   int split = 1;
   // up to two CTAs per SM (the kernel then uses a 4-stage ring), >= 2 k-blocks per slice
   while (split < 8 && tiles * split * 2 <= 2 * 148 && kb / (split * 2) >= 2) split *= 2;
+  // very long K (OPT-1.3B FFN-down, K = 8192) on few tiles: a 16-CTA cluster per tile
+  if (split == 8 && tiles * 16 <= 2 * 148 && kb / 16 >= 8) split = 16;
   p.splits = split;
   p.pdl = pdl_;
   K(rlhf_gemm_decode(&p, stream_), 1);

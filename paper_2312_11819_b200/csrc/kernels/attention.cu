@@ -395,8 +395,19 @@ static int launch_dec(int grid, cudaStream_t st, const uint16_t* q, int H, int S
     case 2: return launch_dec_ns<HD, 2>(grid, st, q, H, Smax, k, v, pos_dev, o);
     case 4: return launch_dec_ns<HD, 4>(grid, st, q, H, Smax, k, v, pos_dev, o);
     case 8: return launch_dec_ns<HD, 8>(grid, st, q, H, Smax, k, v, pos_dev, o);
-    default: return launch_dec_ns<HD, DecCfg<HD>::NS>(grid, st, q, H, Smax, k, v, pos_dev, o);
+    default: break;
   }
+  // one wave: 4 ring slots (3 CTAs / SM) while the (sample, head) grid fits, else 3 slots
+  // (4 CTAs / SM), else 2
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (HD == 128 || grid <= 3 * sms) return launch_dec_ns<HD, DecCfg<HD>::NS>(grid, st, q, H, Smax, k, v, pos_dev, o);
+  if (grid <= 4 * sms) return launch_dec_ns<HD, 3>(grid, st, q, H, Smax, k, v, pos_dev, o);
+  return launch_dec_ns<HD, 2>(grid, st, q, H, Smax, k, v, pos_dev, o);
 }
 
 extern "C" int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax, const void* kcache, const void* vcache,

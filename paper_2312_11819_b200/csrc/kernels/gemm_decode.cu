@@ -373,6 +373,8 @@ int launch(const CUtensorMap& tw, const CUtensorMap& tx, const Args& a, int tile
   if (!init) {
     if (cudaFuncSetAttribute(gemm_decode_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
       return 5;
+    // 16 K-slices per tile = a 16-CTA cluster (non-portable size, allowed on B200)
+    cudaFuncSetAttribute(gemm_decode_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     init = true;
   }
   cudaLaunchConfig_t cfg{};
@@ -403,7 +405,7 @@ extern "C" int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t 
   const int num_kb = (p->K + dec::BK - 1) / dec::BK;
   const int max_kb = bn == 32 ? dec::Cfg<32>::MAX_KB : dec::Cfg<64>::MAX_KB;
   const int splits = p->splits;
-  if (splits != 1 && splits != 2 && splits != 4 && splits != 8) return 2;
+  if (splits != 1 && splits != 2 && splits != 4 && splits != 8 && splits != 16) return 2;
   const int kb_per = (num_kb + splits - 1) / splits;
   // smem ring (weights stream through it); a grid larger than the SM count gets a
   // 4-stage ring so two CTAs fit per SM and every CTA is resident at once

@@ -168,7 +168,7 @@ def test_gemm_decode_fused_layernorm(M, K, N, splits):
     close(out, exp, 2e-2)  # bf16 rounding of h may flip between the two LN evaluations
 
 
-@pytest.mark.parametrize("M,K,N,splits", [(2048, 8192, 16, 8), (1024, 4096, 16, 2), (2048, 2048, 64, 1)])
+@pytest.mark.parametrize("M,K,N,splits", [(2048, 8192, 16, 8), (2048, 8192, 16, 16), (1024, 4096, 16, 2), (2048, 2048, 64, 1)])
 def test_gemm_decode_ring_long_k(M, K, N, splits):
     """K slices longer than the smem ring (OPT-1.3B FFN-down: K = 8192)."""
     from paper_2312_11819_b200 import ops
