@@ -206,6 +206,10 @@ void Engine::forward(const Decoder& m, const int32_t* tokens, int B, int tok_str
 void Engine::attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd) {
   const int d = H * hd;
   const int64_t TT = static_cast<int64_t>(T) * T;
+  static const bool unfused = getenv("RLHF_ATTN_UNFUSED") != nullptr;  // A/B switch for timing
+  if (!unfused && hd == 64 && T % 128 == 0 && T <= 512) {
+    K(rlhf_attn_fwd_fused(qkv, B, H, hd, T, 1.0f / std::sqrt(static_cast<float>(hd)), P, stream_), 1);
+  } else {
   rlhf_gemm_params s{};
   s.M = T; s.N = T; s.K = hd; s.batch = B * H; s.batch_h = H;
   s.A = qkv; s.lda = 3 * d; s.a_stride_h = hd; s.a_stride_b = static_cast<int64_t>(T) * 3 * d;
@@ -215,6 +219,7 @@ void Engine::attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B,
   s.causal = 1;
   gemm(s);
   K(rlhf_attn_softmax(ar_.scores, P, B * H, T, stream_), 1);
+  }
   rlhf_gemm_params pv{};
   pv.M = T; pv.N = hd; pv.K = T; pv.batch = B * H; pv.batch_h = H;
   pv.A = P; pv.lda = T; pv.a_stride_h = TT; pv.a_stride_b = H * TT;

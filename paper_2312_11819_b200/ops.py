@@ -142,3 +142,15 @@ def attn_decode(qkv: torch.Tensor, kcache: torch.Tensor, vcache: torch.Tensor, p
     if rc:
         raise RuntimeError(f"rlhf_attn_decode failed ({rc})")
     return out
+
+
+def attn_fwd_fused(qkv: torch.Tensor, B: int, H: int, S: int, alpha: float) -> torch.Tensor:
+    """P = bf16(causal softmax(alpha Q K^T)) per (b, h) from packed qkv rows (rlhf_attn_fwd_fused)."""
+    L = lib()
+    L.rlhf_attn_fwd_fused.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_void_p]
+    hd = qkv.shape[1] // (3 * H)
+    P = torch.zeros(B, H, S, S, device=qkv.device, dtype=torch.bfloat16)
+    rc = L.rlhf_attn_fwd_fused(qkv.data_ptr(), B, H, hd, S, alpha, P.data_ptr(), _stream())
+    if rc:
+        raise RuntimeError(f"rlhf_attn_fwd_fused failed ({rc})")
+    return P

@@ -48,3 +48,24 @@ def test_attn_decode_large_grid_matches_torch(ctx):
     p = torch.softmax(s, -1).bfloat16().float()
     ref = (p @ vc[:, :, :ctx].float()).view(B, d)
     torch.testing.assert_close(got, ref, atol=2e-2, rtol=2e-2)
+
+
+@pytest.mark.parametrize("B,H,S", [(2, 3, 128), (2, 12, 512), (3, 4, 256)])
+def test_attn_fwd_fused_matches_torch(B, H, S):
+    """Fused scores + causal softmax (tcgen05, TMEM online softmax) vs fp32 torch:
+    probabilities within bf16 rounding; exact zeros above the diagonal of each block."""
+    import torch
+    from paper_2312_11819_b200 import ops
+    torch.manual_seed(S + H)
+    hd = 64
+    d = H * hd
+    qkv = (torch.randn(B * S, 3 * d, device="cuda") * 1.5).bfloat16()
+    P = ops.attn_fwd_fused(qkv, B, H, S, 0.125).float()
+    q = qkv[:, :d].float().view(B, S, H, hd).transpose(1, 2)
+    k = qkv[:, d:2 * d].float().view(B, S, H, hd).transpose(1, 2)
+    s = (q @ k.transpose(-1, -2)) * 0.125
+    mask = torch.ones(S, S, device="cuda", dtype=torch.bool).tril()
+    ref = torch.softmax(s.masked_fill(~mask, float("-inf")), -1)
+    torch.cuda.synchronize()
+    assert (P - ref).abs().max().item() <= 4e-3 * ref.abs().max().item() + 1e-6
+    assert (P[..., ~mask] == 0).all()
