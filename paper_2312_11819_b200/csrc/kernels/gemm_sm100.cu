@@ -43,7 +43,7 @@ struct TileCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES = kEpiWarps * 32 * kStagePitch * 4;  // per-epilogue-warp transpose tiles
   // narrow tiles serve decode (few k-blocks per unit): 3 stages -> 2 CTAs/SM
-  static constexpr int RAW_STAGES = BN <= 64 ? 3 : (218 * 1024 - EPI_BYTES) / STAGE_BYTES;
+  static constexpr int RAW_STAGES = BN <= 32 ? 3 : (218 * 1024 - EPI_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = RAW_STAGES > 8 ? 8 : RAW_STAGES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * BN;
