@@ -57,9 +57,17 @@ typedef struct rlhf_gemm_params {
   void* workspace; size_t workspace_bytes;
   int* counters; int counters_len;
   unsigned long long* probe; /* optional: per-CTA phase timestamps (clock64), 8 per CTA */
+  /* optional, column-major swap-AB outputs only (LM head of a decode step): instead of
+   * storing C, write per (128-row tile, column n) the top-2 of the tile's rows as
+   * float4 {max, bits(argmax, lowest id on ties), second, 0} at top2[(tile*N + n)*4] */
+  float* top2;
 } rlhf_gemm_params;
 
 int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t s);
+/* Merge per-tile top-2 partials (rlhf_gemm_params.top2) of `tiles` tiles: greedy token
+ * (ties -> lowest id) -> tok[b*tok_stride + *pos + 1], margin (top1 - top2) likewise. */
+int rlhf_argmax_tiles(const float* top2, int tiles, int B, int32_t* tok, int64_t tok_stride, const int* pos,
+                      float* margin, rlhf_stream_t s);
 
 /* ---- decode GEMM (Generation): Y^T[N, M] = W[M, K] . X[N, K]^T, N <= 64 -----
  * swap-AB tcgen05; each 128-row weight tile is a thread-block cluster of `splits`

@@ -223,6 +223,7 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
     dec_f_.alloc(static_cast<size_t>(gen_B_) * cfg_.actor.d_ff * 2);
     dec_hf_.alloc(static_cast<size_t>(gen_B_) * ad * 2);
     dec_logits_.alloc(static_cast<size_t>(gen_B_) * cfg_.actor.vocab * 4);
+    dec_top2_.alloc(static_cast<size_t>((cfg_.actor.vocab + 127) / 128) * gen_B_ * 16);
     argmax_ws_.alloc(static_cast<size_t>(gen_B_) * 64 * 4 * 4);
   }
   pos_.alloc(16);

@@ -98,6 +98,7 @@ class Engine {
   void lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits);
   void generate(const Decoder& m, int B, bool teacher_forced);
   void decode_step(const Decoder& m, int B);
+  void lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t* dst);
   void train_actor(Decoder& m, int B, ncclComm_t comm);
   void train_critic(Decoder& m, int B, ncclComm_t comm);
   void adam(Decoder& m, float lr);
@@ -145,6 +146,7 @@ class Engine {
   DevBuf tokens_, tok2_, pred_, margin_, pos_, prompt_stage_;
   DevBuf logp_old_, logp_ref_, values_, score_, rewards_, adv_, ret_, logp_new_, values_new_, gbuf_, loss_, out2_, score2_;
   DevBuf loop_ws_;  // persistent decode loop workspace
+  DevBuf dec_top2_;  // LM-head per-tile top-2 partials [V/128][B] x float4
   DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_hf_, dec_logits_, argmax_ws_;
   cudaGraphExec_t decode_graph_ = nullptr;
   int graph_launches_ = 0;

@@ -390,10 +390,26 @@ void Engine::decode_step(const Decoder& m, int B) {
     return;
   }
   K(rlhf_layernorm(x, m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), dec_hf_.as<uint16_t>(), nullptr, nullptr, B, d, stream_), 1);
-  linear_decode(m.T(RLHF_T_TOK_EMB), V, d, dec_hf_.as<uint16_t>(), B, nullptr, dec_logits_.as<float>(), true, false, nullptr);
   int32_t* dst = graph_for_pred_ ? pred_.as<int32_t>() : tokens_.as<int32_t>();
-  K(rlhf_argmax_tokens(dec_logits_.as<float>(), B, V, dst, S_, pos, margin_.as<float>(), argmax_ws_.as<float>(), stream_), 2);
+  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);
   K(rlhf_add_int(pos, 1, stream_), 1);
+}
+
+// Tied LM head of the final hidden rows hf [B, d] fused with the greedy sampler: the
+// swap-AB GEMM keeps only each 128-token tile's top-2 per sample (logits never stored),
+// then one warp per sample merges the tiles -> dst[b*S + *pos + 1] and the margin.
+void Engine::lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t* dst) {
+  const int d = m.a.d_model, V = m.a.vocab;
+  rlhf_gemm_params q{};
+  q.M = V; q.N = B; q.K = d; q.batch = 1; q.batch_h = 1;
+  q.A = m.T(RLHF_T_TOK_EMB); q.lda = d;
+  q.B = hf; q.ldb = d;
+  q.C = dec_logits_.p; q.c_f32 = 1; q.c_rs = 1; q.c_cs = V;
+  q.alpha = 1.0f;
+  q.top2 = dec_top2_.as<float>();
+  gemm(q);
+  K(rlhf_argmax_tiles(dec_top2_.as<float>(), (V + 127) / 128, B, dst, S_, pos_.as<int>(), margin_.as<float>(), stream_),
+    1);
 }
 
 // Greedy generation of R tokens for the B prompts already in tokens_[:, :P].
@@ -403,12 +419,10 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   // prefill: forward over the prompt, K/V stored for every prompt position
   forward(m, tokens_.as<int32_t>(), B, S_, P_, false, &kv_);
   K(rlhf_gather_rows(ar_.hf, dec_hf_.p, B, P_, 1, P_ - 1, d, 2, stream_), 1);
-  linear_decode(m.T(RLHF_T_TOK_EMB), V, d, dec_hf_.as<uint16_t>(), B, nullptr, dec_logits_.as<float>(), true, false, nullptr);
   const int start = P_ - 1;
   cudaMemcpyAsync(pos_.p, &start, sizeof(int), cudaMemcpyHostToDevice, stream_);
   int32_t* dst = teacher_forced ? pred_.as<int32_t>() : tokens_.as<int32_t>();
-  K(rlhf_argmax_tokens(dec_logits_.as<float>(), B, V, dst, S_, pos_.as<int>(), margin_.as<float>(), argmax_ws_.as<float>(),
-                       stream_), 2);
+  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);
   K(rlhf_add_int(pos_.as<int>(), 1, stream_), 1);
   cudaEventRecord(ev_[1], stream_);  // prefill done
   if (R_ <= 1) return;

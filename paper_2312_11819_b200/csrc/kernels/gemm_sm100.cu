@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cfloat>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -45,7 +46,8 @@ struct TileCfg {
   // narrow tiles serve decode (few k-blocks per unit): 3 stages -> 2 CTAs/SM
   static constexpr int RAW_STAGES = BN <= 32 ? 3 : (218 * 1024 - EPI_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = RAW_STAGES > 8 ? 8 : RAW_STAGES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+  static constexpr int TOP2_BYTES = 4 * 32 * 16;  // per-quarter top-2 of a 32-column chunk
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + TOP2_BYTES + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -68,6 +70,7 @@ struct GemmArgs {
   int* counters;
   unsigned long long* probe;
   int debug;
+  float* top2;  // column-major top-2 epilogue (decode LM head): [tile][N] x float4
 };
 
 __device__ __forceinline__ unsigned long long clk() {
@@ -367,7 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);
+  float4* t2s = reinterpret_cast<float4*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);  // [4][32]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES + Cfg::TOP2_BYTES);
   uint64_t* empty_bar = full_bar + Cfg::STAGES;
   uint64_t* tfull = empty_bar + Cfg::STAGES;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;               // [2] accumulator drained
@@ -517,7 +521,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (c == half) PROBE(9);
         if constexpr (!row_major) {
-          if (!part) epi_column32(e, w.b, w.h, mq + static_cast<int>(lane), w.n0 + c * 32, st + lane * kStagePitch);
+          if (e.top2) {  // per column: top-2 over this tile's rows (lane j scans staged column j)
+            float4 keep = make_float4(-FLT_MAX, __int_as_float(0x7fffffff), -FLT_MAX, 0.f);
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) {
+              const int m = mq + r;
+              if (m >= e.M) break;
+              const float x = st[r * kStagePitch + lane] * e.alpha;
+              if (x > keep.x) {  // rows ascend: ties keep the lower id
+                keep.z = keep.x;
+                keep.x = x;
+                keep.y = __int_as_float(m);
+              } else {
+                keep.z = fmaxf(keep.z, x);
+              }
+            }
+            t2s[q * 32 + lane] = keep;
+            named_bar_sync(2, 32 * kEpiWarps);
+            if (q == 0) {
+              float4 r = t2s[lane];
+#pragma unroll
+              for (int qq = 1; qq < 4; ++qq) {
+                const float4 o = t2s[qq * 32 + lane];
+                if (o.x > r.x || (o.x == r.x && __float_as_int(o.y) < __float_as_int(r.y))) {
+                  r = make_float4(o.x, o.y, fmaxf(r.x, o.z), 0.f);
+                } else {
+                  r.z = fmaxf(r.z, o.x);
+                }
+              }
+              const int n = w.n0 + c * 32 + static_cast<int>(lane);
+              if (n < e.N) reinterpret_cast<float4*>(e.top2)[static_cast<size_t>(w.m_tile) * e.N + n] = r;
+            }
+            named_bar_sync(2, 32 * kEpiWarps);
+          } else if (!part) {
+            epi_column32(e, w.b, w.h, mq + static_cast<int>(lane), w.n0 + c * 32, st + lane * kStagePitch);
+          }
         }
         if (row_major || part) {
           // lane l owns rows l/4 + 8i (i < 4), columns 8*(l%4)..+8 -> 64 B contiguous per row
@@ -1024,6 +1062,9 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
   a.residual = p->residual;
   a.causal = p->causal;
   a.probe = p->probe;
+  a.top2 = p->top2;
+  if (a.top2 && (p->c_cs == 1 || p->split_k > 1 || p->batch != 1 || bn != 32 && bn != 64 && bn != 128 && bn != 256))
+    return 2;
   {
     static int dbg = -1;
     if (dbg < 0) dbg = getenv("RLHF_GEMM_DEBUG") ? atoi(getenv("RLHF_GEMM_DEBUG")) : 0;
