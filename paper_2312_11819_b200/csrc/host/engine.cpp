@@ -149,58 +149,13 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
   if (hosts_[4]) init_decoder(shadow_actor_, fixed(cfg_.actor, 0), rlhf_model_seed(cfg_.seed, 0), false);
   if (hosts_[5]) init_decoder(shadow_critic_, fixed(cfg_.critic, 1), rlhf_model_seed(cfg_.seed, 1), false);
 
-  // ---- activation arena: capacities = max over hosted models ------------------
-  Arena& A = ar_;
-  A.B = Bcap_;
-  A.S = S_;
-  A.R = R_;
-  for (const rlhf_arch* a : {&cfg_.actor, &cfg_.critic}) {
-    A.d = std::max(A.d, a->d_model);
-    A.ff = std::max(A.ff, a->d_ff);
-    A.H = std::max(A.H, a->n_heads);
-    A.V = std::max(A.V, a->vocab);
-    A.L = std::max(A.L, a->n_layers);
+  // ---- activation arenas: the main one, plus a forward-only one for the second
+  // stream of the Co-located Forward stage (Critic + Reward beside Actor + Ref)
+  build_arena(ar_main_, hosts_[0] || hosts_[1]);
+  if (tag_ == StrategyTag::Colocated) {
+    build_arena(ar_side_, true);  // also trains the Critic beside the Actor
+    CK(cudaStreamCreateWithFlags(&stream_side_, cudaStreamNonBlocking));
   }
-  A.T = static_cast<int64_t>(Bcap_) * S_;
-  A.Z = static_cast<int64_t>(Bcap_) * A.H;
-  auto mk = [&](size_t bytes) {
-    DevBuf* b = new DevBuf(bytes);
-    A.owned.push_back(b);
-    return b->p;
-  };
-  const bool trains = hosts_[0] || hosts_[1];
-  const int64_t T = A.T, d = A.d, SS = static_cast<int64_t>(A.S) * A.S, BR = static_cast<int64_t>(Bcap_) * R_;
-  const int64_t Ls = trains ? A.L : 1;  // layers of saved activations (inference-only ranks keep one)
-  A.xres = static_cast<float*>(mk((2 * Ls + 1) * T * d * 4));
-  A.mean = static_cast<float*>(mk((2 * Ls + 1) * T * 4));
-  A.rstd = static_cast<float*>(mk((2 * Ls + 1) * T * 4));
-  A.h1 = static_cast<uint16_t*>(mk(Ls * T * d * 2));
-  A.qkv = static_cast<uint16_t*>(mk(Ls * T * 3 * d * 2));
-  A.P = static_cast<uint16_t*>(mk(Ls * A.Z * SS * 2));
-  A.o = static_cast<uint16_t*>(mk(Ls * T * d * 2));
-  A.h2 = static_cast<uint16_t*>(mk(Ls * T * d * 2));
-  A.f = static_cast<uint16_t*>(mk(Ls * T * A.ff * 2));
-  A.hf = static_cast<uint16_t*>(mk(T * d * 2));
-  A.scores = static_cast<float*>(mk(A.Z * SS * 4));
-  A.dS = static_cast<uint16_t*>(mk(trains ? A.Z * SS * 2 : 16));
-  A.hf_resp = static_cast<uint16_t*>(mk(BR * d * 2));
-  A.logits = static_cast<float*>(mk(BR * A.V * 4));
-  A.lse = static_cast<float*>(mk(BR * 4));
-  A.dz = static_cast<uint16_t*>(mk(trains ? BR * A.V * 2 : 16));
-  A.dhf_resp = static_cast<float*>(mk(trains ? BR * d * 4 : 16));
-  A.dres = static_cast<float*>(mk(trains ? T * d * 4 : 16));
-  A.dhf = static_cast<float*>(mk(trains ? T * d * 4 : 16));
-  A.dh = static_cast<float*>(mk(trains ? T * d * 4 : 16));
-  A.g = static_cast<uint16_t*>(mk(trains ? T * d * 2 : 16));
-  A.dpre = static_cast<uint16_t*>(mk(trains ? T * A.ff * 2 : 16));
-  A.dov = static_cast<uint16_t*>(mk(trains ? T * d * 2 : 16));
-  A.dqkv = static_cast<uint16_t*>(mk(trains ? T * 3 * d * 2 : 16));
-  A.ws_floats = std::max<size_t>(static_cast<size_t>((T + 31) / 32) * 2 * d, 64 * static_cast<size_t>(std::max<int64_t>(3 * d, A.ff)));
-  A.ws = static_cast<float*>(mk(A.ws_floats * 4));
-  A.gemm_ws_bytes = 64ull << 20;
-  A.gemm_ws = static_cast<float*>(mk(A.gemm_ws_bytes));
-  A.counters_len = 1 << 16;
-  A.counters = static_cast<int*>(mk(A.counters_len * 4));
 
   // ---- generation state (the generator: Actor or ShadowActor) -----------------
   if (hosts_[0] && tag_ != StrategyTag::Disaggregated) generator_ = &actor_;
@@ -234,7 +189,8 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
   pred_.alloc(bs * 4);
   margin_.alloc(bs * 4);
   prompt_stage_.alloc(static_cast<size_t>(Bg_) * P_ * 4);
-  for (DevBuf* b : {&logp_old_, &logp_ref_, &values_, &rewards_, &adv_, &ret_, &logp_new_, &values_new_, &gbuf_, &out2_})
+  for (DevBuf* b : {&logp_old_, &logp_ref_, &values_, &rewards_, &adv_, &ret_, &logp_new_, &values_new_, &gbuf_, &gbuf2_,
+                    &out2_})
     b->alloc(br * 4);
   score_.alloc(static_cast<size_t>(Bcap_) * 4);
   score2_.alloc(static_cast<size_t>(Bcap_) * 4);
@@ -260,6 +216,7 @@ Engine::~Engine() {
     if (c) nccl().CommDestroy(c);
   for (auto& e : ev_) cudaEventDestroy(e);
   if (stream_) cudaStreamDestroy(stream_);
+  if (stream_side_) cudaStreamDestroy(stream_side_);
 }
 
 void Engine::allreduce_grads(Decoder& m, ncclComm_t comm) {
@@ -288,22 +245,22 @@ void Engine::train_actor(Decoder& m, int B, ncclComm_t comm) {
   lm_logprobs(m, tokens_.as<int32_t>(), B, logp_new_.as<float>(), true);
   K(rlhf_ppo_actor_loss(logp_new_.as<float>(), logp_old_.as<float>(), adv_.as<float>(), BR, cfg_.cliprange, denom,
                         gbuf_.as<float>(), loss_.as<float>(), stream_), 1);
-  K(rlhf_logprob_bwd(ar_.logits, ar_.lse, gbuf_.as<float>(), BR, V, tokens_.as<int32_t>(), S_, P_, R_, ar_.dz, stream_), 1);
+  K(rlhf_logprob_bwd(arp_->logits, arp_->lse, gbuf_.as<float>(), BR, V, tokens_.as<int32_t>(), S_, P_, R_, arp_->dz, stream_), 1);
   // dhf_resp = dz E ; dE += dz^T hf_resp
   rlhf_gemm_params p{};
   p.M = BR; p.N = d; p.K = V; p.batch = 1; p.batch_h = 1;
-  p.A = ar_.dz; p.lda = V;
+  p.A = arp_->dz; p.lda = V;
   p.B = m.T(RLHF_T_TOK_EMB); p.b_mn_major = 1; p.ldb = d;
-  p.C = ar_.dhf_resp; p.c_f32 = 1; p.c_rs = d; p.c_cs = 1; p.alpha = 1.0f;
+  p.C = arp_->dhf_resp; p.c_f32 = 1; p.c_rs = d; p.c_cs = 1; p.alpha = 1.0f;
   gemm(p);
   rlhf_gemm_params q{};
   q.M = V; q.N = d; q.K = BR; q.batch = 1; q.batch_h = 1;
-  q.A = ar_.dz; q.a_mn_major = 1; q.lda = V;
-  q.B = ar_.hf_resp; q.b_mn_major = 1; q.ldb = d;
+  q.A = arp_->dz; q.a_mn_major = 1; q.lda = V;
+  q.B = arp_->hf_resp; q.b_mn_major = 1; q.ldb = d;
   q.C = m.G(RLHF_T_TOK_EMB); q.c_f32 = 1; q.c_rs = d; q.c_cs = 1; q.alpha = 1.0f; q.accumulate = 1;
   gemm(q);
-  cudaMemsetAsync(ar_.dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
-  K(rlhf_scatter_rows_f32(ar_.dhf_resp, ar_.dhf, B, S_, R_, P_ - 1, d, stream_), 1);
+  cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
+  K(rlhf_scatter_rows_f32(arp_->dhf_resp, arp_->dhf, B, S_, R_, P_ - 1, d, stream_), 1);
   backward(m, tokens_.as<int32_t>(), B, S_);
   allreduce_grads(m, comm);
   adam(m, cfg_.lr_actor);
@@ -314,12 +271,12 @@ void Engine::train_critic(Decoder& m, int B, ncclComm_t comm) {
   const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator : static_cast<float>(BR);
   cudaMemsetAsync(m.grad.p, 0, static_cast<size_t>(m.n) * 4, stream_);
   forward(m, tokens_.as<int32_t>(), B, S_, S_, true, nullptr);
-  K(rlhf_scalar_head(ar_.hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, d, values_new_.as<float>(), stream_), 1);
+  K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, d, values_new_.as<float>(), stream_), 1);
   K(rlhf_ppo_critic_loss(values_new_.as<float>(), values_.as<float>(), ret_.as<float>(), BR, cfg_.cliprange_value, denom,
-                         gbuf_.as<float>(), loss_.as<float>() + 1, stream_), 1);
-  cudaMemsetAsync(ar_.dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
-  K(rlhf_scalar_head_bwd(ar_.hf, m.T(RLHF_T_VHEAD), gbuf_.as<float>(), B, S_, R_, P_ - 1, d, ar_.dhf, m.G(RLHF_T_VHEAD),
-                         ar_.ws, stream_), 2);
+                         gbuf2_.as<float>(), loss_.as<float>() + 1, stream_), 1);
+  cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
+  K(rlhf_scalar_head_bwd(arp_->hf, m.T(RLHF_T_VHEAD), gbuf2_.as<float>(), B, S_, R_, P_ - 1, d, arp_->dhf, m.G(RLHF_T_VHEAD),
+                         arp_->ws, stream_), 2);
   backward(m, tokens_.as<int32_t>(), B, S_);
   allreduce_grads(m, comm);
   adam(m, cfg_.lr_critic);
@@ -332,11 +289,66 @@ void Engine::score_logp(const Decoder& m, const int32_t* tok, int B, float* logp
 }
 void Engine::score_values(const Decoder& m, const int32_t* tok, int B, float* values) {
   forward(m, tok, B, S_, S_, false, nullptr);
-  K(rlhf_scalar_head(ar_.hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, m.a.d_model, values, stream_), 1);
+  K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, m.a.d_model, values, stream_), 1);
 }
 void Engine::score_reward(const Decoder& m, const int32_t* tok, int B, float* score) {
   forward(m, tok, B, S_, S_, false, nullptr);
-  K(rlhf_scalar_head(ar_.hf, m.T(RLHF_T_VHEAD), B, S_, 1, S_ - 1, m.a.d_model, score, stream_), 1);
+  K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, 1, S_ - 1, m.a.d_model, score, stream_), 1);
+}
+
+// Activation arena: capacities = max over hosted models.  `trains` keeps every layer's
+// saved activations and the backward buffers; a forward-only arena keeps one layer.
+void Engine::build_arena(Arena& A, bool trains) {
+  A.B = Bcap_;
+  A.S = S_;
+  A.R = R_;
+  for (const rlhf_arch* a : {&cfg_.actor, &cfg_.critic}) {
+    A.d = std::max(A.d, a->d_model);
+    A.ff = std::max(A.ff, a->d_ff);
+    A.H = std::max(A.H, a->n_heads);
+    A.V = std::max(A.V, a->vocab);
+    A.L = std::max(A.L, a->n_layers);
+  }
+  A.T = static_cast<int64_t>(Bcap_) * S_;
+  A.Z = static_cast<int64_t>(Bcap_) * A.H;
+  auto mk = [&](size_t bytes) {
+    DevBuf* b = new DevBuf(bytes);
+    A.owned.push_back(b);
+    return b->p;
+  };
+  const int64_t T = A.T, d = A.d, SS = static_cast<int64_t>(A.S) * A.S, BR = static_cast<int64_t>(Bcap_) * R_;
+  const int64_t Ls = trains ? A.L : 1;  // layers of saved activations (inference-only ranks keep one)
+  A.xres = static_cast<float*>(mk((2 * Ls + 1) * T * d * 4));
+  A.mean = static_cast<float*>(mk((2 * Ls + 1) * T * 4));
+  A.rstd = static_cast<float*>(mk((2 * Ls + 1) * T * 4));
+  A.h1 = static_cast<uint16_t*>(mk(Ls * T * d * 2));
+  A.qkv = static_cast<uint16_t*>(mk(Ls * T * 3 * d * 2));
+  A.P = static_cast<uint16_t*>(mk(Ls * A.Z * SS * 2));
+  A.o = static_cast<uint16_t*>(mk(Ls * T * d * 2));
+  A.h2 = static_cast<uint16_t*>(mk(Ls * T * d * 2));
+  A.f = static_cast<uint16_t*>(mk(Ls * T * A.ff * 2));
+  A.hf = static_cast<uint16_t*>(mk(T * d * 2));
+  A.scores = static_cast<float*>(mk(A.Z * SS * 4));
+  A.dS = static_cast<uint16_t*>(mk(trains ? A.Z * SS * 2 : 16));
+  A.hf_resp = static_cast<uint16_t*>(mk(BR * d * 2));
+  A.logits = static_cast<float*>(mk(BR * A.V * 4));
+  A.lse = static_cast<float*>(mk(BR * 4));
+  A.dz = static_cast<uint16_t*>(mk(trains ? BR * A.V * 2 : 16));
+  A.dhf_resp = static_cast<float*>(mk(trains ? BR * d * 4 : 16));
+  A.dres = static_cast<float*>(mk(trains ? T * d * 4 : 16));
+  A.dhf = static_cast<float*>(mk(trains ? T * d * 4 : 16));
+  A.dh = static_cast<float*>(mk(trains ? T * d * 4 : 16));
+  A.g = static_cast<uint16_t*>(mk(trains ? T * d * 2 : 16));
+  A.dpre = static_cast<uint16_t*>(mk(trains ? T * A.ff * 2 : 16));
+  A.dov = static_cast<uint16_t*>(mk(trains ? T * d * 2 : 16));
+  A.dqkv = static_cast<uint16_t*>(mk(trains ? T * 3 * d * 2 : 16));
+  A.ws_floats = std::max<size_t>(static_cast<size_t>((T + 31) / 32) * 2 * d, 64 * static_cast<size_t>(std::max<int64_t>(3 * d, A.ff)));
+  A.ws = static_cast<float*>(mk(A.ws_floats * 4));
+  A.gemm_ws_bytes = 64ull << 20;
+  A.gemm_ws = static_cast<float*>(mk(A.gemm_ws_bytes));
+  A.counters_len = 1 << 16;
+  A.counters = static_cast<int*>(mk(A.counters_len * 4));
+
 }
 
 void Engine::gae(int B) {
@@ -374,15 +386,35 @@ void Engine::step(const int32_t* prompts_host, rlhf_step_report* rep) {
       place_prompts(prompt_stage_.as<int32_t>(), 0);
       generate(actor_, Bg, false);
       cudaEventRecord(ev_[2], stream_);
-      // Forward x4 in the reference's order (workload.cpp:119)
-      score_logp(actor_, tok, Bg, logp_old_.as<float>());
+      // Forward x4 (workload.cpp:119 lists Actor, Critic, Ref, Reward; they are
+      // independent): Critic + Reward on a second stream with their own arena, Actor +
+      // Ref on the main stream, joined before the experience-buffer barrier
+      cudaEventRecord(ev_[6], stream_);
+      CK(cudaStreamWaitEvent(stream_side_, ev_[6], 0));
+      std::swap(stream_, stream_side_);
+      arp_ = &ar_side_;
       score_values(critic_, tok, Bg, values_.as<float>());
-      score_logp(ref_, tok, Bg, logp_ref_.as<float>());
       score_reward(reward_, tok, Bg, score_.as<float>());
+      cudaEventRecord(ev_[7], stream_);
+      std::swap(stream_, stream_side_);
+      arp_ = &ar_main_;
+      score_logp(actor_, tok, Bg, logp_old_.as<float>());
+      score_logp(ref_, tok, Bg, logp_ref_.as<float>());
+      CK(cudaStreamWaitEvent(stream_, ev_[7], 0));
       cudaEventRecord(ev_[3], stream_);
       gae(Bg);
-      train_actor(actor_, Bg, actor_comm_);
+      // TrainFB(Actor) and TrainFB(Critic) are independent given the experience buffer:
+      // the Critic trains on the second stream / arena
+      cudaEventRecord(ev_[6], stream_);
+      CK(cudaStreamWaitEvent(stream_side_, ev_[6], 0));
+      std::swap(stream_, stream_side_);
+      arp_ = &ar_side_;
       train_critic(critic_, Bg, critic_comm_);
+      cudaEventRecord(ev_[7], stream_);
+      std::swap(stream_, stream_side_);
+      arp_ = &ar_main_;
+      train_actor(actor_, Bg, actor_comm_);
+      CK(cudaStreamWaitEvent(stream_, ev_[7], 0));
       cudaEventRecord(ev_[4], stream_);
       break;
     }

@@ -108,6 +108,7 @@ class Engine {
   void score_values(const Decoder& m, const int32_t* tok, int B, float* values);
   void score_reward(const Decoder& m, const int32_t* tok, int B, float* score);
   void gae(int B);
+  void build_arena(Arena& A, bool trains);
   void place_prompts(const int32_t* dev_prompts, int row0);
 
   // GEMM helpers (all go through rlhf_gemm)
@@ -131,6 +132,7 @@ class Engine {
   PlacementPlan plan_;
   StrategyTag tag_ = StrategyTag::Colocated;
   cudaStream_t stream_ = nullptr;
+  cudaStream_t stream_side_ = nullptr;  // second stream of the Co-located Forward stage
   ncclComm_t world_ = nullptr, actor_comm_ = nullptr, critic_comm_ = nullptr;
   double comm_bytes_ = 0;
   std::vector<int> sample_ids_;
@@ -140,11 +142,13 @@ class Engine {
 
   Decoder actor_, critic_, ref_, reward_, shadow_actor_, shadow_critic_;
   Decoder* generator_ = nullptr;
-  Arena ar_;
+  Arena ar_main_, ar_side_;   // activation arenas (main stream / second Forward stream)
+  Arena* arp_ = &ar_main_;  // the arena the stream_ currently in use writes
   KVCache kv_;
   // per-step buffers
   DevBuf tokens_, tok2_, pred_, margin_, pos_, prompt_stage_;
-  DevBuf logp_old_, logp_ref_, values_, score_, rewards_, adv_, ret_, logp_new_, values_new_, gbuf_, loss_, out2_, score2_;
+  DevBuf logp_old_, logp_ref_, values_, score_, rewards_, adv_, ret_, logp_new_, values_new_, gbuf_, gbuf2_, loss_, out2_,
+      score2_;
   DevBuf loop_ws_;  // persistent decode loop workspace
   DevBuf dec_top2_;  // LM-head per-tile top-2 partials [V/128][B] x float4
   DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_hf_, dec_logits_, argmax_ws_;

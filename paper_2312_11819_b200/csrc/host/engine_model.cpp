@@ -48,11 +48,11 @@ void Engine::kcheck(int status, const char* what) {
 
 void Engine::gemm(rlhf_gemm_params& p) {
   if (p.split_k > 1) {
-    p.workspace = ar_.gemm_ws;
-    p.workspace_bytes = ar_.gemm_ws_bytes;
-    p.counters = ar_.counters;
-    p.counters_len = ar_.counters_len;
-    if (rlhf_gemm_workspace_bytes(&p) > ar_.gemm_ws_bytes) p.split_k = 1;
+    p.workspace = arp_->gemm_ws;
+    p.workspace_bytes = arp_->gemm_ws_bytes;
+    p.counters = arp_->counters;
+    p.counters_len = arp_->counters_len;
+    if (rlhf_gemm_workspace_bytes(&p) > arp_->gemm_ws_bytes) p.split_k = 1;
   }
   K(rlhf_gemm(&p, stream_), 1);
 }
@@ -166,25 +166,25 @@ void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool tr
 
 // Teacher-forced forward over positions [0, T) of B sequences (row r = b*T + i).
 // save: keep every layer's activations for backward (TrainFB); kv: store K/V
-// (Generation prefill).  Result: final-LN hidden states in ar_.hf (bf16).
+// (Generation prefill).  Result: final-LN hidden states in arp_->hf (bf16).
 void Engine::forward(const Decoder& m, const int32_t* tokens, int B, int tok_stride, int T, bool save, KVCache* kv) {
   const rlhf_arch& a = m.a;
   const int d = a.d_model, H = a.n_heads, hd = d / H, ff = a.d_ff, L = a.n_layers;
   const int rows = B * T;
   const int64_t Td = static_cast<int64_t>(rows) * d;
-  auto X = [&](int k) { return ar_.xres + (save ? static_cast<int64_t>(k) * ar_.T * ar_.d : 0); };
-  auto MEAN = [&](int k) { return save ? ar_.mean + static_cast<int64_t>(k) * ar_.T : nullptr; };
-  auto RSTD = [&](int k) { return save ? ar_.rstd + static_cast<int64_t>(k) * ar_.T : nullptr; };
+  auto X = [&](int k) { return arp_->xres + (save ? static_cast<int64_t>(k) * arp_->T * arp_->d : 0); };
+  auto MEAN = [&](int k) { return save ? arp_->mean + static_cast<int64_t>(k) * arp_->T : nullptr; };
+  auto RSTD = [&](int k) { return save ? arp_->rstd + static_cast<int64_t>(k) * arp_->T : nullptr; };
   auto slot = [&](uint16_t* base, int64_t per, int l) { return base + (save ? static_cast<int64_t>(l) * per : 0); };
   (void)Td;
   K(rlhf_embed(tokens, tok_stride, B, T, 0, nullptr, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, X(0), stream_), 1);
   for (int l = 0; l < L; ++l) {
-    uint16_t* h1 = slot(ar_.h1, ar_.T * ar_.d, l);
-    uint16_t* qkv = slot(ar_.qkv, ar_.T * 3 * ar_.d, l);
-    uint16_t* P = slot(ar_.P, ar_.Z * ar_.S * ar_.S, l);
-    uint16_t* o = slot(ar_.o, ar_.T * ar_.d, l);
-    uint16_t* h2 = slot(ar_.h2, ar_.T * ar_.d, l);
-    uint16_t* f = slot(ar_.f, ar_.T * ar_.ff, l);
+    uint16_t* h1 = slot(arp_->h1, arp_->T * arp_->d, l);
+    uint16_t* qkv = slot(arp_->qkv, arp_->T * 3 * arp_->d, l);
+    uint16_t* P = slot(arp_->P, arp_->Z * arp_->S * arp_->S, l);
+    uint16_t* o = slot(arp_->o, arp_->T * arp_->d, l);
+    uint16_t* h2 = slot(arp_->h2, arp_->T * arp_->d, l);
+    uint16_t* f = slot(arp_->f, arp_->T * arp_->ff, l);
     float* xin = X(2 * l);
     float* xmid = X(2 * l + 1);
     float* xout = X(2 * l + 2);
@@ -198,7 +198,7 @@ void Engine::forward(const Decoder& m, const int32_t* tokens, int B, int tok_str
     linear(h2, rows, d, m.T(RLHF_T_W1, l), ff, m.T(RLHF_T_B1, l), f, false, true, nullptr);
     linear(f, rows, ff, m.T(RLHF_T_W2, l), d, m.T(RLHF_T_B2, l), xout, true, false, xmid);
   }
-  K(rlhf_layernorm(X(2 * L), m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), ar_.hf, MEAN(2 * L), RSTD(2 * L), rows, d, stream_), 1);
+  K(rlhf_layernorm(X(2 * L), m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), arp_->hf, MEAN(2 * L), RSTD(2 * L), rows, d, stream_), 1);
 }
 
 // S = softmax(Q K^T / sqrt(hd)) (causal), O = P V — batched over (b, h) straight
@@ -214,11 +214,11 @@ void Engine::attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B,
   s.M = T; s.N = T; s.K = hd; s.batch = B * H; s.batch_h = H;
   s.A = qkv; s.lda = 3 * d; s.a_stride_h = hd; s.a_stride_b = static_cast<int64_t>(T) * 3 * d;
   s.B = qkv + d; s.ldb = 3 * d; s.b_stride_h = hd; s.b_stride_b = static_cast<int64_t>(T) * 3 * d;
-  s.C = ar_.scores; s.c_f32 = 1; s.c_rs = T; s.c_cs = 1; s.c_stride_h = TT; s.c_stride_b = H * TT;
+  s.C = arp_->scores; s.c_f32 = 1; s.c_rs = T; s.c_cs = 1; s.c_stride_h = TT; s.c_stride_b = H * TT;
   s.alpha = 1.0f / std::sqrt(static_cast<float>(hd));
   s.causal = 1;
   gemm(s);
-  K(rlhf_attn_softmax(ar_.scores, P, B * H, T, stream_), 1);
+  K(rlhf_attn_softmax(arp_->scores, P, B * H, T, stream_), 1);
   }
   rlhf_gemm_params pv{};
   pv.M = T; pv.N = hd; pv.K = T; pv.batch = B * H; pv.batch_h = H;
@@ -240,14 +240,14 @@ void Engine::attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_
   dp.M = T; dp.N = T; dp.K = hd; dp.batch = B * H; dp.batch_h = H;
   dp.A = dov; dp.lda = d; dp.a_stride_h = hd; dp.a_stride_b = ob;
   dp.B = qkv + 2 * d; dp.ldb = 3 * d; dp.b_stride_h = hd; dp.b_stride_b = qb;
-  dp.C = ar_.scores; dp.c_f32 = 1; dp.c_rs = T; dp.c_cs = 1; dp.c_stride_h = TT; dp.c_stride_b = H * TT;
+  dp.C = arp_->scores; dp.c_f32 = 1; dp.c_rs = T; dp.c_cs = 1; dp.c_stride_h = TT; dp.c_stride_b = H * TT;
   dp.alpha = 1.0f; dp.causal = 1;
   gemm(dp);
-  K(rlhf_attn_softmax_bwd(P, ar_.scores, ar_.dS, B * H, T, 1.0f / std::sqrt(static_cast<float>(hd)), stream_), 1);
+  K(rlhf_attn_softmax_bwd(P, arp_->scores, arp_->dS, B * H, T, 1.0f / std::sqrt(static_cast<float>(hd)), stream_), 1);
   // dQ = dS K
   rlhf_gemm_params dq{};
   dq.M = T; dq.N = hd; dq.K = T; dq.batch = B * H; dq.batch_h = H;
-  dq.A = ar_.dS; dq.lda = T; dq.a_stride_h = TT; dq.a_stride_b = H * TT;
+  dq.A = arp_->dS; dq.lda = T; dq.a_stride_h = TT; dq.a_stride_b = H * TT;
   dq.B = qkv + d; dq.b_mn_major = 1; dq.ldb = 3 * d; dq.b_stride_h = hd; dq.b_stride_b = qb;
   dq.C = dqkv; dq.c_rs = 3 * d; dq.c_cs = 1; dq.c_stride_h = hd; dq.c_stride_b = qb;
   dq.alpha = 1.0f; dq.causal = 2;
@@ -255,7 +255,7 @@ void Engine::attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_
   // dK = dS^T Q
   rlhf_gemm_params dk{};
   dk.M = T; dk.N = hd; dk.K = T; dk.batch = B * H; dk.batch_h = H;
-  dk.A = ar_.dS; dk.a_mn_major = 1; dk.lda = T; dk.a_stride_h = TT; dk.a_stride_b = H * TT;
+  dk.A = arp_->dS; dk.a_mn_major = 1; dk.lda = T; dk.a_stride_h = TT; dk.a_stride_b = H * TT;
   dk.B = qkv; dk.b_mn_major = 1; dk.ldb = 3 * d; dk.b_stride_h = hd; dk.b_stride_b = qb;
   dk.C = dqkv + d; dk.c_rs = 3 * d; dk.c_cs = 1; dk.c_stride_h = hd; dk.c_stride_b = qb;
   dk.alpha = 1.0f; dk.causal = 3;
@@ -270,17 +270,17 @@ void Engine::attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_
   gemm(dv);
 }
 
-// dL/dhf is in ar_.dhf (fp32 [B*S, d]); accumulates every parameter gradient of m.
+// dL/dhf is in arp_->dhf (fp32 [B*S, d]); accumulates every parameter gradient of m.
 void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
   const rlhf_arch& a = m.a;
   const int d = a.d_model, H = a.n_heads, hd = d / H, ff = a.d_ff, L = a.n_layers;
   const int rows = B * S;
-  auto X = [&](int k) { return ar_.xres + static_cast<int64_t>(k) * ar_.T * ar_.d; };
-  auto MEAN = [&](int k) { return ar_.mean + static_cast<int64_t>(k) * ar_.T; };
-  auto RSTD = [&](int k) { return ar_.rstd + static_cast<int64_t>(k) * ar_.T; };
-  cudaMemsetAsync(ar_.dres, 0, static_cast<size_t>(rows) * d * 4, stream_);
-  K(rlhf_layernorm_bwd(ar_.dhf, X(2 * L), MEAN(2 * L), RSTD(2 * L), m.T(RLHF_T_LNF_G), ar_.dres, m.G(RLHF_T_LNF_G),
-                       m.G(RLHF_T_LNF_B), rows, d, ar_.ws, ar_.ws_floats, stream_), 2);
+  auto X = [&](int k) { return arp_->xres + static_cast<int64_t>(k) * arp_->T * arp_->d; };
+  auto MEAN = [&](int k) { return arp_->mean + static_cast<int64_t>(k) * arp_->T; };
+  auto RSTD = [&](int k) { return arp_->rstd + static_cast<int64_t>(k) * arp_->T; };
+  cudaMemsetAsync(arp_->dres, 0, static_cast<size_t>(rows) * d * 4, stream_);
+  K(rlhf_layernorm_bwd(arp_->dhf, X(2 * L), MEAN(2 * L), RSTD(2 * L), m.T(RLHF_T_LNF_G), arp_->dres, m.G(RLHF_T_LNF_G),
+                       m.G(RLHF_T_LNF_B), rows, d, arp_->ws, arp_->ws_floats, stream_), 2);
   // dW[N_out, K_in] += dY[T, N_out]^T X[T, K_in]
   auto wgrad = [&](const uint16_t* dY, int N_out, const uint16_t* Xin, int K_in, float* dW) {
     rlhf_gemm_params p{};
@@ -312,36 +312,36 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
     gemm(p);
   };
   for (int l = L - 1; l >= 0; --l) {
-    const int64_t Tn = ar_.T;
-    const uint16_t* h1 = ar_.h1 + l * Tn * ar_.d;
-    const uint16_t* qkv = ar_.qkv + l * Tn * 3 * ar_.d;
-    const uint16_t* P = ar_.P + l * ar_.Z * ar_.S * ar_.S;
-    const uint16_t* o = ar_.o + l * Tn * ar_.d;
-    const uint16_t* h2 = ar_.h2 + l * Tn * ar_.d;
-    const uint16_t* f = ar_.f + l * Tn * ar_.ff;
+    const int64_t Tn = arp_->T;
+    const uint16_t* h1 = arp_->h1 + l * Tn * arp_->d;
+    const uint16_t* qkv = arp_->qkv + l * Tn * 3 * arp_->d;
+    const uint16_t* P = arp_->P + l * arp_->Z * arp_->S * arp_->S;
+    const uint16_t* o = arp_->o + l * Tn * arp_->d;
+    const uint16_t* h2 = arp_->h2 + l * Tn * arp_->d;
+    const uint16_t* f = arp_->f + l * Tn * arp_->ff;
     // FFN: x_out = x_mid + relu(h2 W1^T + b1) W2^T + b2
-    K(rlhf_round_bf16(ar_.dres, ar_.g, static_cast<int64_t>(rows) * d, stream_), 1);
-    K(rlhf_colsum_bf16(ar_.g, rows, d, m.G(RLHF_T_B2, l), ar_.ws, stream_), 2);
-    wgrad(ar_.g, d, f, ff, m.G(RLHF_T_W2, l));
-    dgrad(ar_.g, d, m.T(RLHF_T_W2, l), ff, ar_.dpre, false, f);
-    K(rlhf_colsum_bf16(ar_.dpre, rows, ff, m.G(RLHF_T_B1, l), ar_.ws, stream_), 2);
-    wgrad(ar_.dpre, ff, h2, d, m.G(RLHF_T_W1, l));
-    dgrad(ar_.dpre, ff, m.T(RLHF_T_W1, l), d, ar_.dh, true, nullptr);
-    K(rlhf_layernorm_bwd(ar_.dh, X(2 * l + 1), MEAN(2 * l + 1), RSTD(2 * l + 1), m.T(RLHF_T_LN2_G, l), ar_.dres,
-                         m.G(RLHF_T_LN2_G, l), m.G(RLHF_T_LN2_B, l), rows, d, ar_.ws, ar_.ws_floats, stream_), 2);
+    K(rlhf_round_bf16(arp_->dres, arp_->g, static_cast<int64_t>(rows) * d, stream_), 1);
+    K(rlhf_colsum_bf16(arp_->g, rows, d, m.G(RLHF_T_B2, l), arp_->ws, stream_), 2);
+    wgrad(arp_->g, d, f, ff, m.G(RLHF_T_W2, l));
+    dgrad(arp_->g, d, m.T(RLHF_T_W2, l), ff, arp_->dpre, false, f);
+    K(rlhf_colsum_bf16(arp_->dpre, rows, ff, m.G(RLHF_T_B1, l), arp_->ws, stream_), 2);
+    wgrad(arp_->dpre, ff, h2, d, m.G(RLHF_T_W1, l));
+    dgrad(arp_->dpre, ff, m.T(RLHF_T_W1, l), d, arp_->dh, true, nullptr);
+    K(rlhf_layernorm_bwd(arp_->dh, X(2 * l + 1), MEAN(2 * l + 1), RSTD(2 * l + 1), m.T(RLHF_T_LN2_G, l), arp_->dres,
+                         m.G(RLHF_T_LN2_G, l), m.G(RLHF_T_LN2_B, l), rows, d, arp_->ws, arp_->ws_floats, stream_), 2);
     // attention block: x_mid = x_in + attn(h1) Wo^T + bo
-    K(rlhf_round_bf16(ar_.dres, ar_.g, static_cast<int64_t>(rows) * d, stream_), 1);
-    K(rlhf_colsum_bf16(ar_.g, rows, d, m.G(RLHF_T_BO, l), ar_.ws, stream_), 2);
-    wgrad(ar_.g, d, o, d, m.G(RLHF_T_WO, l));
-    dgrad(ar_.g, d, m.T(RLHF_T_WO, l), d, ar_.dov, false, nullptr);
-    attention_bwd(qkv, P, ar_.dov, ar_.dqkv, B, S, H, hd);
-    K(rlhf_colsum_bf16(ar_.dqkv, rows, 3 * d, m.G(RLHF_T_BQKV, l), ar_.ws, stream_), 2);
-    wgrad(ar_.dqkv, 3 * d, h1, d, m.G(RLHF_T_WQKV, l));
-    dgrad(ar_.dqkv, 3 * d, m.T(RLHF_T_WQKV, l), d, ar_.dh, true, nullptr);
-    K(rlhf_layernorm_bwd(ar_.dh, X(2 * l), MEAN(2 * l), RSTD(2 * l), m.T(RLHF_T_LN1_G, l), ar_.dres, m.G(RLHF_T_LN1_G, l),
-                         m.G(RLHF_T_LN1_B, l), rows, d, ar_.ws, ar_.ws_floats, stream_), 2);
+    K(rlhf_round_bf16(arp_->dres, arp_->g, static_cast<int64_t>(rows) * d, stream_), 1);
+    K(rlhf_colsum_bf16(arp_->g, rows, d, m.G(RLHF_T_BO, l), arp_->ws, stream_), 2);
+    wgrad(arp_->g, d, o, d, m.G(RLHF_T_WO, l));
+    dgrad(arp_->g, d, m.T(RLHF_T_WO, l), d, arp_->dov, false, nullptr);
+    attention_bwd(qkv, P, arp_->dov, arp_->dqkv, B, S, H, hd);
+    K(rlhf_colsum_bf16(arp_->dqkv, rows, 3 * d, m.G(RLHF_T_BQKV, l), arp_->ws, stream_), 2);
+    wgrad(arp_->dqkv, 3 * d, h1, d, m.G(RLHF_T_WQKV, l));
+    dgrad(arp_->dqkv, 3 * d, m.T(RLHF_T_WQKV, l), d, arp_->dh, true, nullptr);
+    K(rlhf_layernorm_bwd(arp_->dh, X(2 * l), MEAN(2 * l), RSTD(2 * l), m.T(RLHF_T_LN1_G, l), arp_->dres, m.G(RLHF_T_LN1_G, l),
+                         m.G(RLHF_T_LN1_B, l), rows, d, arp_->ws, arp_->ws_floats, stream_), 2);
   }
-  K(rlhf_embed_bwd(tokens, S, B, S, ar_.dres, d, m.G(RLHF_T_TOK_EMB), m.G(RLHF_T_POS_EMB), stream_), 1);
+  K(rlhf_embed_bwd(tokens, S, B, S, arp_->dres, d, m.G(RLHF_T_TOK_EMB), m.G(RLHF_T_POS_EMB), stream_), 1);
 }
 
 // Per-token logprobs of the response tokens under m (tied LM head); logits and
@@ -349,9 +349,9 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
 void Engine::lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits) {
   const int d = m.a.d_model, V = m.a.vocab;
   (void)keep_logits;
-  K(rlhf_gather_rows(ar_.hf, ar_.hf_resp, B, S_, R_, P_ - 1, d, 2, stream_), 1);
-  linear(ar_.hf_resp, B * R_, d, m.T(RLHF_T_TOK_EMB), V, nullptr, ar_.logits, true, false, nullptr);
-  K(rlhf_logprob(ar_.logits, B * R_, V, tokens, S_, P_, R_, logp, ar_.lse, stream_), 1);
+  K(rlhf_gather_rows(arp_->hf, arp_->hf_resp, B, S_, R_, P_ - 1, d, 2, stream_), 1);
+  linear(arp_->hf_resp, B * R_, d, m.T(RLHF_T_TOK_EMB), V, nullptr, arp_->logits, true, false, nullptr);
+  K(rlhf_logprob(arp_->logits, B * R_, V, tokens, S_, P_, R_, logp, arp_->lse, stream_), 1);
 }
 
 // One decode step at position *pos: embed -> L x (LN, qkv, KV store, attention,
@@ -418,7 +418,7 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   const int d = m.a.d_model, V = m.a.vocab;
   // prefill: forward over the prompt, K/V stored for every prompt position
   forward(m, tokens_.as<int32_t>(), B, S_, P_, false, &kv_);
-  K(rlhf_gather_rows(ar_.hf, dec_hf_.p, B, P_, 1, P_ - 1, d, 2, stream_), 1);
+  K(rlhf_gather_rows(arp_->hf, dec_hf_.p, B, P_, 1, P_ - 1, d, 2, stream_), 1);
   const int start = P_ - 1;
   cudaMemcpyAsync(pos_.p, &start, sizeof(int), cudaMemcpyHostToDevice, stream_);
   int32_t* dst = teacher_forced ? pred_.as<int32_t>() : tokens_.as<int32_t>();
