@@ -149,11 +149,13 @@ int rlhf_gather_rows(const void* src, void* dst, int B, int S, int R, int off, i
                      rlhf_stream_t s);
 int rlhf_scatter_rows_f32(const float* src, float* dst, int B, int S, int R, int off, int d, rlhf_stream_t s);
 
-/* Fused causal scores + softmax (S % 128 == 0, S <= 512, hd == 64): P[z][i][j] =
- * bf16(softmax_j<=i(alpha * q_i . k_j)) for z = b*H + h, zeros above the diagonal up to the
- * end of each 128-row block; q / k read from packed qkv rows [B*S, 3*H*hd].  Replaces
- * QK^T GEMM (fp32 scores) + rlhf_attn_softmax. */
-int rlhf_attn_fwd_fused(const void* qkv, int B, int H, int hd, int S, float alpha, void* P, rlhf_stream_t s);
+/* Fused causal attention forward (S % 128 == 0, S <= 512, hd == 64): per (b, h, 128 query
+ * rows) the scores alpha*QK^T live in TMEM, an online softmax produces p = bf16(softmax), and
+ * (O != NULL) O[b*S + i][h*hd + e] = bf16(sum_j p_ij v_j) accumulates in TMEM from the P tiles
+ * in shared memory; (P != NULL) P[z][i][j] is stored for backward (zeros above the diagonal
+ * up to the end of each 128-row block).  q / k / v come from packed qkv rows [B*S, 3*H*hd].
+ * Replaces QK^T GEMM + rlhf_attn_softmax (+ the P.V GEMM when O != NULL). */
+int rlhf_attn_fwd_fused(const void* qkv, int B, int H, int hd, int S, float alpha, void* P, void* O, rlhf_stream_t s);
 
 /* ---- attention (Generation prefill, Forward, TrainFB) ---------------------
  * Row-wise causal softmax of scores [Z, S, S] (f32) -> probs bf16 (zeros above

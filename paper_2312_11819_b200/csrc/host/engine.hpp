@@ -92,7 +92,7 @@ class Engine {
   // ---- building blocks (engine_model.cpp) ----
   void init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool trainable);
   void forward(const Decoder& m, const int32_t* tokens, int B, int tok_stride, int T, bool save, KVCache* kv);
-  void attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd);
+  void attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd, bool keep_p);
   void attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_t* dov, uint16_t* dqkv, int B, int T, int H, int hd);
   void backward(Decoder& m, const int32_t* tokens, int B, int S);
   void lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits);

@@ -191,7 +191,7 @@ void Engine::forward(const Decoder& m, const int32_t* tokens, int B, int tok_str
     K(rlhf_layernorm(xin, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h1, MEAN(2 * l), RSTD(2 * l), rows, d, stream_), 1);
     linear(h1, rows, d, m.T(RLHF_T_WQKV, l), 3 * d, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr);
     if (kv) K(rlhf_kv_store(qkv, B, T, 0, nullptr, H, hd, kv->Smax, kv->Kc(l), kv->Vc(l), stream_), 1);
-    attention_fwd(qkv, P, o, B, T, H, hd);
+    attention_fwd(qkv, P, o, B, T, H, hd, save);
     linear(o, rows, d, m.T(RLHF_T_WO, l), d, m.T(RLHF_T_BO, l), xmid, true, false, xin);
     K(rlhf_layernorm(xmid, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h2, MEAN(2 * l + 1), RSTD(2 * l + 1), rows, d,
                      stream_), 1);
@@ -203,13 +203,16 @@ void Engine::forward(const Decoder& m, const int32_t* tokens, int B, int tok_str
 
 // S = softmax(Q K^T / sqrt(hd)) (causal), O = P V — batched over (b, h) straight
 // out of the packed qkv rows; P kept (bf16) for backward.
-void Engine::attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd) {
+void Engine::attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd, bool keep_p) {
   const int d = H * hd;
   const int64_t TT = static_cast<int64_t>(T) * T;
   static const bool unfused = getenv("RLHF_ATTN_UNFUSED") != nullptr;  // A/B switch for timing
   if (!unfused && hd == 64 && T % 128 == 0 && T <= 512) {
-    K(rlhf_attn_fwd_fused(qkv, B, H, hd, T, 1.0f / std::sqrt(static_cast<float>(hd)), P, stream_), 1);
-  } else {
+    // one kernel: scores in TMEM, softmax, P.V in TMEM; P kept only for backward
+    K(rlhf_attn_fwd_fused(qkv, B, H, hd, T, 1.0f / std::sqrt(static_cast<float>(hd)), keep_p ? P : nullptr, o, stream_),
+      1);
+    return;
+  }
   rlhf_gemm_params s{};
   s.M = T; s.N = T; s.K = hd; s.batch = B * H; s.batch_h = H;
   s.A = qkv; s.lda = 3 * d; s.a_stride_h = hd; s.a_stride_b = static_cast<int64_t>(T) * 3 * d;
@@ -219,7 +222,6 @@ void Engine::attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B,
   s.causal = 1;
   gemm(s);
   K(rlhf_attn_softmax(arp_->scores, P, B * H, T, stream_), 1);
-  }
   rlhf_gemm_params pv{};
   pv.M = T; pv.N = hd; pv.K = T; pv.batch = B * H; pv.batch_h = H;
   pv.A = P; pv.lda = T; pv.a_stride_h = TT; pv.a_stride_b = H * TT;

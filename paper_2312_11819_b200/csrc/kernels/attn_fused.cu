@@ -1,5 +1,5 @@
-// attn_fused.cu — causal attention scores + softmax in one tcgen05 kernel (prefill,
-// Forward x4, TrainFB forward), for sequences S <= 512 and head dim 64.
+// attn_fused.cu — causal attention forward in one tcgen05 kernel (prefill, Forward x4,
+// TrainFB forward) for sequences S <= 512 and head dim 64: scores, softmax and P.V.
 //
 // The unfused path writes the fp32 score matrix S = alpha Q K^T (B*H*S*S*4 bytes,
 // 400 MB per layer for c2) and reads it back in a separate softmax kernel.  Here one
@@ -8,7 +8,10 @@
 // fp32 score tile into TMEM (<= 512 columns), and four epilogue warps (one TMEM lane
 // quarter each, thread = query row) run an online max / sum pass and a second pass that
 // writes P = bf16(exp(s - max) / sum) (zeros above the diagonal) through a shared-memory
-// transpose as coalesced row segments.  Only P (bf16) reaches HBM.  Eight epilogue
+// transpose as coalesced row segments (training only), and into a shared-memory P tile
+// (SW128, K-major) from which tcgen05.mma accumulates O = P V in TMEM (columns [0, 64),
+// reused once key tile 0 has been consumed; V overwrites K in shared memory after the
+// QK^T MMAs).  Inference forwards never write P to HBM.  Eight epilogue
 // warps (two per lane quarter) split the column chunks; exponentials use ex2.approx
 // (__expf, ~2 ulp).
 //
@@ -32,22 +35,36 @@ constexpr int BMq = 128, HD = 64, kEpi = 8, kThreads = 64 + 32 * kEpi, kMaxS = 5
 constexpr int Q_BYTES = BMq * HD * 2;   // 16 KB
 constexpr int KT_BYTES = BMq * HD * 2;  // one 128-key tile, 16 KB
 constexpr int STG_PITCH = 40;           // bf16 staging row pitch (80 B: conflict-light)
-constexpr int SMEM = Q_BYTES + (kMaxS / BMq) * KT_BYTES + kEpi * 32 * STG_PITCH * 2 + 4 * BMq * 4 + 1024 + 128;
+constexpr int PB_BYTES = BMq * BMq * 2;  // one 128 x 128 bf16 P tile (two SW128 64-key blocks)
+constexpr int STG_BYTES = kEpi * 32 * STG_PITCH * 2;
+// dynamic shared memory by mode: the P tile only when O is produced, the P staging only
+// when P is stored (so the P-only and O-only kernels fit two CTAs per SM)
+__host__ __device__ constexpr int smem_bytes(bool want_p, bool want_o) {
+  return Q_BYTES + (kMaxS / BMq) * KT_BYTES + (want_o ? PB_BYTES : 0) + (want_p ? STG_BYTES : 0) + 4 * BMq * 4 + 1024 + 256;
+}
+constexpr int SMEM = smem_bytes(true, true);
 
 __device__ __forceinline__ uint16_t f2b(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, int H, int S,
-                    float alpha, uint16_t* __restrict__ P) {
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, int H, int S, float alpha, uint16_t* __restrict__ P,
+                    uint16_t* __restrict__ O, int64_t ldo) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sq = smem;
-  uint8_t* sk = smem + Q_BYTES;
-  uint16_t* stg = reinterpret_cast<uint16_t*>(sk + (kMaxS / BMq) * KT_BYTES);
-  float* rowst = reinterpret_cast<float*>(stg + kEpi * 32 * STG_PITCH);  // [2 halves][max, sum][128 rows]
+  uint8_t* skv = smem + Q_BYTES;                      // K tiles, then (after the QK MMAs) V tiles
+  const bool want_o = O != nullptr, want_p = P != nullptr;
+  uint8_t* spb = skv + (kMaxS / BMq) * KT_BYTES;      // P tile (A operand of P.V)
+  uint16_t* stg = reinterpret_cast<uint16_t*>(spb + (want_o ? PB_BYTES : 0));
+  float* rowst = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(stg) + (want_p ? STG_BYTES : 0));  // [2][2][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(rowst + 4 * BMq);
-  uint64_t* done = full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* done = full + 1;   // QK^T MMAs complete
+  uint64_t* vfull = done + 1;  // V tiles landed
+  uint64_t* pfull = vfull + 1;  // P tile written by the epilogue warps
+  uint64_t* pfree = pfull + 1;  // P.V MMAs done with the P tile
+  uint64_t* ofull = pfree + 1;  // O accumulated
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 1);
 
   const int mb = blockIdx.x, z = blockIdx.y, b = z / H, h = z % H;
   const int m0 = mb * BMq;
@@ -56,12 +73,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(full, 1);
     mbar_init(done, 1);
+    mbar_init(vfull, 1);
+    mbar_init(pfull, kEpi);
+    mbar_init(pfree, 1);
+    mbar_init(ofull, 1);
     mbar_fence_init();
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
   }
-  int tcols = 128;  // causal extent (nkt * 128 columns), rounded up to a power of two
-  while (tcols < nkt * BMq) tcols *= 2;
+  int tcols = 128;  // score tile (nkt * 128 columns) rounded up to a power of two; O reuses
+  while (tcols < nkt * BMq) tcols *= 2;  // columns [0, 64) once key tile 0 is consumed
   if (warp == 1) tmem_alloc(tmem_slot, tcols);
   tc_fence_before();
   __syncthreads();
@@ -72,7 +94,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       mbar_arrive_expect_tx(full, Q_BYTES + nkt * KT_BYTES);
       tma_load_4d(sq, &tmQ, full, 0, h, m0, b);
-      for (int t = 0; t < nkt; ++t) tma_load_4d(sk + t * KT_BYTES, &tmK, full, 0, h, t * BMq, b);
+      for (int t = 0; t < nkt; ++t) tma_load_4d(skv + t * KT_BYTES, &tmK, full, 0, h, t * BMq, b);
+      if (want_o) {  // V tiles overwrite K once the QK^T MMAs have read it
+        mbar_wait(done, 0);
+        mbar_arrive_expect_tx(vfull, nkt * KT_BYTES);
+        for (int t = 0; t < nkt; ++t) tma_load_4d(skv + t * KT_BYTES, &tmV, vfull, 0, h, t * BMq, b);
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -81,13 +108,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t a = smem_u32(sq);
       for (int t = 0; t < nkt; ++t) {
-        const uint32_t bk = smem_u32(sk + t * KT_BYTES);
+        const uint32_t bk = smem_u32(skv + t * KT_BYTES);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
           umma_bf16(tmem + t * BMq, umma_desc_sw128(a + k * 32, 16, 1024), umma_desc_sw128(bk + k * 32, 16, 1024), idesc,
                     k > 0 ? 1u : 0u);
       }
       umma_commit(done);
+      if (want_o) {
+        // O[128 x 64] += P_t[128 x 128 keys] . V_t[128 keys x 64], key tiles in order
+        const uint32_t idv = umma_idesc_bf16(BMq, HD, 0, 1);
+        mbar_wait(vfull, 0);
+        for (int t = 0; t < nkt; ++t) {
+          mbar_wait(pfull, t & 1);
+          tc_fence_after();
+          const uint32_t pa = smem_u32(spb), vb = smem_u32(skv + t * KT_BYTES);
+#pragma unroll
+          for (int kb2 = 0; kb2 < 2; ++kb2)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_bf16(tmem, umma_desc_sw128(pa + kb2 * (PB_BYTES / 2) + k * 32, 16, 1024),
+                        umma_desc_sw128(vb + (kb2 * 4 + k) * 2048, 8192, 1024), idv,
+                        (t > 0 || kb2 > 0 || k > 0) ? 1u : 0u);
+          umma_commit(pfree);
+        }
+        umma_commit(ofull);
+      }
     }
     __syncwarp();
   } else {
@@ -98,7 +144,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int i = m0 + il;
     const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const int nch = (m0 + q * 32 + 32) / 32;  // chunks holding any j <= (this warp's last row)
-    const int nout = (m0 + BMq) / 32;         // chunks written (the block's causal extent)
     mbar_wait(done, 0);
     tc_fence_after();
     float mx = -FLT_MAX, sum = 0.f;
@@ -130,36 +175,74 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const float inv = 1.0f / sum;
     uint16_t* st = stg + (warp - 2) * 32 * STG_PITCH;
-    uint16_t* prow0 = P + (static_cast<int64_t>(z) * S + m0 + q * 32) * S;
-    for (int c = half; c < nout; c += 2) {
-      uint32_t pk[16];
-      if (c < nch) {
-        float v[32];
-        tmem_ld32(tq + c * 32, v);
+    uint16_t* prow0 = want_p ? P + (static_cast<int64_t>(z) * S + m0 + q * 32) * S : nullptr;
+    for (int t = 0; t < nkt; ++t) {
+      if (want_o && t >= 1) mbar_wait(pfree, (t - 1) & 1);  // the MMA has read tile t-1
+      uint8_t* pbuf = spb;
+      for (int cc = half; cc < 4; cc += 2) {
+        const int c = t * 4 + cc;
+        uint32_t pk[16];
+        if (c < nch) {
+          float v[32];
+          tmem_ld32(tq + c * 32, v);
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          const int j = c * 32 + 2 * t;
-          const float p0 = j <= i ? __expf(v[2 * t] * alpha - mx) * inv : 0.f;
-          const float p1 = j + 1 <= i ? __expf(v[2 * t + 1] * alpha - mx) * inv : 0.f;
-          pk[t] = static_cast<uint32_t>(f2b(p0)) | (static_cast<uint32_t>(f2b(p1)) << 16);
+          for (int u = 0; u < 16; ++u) {
+            const int j = c * 32 + 2 * u;
+            const float p0 = j <= i ? __expf(v[2 * u] * alpha - mx) * inv : 0.f;
+            const float p1 = j + 1 <= i ? __expf(v[2 * u + 1] * alpha - mx) * inv : 0.f;
+            pk[u] = static_cast<uint32_t>(f2b(p0)) | (static_cast<uint32_t>(f2b(p1)) << 16);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) pk[u] = 0u;
         }
-      } else {
+        if (want_o) {  // SW128 K-major P tile: byte(r, key) = blk*16K + r*128 + ((key%64/8) ^ (r%8))*16 + (key%8)*2
+          uint8_t* rowp = pbuf + (cc >> 1) * (PB_BYTES / 2) + il * 128;
 #pragma unroll
-        for (int t = 0; t < 16; ++t) pk[t] = 0u;
+          for (int u = 0; u < 4; ++u) {
+            const int ch = (cc & 1) * 4 + u;
+            *reinterpret_cast<uint4*>(rowp + ((ch ^ (il & 7)) << 4)) =
+                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          }
+        }
+        if (want_p) {  // probabilities for backward: transpose through smem, row segments
+          uint32_t* srow = reinterpret_cast<uint32_t*>(st + lane * STG_PITCH);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) srow[u] = pk[u];
+          __syncwarp();
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = static_cast<int>(lane >> 2) + 8 * r, seg = static_cast<int>(lane & 3);
+            const uint4 val = *reinterpret_cast<const uint4*>(st + row * STG_PITCH + seg * 8);
+            *reinterpret_cast<uint4*>(prow0 + static_cast<int64_t>(row) * S + c * 32 + seg * 8) = val;
+          }
+          __syncwarp();
+        }
       }
-      // transpose through smem: row `lane` of this warp's 32 x 32 bf16 block
-      uint32_t* srow = reinterpret_cast<uint32_t*>(st + lane * STG_PITCH);
-#pragma unroll
-      for (int t = 0; t < 16; ++t) srow[t] = pk[t];
-      __syncwarp();
-      // 32 rows x 64 B: lane -> (row lane/4 + 8 r, 16 B segment lane%4)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int row = static_cast<int>(lane >> 2) + 8 * r, seg = static_cast<int>(lane & 3);
-        const uint4 val = *reinterpret_cast<const uint4*>(st + row * STG_PITCH + seg * 8);
-        *reinterpret_cast<uint4*>(prow0 + static_cast<int64_t>(row) * S + c * 32 + seg * 8) = val;
+      if (want_o) {  // P tile t visible to the tensor core; this warp's score reads are done
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pfull);
       }
-      __syncwarp();
+    }
+    if (want_o && half == 0) {  // O rows of this quarter: TMEM columns [0, 64) -> bf16
+      mbar_wait(ofull, 0);
+      tc_fence_after();
+      uint16_t* orow = O + (static_cast<int64_t>(b) * S + i) * ldo + h * HD;
+#pragma unroll
+      for (int cch = 0; cch < 2; ++cch) {
+        float v[32];
+        tmem_ld32(tq + cch * 32, v);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            w[e] = static_cast<uint32_t>(f2b(v[8 * u + 2 * e])) | (static_cast<uint32_t>(f2b(v[8 * u + 2 * e + 1])) << 16);
+          *reinterpret_cast<uint4*>(orow + cch * 32 + u * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
     }
   }
   tc_fence_before();
@@ -205,12 +288,14 @@ int qkv_map(CUtensorMap* m, const void* base, int H, int S, int B, int64_t ld) {
 
 using namespace rlhf;
 
-extern "C" int rlhf_attn_fwd_fused(const void* qkv, int B, int H, int hd, int S, float alpha, void* P,
+extern "C" int rlhf_attn_fwd_fused(const void* qkv, int B, int H, int hd, int S, float alpha, void* P, void* O,
                                    rlhf_stream_t stream) {
-  if (hd != af::HD || S % af::BMq || S > af::kMaxS || B < 1 || H < 1) return 2;
+  if (hd != af::HD || S % af::BMq || S > af::kMaxS || B < 1 || H < 1 || (!P && !O)) return 2;
   const int d = H * hd;
-  CUtensorMap tq, tk;
-  if (af::qkv_map(&tq, qkv, H, S, B, 3 * d) || af::qkv_map(&tk, static_cast<const uint16_t*>(qkv) + d, H, S, B, 3 * d))
+  const auto* base = static_cast<const uint16_t*>(qkv);
+  CUtensorMap tq, tk, tv;
+  if (af::qkv_map(&tq, base, H, S, B, 3 * d) || af::qkv_map(&tk, base + d, H, S, B, 3 * d) ||
+      af::qkv_map(&tv, base + 2 * d, H, S, B, 3 * d))
     return 2;
   static bool init = false;
   if (!init) {
@@ -219,7 +304,7 @@ extern "C" int rlhf_attn_fwd_fused(const void* qkv, int B, int H, int hd, int S,
     init = true;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  af::attn_fwd_kernel<<<dim3(S / af::BMq, B * H), af::kThreads, af::SMEM, s>>>(tq, tk, H, S, alpha,
-                                                                                 static_cast<uint16_t*>(P));
+  af::attn_fwd_kernel<<<dim3(S / af::BMq, B * H), af::kThreads, af::smem_bytes(P != nullptr, O != nullptr), s>>>(
+      tq, tk, tv, H, S, alpha, static_cast<uint16_t*>(P), static_cast<uint16_t*>(O), static_cast<int64_t>(d));
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }

@@ -144,13 +144,17 @@ def attn_decode(qkv: torch.Tensor, kcache: torch.Tensor, vcache: torch.Tensor, p
     return out
 
 
-def attn_fwd_fused(qkv: torch.Tensor, B: int, H: int, S: int, alpha: float) -> torch.Tensor:
-    """P = bf16(causal softmax(alpha Q K^T)) per (b, h) from packed qkv rows (rlhf_attn_fwd_fused)."""
+def attn_fwd_fused(qkv: torch.Tensor, B: int, H: int, S: int, alpha: float, want_p: bool = True, want_o: bool = True):
+    """Fused causal attention forward (rlhf_attn_fwd_fused) from packed qkv rows:
+    returns (P bf16 [B, H, S, S] or None, O bf16 [B*S, H*hd] or None)."""
     L = lib()
-    L.rlhf_attn_fwd_fused.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_void_p]
+    L.rlhf_attn_fwd_fused.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]
     hd = qkv.shape[1] // (3 * H)
-    P = torch.zeros(B, H, S, S, device=qkv.device, dtype=torch.bfloat16)
-    rc = L.rlhf_attn_fwd_fused(qkv.data_ptr(), B, H, hd, S, alpha, P.data_ptr(), _stream())
+    P = torch.zeros(B, H, S, S, device=qkv.device, dtype=torch.bfloat16) if want_p else None
+    O = torch.zeros(B * S, H * hd, device=qkv.device, dtype=torch.bfloat16) if want_o else None
+    rc = L.rlhf_attn_fwd_fused(qkv.data_ptr(), B, H, hd, S, alpha, P.data_ptr() if want_p else None,
+                               O.data_ptr() if want_o else None, _stream())
     if rc:
         raise RuntimeError(f"rlhf_attn_fwd_fused failed ({rc})")
-    return P
+    return P, O

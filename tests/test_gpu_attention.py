@@ -52,20 +52,30 @@ def test_attn_decode_large_grid_matches_torch(ctx):
 
 @pytest.mark.parametrize("B,H,S", [(2, 3, 128), (2, 12, 512), (3, 4, 256)])
 def test_attn_fwd_fused_matches_torch(B, H, S):
-    """Fused scores + causal softmax (tcgen05, TMEM online softmax) vs fp32 torch:
-    probabilities within bf16 rounding; exact zeros above the diagonal of each block."""
+    """Fused attention forward (tcgen05 scores in TMEM, online softmax, P tiles in smem,
+    P.V accumulated in TMEM) vs fp32 torch: P within bf16 rounding with exact zeros above
+    the diagonal, O = bf16(P_bf16 V) within bf16 rounding; P-only and O-only modes agree."""
     import torch
     from paper_2312_11819_b200 import ops
     torch.manual_seed(S + H)
     hd = 64
     d = H * hd
     qkv = (torch.randn(B * S, 3 * d, device="cuda") * 1.5).bfloat16()
-    P = ops.attn_fwd_fused(qkv, B, H, S, 0.125).float()
+    P, O = ops.attn_fwd_fused(qkv, B, H, S, 0.125)
     q = qkv[:, :d].float().view(B, S, H, hd).transpose(1, 2)
     k = qkv[:, d:2 * d].float().view(B, S, H, hd).transpose(1, 2)
+    v = qkv[:, 2 * d:].float().view(B, S, H, hd).transpose(1, 2)
     s = (q @ k.transpose(-1, -2)) * 0.125
     mask = torch.ones(S, S, device="cuda", dtype=torch.bool).tril()
     ref = torch.softmax(s.masked_fill(~mask, float("-inf")), -1)
     torch.cuda.synchronize()
-    assert (P - ref).abs().max().item() <= 4e-3 * ref.abs().max().item() + 1e-6
-    assert (P[..., ~mask] == 0).all()
+    Pf = P.float()
+    assert (Pf - ref).abs().max().item() <= 4e-3 * ref.abs().max().item() + 1e-6
+    assert (Pf[..., ~mask] == 0).all()
+    # O from the kernel's own bf16 probabilities (the rounding contract), fp32 accumulation
+    o_ref = (Pf @ v).transpose(1, 2).reshape(B * S, d)
+    assert (O.float() - o_ref).abs().max().item() <= 1e-2 * o_ref.abs().max().item() + 1e-3
+    P2, _ = ops.attn_fwd_fused(qkv, B, H, S, 0.125, want_o=False)
+    _, O2 = ops.attn_fwd_fused(qkv, B, H, S, 0.125, want_p=False)
+    torch.cuda.synchronize()
+    assert torch.equal(P2, P) and torch.equal(O2, O)

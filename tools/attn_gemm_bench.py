@@ -57,10 +57,14 @@ import ctypes as C  # noqa: E402
 
 Pf = torch.zeros(B, H, S, S, device="cuda", dtype=torch.bfloat16)
 L = lib()
-L.rlhf_attn_fwd_fused.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_void_p]
+L.rlhf_attn_fwd_fused.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_void_p,
+                                  C.c_void_p]
 L.rlhf_attn_softmax.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-for name, f in [("fused QK+softmax", lambda: L.rlhf_attn_fwd_fused(qkv.data_ptr(), B, H, hd, S, 0.125, Pf.data_ptr(), st)),
+for name, f in [("fused -> P", lambda: L.rlhf_attn_fwd_fused(qkv.data_ptr(), B, H, hd, S, 0.125, Pf.data_ptr(), None, st)),
+                ("fused -> O", lambda: L.rlhf_attn_fwd_fused(qkv.data_ptr(), B, H, hd, S, 0.125, None, out_o.data_ptr(), st)),
+                ("fused -> P, O", lambda: L.rlhf_attn_fwd_fused(qkv.data_ptr(), B, H, hd, S, 0.125, Pf.data_ptr(),
+                                                                out_o.data_ptr(), st)),
                 ("softmax only", lambda: L.rlhf_attn_softmax(out_s.data_ptr(), Pf.data_ptr(), B * H, S, st))]:
     for _ in range(3):
         f()
