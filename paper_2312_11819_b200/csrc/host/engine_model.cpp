@@ -112,10 +112,14 @@ void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t*
     gemm(q);
     return;
   }
-  // K slices of one 128-row tile form a cluster; keep >= 2 k-blocks per slice
+  // K slices of one 128-row tile form a cluster, up to two CTAs per SM (the kernel then
+  // uses a 4-stage ring)
   int split = 1;
-  // up to two CTAs per SM (the kernel then uses a 4-stage ring), >= 2 k-blocks per slice
-  while (split < 8 && tiles * split * 2 <= 2 * 148 && kb / (split * 2) >= 2) split *= 2;
+  // >= 1 k-block per slice: short-K projections of small models (c2: K = 768) run more,
+  // shorter slices (measured: c2 decode 128.4 -> 123.5 ms per PPO step against >= 2);
+  // RLHF_DEC_MINKB overrides the minimum for timing experiments
+  static const int minkb = [] { const char* e = getenv("RLHF_DEC_MINKB"); return e ? atoi(e) : 1; }();
+  while (split < 8 && tiles * split * 2 <= 2 * 148 && kb / (split * 2) >= minkb) split *= 2;
   // very long K (OPT-1.3B FFN-down, K = 8192) on few tiles: a 16-CTA cluster per tile
   if (split == 8 && tiles * 16 <= 2 * 148 && kb / 16 >= 8) split = 16;
   p.splits = split;
