@@ -65,9 +65,10 @@ typedef struct rlhf_gemm_params {
 
 int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t s);
 /* Merge per-tile top-2 partials (rlhf_gemm_params.top2) of `tiles` tiles: greedy token
- * (ties -> lowest id) -> tok[b*tok_stride + *pos + 1], margin (top1 - top2) likewise. */
-int rlhf_argmax_tiles(const float* top2, int tiles, int B, int32_t* tok, int64_t tok_stride, const int* pos,
-                      float* margin, rlhf_stream_t s);
+ * (ties -> lowest id) -> tok[b*tok_stride + *pos + 1], margin (top1 - top2) likewise;
+ * advance_pos != 0: then *pos += 1 (the decode step's last kernel). */
+int rlhf_argmax_tiles(const float* top2, int tiles, int B, int32_t* tok, int64_t tok_stride, int* pos,
+                      float* margin, int advance_pos, rlhf_stream_t s);
 
 /* ---- decode GEMM (Generation): Y^T[N, M] = W[M, K] . X[N, K]^T, N <= 64 -----
  * swap-AB tcgen05; each 128-row weight tile is a thread-block cluster of `splits`
@@ -130,6 +131,10 @@ int rlhf_gemm_block_n(const rlhf_gemm_params* p); /* tile width the dispatcher p
  * p = p0 + i, with p0 = *p0_dev when p0_dev != NULL (decode steps in a graph). */
 int rlhf_embed(const int32_t* tokens, int64_t tok_stride, int B, int T, int p0, const int* p0_dev,
                const void* tok_emb, const void* pos_emb, int d, float* x, rlhf_stream_t s);
+/* Decode step entry: x[b] = tok_emb[tokens[b*tok_stride + *pos]] + pos_emb[*pos] (f32) and
+ * y[b] = bf16(LN(x[b]) * ln_g + ln_b) (layer 0's LN1), one launch. */
+int rlhf_embed_ln(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev, const void* tok_emb,
+                  const void* pos_emb, int d, float* x, const void* ln_g, const void* ln_b, void* y, rlhf_stream_t s);
 /* tok_emb grad (+ pos grad) scatter-add of dx [B*T, d] (TrainFB). */
 int rlhf_embed_bwd(const int32_t* tokens, int64_t tok_stride, int B, int T, const float* dx, int d,
                    float* dtok_emb, float* dpos_emb, rlhf_stream_t s);

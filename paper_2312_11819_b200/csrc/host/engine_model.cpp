@@ -375,11 +375,15 @@ void Engine::decode_step(const Decoder& m, int B) {
   // RLHF_DECODE_SKIP (debug timing only, results become wrong): bit 0 LN, 1 attention,
   // 2 qkv GEMM, 3 o-proj, 4 FFN GEMMs, 5 LM head + argmax
   static const int skip = [] { const char* e = getenv("RLHF_DECODE_SKIP"); return e ? atoi(e) : 0; }();
-  K(rlhf_embed(tok, S_, B, 1, 0, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x, stream_), 1);
-  // per layer 7 launches: LN1, [QKV GEMM + KV-cache store], attention,
-  // [O-proj + residual], LN2, [FFN-up + ReLU], [FFN-down + residual]
+  K(rlhf_embed_ln(tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x, m.T(RLHF_T_LN1_G, 0),
+                  m.T(RLHF_T_LN1_B, 0), h, stream_),
+    1);
+  // per layer 7 launches: LN1 (layer 0: fused with the embedding), [QKV GEMM + KV-cache
+  // store], attention, [O-proj + residual], LN2, [FFN-up + ReLU], [FFN-down + residual];
+  // then final LN, [LM head + per-tile top-2], [merge -> token, *pos += 1]
   for (int l = 0; l < a.n_layers; ++l) {
-    if (!(skip & 1)) K(rlhf_layernorm(x, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h, nullptr, nullptr, B, d, stream_), 1);
+    if (l > 0 && !(skip & 1))  // layer 0's LN1 ran in rlhf_embed_ln
+      K(rlhf_layernorm(x, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h, nullptr, nullptr, B, d, stream_), 1);
     if (!(skip & 4))
       linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr, nullptr, nullptr,
                     nullptr, l);
@@ -397,8 +401,7 @@ void Engine::decode_step(const Decoder& m, int B) {
   }
   K(rlhf_layernorm(x, m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), dec_hf_.as<uint16_t>(), nullptr, nullptr, B, d, stream_), 1);
   int32_t* dst = graph_for_pred_ ? pred_.as<int32_t>() : tokens_.as<int32_t>();
-  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);
-  K(rlhf_add_int(pos, 1, stream_), 1);
+  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);  // also advances *pos
 }
 
 // Tied LM head of the final hidden rows hf [B, d] fused with the greedy sampler: the
@@ -414,7 +417,8 @@ void Engine::lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t
   q.alpha = 1.0f;
   q.top2 = dec_top2_.as<float>();
   gemm(q);
-  K(rlhf_argmax_tiles(dec_top2_.as<float>(), (V + 127) / 128, B, dst, S_, pos_.as<int>(), margin_.as<float>(), stream_),
+  K(rlhf_argmax_tiles(dec_top2_.as<float>(), (V + 127) / 128, B, dst, S_, pos_.as<int>(), margin_.as<float>(), 1,
+                      stream_),
     1);
 }
 
@@ -428,8 +432,7 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   const int start = P_ - 1;
   cudaMemcpyAsync(pos_.p, &start, sizeof(int), cudaMemcpyHostToDevice, stream_);
   int32_t* dst = teacher_forced ? pred_.as<int32_t>() : tokens_.as<int32_t>();
-  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);
-  K(rlhf_add_int(pos_.as<int>(), 1, stream_), 1);
+  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);  // also advances *pos
   cudaEventRecord(ev_[1], stream_);  // prefill done
   if (R_ <= 1) return;
   if (opt_.use_cuda_graph == 3) {

@@ -164,26 +164,33 @@ __global__ void argmax_merge_kernel(const float* __restrict__ ws, int B, int32_t
 }
 
 // one warp per sample: merge the LM-head GEMM's per-tile top-2 partials
+// One CTA: warp w merges samples w, w+32, ...; afterwards the position counter
+// advances (the decode step's last kernel, so no separate increment launch).
 __global__ void argmax_tiles_kernel(const float4* __restrict__ t2, int tiles, int B, int32_t* __restrict__ tok,
-                                    int64_t S, const int* __restrict__ pos_dev, float* __restrict__ margin) {
+                                    int64_t S, int* __restrict__ pos_dev, float* __restrict__ margin, int advance) {
   pdl_entry();
-  const int b = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
-  if (b >= B) return;
-  Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
-  for (int i = lane; i < tiles; i += 32) {
-    const float4 o = t2[static_cast<int64_t>(i) * B + b];
-    t = top2_merge(t, Top2{o.x, __float_as_int(o.y), o.z});
-  }
+  const int lane = threadIdx.x & 31, nw = blockDim.x / 32;
+  const int pos = *pos_dev;
+  for (int b = threadIdx.x / 32; b < B; b += nw) {
+    Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
+    for (int i = lane; i < tiles; i += 32) {
+      const float4 o = t2[static_cast<int64_t>(i) * B + b];
+      t = top2_merge(t, Top2{o.x, __float_as_int(o.y), o.z});
+    }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    Top2 u{__shfl_xor_sync(0xffffffffu, t.v1, o), __shfl_xor_sync(0xffffffffu, t.i1, o), __shfl_xor_sync(0xffffffffu, t.v2, o)};
-    t = top2_merge(t, u);
+    for (int o = 16; o; o >>= 1) {
+      Top2 u{__shfl_xor_sync(0xffffffffu, t.v1, o), __shfl_xor_sync(0xffffffffu, t.i1, o),
+             __shfl_xor_sync(0xffffffffu, t.v2, o)};
+      t = top2_merge(t, u);
+    }
+    if (lane == 0) {
+      const int64_t at = static_cast<int64_t>(b) * S + pos + 1;
+      tok[at] = t.i1;
+      if (margin) margin[at] = t.v1 - t.v2;
+    }
   }
-  if (lane == 0) {
-    const int64_t at = static_cast<int64_t>(b) * S + *pos_dev + 1;
-    tok[at] = t.i1;
-    if (margin) margin[at] = t.v1 - t.v2;
-  }
+  __syncthreads();  // every warp has read the position
+  if (advance && threadIdx.x == 0) *pos_dev = pos + 1;
 }
 
 // out[b*R + j] = hf[b*S + off + j] . w   (warp per row)
@@ -349,9 +356,10 @@ extern "C" int rlhf_ppo_critic_loss(const float* v, const float* v_old, const fl
   return HST();
 }
 
-extern "C" int rlhf_argmax_tiles(const float* top2, int tiles, int B, int32_t* tok, int64_t tok_stride, const int* pos,
-                                 float* margin, rlhf_stream_t s) {
+extern "C" int rlhf_argmax_tiles(const float* top2, int tiles, int B, int32_t* tok, int64_t tok_stride, int* pos,
+                                 float* margin, int advance_pos, rlhf_stream_t s) {
   if (tiles < 1 || B < 1 || !pos) return 2;
-  return launch_k(argmax_tiles_kernel, dim3((B + 3) / 4), dim3(128), 0, reinterpret_cast<cudaStream_t>(s),
-                  reinterpret_cast<const float4*>(top2), tiles, B, tok, tok_stride, pos, margin);
+  const int warps = B < 32 ? B : 32;
+  return launch_k(argmax_tiles_kernel, dim3(1), dim3(32 * warps), 0, reinterpret_cast<cudaStream_t>(s),
+                  reinterpret_cast<const float4*>(top2), tiles, B, tok, tok_stride, pos, margin, advance_pos);
 }

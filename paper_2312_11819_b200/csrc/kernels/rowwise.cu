@@ -57,6 +57,65 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tokens, int64_t tok
   atomicAdd(dP + static_cast<int64_t>(i) * d + c, g);
 }
 
+// Decode step entry: x[b] = tok_emb[tokens[b*stride + *pos]] + pos_emb[*pos] (fp32, the
+// residual stream) and y[b] = bf16(LN1_layer0(x[b])), one warp per sample.  Waits on its
+// predecessor before triggering dependents (the step chain relies on it, see attention.cu).
+template <int VPL>
+__global__ void embed_ln_kernel(const int32_t* __restrict__ tokens, int64_t tok_stride, const int* __restrict__ pos_dev,
+                                const uint16_t* __restrict__ E, const uint16_t* __restrict__ Pm, int d,
+                                float* __restrict__ x, const uint16_t* __restrict__ g, const uint16_t* __restrict__ bta,
+                                uint16_t* __restrict__ y, int B) {
+  pdl_entry();
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= B) return;
+  const int p = *pos_dev;
+  const int id = tokens[static_cast<int64_t>(row) * tok_stride + p];
+  const uint2* e2 = reinterpret_cast<const uint2*>(E + static_cast<int64_t>(id) * d);
+  const uint2* p2 = reinterpret_cast<const uint2*>(Pm + static_cast<int64_t>(p) * d);
+  const uint2* g2 = reinterpret_cast<const uint2*>(g);
+  const uint2* b2 = reinterpret_cast<const uint2*>(bta);
+  float4* xr = reinterpret_cast<float4*>(x + static_cast<int64_t>(row) * d);
+  const int q = d / 4;
+  float4 v[VPL];
+  uint2 gg[VPL], bb[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c = lane + 32 * k;
+    if (c < q) {
+      const uint2 ev = e2[c], pv = p2[c];
+      v[k] = make_float4(bf2f(ev.x & 0xFFFFu) + bf2f(pv.x & 0xFFFFu), bf2f(ev.x >> 16) + bf2f(pv.x >> 16),
+                         bf2f(ev.y & 0xFFFFu) + bf2f(pv.y & 0xFFFFu), bf2f(ev.y >> 16) + bf2f(pv.y >> 16));
+      xr[c] = v[k];
+      gg[k] = g2[c];
+      bb[k] = b2[c];
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k)
+    if (lane + 32 * k < q) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  const float mu = warp_sum(s) / d;
+  float vs = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k)
+    if (lane + 32 * k < q)
+      vs += (v[k].x - mu) * (v[k].x - mu) + (v[k].y - mu) * (v[k].y - mu) + (v[k].z - mu) * (v[k].z - mu) +
+            (v[k].w - mu) * (v[k].w - mu);
+  const float rs = 1.0f / sqrtf(warp_sum(vs) / d + 1e-5f);
+  uint2* yr = reinterpret_cast<uint2*>(y + static_cast<int64_t>(row) * d);
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c = lane + 32 * k;
+    if (c >= q) continue;
+    const float o0 = (v[k].x - mu) * rs * bf2f(gg[k].x & 0xFFFFu) + bf2f(bb[k].x & 0xFFFFu);
+    const float o1 = (v[k].y - mu) * rs * bf2f(gg[k].x >> 16) + bf2f(bb[k].x >> 16);
+    const float o2 = (v[k].z - mu) * rs * bf2f(gg[k].y & 0xFFFFu) + bf2f(bb[k].y & 0xFFFFu);
+    const float o3 = (v[k].w - mu) * rs * bf2f(gg[k].y >> 16) + bf2f(bb[k].y >> 16);
+    yr[c] = make_uint2(f2bf(o0) | (static_cast<uint32_t>(f2bf(o1)) << 16), f2bf(o2) | (static_cast<uint32_t>(f2bf(o3)) << 16));
+  }
+}
+
 // One warp per row, row held in registers (d <= 4096): a single round trip to
 // memory for x, gamma and beta, then two register passes (mean, variance).
 template <int VPL>  // float4 vectors per lane
@@ -404,4 +463,19 @@ extern "C" int rlhf_adamw(float* master, float* m, float* v, const float* grad, 
   adamw_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, S(s)>>>(master, m, v, grad, static_cast<uint16_t*>(w_bf16), n,
                                                                           lr, beta1, beta2, eps, weight_decay, bc1, bc2);
   return cuda_status();
+}
+
+extern "C" int rlhf_embed_ln(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev, const void* tok_emb,
+                             const void* pos_emb, int d, float* x, const void* ln_g, const void* ln_b, void* y,
+                             rlhf_stream_t s) {
+  if (d % 4 || d > 4096 || !pos_dev) return 2;
+  const dim3 grid((B + 7) / 8), blk(256);
+  const auto* E = static_cast<const uint16_t*>(tok_emb);
+  const auto* Pm = static_cast<const uint16_t*>(pos_emb);
+  const auto* g = static_cast<const uint16_t*>(ln_g);
+  const auto* b = static_cast<const uint16_t*>(ln_b);
+  auto* yp = static_cast<uint16_t*>(y);
+  if (d <= 1024) return launch_k(embed_ln_kernel<8>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
+  if (d <= 2048) return launch_k(embed_ln_kernel<16>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
+  return launch_k(embed_ln_kernel<32>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
 }
