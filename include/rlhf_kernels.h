@@ -61,6 +61,12 @@ typedef struct rlhf_gemm_params {
    * storing C, write per (128-row tile, column n) the top-2 of the tile's rows as
    * float4 {max, bits(argmax, lowest id on ties), second, 0} at top2[(tile*N + n)*4] */
   float* top2;
+  /* optional, row-major C = logits [rows, V] (LM head of a forward that needs no backward):
+   * instead of storing C, write per (row, 128-column half of a 256-wide N tile) the
+   * (max, sum exp(z - max)) of the row's logits to lse_part[(row*tiles_n + n_tile)*2 + half]
+   * (float2) and the target logit z[row, y] to lse_tgt[row], y = lse_tokens[b*lse_S + lse_P + j]
+   * for row = b*lse_R + j.  Only on the CTA-pair path (status 2 otherwise). */
+  float* lse_part; float* lse_tgt; const int32_t* lse_tokens; int lse_S, lse_P, lse_R;
 } rlhf_gemm_params;
 
 int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t s);
@@ -178,6 +184,8 @@ int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax, const void
 
 /* ---- heads, experience, PPO (Generation, Forward, TrainFB) ---------------- */
 /* logp[r] = z[r, y_r] - logsumexp(z[r, :]), y_r = tokens[b*S + P + j] for r = b*R + j; lse saved. */
+/* logp[r] = lse_tgt[r] - logsumexp over the lse_part partials of row r (2*tiles_n per row). */
+int rlhf_lse_merge(const float* lse_part, const float* lse_tgt, int rows, int parts, float* logp, rlhf_stream_t s);
 int rlhf_logprob(const float* logits, int rows, int V, const int32_t* tokens, int S, int P, int R,
                  float* logp, float* lse, rlhf_stream_t s);
 /* dz[r, v] = bf16(g[r] * (1[v == y_r] - exp(z[r,v] - lse[r]))) */

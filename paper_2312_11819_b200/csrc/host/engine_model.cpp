@@ -354,8 +354,27 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
 // lse stay in the arena for the backward when keep_logits.
 void Engine::lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits) {
   const int d = m.a.d_model, V = m.a.vocab;
-  (void)keep_logits;
   K(rlhf_gather_rows(arp_->hf, arp_->hf_resp, B, S_, R_, P_ - 1, d, 2, stream_), 1);
+  if (!keep_logits) {
+    // no backward: the LM-head GEMM epilogue reduces each row's logits to per-tile
+    // (max, sum exp) partials + the target logit; the logits never reach HBM
+    rlhf_gemm_params p{};
+    p.M = B * R_; p.N = V; p.K = d; p.batch = 1; p.batch_h = 1;
+    p.A = arp_->hf_resp; p.lda = d;
+    p.B = m.T(RLHF_T_TOK_EMB); p.ldb = d;
+    p.C = arp_->logits; p.c_f32 = 1; p.c_rs = V; p.c_cs = 1;
+    p.alpha = 1.0f;
+    p.lse_part = arp_->logits;  // (max, sum) partials: rows x tiles x 2 float2, far below the logits' size
+    p.lse_tgt = arp_->lse;
+    p.lse_tokens = tokens; p.lse_S = S_; p.lse_P = P_; p.lse_R = R_;
+    const int st = rlhf_gemm(&p, stream_);
+    if (st == 0) {
+      ++launches_;
+      K(rlhf_lse_merge(arp_->logits, arp_->lse, B * R_, 2 * ((V + 255) / 256), logp, stream_), 1);
+      return;
+    }
+    if (st != 2) kcheck(st, "rlhf_gemm (LM head, log-sum-exp epilogue)");
+  }
   linear(arp_->hf_resp, B * R_, d, m.T(RLHF_T_TOK_EMB), V, nullptr, arp_->logits, true, false, nullptr);
   K(rlhf_logprob(arp_->logits, B * R_, V, tokens, S_, P_, R_, logp, arp_->lse, stream_), 1);
 }

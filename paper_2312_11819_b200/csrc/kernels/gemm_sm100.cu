@@ -71,6 +71,10 @@ struct GemmArgs {
   unsigned long long* probe;
   int debug;
   float* top2;  // column-major top-2 epilogue (decode LM head): [tile][N] x float4
+  float2* lse_part;  // row-major log-sum-exp epilogue (pair path): [row][tiles_n][2 halves]
+  float* lse_tgt;
+  const int32_t* lse_tok;
+  int lse_S, lse_P, lse_R;
 };
 
 __device__ __forceinline__ unsigned long long clk() {
@@ -843,6 +847,14 @@ __global__ void __launch_bounds__(pair::THREADS, 1)
       tc_fence_after();
       const uint32_t tbase = tmem + tq + static_cast<uint32_t>(acc * PBN);
       const int mq = w.m0 + static_cast<int>(rank) * BM + q * 32;
+      // log-sum-exp mode: lane = row, running (max, sum) over this warp's columns
+      const int mrow = mq + static_cast<int>(lane);
+      int tgt = -1;
+      if (e.lse_part && mrow < e.M) {
+        const int bb = mrow / e.lse_R, jj = mrow % e.lse_R;
+        tgt = e.lse_tok[static_cast<int64_t>(bb) * e.lse_S + e.lse_P + jj];
+      }
+      float lm = -FLT_MAX, ls = 0.f;
 #pragma unroll 1
       for (int c = half; c < NCH; c += 2) {
         float v[32];
@@ -855,6 +867,26 @@ __global__ void __launch_bounds__(pair::THREADS, 1)
           tc_fence_before();
           if (lane == 0) arrive_remote(mapa(smem_u32(&tempty[acc]), 0));
         }
+        if (e.lse_part) {
+          const int nc0 = w.n0 + c * 32;
+          float cm = -FLT_MAX;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (nc0 + j < e.N) cm = fmaxf(cm, v[j] * e.alpha);
+          const float nm = fmaxf(lm, cm);
+          float cs = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (nc0 + j < e.N) cs += __expf(v[j] * e.alpha - nm);
+          ls = (lm == -FLT_MAX ? 0.f : ls * __expf(lm - nm)) + cs;
+          lm = nm;
+          if (tgt >= nc0 && tgt < nc0 + 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (tgt == nc0 + j) e.lse_tgt[mrow] = v[j] * e.alpha;
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) st[lane * kStagePitch + j] = v[j];
         __syncwarp();
@@ -866,6 +898,8 @@ __global__ void __launch_bounds__(pair::THREADS, 1)
         epi_rows4(e, w.b, w.h, mq + rr0, w.n0 + c * 32 + cc, sv, st + rr0 * kStagePitch + cc, kStagePitch);
         __syncwarp();
       }
+      if (e.lse_part && mrow < e.M)
+        e.lse_part[(static_cast<int64_t>(mrow) * e.tiles_n + w.n_tile) * 2 + half] = make_float2(lm, ls);
     }
   }
   tc_fence_before();
@@ -1063,6 +1097,13 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
   a.causal = p->causal;
   a.probe = p->probe;
   a.top2 = p->top2;
+  a.lse_part = reinterpret_cast<float2*>(p->lse_part);
+  a.lse_tgt = p->lse_tgt;
+  a.lse_tok = p->lse_tokens;
+  a.lse_S = p->lse_S;
+  a.lse_P = p->lse_P;
+  a.lse_R = p->lse_R;
+  if (a.lse_part && (!p->lse_tgt || !p->lse_tokens || p->lse_R < 1 || p->batch != 1)) return 2;
   if (a.top2 && (p->c_cs == 1 || p->split_k > 1 || p->batch != 1 || bn != 32 && bn != 64 && bn != 128 && bn != 256))
     return 2;
   {
@@ -1077,6 +1118,7 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
     a.counters = p->counters;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (a.lse_part && !pair_mode) return 2;  // the log-sum-exp epilogue lives on the pair path
   if (pair_mode) {
     a.tiles_m = (p->M + pair::PBM - 1) / pair::PBM;
     a.tiles_n = (p->N + pair::PBN - 1) / pair::PBN;

@@ -81,6 +81,29 @@ __global__ void logprob_kernel(const float* __restrict__ z, int V, const int32_t
   }
 }
 
+// one warp per row: merge the LM-head GEMM's (max, sumexp) partials, logp = z_y - lse
+__global__ void lse_merge_kernel(const float2* __restrict__ part, const float* __restrict__ tgt, int rows, int parts,
+                                 float* __restrict__ logp) {
+  const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float m = -FLT_MAX, s = 0.f;
+  for (int k = lane; k < parts; k += 32) {
+    const float2 p = part[static_cast<int64_t>(r) * parts + k];
+    if (p.x == -FLT_MAX) continue;
+    const float mm = fmaxf(m, p.x);
+    s = (m == -FLT_MAX ? 0.f : s * expf(m - mm)) + p.y * expf(p.x - mm);
+    m = mm;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mm = fmaxf(m, m2);
+    s = (m == -FLT_MAX ? 0.f : s * expf(m - mm)) + (m2 == -FLT_MAX ? 0.f : s2 * expf(m2 - mm));
+    m = mm;
+  }
+  if (lane == 0) logp[r] = tgt[r] - (m + logf(s));
+}
+
 __global__ void logprob_bwd_kernel(const float* __restrict__ z, const float* __restrict__ lse, const float* __restrict__ g,
                                    int V, const int32_t* __restrict__ tok, int S, int P, int R, uint16_t* __restrict__ dz) {
   const int r = blockIdx.x;
@@ -362,4 +385,11 @@ extern "C" int rlhf_argmax_tiles(const float* top2, int tiles, int B, int32_t* t
   const int warps = B < 32 ? B : 32;
   return launch_k(argmax_tiles_kernel, dim3(1), dim3(32 * warps), 0, reinterpret_cast<cudaStream_t>(s),
                   reinterpret_cast<const float4*>(top2), tiles, B, tok, tok_stride, pos, margin, advance_pos);
+}
+
+extern "C" int rlhf_lse_merge(const float* lse_part, const float* lse_tgt, int rows, int parts, float* logp,
+                              rlhf_stream_t s) {
+  if (rows < 1 || parts < 1) return 2;
+  lse_merge_kernel<<<(rows + 7) / 8, 256, 0, HS(s)>>>(reinterpret_cast<const float2*>(lse_part), lse_tgt, rows, parts, logp);
+  return HST();
 }

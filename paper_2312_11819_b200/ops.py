@@ -27,7 +27,9 @@ class GemmParams(C.Structure):
                 ("aux", C.c_void_p), ("aux_rs", C.c_int64), ("aux_cs", C.c_int64),
                 ("residual", C.c_void_p), ("causal", C.c_int), ("split_k", C.c_int), ("block_n", C.c_int),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
-                ("counters", C.c_void_p), ("counters_len", C.c_int), ("probe", C.c_void_p), ("top2", C.c_void_p)]
+                ("counters", C.c_void_p), ("counters_len", C.c_int), ("probe", C.c_void_p), ("top2", C.c_void_p),
+                ("lse_part", C.c_void_p), ("lse_tgt", C.c_void_p), ("lse_tokens", C.c_void_p), ("lse_S", C.c_int),
+                ("lse_P", C.c_int), ("lse_R", C.c_int)]
 
 
 def _stream():

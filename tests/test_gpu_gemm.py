@@ -242,3 +242,39 @@ def test_gemm_row_major_split_k_accumulate(M, N, K, split):
     torch.cuda.synchronize()
     close(outs[0], base + ref(a, b, True, True), 1e-5 * K ** 0.5 + 1e-5)
     assert torch.equal(outs[0], outs[1])
+
+
+def test_gemm_pair_lse_epilogue_logprobs():
+    """LM-head GEMM with the log-sum-exp epilogue (logits never stored) + rlhf_lse_merge
+    == log_softmax(X W^T) gathered at the targets (fp32 torch reference)."""
+    import ctypes as C
+    from paper_2312_11819_b200.capi import lib
+    from paper_2312_11819_b200.ops import GemmParams, _stream
+    Bq, R, P, d, V = 16, 128, 8, 768, 8000
+    S = P + R
+    rows = Bq * R
+    torch.manual_seed(3)
+    x = (torch.randn(rows, d, device="cuda") * 0.5).bfloat16()
+    w = (torch.randn(V, d, device="cuda") * 0.1).bfloat16()
+    tokens = torch.randint(0, V, (Bq, S), device="cuda", dtype=torch.int32)
+    tiles = (V + 255) // 256
+    part = torch.empty(rows * tiles * 2 * 2, device="cuda")
+    tgt = torch.empty(rows, device="cuda")
+    logp = torch.empty(rows, device="cuda")
+    dummy = torch.empty(1, device="cuda")
+    p = GemmParams()
+    p.M, p.N, p.K, p.batch, p.batch_h = rows, V, d, 1, 1
+    p.A, p.lda, p.B, p.ldb = x.data_ptr(), d, w.data_ptr(), d
+    p.C, p.c_f32, p.c_rs, p.c_cs, p.alpha = dummy.data_ptr(), 1, V, 1, 1.0
+    p.lse_part, p.lse_tgt, p.lse_tokens = part.data_ptr(), tgt.data_ptr(), tokens.data_ptr()
+    p.lse_S, p.lse_P, p.lse_R = S, P, R
+    L = lib()
+    L.rlhf_gemm.argtypes = [C.POINTER(GemmParams), C.c_void_p]
+    L.rlhf_lse_merge.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    assert L.rlhf_gemm(C.byref(p), _stream()) == 0
+    assert L.rlhf_lse_merge(part.data_ptr(), tgt.data_ptr(), rows, 2 * tiles, logp.data_ptr(), _stream()) == 0
+    z = x.float() @ w.float().t()
+    y = tokens[:, P:].reshape(-1).long()
+    ref = torch.log_softmax(z, -1).gather(1, y[:, None])[:, 0]
+    torch.cuda.synchronize()
+    assert (logp - ref).abs().max().item() < 2e-3
