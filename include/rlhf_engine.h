@@ -85,6 +85,14 @@ int rlhf_task_graph(int structure /*0 ACShare, 1 ACNonShare*/, int batch, int mi
 int rlhf_plan(const char* strategy, int n_devices, int zero_level, double inference_ratio,
               int tp_gen, uint32_t out_mask[6], int* out_role, char* enc, int enc_len);
 
+/* Memory model of a placement (model_state_bytes / activation_bytes / validate_plan,
+ * reference costmodel.hpp:48-50, placement.hpp:104-117): per device, the model-state
+ * bytes (16 B/param train split by ZeRO level, 2 B/param inference, / tp) and the total
+ * with activations; feasible = every device within 95 % of its HBM (180 GB per B200). */
+int rlhf_validate_plan(const char* strategy, int n_devices, int zero_level, double inference_ratio, int tp_gen,
+                       double actor_params, double critic_params, int batch, int prompt_len, int gen_len,
+                       double* state_bytes, double* total_bytes, int* feasible);
+
 /* Communication schedule the plan induces (derive_comm_schedule): per op
  * kind (CollectiveKind), attach (0 Before, 1 After), anchor task, payload. */
 int rlhf_comm_schedule(const char* strategy, int n_devices, int batch, int prompt_len, int gen_len,

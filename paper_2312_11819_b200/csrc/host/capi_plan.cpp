@@ -170,3 +170,40 @@ extern "C" int rlhf_comm_schedule(const char* strategy, int n_devices, int batch
     return capi_status(e);
   }
 }
+
+extern "C" int rlhf_validate_plan(const char* strategy, int n_devices, int zero_level, double inference_ratio, int tp_gen,
+                                  double actor_params, double critic_params, int batch, int prompt_len, int gen_len,
+                                  double* state_bytes, double* total_bytes, int* feasible) {
+  try {
+    const ClusterTopology t = ClusterTopology::b200_box(n_devices);
+    ModelSizes sz;
+    sz.actor = sz.ref = actor_params;
+    sz.critic = sz.reward = critic_params;
+    LoopParams lp;
+    lp.batch_size = batch;
+    lp.micro_batches = 1;
+    lp.rollout_nums = 1;
+    lp.ppo_epochs = 1;
+    lp.prompt_len = prompt_len;
+    lp.gen_len = gen_len;
+    StrategyConfig sc;
+    sc.name = strategy;
+    sc.zero_level = zero_level;
+    sc.inference_ratio = inference_ratio;
+    sc.tp_gen = tp_gen;
+    const BuiltStrategy b = build_strategy(sc, t, build_pipeline(PipelineStructure::ACNonShare, sz, lp));
+    const CostModel c{};
+    for (int d = 0; d < n_devices; ++d) state_bytes[d] = total_bytes[d] = 0.0;
+    for (const auto& [m, cfg] : b.plan.assignments) {
+      if (!b.pipeline.has_model(m)) continue;
+      const double st = model_state_bytes(b.pipeline.model(m), cfg, c.mem);
+      for (int d : cfg.devices) state_bytes[d] += st;
+    }
+    const FeasibilityReport rep = validate_plan(b.plan, b.pipeline, c, t);
+    for (const auto& [d, bytes] : rep.per_device_bytes) total_bytes[d] = bytes;
+    *feasible = rep.feasible ? 1 : 0;
+    return 0;
+  } catch (const std::exception& e) {
+    return capi_status(e);
+  }
+}

@@ -177,3 +177,25 @@ def test_library_exports_every_declared_symbol(L):
         assert names, h
         for n in names:
             assert hasattr(L, n), f"{n} declared in {h} but not exported"
+
+
+@pytest.mark.parametrize("zero,state_gb,feasible", [(0, 242.6, False), (1, 101.1, True), (2, 77.5, True), (3, 54.0, True)])
+def test_memory_model_colocated_llama7b(L, zero, state_gb, feasible):
+    """c4 Co-located on 8 B200s with four 7B models (6.74e9 params):
+    per-GPU model states Z0 ~243 GB (over the 95 % x 180 GB budget), Z1 ~101, Z2 ~78,
+    Z3 ~54 GB; totals add the activation model (costmodel.hpp:48-50, placement.hpp:104-117)."""
+    n = 8
+    st = (C.c_double * n)()
+    tot = (C.c_double * n)()
+    ok = C.c_int()
+    L.rlhf_validate_plan.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double, C.c_double, C.c_int,
+                                     C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int)]
+    assert L.rlhf_validate_plan(b"colocated", n, zero, 0.5, 1, 6.74e9, 6.74e9, 64, 256, 256, st, tot,
+                                C.byref(ok)) == 0
+    for d in range(n):
+        assert abs(st[d] / 1e9 - state_gb) < 0.6, (d, st[d] / 1e9)
+        assert tot[d] >= st[d]
+    assert bool(ok.value) == (max(tot) <= 0.95 * 180e9)
+    if not feasible:
+        assert not ok.value
