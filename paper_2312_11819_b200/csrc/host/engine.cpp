@@ -153,8 +153,17 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
   // stream of the Co-located Forward stage (Critic + Reward beside Actor + Ref)
   build_arena(ar_main_, hosts_[0] || hosts_[1]);
   if (tag_ == StrategyTag::Colocated) {
-    build_arena(ar_side_, true);  // also trains the Critic beside the Actor
-    CK(cudaStreamCreateWithFlags(&stream_side_, cudaStreamNonBlocking));
+    // Critic-shaped arena for the second stream (Critic/Reward forwards, Critic training);
+    // when it does not fit (long sequences, large models) the step stays single-stream
+    try {
+      build_arena(ar_side_, true, true);
+      CK(cudaStreamCreateWithFlags(&stream_side_, cudaStreamNonBlocking));
+    } catch (const DeviceError&) {
+      for (DevBuf* b : ar_side_.owned) delete b;
+      ar_side_.owned.clear();
+      cudaGetLastError();
+      stream_side_ = nullptr;
+    }
   }
 
   // ---- generation state (the generator: Actor or ShadowActor) -----------------
@@ -298,15 +307,16 @@ void Engine::score_reward(const Decoder& m, const int32_t* tok, int B, float* sc
 
 // Activation arena: capacities = max over hosted models.  `trains` keeps every layer's
 // saved activations and the backward buffers; a forward-only arena keeps one layer.
-void Engine::build_arena(Arena& A, bool trains) {
+void Engine::build_arena(Arena& A, bool trains, bool critic_only) {
   A.B = Bcap_;
   A.S = S_;
   A.R = R_;
   for (const rlhf_arch* a : {&cfg_.actor, &cfg_.critic}) {
+    if (critic_only && a == &cfg_.actor) continue;
     A.d = std::max(A.d, a->d_model);
     A.ff = std::max(A.ff, a->d_ff);
     A.H = std::max(A.H, a->n_heads);
-    A.V = std::max(A.V, a->vocab);
+    A.V = std::max(A.V, critic_only ? 1 : a->vocab);  // scalar heads only: no logits
     A.L = std::max(A.L, a->n_layers);
   }
   A.T = static_cast<int64_t>(Bcap_) * S_;
@@ -389,32 +399,40 @@ void Engine::step(const int32_t* prompts_host, rlhf_step_report* rep) {
       // Forward x4 (workload.cpp:119 lists Actor, Critic, Ref, Reward; they are
       // independent): Critic + Reward on a second stream with their own arena, Actor +
       // Ref on the main stream, joined before the experience-buffer barrier
-      cudaEventRecord(ev_[6], stream_);
-      CK(cudaStreamWaitEvent(stream_side_, ev_[6], 0));
-      std::swap(stream_, stream_side_);
-      arp_ = &ar_side_;
+      if (stream_side_) {
+        cudaEventRecord(ev_[6], stream_);
+        CK(cudaStreamWaitEvent(stream_side_, ev_[6], 0));
+        std::swap(stream_, stream_side_);
+        arp_ = &ar_side_;
+      }
       score_values(critic_, tok, Bg, values_.as<float>());
       score_reward(reward_, tok, Bg, score_.as<float>());
-      cudaEventRecord(ev_[7], stream_);
-      std::swap(stream_, stream_side_);
-      arp_ = &ar_main_;
+      if (stream_side_) {
+        cudaEventRecord(ev_[7], stream_);
+        std::swap(stream_, stream_side_);
+        arp_ = &ar_main_;
+      }
       score_logp(actor_, tok, Bg, logp_old_.as<float>());
       score_logp(ref_, tok, Bg, logp_ref_.as<float>());
-      CK(cudaStreamWaitEvent(stream_, ev_[7], 0));
+      if (stream_side_) CK(cudaStreamWaitEvent(stream_, ev_[7], 0));
       cudaEventRecord(ev_[3], stream_);
       gae(Bg);
       // TrainFB(Actor) and TrainFB(Critic) are independent given the experience buffer:
       // the Critic trains on the second stream / arena
-      cudaEventRecord(ev_[6], stream_);
-      CK(cudaStreamWaitEvent(stream_side_, ev_[6], 0));
-      std::swap(stream_, stream_side_);
-      arp_ = &ar_side_;
+      if (stream_side_) {
+        cudaEventRecord(ev_[6], stream_);
+        CK(cudaStreamWaitEvent(stream_side_, ev_[6], 0));
+        std::swap(stream_, stream_side_);
+        arp_ = &ar_side_;
+      }
       train_critic(critic_, Bg, critic_comm_);
-      cudaEventRecord(ev_[7], stream_);
-      std::swap(stream_, stream_side_);
-      arp_ = &ar_main_;
+      if (stream_side_) {
+        cudaEventRecord(ev_[7], stream_);
+        std::swap(stream_, stream_side_);
+        arp_ = &ar_main_;
+      }
       train_actor(actor_, Bg, actor_comm_);
-      CK(cudaStreamWaitEvent(stream_, ev_[7], 0));
+      if (stream_side_) CK(cudaStreamWaitEvent(stream_, ev_[7], 0));
       cudaEventRecord(ev_[4], stream_);
       break;
     }

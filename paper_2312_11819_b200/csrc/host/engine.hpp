@@ -108,7 +108,7 @@ class Engine {
   void score_values(const Decoder& m, const int32_t* tok, int B, float* values);
   void score_reward(const Decoder& m, const int32_t* tok, int B, float* score);
   void gae(int B);
-  void build_arena(Arena& A, bool trains);
+  void build_arena(Arena& A, bool trains, bool critic_only = false);
   void place_prompts(const int32_t* dev_prompts, int row0);
 
   // GEMM helpers (all go through rlhf_gemm)
