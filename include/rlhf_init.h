@@ -24,7 +24,9 @@ extern "C" {
 /* ---- model shape --------------------------------------------------------- */
 
 typedef struct rlhf_arch {
-  int family;        /* 0 = OPT (pre-LN LayerNorm, ReLU, learned positions, tied LM head) */
+  int family;        /* 0 = OPT (pre-LN LayerNorm, ReLU, learned positions, tied LM head);
+                        1 = LLaMA (pre-norm RMSNorm eps 1e-6, SwiGLU FFN, rotary positions theta 1e4,
+                            no biases, untied LM head) */
   int vocab;
   int d_model;
   int n_layers;
@@ -53,6 +55,7 @@ enum {
   RLHF_T_LNF_G,       /* [d] */
   RLHF_T_LNF_B,
   RLHF_T_VHEAD,       /* [d] (scalar_head only, else size 0) */
+  RLHF_T_LM_HEAD,     /* [V, d] untied LM head (LLaMA, !scalar_head; else size 0) */
   RLHF_T_COUNT
 };
 #define RLHF_LAYER_FIRST RLHF_T_LN1_G
@@ -64,7 +67,17 @@ static inline int64_t rlhf_align64(int64_t n) { return (n + 63) & ~(int64_t)63; 
 /* Element count of tensor `t` (layer-independent). */
 static inline int64_t rlhf_tensor_numel(const rlhf_arch* a, int t) {
   const int64_t V = a->vocab, d = a->d_model, f = a->d_ff;
+  if (a->family == 1) { /* LLaMA: W1 = [gate (ff rows) | up (ff rows)]; no biases, no LN betas, no positions */
+    switch (t) {
+      case RLHF_T_POS_EMB: case RLHF_T_LN1_B: case RLHF_T_LN2_B: case RLHF_T_LNF_B:
+      case RLHF_T_BQKV: case RLHF_T_BO: case RLHF_T_B1: case RLHF_T_B2: return 0;
+      case RLHF_T_W1: return 2 * f * d;
+      case RLHF_T_LM_HEAD: return a->scalar_head ? 0 : V * d;
+      default: break;
+    }
+  }
   switch (t) {
+    case RLHF_T_LM_HEAD: return 0;
     case RLHF_T_TOK_EMB: return V * d;
     case RLHF_T_POS_EMB: return (int64_t)a->max_pos * d;
     case RLHF_T_WQKV: return 3 * d * d;
@@ -99,7 +112,16 @@ static inline int64_t rlhf_tensor_offset(const rlhf_arch* a, int t, int l) {
 
 /* Total flat parameter count (including alignment padding, which stays 0). */
 static inline int64_t rlhf_param_total(const rlhf_arch* a) {
-  return rlhf_tensor_offset(a, RLHF_T_VHEAD, 0) + rlhf_align64(rlhf_tensor_numel(a, RLHF_T_VHEAD));
+  return rlhf_tensor_offset(a, RLHF_T_LM_HEAD, 0) + rlhf_align64(rlhf_tensor_numel(a, RLHF_T_LM_HEAD));
+}
+
+/* Rotary table entry (LLaMA): angle = pos * theta^(-2i/hd) for pair i in [0, hd/2),
+ * evaluated in double and rounded to fp32 so the engine's table and the oracle's agree
+ * bit for bit.  Pair i rotates elements (i, i + hd/2) of each q / k head (HF LLaMA). */
+static inline void rlhf_rope_cos_sin(int pos, int i, int hd, float* c, float* s) {
+  const double ang = (double)pos * pow(10000.0, -2.0 * (double)i / (double)hd);
+  *c = (float)cos(ang);
+  *s = (float)sin(ang);
 }
 
 /* ---- deterministic generators -------------------------------------------- */
@@ -152,6 +174,7 @@ static inline void rlhf_tensor_init_dist(const rlhf_arch* a, int t, double* mean
     case RLHF_T_POS_EMB: *std = 1.0; break;
     case RLHF_T_LN1_G: case RLHF_T_LN2_G: case RLHF_T_LNF_G: *mean = 1.0; *std = 0.05; break;
     case RLHF_T_VHEAD: *std = 1.0 / sqrt((double)a->d_model); break;
+    case RLHF_T_LM_HEAD: *std = 2.0 / sqrt((double)a->d_model); break;
     /* fan-in scaled matrices (unit-variance pre-activations) */
     case RLHF_T_WQKV: case RLHF_T_WO: case RLHF_T_W1: *std = 1.0 / sqrt((double)a->d_model); break;
     case RLHF_T_W2: *std = 1.0 / sqrt((double)a->d_ff); break;

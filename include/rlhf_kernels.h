@@ -151,6 +151,30 @@ int rlhf_layernorm(const float* x, const void* g, const void* b, void* y, float*
 int rlhf_layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd, const void* g,
                        float* dx, float* dg, float* db, int M, int d, float* ws, size_t ws_floats,
                        rlhf_stream_t s);
+/* ---- LLaMA family (rlhf_arch.family == 1) --------------------------------
+ * The reference models the 7B Actor/Critic only through its cost formulas
+ * (workload.hpp:25-60 ModelSizes); these are the element ops
+ * a LLaMA-shaped decoder adds to the OPT path.  pos_emb may be NULL in rlhf_embed /
+ * rlhf_embed_bwd (no learned positions).
+ * RMSNorm: y = bf16(x * rstd * g), rstd = 1/sqrt(mean(x^2) + 1e-6); rstd optional. */
+int rlhf_rmsnorm(const float* x, const void* g, void* y, float* rstd, int M, int d, rlhf_stream_t s);
+/* dx += RMSNorm backward of dy (saved rstd); dg partials -> ws [nblk, d] -> dg (+=). */
+int rlhf_rmsnorm_bwd(const float* dy, const float* x, const float* rstd, const void* g, float* dx, float* dg, int M,
+                     int d, float* ws, size_t ws_floats, rlhf_stream_t s);
+/* Decode step entry of the LLaMA family: x[b] = tok_emb[tokens[b*stride + *pos]], y = RMSNorm(x). */
+int rlhf_embed_rmsnorm(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev, const void* tok_emb,
+                       int d, float* x, const void* g, void* y, rlhf_stream_t s);
+/* Rotary embedding in place on the q and k parts of packed qkv rows [B*T, 3*H*hd] (bf16),
+ * row b*T + i at position p0 + i (p0 = *p0_dev when given); table: float2 (cos, sin)
+ * [positions][hd/2] from rlhf_rope_cos_sin.  inverse: the transpose (backward of dq, dk).
+ * kcache/vcache (optional, [B][H][Smax][hd]): also store the rotated k and v at p. */
+int rlhf_rope_qkv(void* qkv, int B, int T, int p0, const int* p0_dev, int H, int hd, const float* table, int inverse,
+                  void* kcache, void* vcache, int Smax, rlhf_stream_t s);
+/* act[r, j] = bf16(silu(gu[r, j]) * gu[r, ff + j]) over rows x ff. */
+int rlhf_swiglu(const void* gu, void* act, int rows, int ff, rlhf_stream_t s);
+/* dgu[r] = [dact * up * s(g) * (1 + g (1 - s(g))) | dact * silu(g)] (bf16). */
+int rlhf_swiglu_bwd(const void* gu, const void* dact, void* dgu, int rows, int ff, rlhf_stream_t s);
+
 /* out_bf16 = bf16(x) elementwise (n elements). */
 int rlhf_round_bf16(const float* x, void* out, int64_t n, rlhf_stream_t s);
 /* db[n] += sum_m G[m, n] (bf16 G, fp32 sums, fixed order).  ws >= 64*N floats. */

@@ -37,7 +37,13 @@ inline float dotf(const float* a, const float* b, int n) {
 struct Net {
   rlhf_arch a;
   Vec w;  // bf16 parameter values held as fp32, flat layout of rlhf_init.h
-  const float* t(int id, int l = 0) const { return w.data() + rlhf_tensor_offset(&a, id, l); }
+  // tensors absent from the family's layout (size 0) are NULL
+  const float* t(int id, int l = 0) const {
+    return rlhf_tensor_numel(&a, id) ? w.data() + rlhf_tensor_offset(&a, id, l) : nullptr;
+  }
+  bool llama() const { return a.family == 1; }
+  int head_id() const { return llama() ? RLHF_T_LM_HEAD : RLHF_T_TOK_EMB; }
+  Vec rope;  // LLaMA: (cos, sin) [max_pos][hd/2] from rlhf_rope_cos_sin
 };
 
 Net make_net(const rlhf_arch& a, uint64_t seed) {
@@ -62,8 +68,66 @@ Net make_net(const rlhf_arch& a, uint64_t seed) {
     float* dst = n.w.data() + rlhf_tensor_offset(&a, pc.t, pc.l) + pc.i0;
     for (size_t i = 0; i < tmp.size(); ++i) dst[i] = rlhf_bf16_to_f32(tmp[i]);
   }
+  if (n.llama()) {
+    const int hd = a.d_model / a.n_heads, half = hd / 2;
+    n.rope.assign(static_cast<size_t>(a.max_pos) * half * 2, 0.0f);
+    for (int p = 0; p < a.max_pos; ++p)
+      for (int i = 0; i < half; ++i)
+        rlhf_rope_cos_sin(p, i, hd, &n.rope[(static_cast<size_t>(p) * half + i) * 2],
+                          &n.rope[(static_cast<size_t>(p) * half + i) * 2 + 1]);
+  }
   return n;
 }
+
+// ---- LLaMA family (rlhf_arch.family == 1): RMSNorm, rotary q/k, SwiGLU ----------------
+
+// y = bf16(x * rstd * g), rstd = 1/sqrt(mean(x^2) + 1e-6)
+void rmsnorm(const float* x, int M, int d, const float* g, float* y, float* rstd) {
+#pragma omp parallel for schedule(static)
+  for (int m = 0; m < M; ++m) {
+    const float* xr = x + static_cast<size_t>(m) * d;
+    float v = 0;
+    for (int j = 0; j < d; ++j) v += xr[j] * xr[j];
+    const float rs = 1.0f / std::sqrt(v / d + 1e-6f);
+    for (int j = 0; j < d; ++j) y[static_cast<size_t>(m) * d + j] = bfr(xr[j] * rs * g[j]);
+    if (rstd) rstd[m] = rs;
+  }
+}
+
+// dx += rstd * (dy*g - xhat * mean(dy*g*xhat)); dg += dy * xhat
+void rmsnorm_bwd(const float* dy, const float* x, const float* rstd, const float* g, int M, int d, float* dx, float* dg) {
+  for (int m = 0; m < M; ++m) {
+    const float* xr = x + static_cast<size_t>(m) * d;
+    const float* dr = dy + static_cast<size_t>(m) * d;
+    float c = 0;
+    for (int j = 0; j < d; ++j) {
+      const float xh = xr[j] * rstd[m];
+      c += dr[j] * g[j] * xh;
+      dg[j] += dr[j] * xh;
+    }
+    c /= d;
+    for (int j = 0; j < d; ++j) dx[static_cast<size_t>(m) * d + j] += rstd[m] * (dr[j] * g[j] - xr[j] * rstd[m] * c);
+  }
+}
+
+// Rotate q and k of every head of one packed qkv row at position p (HF LLaMA pairing:
+// element i with i + hd/2); inverse = transpose.  Values are bf16-rounded.
+void rope_row(const Net& n, float* row, int p, bool inverse) {
+  const int d = n.a.d_model, hd = d / n.a.n_heads, half = hd / 2;
+  const float sg = inverse ? -1.0f : 1.0f;
+  for (int part = 0; part < 2; ++part)
+    for (int h = 0; h < n.a.n_heads; ++h) {
+      float* v = row + part * d + h * hd;
+      for (int i = 0; i < half; ++i) {
+        const float c = n.rope[(static_cast<size_t>(p) * half + i) * 2], s = sg * n.rope[(static_cast<size_t>(p) * half + i) * 2 + 1];
+        const float x0 = v[i], x1 = v[i + half];
+        v[i] = bfr(x0 * c - x1 * s);
+        v[i + half] = bfr(x1 * c + x0 * s);
+      }
+    }
+}
+
+inline float sigmoid(float g) { return 1.0f / (1.0f + std::exp(-g)); }
 
 // Y[M,N] = X[M,K] . W[N,K]^T (+ bias[N]); fp32 accumulation.
 void linear(const float* X, int M, int K, const float* W, int N, const float* bias, float* Y) {
@@ -175,7 +239,7 @@ Vec forward_chunk(const Net& n, const int32_t* tok, int B, int S, int i0, int i1
       const int r = b * T + (i - i0);
       const int id = tok[static_cast<size_t>(b) * S + i];
       for (int j = 0; j < d; ++j)
-        x[static_cast<size_t>(r) * d + j] = E[static_cast<size_t>(id) * d + j] + Pm[static_cast<size_t>(i) * d + j];
+        x[static_cast<size_t>(r) * d + j] = E[static_cast<size_t>(id) * d + j] + (Pm ? Pm[static_cast<size_t>(i) * d + j] : 0.0f);
     }
   if (sv) {
     const size_t L = static_cast<size_t>(a.n_layers);
@@ -184,13 +248,20 @@ Vec forward_chunk(const Net& n, const int32_t* tok, int B, int S, int i0, int i1
       v->assign(L, Vec());
   }
   Vec h(static_cast<size_t>(M) * d), qkv(static_cast<size_t>(M) * 3 * d), o(static_cast<size_t>(M) * d),
-      tmp(static_cast<size_t>(M) * d), pre(static_cast<size_t>(M) * ff), mean(M), rstd(M);
+      tmp(static_cast<size_t>(M) * d), pre(static_cast<size_t>(M) * ff * (n.llama() ? 2 : 1)), mean(M), rstd(M),
+      act(n.llama() ? static_cast<size_t>(M) * ff : 0);
+  auto norm = [&](int g, int l, float* y) {  // LayerNorm (OPT) / RMSNorm (LLaMA)
+    if (n.llama()) rmsnorm(x.data(), M, d, n.t(g, l), y, rstd.data());
+    else layernorm(x.data(), M, d, n.t(g, l), n.t(g + 1, l), y, mean.data(), rstd.data());
+  };
   for (int l = 0; l < a.n_layers; ++l) {
     if (sv) sv->x_in[l] = x;
-    layernorm(x.data(), M, d, n.t(RLHF_T_LN1_G, l), n.t(RLHF_T_LN1_B, l), h.data(), mean.data(), rstd.data());
+    norm(RLHF_T_LN1_G, l, h.data());
     if (sv) { sv->mean1[l] = mean; sv->rstd1[l] = rstd; sv->h1[l] = h; }
     linear(h.data(), M, d, n.t(RLHF_T_WQKV, l), 3 * d, n.t(RLHF_T_BQKV, l), qkv.data());
     for (float& q : qkv) q = bfr(q);
+    if (n.llama())
+      for (int r = 0; r < M; ++r) rope_row(n, qkv.data() + static_cast<size_t>(r) * 3 * d, i0 + r % T, false);
     if (sv) sv->qkv[l] = qkv;
     for (int b = 0; b < B; ++b)
       for (int i = i0; i < i1; ++i) {
@@ -231,16 +302,28 @@ Vec forward_chunk(const Net& n, const int32_t* tok, int B, int S, int i0, int i1
     linear(o.data(), M, d, n.t(RLHF_T_WO, l), d, n.t(RLHF_T_BO, l), tmp.data());
     for (size_t k = 0; k < x.size(); ++k) x[k] += tmp[k];
     if (sv) sv->x_mid[l] = x;
-    layernorm(x.data(), M, d, n.t(RLHF_T_LN2_G, l), n.t(RLHF_T_LN2_B, l), h.data(), mean.data(), rstd.data());
+    norm(RLHF_T_LN2_G, l, h.data());
     if (sv) { sv->mean2[l] = mean; sv->rstd2[l] = rstd; sv->h2[l] = h; }
-    linear(h.data(), M, d, n.t(RLHF_T_W1, l), ff, n.t(RLHF_T_B1, l), pre.data());
-    for (float& p : pre) p = bfr(p > 0.0f ? p : 0.0f);
-    if (sv) sv->f[l] = pre;
-    linear(pre.data(), M, ff, n.t(RLHF_T_W2, l), d, n.t(RLHF_T_B2, l), tmp.data());
+    if (n.llama()) {  // pre = [gate | up] (bf16), act = bf16(silu(gate) * up)
+      linear(h.data(), M, d, n.t(RLHF_T_W1, l), 2 * ff, nullptr, pre.data());
+      for (float& p : pre) p = bfr(p);
+      for (int m = 0; m < M; ++m)
+        for (int j = 0; j < ff; ++j) {
+          const float g = pre[static_cast<size_t>(m) * 2 * ff + j], u = pre[static_cast<size_t>(m) * 2 * ff + ff + j];
+          act[static_cast<size_t>(m) * ff + j] = bfr(g * sigmoid(g) * u);
+        }
+      if (sv) sv->f[l] = pre;
+      linear(act.data(), M, ff, n.t(RLHF_T_W2, l), d, nullptr, tmp.data());
+    } else {
+      linear(h.data(), M, d, n.t(RLHF_T_W1, l), ff, n.t(RLHF_T_B1, l), pre.data());
+      for (float& p : pre) p = bfr(p > 0.0f ? p : 0.0f);
+      if (sv) sv->f[l] = pre;
+      linear(pre.data(), M, ff, n.t(RLHF_T_W2, l), d, n.t(RLHF_T_B2, l), tmp.data());
+    }
     for (size_t k = 0; k < x.size(); ++k) x[k] += tmp[k];
   }
   Vec hf(static_cast<size_t>(M) * d);
-  layernorm(x.data(), M, d, n.t(RLHF_T_LNF_G), n.t(RLHF_T_LNF_B), hf.data(), mean.data(), rstd.data());
+  norm(RLHF_T_LNF_G, 0, hf.data());
   if (sv) { sv->x_fin = x; sv->meanf = mean; sv->rstdf = rstd; sv->hf = hf; }
   return hf;
 }
@@ -248,7 +331,7 @@ Vec forward_chunk(const Net& n, const int32_t* tok, int B, int S, int i0, int i1
 // LM logits of one hidden row against the tied embedding.
 void logits_row(const Net& n, const float* hrow, float* z) {
   const int V = n.a.vocab, d = n.a.d_model;
-  const float* E = n.t(RLHF_T_TOK_EMB);
+  const float* E = n.t(n.head_id());
   for (int v = 0; v < V; ++v) z[v] = dotf(hrow, E + static_cast<size_t>(v) * d, d);
 }
 
@@ -292,27 +375,53 @@ void backward(const Net& n, const int32_t* tok, int B, int S, const Saved& sv, c
   const rlhf_arch& a = n.a;
   const int d = a.d_model, H = a.n_heads, hd = d / H, ff = a.d_ff, M = B * S;
   const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
-  auto G = [&](int id, int l = 0) { return grad.data() + rlhf_tensor_offset(&a, id, l); };
+  auto G = [&](int id, int l = 0) -> float* {
+    return rlhf_tensor_numel(&a, id) ? grad.data() + rlhf_tensor_offset(&a, id, l) : nullptr;
+  };
   Vec dres(static_cast<size_t>(M) * d, 0.0f);
-  layernorm_bwd(dhf.data(), sv.x_fin.data(), sv.meanf.data(), sv.rstdf.data(), n.t(RLHF_T_LNF_G), M, d,
-                dres.data(), G(RLHF_T_LNF_G), G(RLHF_T_LNF_B));
-  Vec g(static_cast<size_t>(M) * d), df(static_cast<size_t>(M) * ff), dh(static_cast<size_t>(M) * d),
+  auto norm_bwd = [&](const float* dy, const Vec& x, const Vec& mean, const Vec& rstd, int gid, int l) {
+    if (n.llama()) rmsnorm_bwd(dy, x.data(), rstd.data(), n.t(gid, l), M, d, dres.data(), G(gid, l));
+    else layernorm_bwd(dy, x.data(), mean.data(), rstd.data(), n.t(gid, l), M, d, dres.data(), G(gid, l), G(gid + 1, l));
+  };
+  auto colsum = [&](const Vec& Gm, int N, float* db) { if (db) colsum_acc(Gm.data(), M, N, db); };
+  norm_bwd(dhf.data(), sv.x_fin, sv.meanf, sv.rstdf, RLHF_T_LNF_G, 0);
+  Vec g(static_cast<size_t>(M) * d), df(static_cast<size_t>(M) * ff * (n.llama() ? 2 : 1)), dh(static_cast<size_t>(M) * d),
       dqkv(static_cast<size_t>(M) * 3 * d), dov(static_cast<size_t>(M) * d);
   for (int l = a.n_layers - 1; l >= 0; --l) {
     // FFN: x_out = x_mid + relu(h2 W1^T + b1) W2^T + b2
     for (size_t k = 0; k < g.size(); ++k) g[k] = bfr(dres[k]);
-    colsum_acc(g.data(), M, d, G(RLHF_T_B2, l));
-    matmul_tn_acc(g.data(), M, d, sv.f[l].data(), ff, G(RLHF_T_W2, l));
-    matmul_nn(g.data(), M, d, n.t(RLHF_T_W2, l), ff, df.data());
-    for (size_t k = 0; k < df.size(); ++k) df[k] = sv.f[l][k] > 0.0f ? bfr(df[k]) : 0.0f;
-    colsum_acc(df.data(), M, ff, G(RLHF_T_B1, l));
-    matmul_tn_acc(df.data(), M, ff, sv.h2[l].data(), d, G(RLHF_T_W1, l));
-    matmul_nn(df.data(), M, ff, n.t(RLHF_T_W1, l), d, dh.data());
-    layernorm_bwd(dh.data(), sv.x_mid[l].data(), sv.mean2[l].data(), sv.rstd2[l].data(), n.t(RLHF_T_LN2_G, l), M,
-                  d, dres.data(), G(RLHF_T_LN2_G, l), G(RLHF_T_LN2_B, l));
+    colsum(g, d, G(RLHF_T_B2, l));
+    if (n.llama()) {  // SwiGLU backward from the saved [gate | up]
+      const Vec& gu = sv.f[l];
+      Vec act(static_cast<size_t>(M) * ff), dact(static_cast<size_t>(M) * ff);
+      for (int m = 0; m < M; ++m)
+        for (int j = 0; j < ff; ++j) {
+          const float gg = gu[static_cast<size_t>(m) * 2 * ff + j], u = gu[static_cast<size_t>(m) * 2 * ff + ff + j];
+          act[static_cast<size_t>(m) * ff + j] = bfr(gg * sigmoid(gg) * u);
+        }
+      matmul_tn_acc(g.data(), M, d, act.data(), ff, G(RLHF_T_W2, l));
+      matmul_nn(g.data(), M, d, n.t(RLHF_T_W2, l), ff, dact.data());
+      for (int m = 0; m < M; ++m)
+        for (int j = 0; j < ff; ++j) {
+          const float gg = gu[static_cast<size_t>(m) * 2 * ff + j], u = gu[static_cast<size_t>(m) * 2 * ff + ff + j];
+          const float da = bfr(dact[static_cast<size_t>(m) * ff + j]), s = sigmoid(gg);
+          df[static_cast<size_t>(m) * 2 * ff + j] = bfr(da * u * s * (1.0f + gg * (1.0f - s)));
+          df[static_cast<size_t>(m) * 2 * ff + ff + j] = bfr(da * gg * s);
+        }
+      matmul_tn_acc(df.data(), M, 2 * ff, sv.h2[l].data(), d, G(RLHF_T_W1, l));
+      matmul_nn(df.data(), M, 2 * ff, n.t(RLHF_T_W1, l), d, dh.data());
+    } else {
+      matmul_tn_acc(g.data(), M, d, sv.f[l].data(), ff, G(RLHF_T_W2, l));
+      matmul_nn(g.data(), M, d, n.t(RLHF_T_W2, l), ff, df.data());
+      for (size_t k = 0; k < df.size(); ++k) df[k] = sv.f[l][k] > 0.0f ? bfr(df[k]) : 0.0f;
+      colsum(df, ff, G(RLHF_T_B1, l));
+      matmul_tn_acc(df.data(), M, ff, sv.h2[l].data(), d, G(RLHF_T_W1, l));
+      matmul_nn(df.data(), M, ff, n.t(RLHF_T_W1, l), d, dh.data());
+    }
+    norm_bwd(dh.data(), sv.x_mid[l], sv.mean2[l], sv.rstd2[l], RLHF_T_LN2_G, l);
     // Attention block: x_mid = x_in + attn(h1) Wo^T + bo
     for (size_t k = 0; k < g.size(); ++k) g[k] = bfr(dres[k]);
-    colsum_acc(g.data(), M, d, G(RLHF_T_BO, l));
+    colsum(g, d, G(RLHF_T_BO, l));
     matmul_tn_acc(g.data(), M, d, sv.o[l].data(), d, G(RLHF_T_WO, l));
     matmul_nn(g.data(), M, d, n.t(RLHF_T_WO, l), d, dov.data());
     for (float& v : dov) v = bfr(v);
@@ -358,11 +467,12 @@ void backward(const Net& n, const int32_t* tok, int B, int S, const Saved& sv, c
           for (int e = 0; e < hd; ++e) { dq[e] = bfr(accq[e]); dk[e] = bfr(acck[e]); dv[e] = bfr(accv[e]); }
         }
       }
-    colsum_acc(dqkv.data(), M, 3 * d, G(RLHF_T_BQKV, l));
+    if (n.llama())  // dq, dk through the rotation's transpose
+      for (int r = 0; r < M; ++r) rope_row(n, dqkv.data() + static_cast<size_t>(r) * 3 * d, r % S, true);
+    colsum(dqkv, 3 * d, G(RLHF_T_BQKV, l));
     matmul_tn_acc(dqkv.data(), M, 3 * d, sv.h1[l].data(), d, G(RLHF_T_WQKV, l));
     matmul_nn(dqkv.data(), M, 3 * d, n.t(RLHF_T_WQKV, l), d, dh.data());
-    layernorm_bwd(dh.data(), sv.x_in[l].data(), sv.mean1[l].data(), sv.rstd1[l].data(), n.t(RLHF_T_LN1_G, l), M,
-                  d, dres.data(), G(RLHF_T_LN1_G, l), G(RLHF_T_LN1_B, l));
+    norm_bwd(dh.data(), sv.x_in[l], sv.mean1[l], sv.rstd1[l], RLHF_T_LN1_G, l);
   }
   float* dE = G(RLHF_T_TOK_EMB);
   float* dPm = G(RLHF_T_POS_EMB);
@@ -372,7 +482,7 @@ void backward(const Net& n, const int32_t* tok, int B, int S, const Saved& sv, c
       const int id = tok[static_cast<size_t>(b) * S + i];
       for (int j = 0; j < d; ++j) {
         dE[static_cast<size_t>(id) * d + j] += gr[j];
-        dPm[static_cast<size_t>(i) * d + j] += gr[j];
+        if (dPm) dPm[static_cast<size_t>(i) * d + j] += gr[j];
       }
     }
 }
@@ -540,8 +650,8 @@ extern "C" int oracle_ppo_step(const rlhf_ppo_config* cfg_in, const int32_t* tok
       }
     }
     Vec dhr(static_cast<size_t>(Mr) * d);
-    matmul_nn(dz.data(), Mr, V, actor.t(RLHF_T_TOK_EMB), d, dhr.data());
-    matmul_tn_acc(dz.data(), Mr, V, hr.data(), d, grad.data() + rlhf_tensor_offset(&actor.a, RLHF_T_TOK_EMB, 0));
+    matmul_nn(dz.data(), Mr, V, actor.t(actor.head_id()), d, dhr.data());
+    matmul_tn_acc(dz.data(), Mr, V, hr.data(), d, grad.data() + rlhf_tensor_offset(&actor.a, actor.head_id(), 0));
     for (int r = 0; r < Mr; ++r) {
       const int b = r / R, t = P - 1 + r % R;
       std::memcpy(dhf.data() + (static_cast<size_t>(b) * S + t) * d, dhr.data() + static_cast<size_t>(r) * d,

@@ -47,12 +47,18 @@ ARCHS = {
     "opt-125m": dict(vocab=50272, d_model=768, n_layers=12, n_heads=12, d_ff=3072),
     "opt-350m": dict(vocab=50272, d_model=1024, n_layers=24, n_heads=16, d_ff=4096),
     "opt-1.3b": dict(vocab=50272, d_model=2048, n_layers=24, n_heads=32, d_ff=8192),
+    # LLaMA family (family 1: RMSNorm, SwiGLU, rotary, no biases, untied head)
+    "llama-tiny": dict(family=1, vocab=512, d_model=128, n_layers=2, n_heads=2, d_ff=384),
+    "llama-tiny-hd128": dict(family=1, vocab=512, d_model=256, n_layers=2, n_heads=2, d_ff=704),
+    "llama-1b": dict(family=1, vocab=32000, d_model=2048, n_layers=16, n_heads=16, d_ff=5504),
+    "llama-7b": dict(family=1, vocab=32000, d_model=4096, n_layers=32, n_heads=32, d_ff=11008),
 }
 
 
 def make_arch(name: str, max_pos: int, scalar_head: int) -> Arch:
     a = ARCHS[name]
-    return Arch(0, a["vocab"], a["d_model"], a["n_layers"], a["n_heads"], a["d_ff"], max_pos, scalar_head)
+    return Arch(a.get("family", 0), a["vocab"], a["d_model"], a["n_layers"], a["n_heads"], a["d_ff"], max_pos,
+                scalar_head)
 
 
 def make_config(actor: str, critic: str, batch: int, prompt_len: int, gen_len: int, seed: int = 7,
@@ -68,9 +74,7 @@ def make_config(actor: str, critic: str, batch: int, prompt_len: int, gen_len: i
 def param_total(a: Arch) -> int:
     """rlhf_param_total() of include/rlhf_init.h (flat layout incl. 64-element alignment)."""
     al = lambda n: (n + 63) // 64 * 64
-    V, d, f = a.vocab, a.d_model, a.d_ff
-    layer = sum(al(n) for n in (d, d, 3 * d * d, 3 * d, d * d, d, d, d, f * d, f, d * f, d))
-    return al(V * d) + al(a.max_pos * d) + layer * a.n_layers + al(d) + al(d) + al(d if a.scalar_head else 0)
+    return tensor_offset(a, 17) + al(tensor_numel(a, 17))
 
 
 _lib = None
@@ -120,12 +124,21 @@ def check(status: int) -> None:
 
 # ---- flat parameter layout (include/rlhf_init.h) ------------------------------
 TENSOR_NAMES = ["tok", "pos", "ln1_g", "ln1_b", "wqkv", "bqkv", "wo", "bo", "ln2_g", "ln2_b", "w1", "b1", "w2",
-                "b2", "lnf_g", "lnf_b", "vhead"]
+                "b2", "lnf_g", "lnf_b", "vhead", "lm_head"]
 LAYER_FIRST, LAYER_LAST = 2, 13
 
 
 def tensor_numel(a: Arch, t: int) -> int:
     V, d, f = a.vocab, a.d_model, a.d_ff
+    if a.family == 1:
+        if t in (1, 3, 9, 15, 5, 7, 11, 13):  # pos, LN betas, biases
+            return 0
+        if t == 10:
+            return 2 * f * d
+        if t == 17:
+            return 0 if a.scalar_head else V * d
+    if t == 17:
+        return 0
     return {0: V * d, 1: a.max_pos * d, 4: 3 * d * d, 5: 3 * d, 6: d * d, 10: f * d, 11: f, 12: d * f,
             16: d if a.scalar_head else 0}.get(t, d)
 
@@ -151,10 +164,12 @@ def named_slices(a: Arch):
     for l in range(a.n_layers):
         for t in range(LAYER_FIRST, LAYER_LAST + 1):
             out.append((f"l{l}.{TENSOR_NAMES[t]}", tensor_offset(a, t, l), tensor_numel(a, t)))
-    out += [("lnf_g", tensor_offset(a, 14), a.d_model), ("lnf_b", tensor_offset(a, 15), a.d_model)]
+    out += [("lnf_g", tensor_offset(a, 14), a.d_model), ("lnf_b", tensor_offset(a, 15), tensor_numel(a, 15))]
     if a.scalar_head:
         out.append(("vhead", tensor_offset(a, 16), a.d_model))
-    return out
+    if tensor_numel(a, 17):
+        out.append(("lm_head", tensor_offset(a, 17), tensor_numel(a, 17)))
+    return [s for s in out if s[2] > 0]
 
 
 def prompt_tokens(seed: int, batch: int, prompt_len: int, vocab: int, sample_offset: int = 0):

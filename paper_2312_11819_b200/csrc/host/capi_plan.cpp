@@ -71,8 +71,7 @@ extern "C" void rlhf_ppo_config_default(rlhf_ppo_config* c, const rlhf_arch* act
 extern "C" int rlhf_arch_by_name(const char* name, int max_pos, int scalar_head, rlhf_arch* out) {
   try {
     const ArchSpec a = arch_by_name(name);
-    if (a.family != ArchFamily::OPT) throw ConfigError("only the OPT family is executable in this build");
-    out->family = 0;
+    out->family = a.family == ArchFamily::OPT ? 0 : 1;
     out->vocab = a.vocab;
     out->d_model = a.d_model;
     out->n_layers = a.n_layers;

@@ -62,7 +62,8 @@ void validate(const rlhf_ppo_config& c) {
   if (c.batch < 1 || c.prompt_len < 1 || c.gen_len < 1) throw ConfigError("batch, prompt_len, gen_len must be >= 1");
   const int S = c.prompt_len + c.gen_len;
   for (const rlhf_arch* a : {&c.actor, &c.critic}) {
-    if (a->family != 0) throw ConfigError("only the OPT family is executable in this build");
+    if (a->family != 0 && a->family != 1) throw ConfigError("family must be 0 (OPT) or 1 (LLaMA)");
+    if (a->d_model > 4096) throw ConfigError("d_model above 4096 is not supported");
     if (S > a->max_pos) throw ConfigError("prompt_len + gen_len exceeds max_pos");
     if (a->d_model % a->n_heads) throw ConfigError("d_model must divide by n_heads");
     const int hd = a->d_model / a->n_heads;
@@ -184,7 +185,9 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
     dec_h_.alloc(static_cast<size_t>(gen_B_) * ad * 2);
     dec_qkv_.alloc(static_cast<size_t>(gen_B_) * 3 * ad * 2);
     dec_o_.alloc(static_cast<size_t>(gen_B_) * ad * 2);
-    dec_f_.alloc(static_cast<size_t>(gen_B_) * cfg_.actor.d_ff * 2);
+    const bool glu = cfg_.actor.family == 1;  // SwiGLU: gate|up rows, then the gated product
+    dec_f_.alloc(static_cast<size_t>(gen_B_) * cfg_.actor.d_ff * (glu ? 2 : 1) * 2);
+    dec_act_.alloc(glu ? static_cast<size_t>(gen_B_) * cfg_.actor.d_ff * 2 : 16);
     dec_hf_.alloc(static_cast<size_t>(gen_B_) * ad * 2);
     dec_logits_.alloc(static_cast<size_t>(gen_B_) * cfg_.actor.vocab * 4);
     dec_top2_.alloc(static_cast<size_t>((cfg_.actor.vocab + 127) / 128) * gen_B_ * 16);
@@ -259,14 +262,14 @@ void Engine::train_actor(Decoder& m, int B, ncclComm_t comm) {
   rlhf_gemm_params p{};
   p.M = BR; p.N = d; p.K = V; p.batch = 1; p.batch_h = 1;
   p.A = arp_->dz; p.lda = V;
-  p.B = m.T(RLHF_T_TOK_EMB); p.b_mn_major = 1; p.ldb = d;
+  p.B = m.T(m.head_id()); p.b_mn_major = 1; p.ldb = d;
   p.C = arp_->dhf_resp; p.c_f32 = 1; p.c_rs = d; p.c_cs = 1; p.alpha = 1.0f;
   gemm(p);
   rlhf_gemm_params q{};
   q.M = V; q.N = d; q.K = BR; q.batch = 1; q.batch_h = 1;
   q.A = arp_->dz; q.a_mn_major = 1; q.lda = V;
   q.B = arp_->hf_resp; q.b_mn_major = 1; q.ldb = d;
-  q.C = m.G(RLHF_T_TOK_EMB); q.c_f32 = 1; q.c_rs = d; q.c_cs = 1; q.alpha = 1.0f; q.accumulate = 1;
+  q.C = m.G(m.head_id()); q.c_f32 = 1; q.c_rs = d; q.c_cs = 1; q.alpha = 1.0f; q.accumulate = 1;
   gemm(q);
   cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
   K(rlhf_scatter_rows_f32(arp_->dhf_resp, arp_->dhf, B, S_, R_, P_ - 1, d, stream_), 1);
@@ -314,7 +317,8 @@ void Engine::build_arena(Arena& A, bool trains, bool critic_only) {
   for (const rlhf_arch* a : {&cfg_.actor, &cfg_.critic}) {
     if (critic_only && a == &cfg_.actor) continue;
     A.d = std::max(A.d, a->d_model);
-    A.ff = std::max(A.ff, a->d_ff);
+    A.ff = std::max(A.ff, a->d_ff * (a->family == 1 ? 2 : 1));
+    A.ffa = std::max(A.ffa, a->family == 1 ? a->d_ff : 0);
     A.H = std::max(A.H, a->n_heads);
     A.V = std::max(A.V, critic_only ? 1 : a->vocab);  // scalar heads only: no logits
     A.L = std::max(A.L, a->n_layers);
@@ -338,6 +342,7 @@ void Engine::build_arena(Arena& A, bool trains, bool critic_only) {
   A.h2 = static_cast<uint16_t*>(mk(Ls * T * d * 2));
   A.f = static_cast<uint16_t*>(mk(Ls * T * A.ff * 2));
   A.hf = static_cast<uint16_t*>(mk(T * d * 2));
+  A.act = static_cast<uint16_t*>(mk(A.ffa ? T * A.ffa * 2 : 16));
   A.scores = static_cast<float*>(mk(A.Z * SS * 4));
   A.dS = static_cast<uint16_t*>(mk(trains ? A.Z * SS * 2 : 16));
   A.hf_resp = static_cast<uint16_t*>(mk(BR * d * 2));

@@ -35,7 +35,7 @@ struct DevBuf {
   T* as() const { return static_cast<T*>(p); }
 };
 
-// One decoder (OPT family) resident on this device.
+// One decoder (OPT or LLaMA family) resident on this device.
 struct Decoder {
   rlhf_arch a{};
   uint64_t seed = 0;
@@ -44,13 +44,23 @@ struct Decoder {
   DevBuf w;       // bf16 flat
   DevBuf master, m, v, grad;  // fp32 flat (trainable only)
   int adam_step = 0;
-  const uint16_t* T(int t, int l = 0) const { return w.as<uint16_t>() + rlhf_tensor_offset(&a, t, l); }
-  float* G(int t, int l = 0) const { return grad.as<float>() + rlhf_tensor_offset(&a, t, l); }
+  DevBuf rope;    // LLaMA: float2 (cos, sin) [max_pos][hd/2] (rlhf_rope_cos_sin)
+  bool llama() const { return a.family == 1; }
+  // tensors absent from the family's layout (size 0) are NULL
+  const uint16_t* T(int t, int l = 0) const {
+    return rlhf_tensor_numel(&a, t) ? w.as<uint16_t>() + rlhf_tensor_offset(&a, t, l) : nullptr;
+  }
+  float* G(int t, int l = 0) const {
+    return rlhf_tensor_numel(&a, t) ? grad.as<float>() + rlhf_tensor_offset(&a, t, l) : nullptr;
+  }
+  int head_id() const { return llama() ? RLHF_T_LM_HEAD : RLHF_T_TOK_EMB; }  // LM head (tied for OPT)
 };
 
 // Activation arena shared by every model on the rank (they run one at a time).
 struct Arena {
-  int B = 0, S = 0, R = 0, d = 0, ff = 0, H = 0, V = 0, L = 0;  // capacities
+  int B = 0, S = 0, R = 0, d = 0, ff = 0, H = 0, V = 0, L = 0;  // capacities (ff: FFN-up width, 2 d_ff for SwiGLU)
+  int ffa = 0;                                                     // SwiGLU output width (0: OPT only)
+  uint16_t* act = nullptr;                                         // SwiGLU output / its gradient [T, ffa]
   int64_t T = 0, Z = 0;
   std::vector<DevBuf*> owned;
   float *xres = nullptr, *mean = nullptr, *rstd = nullptr;  // [(2L+1)][T*d], [(2L+1)][T]
@@ -95,6 +105,8 @@ class Engine {
   void attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd, bool keep_p);
   void attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_t* dov, uint16_t* dqkv, int B, int T, int H, int hd);
   void backward(Decoder& m, const int32_t* tokens, int B, int S);
+  void norm(const Decoder& m, const float* x, int g, int l, uint16_t* y, float* mean, float* rstd, int rows);
+  void norm_bwd(Decoder& m, const float* dy, const float* x, const float* mean, const float* rstd, int g, int l, int rows);
   void lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits);
   void generate(const Decoder& m, int B, bool teacher_forced);
   void decode_step(const Decoder& m, int B);
@@ -151,7 +163,7 @@ class Engine {
       score2_;
   DevBuf loop_ws_;  // persistent decode loop workspace
   DevBuf dec_top2_;  // LM-head per-tile top-2 partials [V/128][B] x float4
-  DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_hf_, dec_logits_, argmax_ws_;
+  DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_act_, dec_hf_, dec_logits_, argmax_ws_;
   cudaGraphExec_t decode_graph_ = nullptr;
   int graph_launches_ = 0;
   bool graph_for_pred_ = false;

@@ -166,6 +166,34 @@ void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool tr
     m.v.alloc(f.size() * 4);
     m.grad.alloc(f.size() * 4);
   }
+  if (m.llama()) {
+    const int hd = a.d_model / a.n_heads, half = hd / 2;
+    std::vector<float> tab(static_cast<size_t>(a.max_pos) * half * 2);
+    for (int p = 0; p < a.max_pos; ++p)
+      for (int i = 0; i < half; ++i)
+        rlhf_rope_cos_sin(p, i, hd, &tab[(static_cast<size_t>(p) * half + i) * 2], &tab[(static_cast<size_t>(p) * half + i) * 2 + 1]);
+    m.rope.alloc(tab.size() * 4);
+    if (cudaMemcpy(m.rope.p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      throw DeviceError("rotary table upload failed");
+  }
+}
+
+// Pre-norm of the residual stream: LayerNorm (OPT) or RMSNorm (LLaMA; tensor `g`'s
+// beta is absent).  mean is only written for LayerNorm.
+void Engine::norm(const Decoder& m, const float* x, int g, int l, uint16_t* y, float* mean, float* rstd, int rows) {
+  const int d = m.a.d_model;
+  if (m.llama()) K(rlhf_rmsnorm(x, m.T(g, l), y, rstd, rows, d, stream_), 1);
+  else K(rlhf_layernorm(x, m.T(g, l), m.T(g + 1, l), y, mean, rstd, rows, d, stream_), 1);
+}
+
+void Engine::norm_bwd(Decoder& m, const float* dy, const float* x, const float* mean, const float* rstd, int g, int l,
+                      int rows) {
+  const int d = m.a.d_model;
+  if (m.llama())
+    K(rlhf_rmsnorm_bwd(dy, x, rstd, m.T(g, l), arp_->dres, m.G(g, l), rows, d, arp_->ws, arp_->ws_floats, stream_), 2);
+  else
+    K(rlhf_layernorm_bwd(dy, x, mean, rstd, m.T(g, l), arp_->dres, m.G(g, l), m.G(g + 1, l), rows, d, arp_->ws,
+                         arp_->ws_floats, stream_), 2);
 }
 
 // Teacher-forced forward over positions [0, T) of B sequences (row r = b*T + i).
@@ -192,17 +220,26 @@ void Engine::forward(const Decoder& m, const int32_t* tokens, int B, int tok_str
     float* xin = X(2 * l);
     float* xmid = X(2 * l + 1);
     float* xout = X(2 * l + 2);
-    K(rlhf_layernorm(xin, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h1, MEAN(2 * l), RSTD(2 * l), rows, d, stream_), 1);
+    norm(m, xin, RLHF_T_LN1_G, l, h1, MEAN(2 * l), RSTD(2 * l), rows);
     linear(h1, rows, d, m.T(RLHF_T_WQKV, l), 3 * d, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr);
-    if (kv) K(rlhf_kv_store(qkv, B, T, 0, nullptr, H, hd, kv->Smax, kv->Kc(l), kv->Vc(l), stream_), 1);
+    if (m.llama())  // rotary q, k in place (+ the K/V-cache store of the rotated k)
+      K(rlhf_rope_qkv(qkv, B, T, 0, nullptr, H, hd, m.rope.as<float>(), 0, kv ? kv->Kc(l) : nullptr,
+                      kv ? kv->Vc(l) : nullptr, kv ? kv->Smax : 0, stream_), 1);
+    else if (kv)
+      K(rlhf_kv_store(qkv, B, T, 0, nullptr, H, hd, kv->Smax, kv->Kc(l), kv->Vc(l), stream_), 1);
     attention_fwd(qkv, P, o, B, T, H, hd, save);
     linear(o, rows, d, m.T(RLHF_T_WO, l), d, m.T(RLHF_T_BO, l), xmid, true, false, xin);
-    K(rlhf_layernorm(xmid, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h2, MEAN(2 * l + 1), RSTD(2 * l + 1), rows, d,
-                     stream_), 1);
-    linear(h2, rows, d, m.T(RLHF_T_W1, l), ff, m.T(RLHF_T_B1, l), f, false, true, nullptr);
-    linear(f, rows, ff, m.T(RLHF_T_W2, l), d, m.T(RLHF_T_B2, l), xout, true, false, xmid);
+    norm(m, xmid, RLHF_T_LN2_G, l, h2, MEAN(2 * l + 1), RSTD(2 * l + 1), rows);
+    if (m.llama()) {  // f = [gate | up] (kept for backward), act = silu(gate) * up
+      linear(h2, rows, d, m.T(RLHF_T_W1, l), 2 * ff, nullptr, f, false, false, nullptr);
+      K(rlhf_swiglu(f, arp_->act, rows, ff, stream_), 1);
+      linear(arp_->act, rows, ff, m.T(RLHF_T_W2, l), d, nullptr, xout, true, false, xmid);
+    } else {
+      linear(h2, rows, d, m.T(RLHF_T_W1, l), ff, m.T(RLHF_T_B1, l), f, false, true, nullptr);
+      linear(f, rows, ff, m.T(RLHF_T_W2, l), d, m.T(RLHF_T_B2, l), xout, true, false, xmid);
+    }
   }
-  K(rlhf_layernorm(X(2 * L), m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), arp_->hf, MEAN(2 * L), RSTD(2 * L), rows, d, stream_), 1);
+  norm(m, X(2 * L), RLHF_T_LNF_G, 0, arp_->hf, MEAN(2 * L), RSTD(2 * L), rows);
 }
 
 // S = softmax(Q K^T / sqrt(hd)) (causal), O = P V — batched over (b, h) straight
@@ -285,8 +322,10 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
   auto MEAN = [&](int k) { return arp_->mean + static_cast<int64_t>(k) * arp_->T; };
   auto RSTD = [&](int k) { return arp_->rstd + static_cast<int64_t>(k) * arp_->T; };
   cudaMemsetAsync(arp_->dres, 0, static_cast<size_t>(rows) * d * 4, stream_);
-  K(rlhf_layernorm_bwd(arp_->dhf, X(2 * L), MEAN(2 * L), RSTD(2 * L), m.T(RLHF_T_LNF_G), arp_->dres, m.G(RLHF_T_LNF_G),
-                       m.G(RLHF_T_LNF_B), rows, d, arp_->ws, arp_->ws_floats, stream_), 2);
+  norm_bwd(m, arp_->dhf, X(2 * L), MEAN(2 * L), RSTD(2 * L), RLHF_T_LNF_G, 0, rows);
+  auto colsum = [&](const uint16_t* Gm, int N, float* db) {  // bias gradient (absent in LLaMA)
+    if (db) K(rlhf_colsum_bf16(Gm, rows, N, db, arp_->ws, stream_), 2);
+  };
   // dW[N_out, K_in] += dY[T, N_out]^T X[T, K_in]
   auto wgrad = [&](const uint16_t* dY, int N_out, const uint16_t* Xin, int K_in, float* dW) {
     rlhf_gemm_params p{};
@@ -327,25 +366,36 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
     const uint16_t* f = arp_->f + l * Tn * arp_->ff;
     // FFN: x_out = x_mid + relu(h2 W1^T + b1) W2^T + b2
     K(rlhf_round_bf16(arp_->dres, arp_->g, static_cast<int64_t>(rows) * d, stream_), 1);
-    K(rlhf_colsum_bf16(arp_->g, rows, d, m.G(RLHF_T_B2, l), arp_->ws, stream_), 2);
-    wgrad(arp_->g, d, f, ff, m.G(RLHF_T_W2, l));
-    dgrad(arp_->g, d, m.T(RLHF_T_W2, l), ff, arp_->dpre, false, f);
-    K(rlhf_colsum_bf16(arp_->dpre, rows, ff, m.G(RLHF_T_B1, l), arp_->ws, stream_), 2);
-    wgrad(arp_->dpre, ff, h2, d, m.G(RLHF_T_W1, l));
-    dgrad(arp_->dpre, ff, m.T(RLHF_T_W1, l), d, arp_->dh, true, nullptr);
-    K(rlhf_layernorm_bwd(arp_->dh, X(2 * l + 1), MEAN(2 * l + 1), RSTD(2 * l + 1), m.T(RLHF_T_LN2_G, l), arp_->dres,
-                         m.G(RLHF_T_LN2_G, l), m.G(RLHF_T_LN2_B, l), rows, d, arp_->ws, arp_->ws_floats, stream_), 2);
+    colsum(arp_->g, d, m.G(RLHF_T_B2, l));
+    if (m.llama()) {
+      // SwiGLU: act recomputed from the saved [gate | up] (not kept per layer), then
+      // dact (bf16, into the same buffer) -> [dgate | dup]
+      K(rlhf_swiglu(f, arp_->act, rows, ff, stream_), 1);
+      wgrad(arp_->g, d, arp_->act, ff, m.G(RLHF_T_W2, l));
+      dgrad(arp_->g, d, m.T(RLHF_T_W2, l), ff, arp_->act, false, nullptr);
+      K(rlhf_swiglu_bwd(f, arp_->act, arp_->dpre, rows, ff, stream_), 1);
+      wgrad(arp_->dpre, 2 * ff, h2, d, m.G(RLHF_T_W1, l));
+      dgrad(arp_->dpre, 2 * ff, m.T(RLHF_T_W1, l), d, arp_->dh, true, nullptr);
+    } else {
+      wgrad(arp_->g, d, f, ff, m.G(RLHF_T_W2, l));
+      dgrad(arp_->g, d, m.T(RLHF_T_W2, l), ff, arp_->dpre, false, f);
+      colsum(arp_->dpre, ff, m.G(RLHF_T_B1, l));
+      wgrad(arp_->dpre, ff, h2, d, m.G(RLHF_T_W1, l));
+      dgrad(arp_->dpre, ff, m.T(RLHF_T_W1, l), d, arp_->dh, true, nullptr);
+    }
+    norm_bwd(m, arp_->dh, X(2 * l + 1), MEAN(2 * l + 1), RSTD(2 * l + 1), RLHF_T_LN2_G, l, rows);
     // attention block: x_mid = x_in + attn(h1) Wo^T + bo
     K(rlhf_round_bf16(arp_->dres, arp_->g, static_cast<int64_t>(rows) * d, stream_), 1);
-    K(rlhf_colsum_bf16(arp_->g, rows, d, m.G(RLHF_T_BO, l), arp_->ws, stream_), 2);
+    colsum(arp_->g, d, m.G(RLHF_T_BO, l));
     wgrad(arp_->g, d, o, d, m.G(RLHF_T_WO, l));
     dgrad(arp_->g, d, m.T(RLHF_T_WO, l), d, arp_->dov, false, nullptr);
     attention_bwd(qkv, P, arp_->dov, arp_->dqkv, B, S, H, hd);
-    K(rlhf_colsum_bf16(arp_->dqkv, rows, 3 * d, m.G(RLHF_T_BQKV, l), arp_->ws, stream_), 2);
+    if (m.llama())  // dq, dk through the rotation's transpose (the saved q, k are rotated)
+      K(rlhf_rope_qkv(arp_->dqkv, B, S, 0, nullptr, H, hd, m.rope.as<float>(), 1, nullptr, nullptr, 0, stream_), 1);
+    colsum(arp_->dqkv, 3 * d, m.G(RLHF_T_BQKV, l));
     wgrad(arp_->dqkv, 3 * d, h1, d, m.G(RLHF_T_WQKV, l));
     dgrad(arp_->dqkv, 3 * d, m.T(RLHF_T_WQKV, l), d, arp_->dh, true, nullptr);
-    K(rlhf_layernorm_bwd(arp_->dh, X(2 * l), MEAN(2 * l), RSTD(2 * l), m.T(RLHF_T_LN1_G, l), arp_->dres, m.G(RLHF_T_LN1_G, l),
-                         m.G(RLHF_T_LN1_B, l), rows, d, arp_->ws, arp_->ws_floats, stream_), 2);
+    norm_bwd(m, arp_->dh, X(2 * l), MEAN(2 * l), RSTD(2 * l), RLHF_T_LN1_G, l, rows);
   }
   K(rlhf_embed_bwd(tokens, S, B, S, arp_->dres, d, m.G(RLHF_T_TOK_EMB), m.G(RLHF_T_POS_EMB), stream_), 1);
 }
@@ -361,7 +411,7 @@ void Engine::lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* 
     rlhf_gemm_params p{};
     p.M = B * R_; p.N = V; p.K = d; p.batch = 1; p.batch_h = 1;
     p.A = arp_->hf_resp; p.lda = d;
-    p.B = m.T(RLHF_T_TOK_EMB); p.ldb = d;
+    p.B = m.T(m.head_id()); p.ldb = d;
     p.C = arp_->logits; p.c_f32 = 1; p.c_rs = V; p.c_cs = 1;
     p.alpha = 1.0f;
     p.lse_part = arp_->logits;  // (max, sum) partials: rows x tiles x 2 float2, far below the logits' size
@@ -375,7 +425,7 @@ void Engine::lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* 
     }
     if (st != 2) kcheck(st, "rlhf_gemm (LM head, log-sum-exp epilogue)");
   }
-  linear(arp_->hf_resp, B * R_, d, m.T(RLHF_T_TOK_EMB), V, nullptr, arp_->logits, true, false, nullptr);
+  linear(arp_->hf_resp, B * R_, d, m.T(m.head_id()), V, nullptr, arp_->logits, true, false, nullptr);
   K(rlhf_logprob(arp_->logits, B * R_, V, tokens, S_, P_, R_, logp, arp_->lse, stream_), 1);
 }
 
@@ -394,6 +444,26 @@ void Engine::decode_step(const Decoder& m, int B) {
   // RLHF_DECODE_SKIP (debug timing only, results become wrong): bit 0 LN, 1 attention,
   // 2 qkv GEMM, 3 o-proj, 4 FFN GEMMs, 5 LM head + argmax
   static const int skip = [] { const char* e = getenv("RLHF_DECODE_SKIP"); return e ? atoi(e) : 0; }();
+  if (m.llama()) {
+    // LLaMA: RMSNorm, [QKV GEMM], rotary q/k + KV-cache store, attention, [O-proj + residual],
+    // RMSNorm, [gate|up GEMM], SwiGLU, [down + residual]; final RMSNorm, untied head
+    uint16_t* act = dec_act_.as<uint16_t>();
+    K(rlhf_embed_rmsnorm(tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), d, x, m.T(RLHF_T_LN1_G, 0), h, stream_), 1);
+    for (int l = 0; l < a.n_layers; ++l) {
+      if (l > 0) K(rlhf_rmsnorm(x, m.T(RLHF_T_LN1_G, l), h, nullptr, B, d, stream_), 1);
+      linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, nullptr, qkv, false, false, nullptr);
+      K(rlhf_rope_qkv(qkv, B, 1, 0, pos, H, hd, m.rope.as<float>(), 0, kv_.Kc(l), kv_.Vc(l), kv_.Smax, stream_), 1);
+      K(rlhf_attn_decode(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o, stream_), 1);
+      linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, nullptr, x, true, false, x);
+      K(rlhf_rmsnorm(x, m.T(RLHF_T_LN2_G, l), h, nullptr, B, d, stream_), 1);
+      linear_decode(m.T(RLHF_T_W1, l), 2 * ff, d, h, B, nullptr, f, false, false, nullptr);
+      K(rlhf_swiglu(f, act, B, ff, stream_), 1);
+      linear_decode(m.T(RLHF_T_W2, l), d, ff, act, B, nullptr, x, true, false, x);
+    }
+    K(rlhf_rmsnorm(x, m.T(RLHF_T_LNF_G), dec_hf_.as<uint16_t>(), nullptr, B, d, stream_), 1);
+    lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, graph_for_pred_ ? pred_.as<int32_t>() : tokens_.as<int32_t>());
+    return;
+  }
   K(rlhf_embed_ln(tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x, m.T(RLHF_T_LN1_G, 0),
                   m.T(RLHF_T_LN1_B, 0), h, stream_),
     1);
@@ -430,7 +500,7 @@ void Engine::lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t
   const int d = m.a.d_model, V = m.a.vocab;
   rlhf_gemm_params q{};
   q.M = V; q.N = B; q.K = d; q.batch = 1; q.batch_h = 1;
-  q.A = m.T(RLHF_T_TOK_EMB); q.lda = d;
+  q.A = m.T(m.head_id()); q.lda = d;
   q.B = hf; q.ldb = d;
   q.C = dec_logits_.p; q.c_f32 = 1; q.c_rs = 1; q.c_cs = V;
   q.alpha = 1.0f;
@@ -454,7 +524,7 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);  // also advances *pos
   cudaEventRecord(ev_[1], stream_);  // prefill done
   if (R_ <= 1) return;
-  if (opt_.use_cuda_graph == 3) {
+  if (opt_.use_cuda_graph == 3 && !m.llama()) {  // the persistent loop implements the OPT family
     // persistent decode loop: all R-1 steps in one cooperative kernel (opt-in;
     // on one B200 at B = 32 it is not yet faster than the PDL graph)
     rlhf_decode_loop_params lp{};

@@ -1082,7 +1082,7 @@ extern "C" size_t rlhf_decode_loop_workspace_bytes(const rlhf_decode_loop_params
 
 extern "C" int rlhf_decode_loop(const rlhf_decode_loop_params* p, rlhf_stream_t stream) {
   dl::Plan pl;
-  if (!p || dl::plan(p, &pl)) return 2;
+  if (!p || !p->arch || p->arch->family != 0 || dl::plan(p, &pl)) return 2;  // OPT family only
   if (p->steps < 1) return 0;
   if (!p->workspace || p->workspace_bytes < pl.total) return 2;
   const rlhf_arch& A = *p->arch;

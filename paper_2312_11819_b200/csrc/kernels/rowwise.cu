@@ -35,7 +35,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, int64_t tok_str
   const int p = (p0_dev ? *p0_dev : p0) + i;
   const int id = tokens[b * tok_stride + p];
   const uint2 e = *reinterpret_cast<const uint2*>(E + static_cast<int64_t>(id) * d + c);
-  const uint2 q = *reinterpret_cast<const uint2*>(Pm + static_cast<int64_t>(p) * d + c);
+  const uint2 q = Pm ? *reinterpret_cast<const uint2*>(Pm + static_cast<int64_t>(p) * d + c) : make_uint2(0u, 0u);
   float4 o;
   o.x = bf2f(e.x & 0xFFFFu) + bf2f(q.x & 0xFFFFu);
   o.y = bf2f(e.x >> 16) + bf2f(q.x >> 16);
@@ -54,13 +54,13 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tokens, int64_t tok
   const int id = tokens[b * tok_stride + i];
   const float g = dx[idx];
   atomicAdd(dE + static_cast<int64_t>(id) * d + c, g);
-  atomicAdd(dP + static_cast<int64_t>(i) * d + c, g);
+  if (dP) atomicAdd(dP + static_cast<int64_t>(i) * d + c, g);
 }
 
 // Decode step entry: x[b] = tok_emb[tokens[b*stride + *pos]] + pos_emb[*pos] (fp32, the
 // residual stream) and y[b] = bf16(LN1_layer0(x[b])), one warp per sample.  Waits on its
 // predecessor before triggering dependents (the step chain relies on it, see attention.cu).
-template <int VPL>
+template <int VPL, bool RMS>
 __global__ void embed_ln_kernel(const int32_t* __restrict__ tokens, int64_t tok_stride, const int* __restrict__ pos_dev,
                                 const uint16_t* __restrict__ E, const uint16_t* __restrict__ Pm, int d,
                                 float* __restrict__ x, const uint16_t* __restrict__ g, const uint16_t* __restrict__ bta,
@@ -83,26 +83,28 @@ __global__ void embed_ln_kernel(const int32_t* __restrict__ tokens, int64_t tok_
   for (int k = 0; k < VPL; ++k) {
     const int c = lane + 32 * k;
     if (c < q) {
-      const uint2 ev = e2[c], pv = p2[c];
+      const uint2 ev = e2[c], pv = RMS ? make_uint2(0u, 0u) : p2[c];
       v[k] = make_float4(bf2f(ev.x & 0xFFFFu) + bf2f(pv.x & 0xFFFFu), bf2f(ev.x >> 16) + bf2f(pv.x >> 16),
                          bf2f(ev.y & 0xFFFFu) + bf2f(pv.y & 0xFFFFu), bf2f(ev.y >> 16) + bf2f(pv.y >> 16));
       xr[c] = v[k];
       gg[k] = g2[c];
-      bb[k] = b2[c];
+      bb[k] = RMS ? make_uint2(0u, 0u) : b2[c];
     }
   }
   float s = 0.f;
+  if (!RMS) {
 #pragma unroll
-  for (int k = 0; k < VPL; ++k)
-    if (lane + 32 * k < q) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
-  const float mu = warp_sum(s) / d;
+    for (int k = 0; k < VPL; ++k)
+      if (lane + 32 * k < q) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
+  const float mu = RMS ? 0.f : warp_sum(s) / d;  // RMSNorm: no centring
   float vs = 0.f;
 #pragma unroll
   for (int k = 0; k < VPL; ++k)
     if (lane + 32 * k < q)
       vs += (v[k].x - mu) * (v[k].x - mu) + (v[k].y - mu) * (v[k].y - mu) + (v[k].z - mu) * (v[k].z - mu) +
             (v[k].w - mu) * (v[k].w - mu);
-  const float rs = 1.0f / sqrtf(warp_sum(vs) / d + 1e-5f);
+  const float rs = 1.0f / sqrtf(warp_sum(vs) / d + (RMS ? 1e-6f : 1e-5f));
   uint2* yr = reinterpret_cast<uint2*>(y + static_cast<int64_t>(row) * d);
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
@@ -118,7 +120,7 @@ __global__ void embed_ln_kernel(const int32_t* __restrict__ tokens, int64_t tok_
 
 // One warp per row, row held in registers (d <= 4096): a single round trip to
 // memory for x, gamma and beta, then two register passes (mean, variance).
-template <int VPL>  // float4 vectors per lane
+template <int VPL, bool RMS>  // float4 vectors per lane; RMS: RMSNorm (no centring, no beta)
 __global__ void layernorm_kernel(const float* __restrict__ x, const uint16_t* __restrict__ g,
                                  const uint16_t* __restrict__ bta, uint16_t* __restrict__ y, float* __restrict__ mean,
                                  float* __restrict__ rstd, int M, int d) {
@@ -138,21 +140,23 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const uint16_t* __
     if (c < q) {
       v[k] = xr[c];
       gg[k] = g2[c];
-      bb[k] = b2[c];
+      bb[k] = RMS ? make_uint2(0u, 0u) : b2[c];
     }
   }
   float s = 0.f;
+  if (!RMS) {
 #pragma unroll
-  for (int k = 0; k < VPL; ++k)
-    if (lane + 32 * k < q) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
-  const float mu = warp_sum(s) / d;
+    for (int k = 0; k < VPL; ++k)
+      if (lane + 32 * k < q) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
+  const float mu = RMS ? 0.f : warp_sum(s) / d;  // RMSNorm: no centring
   float vs = 0.f;
 #pragma unroll
   for (int k = 0; k < VPL; ++k)
     if (lane + 32 * k < q)
       vs += (v[k].x - mu) * (v[k].x - mu) + (v[k].y - mu) * (v[k].y - mu) + (v[k].z - mu) * (v[k].z - mu) +
             (v[k].w - mu) * (v[k].w - mu);
-  const float rs = 1.0f / sqrtf(warp_sum(vs) / d + 1e-5f);
+  const float rs = 1.0f / sqrtf(warp_sum(vs) / d + (RMS ? 1e-6f : 1e-5f));
   uint2* yr = reinterpret_cast<uint2*>(y + static_cast<int64_t>(row) * d);
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
@@ -175,12 +179,13 @@ constexpr int kLnBwdRows = 64;  // rows per block (8 warps x 8 rows)
 // dx += rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)).  Each warp keeps its
 // rows' dgamma/dbeta column partials in registers (lane owns columns lane+32k),
 // the block reduces its 8 warps in smem in fixed order -> ws[blk][2][d].
-template <int VPL>  // float4 vectors per lane (d <= 128*VPL)
+template <int VPL, bool RMS>  // float4 vectors per lane (d <= 128*VPL); RMS: RMSNorm, dgamma only
 __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
                                      const float* __restrict__ mean, const float* __restrict__ rstd,
                                      const uint16_t* __restrict__ g, float* __restrict__ dx, float* __restrict__ ws,
                                      int M, int d) {
-  extern __shared__ float red[];  // [8 warps][2][d]
+  extern __shared__ float red[];  // [8 warps][NP][d]
+  constexpr int NP = RMS ? 1 : 2;  // column partials per warp: dgamma (, dbeta)
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int r0 = blockIdx.x * kLnBwdRows;
   const int q = d / 4;
@@ -202,7 +207,7 @@ __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* 
     const float4* dr = reinterpret_cast<const float4*>(dy + static_cast<int64_t>(row) * d);
     const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * d);
     float4* o = reinterpret_cast<float4*>(dx + static_cast<int64_t>(row) * d);
-    const float mu = mean[row], rs = rstd[row];
+    const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
     float4 dyv[VPL], xh[VPL], dxo[VPL];
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {  // every load of the row in flight at once
@@ -224,7 +229,7 @@ __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* 
       pg[k].z += dyv[k].z * xh[k].z; pg[k].w += dyv[k].w * xh[k].w;
       pb[k].x += dyv[k].x; pb[k].y += dyv[k].y; pb[k].z += dyv[k].z; pb[k].w += dyv[k].w;
     }
-    a = warp_sum(a) / d;
+    a = RMS ? 0.f : warp_sum(a) / d;
     cs = warp_sum(cs) / d;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
@@ -242,16 +247,16 @@ __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* 
   for (int k = 0; k < VPL; ++k) {
     const int c = lane + 32 * k;
     if (c < q) {
-      reinterpret_cast<float4*>(red + (warp * 2) * d)[c] = pg[k];
-      reinterpret_cast<float4*>(red + (warp * 2 + 1) * d)[c] = pb[k];
+      reinterpret_cast<float4*>(red + (warp * NP) * d)[c] = pg[k];
+      if (!RMS) reinterpret_cast<float4*>(red + (warp * NP + 1) * d)[c] = pb[k];
     }
   }
   __syncthreads();
-  float* wg = ws + static_cast<int64_t>(blockIdx.x) * 2 * d;
-  for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
+  float* wg = ws + static_cast<int64_t>(blockIdx.x) * NP * d;
+  for (int j = threadIdx.x; j < NP * d; j += blockDim.x) {
     const int which = j / d, col = j % d;
     float acc = 0.f;
-    for (int w = 0; w < 8; ++w) acc += red[(w * 2 + which) * d + col];  // fixed warp order
+    for (int w = 0; w < 8; ++w) acc += red[(w * NP + which) * d + col];  // fixed warp order
     wg[j] = acc;
   }
 }
@@ -399,10 +404,46 @@ extern "C" int rlhf_layernorm(const float* x, const void* g, const void* b, void
   const auto* gp = static_cast<const uint16_t*>(g);
   const auto* bp = static_cast<const uint16_t*>(b);
   auto* yp = static_cast<uint16_t*>(y);
-  if (d <= 1024) return launch_k(layernorm_kernel<8>, grid, blk, 0, S(s), x, gp, bp, yp, mean, rstd, M, d);
-  if (d <= 2048) return launch_k(layernorm_kernel<16>, grid, blk, 0, S(s), x, gp, bp, yp, mean, rstd, M, d);
-  if (d <= 4096) return launch_k(layernorm_kernel<32>, grid, blk, 0, S(s), x, gp, bp, yp, mean, rstd, M, d);
+  if (d <= 1024) return launch_k(layernorm_kernel<8, false>, grid, blk, 0, S(s), x, gp, bp, yp, mean, rstd, M, d);
+  if (d <= 2048) return launch_k(layernorm_kernel<16, false>, grid, blk, 0, S(s), x, gp, bp, yp, mean, rstd, M, d);
+  if (d <= 4096) return launch_k(layernorm_kernel<32, false>, grid, blk, 0, S(s), x, gp, bp, yp, mean, rstd, M, d);
   return 2;
+}
+
+extern "C" int rlhf_rmsnorm(const float* x, const void* g, void* y, float* rstd, int M, int d, rlhf_stream_t s) {
+  if (d % 4) return 2;
+  const dim3 grid((M + 7) / 8), blk(256);
+  const auto* gp = static_cast<const uint16_t*>(g);
+  auto* yp = static_cast<uint16_t*>(y);
+  const uint16_t* nb = nullptr;
+  float* nm = nullptr;
+  if (d <= 1024) return launch_k(layernorm_kernel<8, true>, grid, blk, 0, S(s), x, gp, nb, yp, nm, rstd, M, d);
+  if (d <= 2048) return launch_k(layernorm_kernel<16, true>, grid, blk, 0, S(s), x, gp, nb, yp, nm, rstd, M, d);
+  if (d <= 4096) return launch_k(layernorm_kernel<32, true>, grid, blk, 0, S(s), x, gp, nb, yp, nm, rstd, M, d);
+  return 2;
+}
+
+extern "C" int rlhf_rmsnorm_bwd(const float* dy, const float* x, const float* rstd, const void* g, float* dx, float* dg,
+                                int M, int d, float* ws, size_t ws_floats, rlhf_stream_t s) {
+  const int nblk = (M + kLnBwdRows - 1) / kLnBwdRows;
+  if (d % 4 || ws_floats < static_cast<size_t>(nblk) * d) return 2;
+  const size_t sm = static_cast<size_t>(8) * d * 4;
+  const auto* gp = static_cast<const uint16_t*>(g);
+  const float* nm = nullptr;
+  if (d <= 1024) {
+    cudaFuncSetAttribute(layernorm_bwd_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 1024 * 4);
+    layernorm_bwd_kernel<8, true><<<nblk, 256, sm, S(s)>>>(dy, x, nm, rstd, gp, dx, ws, M, d);
+  } else if (d <= 2048) {
+    cudaFuncSetAttribute(layernorm_bwd_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2048 * 4);
+    layernorm_bwd_kernel<16, true><<<nblk, 256, sm, S(s)>>>(dy, x, nm, rstd, gp, dx, ws, M, d);
+  } else if (d <= 4096) {
+    cudaFuncSetAttribute(layernorm_bwd_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096 * 4);
+    layernorm_bwd_kernel<32, true><<<nblk, 256, sm, S(s)>>>(dy, x, nm, rstd, gp, dx, ws, M, d);
+  } else {
+    return 2;
+  }
+  reduce_partials_kernel<<<(d + 63) / 64, 64, 0, S(s)>>>(ws, nblk, d, d, dg, dg, d);
+  return cuda_status();
 }
 
 extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd, const void* g,
@@ -413,11 +454,11 @@ extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* 
   const size_t sm = static_cast<size_t>(16) * d * 4;
   const auto* gp = static_cast<const uint16_t*>(g);
   if (d <= 1024) {
-    cudaFuncSetAttribute(layernorm_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024 * 4);
-    layernorm_bwd_kernel<8><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
+    cudaFuncSetAttribute(layernorm_bwd_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024 * 4);
+    layernorm_bwd_kernel<8, false><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
   } else if (d <= 2048) {
-    cudaFuncSetAttribute(layernorm_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4);
-    layernorm_bwd_kernel<16><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
+    cudaFuncSetAttribute(layernorm_bwd_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4);
+    layernorm_bwd_kernel<16, false><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
   } else {
     return 2;
   }
@@ -475,7 +516,20 @@ extern "C" int rlhf_embed_ln(const int32_t* tokens, int64_t tok_stride, int B, c
   const auto* g = static_cast<const uint16_t*>(ln_g);
   const auto* b = static_cast<const uint16_t*>(ln_b);
   auto* yp = static_cast<uint16_t*>(y);
-  if (d <= 1024) return launch_k(embed_ln_kernel<8>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
-  if (d <= 2048) return launch_k(embed_ln_kernel<16>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
-  return launch_k(embed_ln_kernel<32>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
+  if (d <= 1024) return launch_k(embed_ln_kernel<8, false>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
+  if (d <= 2048) return launch_k(embed_ln_kernel<16, false>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
+  return launch_k(embed_ln_kernel<32, false>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
+}
+
+extern "C" int rlhf_embed_rmsnorm(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev,
+                                  const void* tok_emb, int d, float* x, const void* g, void* y, rlhf_stream_t s) {
+  if (d % 4 || d > 4096 || !pos_dev) return 2;
+  const dim3 grid((B + 7) / 8), blk(256);
+  const auto* E = static_cast<const uint16_t*>(tok_emb);
+  const auto* gp = static_cast<const uint16_t*>(g);
+  const uint16_t* nil = nullptr;
+  auto* yp = static_cast<uint16_t*>(y);
+  if (d <= 1024) return launch_k(embed_ln_kernel<8, true>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, nil, d, x, gp, nil, yp, B);
+  if (d <= 2048) return launch_k(embed_ln_kernel<16, true>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, nil, d, x, gp, nil, yp, B);
+  return launch_k(embed_ln_kernel<32, true>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, nil, d, x, gp, nil, yp, B);
 }

@@ -10,7 +10,14 @@ straight-through in autograd, so gradients here are exact float64 gradients of
 the rounded forward -- the oracle (which also rounds gradients to bf16 at GEMM
 inputs) must agree within the tolerances in tests/test_oracle_golden.py.
 
-Numerics: DeepSpeed-Chat step 3.  Run:
+Numerics: DeepSpeed-Chat step 3.  Two fixtures:
+  c1_golden.npz        OPT-style tiny decoder (family 0)
+  c1_llama_golden.npz  LLaMA-style tiny decoder (family 1: RMSNorm, rotary, SwiGLU,
+                       untied head).  Its torch restatement is itself pinned against
+                       Hugging Face transformers' LlamaForCausalLM (float64, rounding
+                       off) before the fixture is written, and the HF logprobs of the
+                       golden tokens are stored (hf_logp) for a direct oracle-vs-HF test.
+Run:
     python tests/golden/make_golden.py
 """
 from __future__ import annotations
@@ -26,7 +33,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # ---- rlhf_init.h re-implemented in numpy -----------------------------------
 M64 = (1 << 64) - 1
 T_TOK, T_POS, T_LN1G, T_LN1B, T_WQKV, T_BQKV, T_WO, T_BO, T_LN2G, T_LN2B, T_W1, T_B1, T_W2, T_B2, \
-    T_LNFG, T_LNFB, T_VHEAD = range(17)
+    T_LNFG, T_LNFB, T_VHEAD, T_LMHEAD = range(18)
 LAYER_T = list(range(T_LN1G, T_B2 + 1))
 
 
@@ -66,6 +73,8 @@ def stream_of(seed, t, l):
 
 
 def init_dist(arch, t):
+    if t == T_LMHEAD:
+        return 0.0, 2.0 / np.sqrt(arch["d"])
     if t == T_TOK:
         return 0.0, 2.0 / np.sqrt(arch["d"])
     if t == T_POS:
@@ -83,11 +92,16 @@ def init_dist(arch, t):
 
 def shape_of(arch, t):
     V, d, f, mp = arch["V"], arch["d"], arch["ff"], arch["max_pos"]
-    return {T_TOK: (V, d), T_POS: (mp, d), T_WQKV: (3 * d, d), T_BQKV: (3 * d,), T_WO: (d, d),
+    if arch.get("family", 0) == 1 and t == T_W1:
+        return (2 * f, d)  # [gate | up]
+    return {T_LMHEAD: (V, d), T_TOK: (V, d), T_POS: (mp, d), T_WQKV: (3 * d, d), T_BQKV: (3 * d,), T_WO: (d, d),
             T_W1: (f, d), T_B1: (f,), T_W2: (d, f), T_VHEAD: (d,)}.get(t, (d,))
 
 
 def make_weights(arch, seed, scalar_head):
+    if arch.get("family", 0) == 1:
+        return make_weights_llama(arch, seed, scalar_head)
+
     def gen(t, l):
         shp = shape_of(arch, t)
         mean, std = init_dist(arch, t)
@@ -98,6 +112,22 @@ def make_weights(arch, seed, scalar_head):
         w["layers"].append({n: gen(t, l) for n, t in zip(names, LAYER_T)})
     if scalar_head:
         w["vhead"] = gen(T_VHEAD, 0)
+    return w
+
+
+def make_weights_llama(arch, seed, scalar_head):
+    def gen(t, l):
+        shp = shape_of(arch, t)
+        mean, std = init_dist(arch, t)
+        return torch.tensor(to_bf16(mean + std * normal(stream_of(seed, t, l), int(np.prod(shp)))).reshape(shp))
+    w = {"tok": gen(T_TOK, 0), "lnf_g": gen(T_LNFG, 0), "layers": []}
+    names = {"ln1_g": T_LN1G, "wqkv": T_WQKV, "wo": T_WO, "ln2_g": T_LN2G, "w1": T_W1, "w2": T_W2}
+    for l in range(arch["L"]):
+        w["layers"].append({n: gen(t, l) for n, t in names.items()})
+    if scalar_head:
+        w["vhead"] = gen(T_VHEAD, 0)
+    else:
+        w["lm_head"] = gen(T_LMHEAD, 0)
     return w
 
 
@@ -127,8 +157,84 @@ def layernorm(x, g, b):
     return (x - mu) / torch.sqrt(var + 1e-5) * g + b
 
 
+def rmsnorm(x, g):
+    return x / torch.sqrt((x * x).mean(-1, keepdim=True) + 1e-6) * g
+
+
+def rope_tables(S, hd):
+    """rlhf_rope_cos_sin: angle in float64, cos/sin rounded to float32."""
+    i = np.arange(hd // 2, dtype=np.float64)
+    ang = np.arange(S, dtype=np.float64)[:, None] * np.power(10000.0, -2.0 * i / hd)[None]
+    return (torch.tensor(np.cos(ang).astype(np.float32).astype(np.float64)),
+            torch.tensor(np.sin(ang).astype(np.float32).astype(np.float64)))
+
+
+def rope(x, c, s):
+    """x [B,H,S,hd]: pair (i, i + hd/2) rotated by position angle (HF LLaMA rotate_half)."""
+    half = x.shape[-1] // 2
+    x0, x1 = x[..., :half], x[..., half:]
+    return torch.cat([x0 * c - x1 * s, x1 * c + x0 * s], -1)
+
+
+def decoder_llama(w, tok, arch, r=None):
+    """LLaMA family: tok [B,S] -> final RMSNorm hidden [B,S,d]; r = rounding (rb, or identity)."""
+    r = r or rb
+    B, S = tok.shape
+    d, H, ff = arch["d"], arch["H"], arch["ff"]
+    hd = d // H
+    c, s = rope_tables(S, hd)
+    x = w["tok"][tok]
+    mask = torch.ones(S, S, dtype=torch.bool).tril()
+    for lw in w["layers"]:
+        h = r(rmsnorm(x, lw["ln1_g"]))
+        qkv = r(h @ lw["wqkv"].T)
+        q, k, v = qkv.split(d, -1)
+        q = r(rope(q.view(B, S, H, hd).transpose(1, 2), c, s))
+        k = r(rope(k.view(B, S, H, hd).transpose(1, 2), c, s))
+        v = v.view(B, S, H, hd).transpose(1, 2)
+        sc = (q @ k.transpose(-1, -2)) * (1.0 / np.sqrt(hd))
+        sc = sc.masked_fill(~mask, float("-inf"))
+        p = r(torch.softmax(sc, -1))
+        o = r((p @ v).transpose(1, 2).reshape(B, S, d))
+        x = x + o @ lw["wo"].T
+        h2 = r(rmsnorm(x, lw["ln2_g"]))
+        gu = r(h2 @ lw["w1"].T)
+        g, u = gu.split(ff, -1)
+        a = r(g * torch.sigmoid(g) * u)
+        x = x + a @ lw["w2"].T
+    return r(rmsnorm(x, w["lnf_g"]))
+
+
+def hf_llama(w, arch):
+    """The same weights in transformers' LlamaForCausalLM (float64)."""
+    from transformers import LlamaConfig, LlamaForCausalLM
+    d, ff = arch["d"], arch["ff"]
+    cfg = LlamaConfig(vocab_size=arch["V"], hidden_size=d, intermediate_size=ff, num_hidden_layers=arch["L"],
+                      num_attention_heads=arch["H"], num_key_value_heads=arch["H"], rms_norm_eps=1e-6,
+                      rope_theta=10000.0, max_position_embeddings=arch["max_pos"], tie_word_embeddings=False,
+                      attention_bias=False, mlp_bias=False)
+    m = LlamaForCausalLM(cfg).double().eval()
+    with torch.no_grad():
+        m.model.embed_tokens.weight.copy_(w["tok"])
+        for lw, L in zip(w["layers"], m.model.layers):
+            L.self_attn.q_proj.weight.copy_(lw["wqkv"][:d])
+            L.self_attn.k_proj.weight.copy_(lw["wqkv"][d:2 * d])
+            L.self_attn.v_proj.weight.copy_(lw["wqkv"][2 * d:])
+            L.self_attn.o_proj.weight.copy_(lw["wo"])
+            L.mlp.gate_proj.weight.copy_(lw["w1"][:ff])
+            L.mlp.up_proj.weight.copy_(lw["w1"][ff:])
+            L.mlp.down_proj.weight.copy_(lw["w2"])
+            L.input_layernorm.weight.copy_(lw["ln1_g"])
+            L.post_attention_layernorm.weight.copy_(lw["ln2_g"])
+        m.model.norm.weight.copy_(w["lnf_g"])
+        m.lm_head.weight.copy_(w["lm_head"])
+    return m
+
+
 def decoder(w, tok, arch):
     """tok [B,S] long -> final-LN hidden [B,S,d] (bf16-rounded)."""
+    if arch.get("family", 0) == 1:
+        return decoder_llama(w, tok, arch)
     B, S = tok.shape
     d, H = arch["d"], arch["H"]
     hd = d // H
@@ -153,17 +259,36 @@ def decoder(w, tok, arch):
 
 
 def params_of(w):
-    ps = [w["tok"], w["pos"]]
+    """Parameters in the flat layout order of rlhf_init.h (absent tensors skipped)."""
+    ps = [w["tok"]] + ([w["pos"]] if "pos" in w else [])
     for lw in w["layers"]:
         ps += list(lw.values())
-    ps += [w["lnf_g"], w["lnf_b"]]
+    ps += [w["lnf_g"]] + ([w["lnf_b"]] if "lnf_b" in w else [])
     if "vhead" in w:
         ps.append(w["vhead"])
+    if "lm_head" in w:
+        ps.append(w["lm_head"])
     return ps
 
 
+def param_names(w, arch):
+    names = ["tok"] + (["pos"] if "pos" in w else [])
+    names += [f"l{l}.{k}" for l in range(arch["L"]) for k in w["layers"][l]]
+    names += ["lnf_g"] + (["lnf_b"] if "lnf_b" in w else [])
+    names += (["vhead"] if "vhead" in w else []) + (["lm_head"] if "lm_head" in w else [])
+    return names
+
+
+def head_of(w):
+    return w["lm_head"] if "lm_head" in w else w["tok"]
+
+
 def main():
-    arch = dict(V=512, d=128, L=2, H=2, ff=512, max_pos=64)
+    run(dict(V=512, d=128, L=2, H=2, ff=512, max_pos=64), "c1_golden.npz")
+    run(dict(family=1, V=512, d=128, L=2, H=2, ff=384, max_pos=64), "c1_llama_golden.npz")
+
+
+def run(arch, fname):
     B, P, R = 4, 16, 16
     S = P + R
     seed, prompt_seed = 7, 1000
@@ -183,13 +308,13 @@ def main():
         for step in range(R):
             t = P - 1 + step
             hf = decoder(actor, tok[:, : t + 1], arch)
-            z = hf[:, t] @ actor["tok"].T
+            z = hf[:, t] @ head_of(actor).T
             top = torch.topk(z, 2, -1)
             tok[:, t + 1] = top.indices[:, 0]
             margins[:, step] = (top.values[:, 0] - top.values[:, 1]).numpy()
 
     def logprobs(w, hf):
-        z = hf[:, P - 1:S - 1] @ w["tok"].T
+        z = hf[:, P - 1:S - 1] @ head_of(w).T
         return torch.log_softmax(z, -1).gather(-1, tok[:, P:, None])[..., 0]
 
     with torch.no_grad():
@@ -225,16 +350,14 @@ def main():
 
     def grad_summary(w):
         out = {}
-        names = ["tok", "pos"] + [f"l{l}.{k}" for l in range(arch["L"]) for k in w["layers"][l]] + ["lnf_g", "lnf_b"]
-        if "vhead" in w:
-            names.append("vhead")
-        for name, p in zip(names, params_of(w)):
+        for name, p in zip(param_names(w, arch), params_of(w)):
             g = p.grad.detach().numpy().ravel()
             out[name] = (g[:256].astype(np.float32), float(np.linalg.norm(g)), float(g.sum()))
         return out
 
     fx = dict(
         config=np.array([B, P, R, seed, prompt_seed]), arch=np.array([arch[k] for k in ("V", "d", "L", "H", "ff", "max_pos")]),
+        family=np.array(arch.get("family", 0)),
         tokens=tok.numpy().astype(np.int32), margins=margins.astype(np.float32),
         logp_old=logp_old.numpy().astype(np.float32), logp_ref=logp_ref.numpy().astype(np.float32),
         values=values.numpy().astype(np.float32), score=score.numpy().astype(np.float32),
@@ -245,8 +368,22 @@ def main():
         for name, (head, norm, tot) in grad_summary(w).items():
             fx[f"{tag}_grad/{name}/head"] = head
             fx[f"{tag}_grad/{name}/stats"] = np.array([norm, tot])
-    np.savez_compressed(os.path.join(HERE, "c1_golden.npz"), **fx)
-    print("wrote", os.path.join(HERE, "c1_golden.npz"), "losses", fx["losses"], "min margin", margins.min())
+    if arch.get("family", 0) == 1:
+        # pin the restatement's semantics against transformers' LLaMA (rounding off), then
+        # store HF's own logprobs of the golden tokens for the oracle-vs-HF test
+        actor_d = {k: (v.detach() if torch.is_tensor(v) else [{n: t.detach() for n, t in lw.items()} for lw in v])
+                   for k, v in actor.items()}
+        m = hf_llama(actor_d, arch)
+        with torch.no_grad():
+            z_hf = m(tok).logits
+            z_me = decoder_llama(actor_d, tok, arch, r=lambda t: t) @ actor_d["lm_head"].T
+            err = (z_hf - z_me).abs().max().item()
+            assert err < 1e-4, f"LLaMA restatement differs from transformers by {err}"
+            hf_logp = torch.log_softmax(z_hf[:, P - 1:S - 1], -1).gather(-1, tok[:, P:, None])[..., 0]
+        fx["hf_logp"] = hf_logp.numpy().astype(np.float32)
+        fx["hf_max_abs_logit_diff"] = np.array(err)
+    np.savez_compressed(os.path.join(HERE, fname), **fx)
+    print("wrote", os.path.join(HERE, fname), "losses", fx["losses"], "min margin", margins.min())
 
 
 if __name__ == "__main__":

@@ -1,7 +1,8 @@
 """End-to-end parity of one PPO step: CUDA engine (through the C-ABI) vs the CPU oracle.
 
 Config c1 (BASELINE.json configs[0]): tiny decoder x4, batch 4, prompt 16 +
-response 16, Co-located on one GPU.  The oracle is run teacher-forced on the
+response 16, Co-located on one GPU — for the OPT family and for the LLaMA family
+(RMSNorm, rotary, SwiGLU, untied head; head_dim 64 and 128, the 7B's).  The oracle is run teacher-forced on the
 GPU's own generated sequences, so every downstream quantity is compared on
 identical inputs.  Tolerances:
   * greedy tokens: bit-exact wherever the oracle's top-2 margin > 1e-2;
@@ -21,10 +22,10 @@ from tests import oracle_lib
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def run():
+@pytest.fixture(scope="module", params=["tiny", "llama-tiny", "llama-tiny-hd128"])
+def run(request):
     from paper_2312_11819_b200.engine import Engine
-    cfg = make_config("tiny", "tiny", 4, 16, 16)
+    cfg = make_config(request.param, request.param, 4, 16, 16)
     eng = Engine(cfg)
     init_actor = eng.read("actor_params").copy()
     rep = eng.step()
@@ -39,7 +40,8 @@ def test_initial_weights_match_input_spec(run):
     from tests.golden import make_golden as mg
     cfg, _, _, _, _, init_actor = run
     a = cfg.actor
-    w = mg.make_weights(dict(V=a.vocab, d=a.d_model, L=a.n_layers, H=a.n_heads, ff=a.d_ff, max_pos=a.max_pos),
+    w = mg.make_weights(dict(family=a.family, V=a.vocab, d=a.d_model, L=a.n_layers, H=a.n_heads, ff=a.d_ff,
+                             max_pos=a.max_pos),
                         cfg.seed * 16, False)
     flat = init_actor.view(np.uint16)
     for (name, off, n), p in zip(named_slices(a), mg.params_of(w)):
@@ -94,8 +96,11 @@ def test_updated_weights(run, tag, lr):
 
 
 def test_teacher_forced_decode_matches_oracle_greedy(run):
-    cfg, eng, _, out, ora, _ = run
-    pred, margin = eng.greedy_check(out["tokens"])
+    from paper_2312_11819_b200.engine import Engine
+    cfg, _, _, out, ora, _ = run
+    # a fresh engine: the stepped one's Actor has taken its AdamW step, the oracle's
+    # greedy predictions are those of the initial weights
+    pred, margin = Engine(cfg).greedy_check(out["tokens"])
     m = ora["greedy_margin"] > 1e-2
     np.testing.assert_array_equal(pred[m], ora["greedy_pred"][m])
     np.testing.assert_allclose(margin, ora["greedy_margin"], atol=5e-2)

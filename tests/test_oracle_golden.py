@@ -14,18 +14,26 @@ import pytest
 from paper_2312_11819_b200.capi import make_config, named_slices
 from tests import oracle_lib
 
-GOLD = os.path.join(os.path.dirname(__file__), "golden", "c1_golden.npz")
+GOLD_DIR = os.path.join(os.path.dirname(__file__), "golden")
+# (fixture, architecture): the OPT-style c1 decoder and its LLaMA-style counterpart
+FIXTURES = {"opt": ("c1_golden.npz", "tiny"), "llama": ("c1_llama_golden.npz", "llama-tiny")}
+
+
+@pytest.fixture(scope="module", params=sorted(FIXTURES))
+def family(request):
+    return request.param
 
 
 @pytest.fixture(scope="module")
-def gold():
-    return np.load(GOLD)
+def gold(family):
+    return np.load(os.path.join(GOLD_DIR, FIXTURES[family][0]))
 
 
 @pytest.fixture(scope="module")
-def cfg(gold):
+def cfg(gold, family):
     B, P, R, seed, pseed = (int(x) for x in gold["config"])
-    return make_config("tiny", "tiny", B, P, R, seed=seed, prompt_seed=pseed)
+    name = FIXTURES[family][1]
+    return make_config(name, name, B, P, R, seed=seed, prompt_seed=pseed)
 
 
 @pytest.fixture(scope="module")
@@ -37,6 +45,17 @@ def test_config_matches_golden_arch(cfg, gold):
     V, d, L, H, ff, mp = (int(x) for x in gold["arch"])
     a = cfg.actor
     assert (a.vocab, a.d_model, a.n_layers, a.n_heads, a.d_ff, a.max_pos) == (V, d, L, H, ff, mp)
+    assert a.family == int(gold["family"])
+
+
+def test_llama_oracle_matches_transformers(cfg, gold, forced, family):
+    """The LLaMA oracle against Hugging Face transformers' LlamaForCausalLM itself (float64, no
+    rounding points; the fixture generator also checked its torch restatement against HF to
+    <1e-4 in the logits): logprobs of the golden sequences agree to the bf16-rounding spread."""
+    if family != "llama":
+        pytest.skip("OPT fixture has no transformers pin")
+    assert float(gold["hf_max_abs_logit_diff"]) < 1e-4
+    np.testing.assert_allclose(forced["logp_old"], gold["hf_logp"], atol=6e-2)
 
 
 def test_greedy_generation_matches_golden(cfg, gold):
@@ -100,7 +119,7 @@ def oracle_params(cfg):
     """Initial actor weights from the golden generator's numpy port of rlhf_init.h."""
     from tests.golden import make_golden as mg
     a = cfg.actor
-    arch = dict(V=a.vocab, d=a.d_model, L=a.n_layers, H=a.n_heads, ff=a.d_ff, max_pos=a.max_pos)
+    arch = dict(family=a.family, V=a.vocab, d=a.d_model, L=a.n_layers, H=a.n_heads, ff=a.d_ff, max_pos=a.max_pos)
     w = mg.make_weights(arch, cfg.seed * 16 + 0, False)
     flat = np.zeros(len(forced_len := oracle_lib.param_total(a)) if False else oracle_lib.param_total(a), np.float32)
     ps = mg.params_of(w)
