@@ -42,6 +42,11 @@ WORKLOADS = {
     # c3 / c5 shapes (B=64 over 8 GPUs in the paper's setting; per-GPU 16 here)
     "c3": dict(actor="opt-1.3b", critic="opt-350m", batch=16, prompt=256, gen=256,
                name="c3: OPT-1.3B Actor/Ref + OPT-350m-shaped Critic/Reward, batch 16/GPU, prompt 256 + response 256"),
+    # c4 (LLaMA-7B Actor/Critic, Disaggregated on 8 GPUs) needs ZeRO-3 sharding;
+    # this is the LLaMA-family step at the largest shape that runs unsharded on one B200
+    "c4-llama1b": dict(actor="llama-1b", critic="llama-1b", batch=16, prompt=256, gen=256,
+                       name="c4 family study: LLaMA-shaped 1B (d 2048, 16 layers, head_dim 128, SwiGLU 5504, "
+                            "V 32000) x4, batch 16/GPU, prompt 256 + response 256"),
     "c5-r1024": dict(actor="opt-1.3b", critic="opt-350m", batch=16, prompt=256, gen=1024,
                      name="c5: OPT-1.3B/350m, batch 16/GPU, prompt 256 + response 1024"),
 }
@@ -102,7 +107,8 @@ def decode_bytes_per_step(a, B, P, R):
     """Algorithmic HBM bytes of one decode step (weights once + KV read), averaged over the R-1 steps.
     SURVEY.md §8(d): sum_t [2 P_w + Bg (P+t) 4 L d]."""
     d, L, V, ff = a.d_model, a.n_layers, a.vocab, a.d_ff
-    p_w = L * (4 * d * d + 2 * d * ff) + V * d  # matmul weights incl. the tied LM head
+    nff = 3 if a.family == 1 else 2  # SwiGLU: gate, up, down
+    p_w = L * (4 * d * d + nff * d * ff) + V * d  # matmul weights incl. the LM head
     kv = sum(4 * L * d * B * (P + s) for s in range(1, R))
     return (2.0 * p_w * (R - 1) + kv) / max(1, R - 1)
 
@@ -151,7 +157,7 @@ def gemm_roofline(a, B, S, tflops_peak):
     (FFN up-projection, M = B*S tokens), through the C-ABI."""
     import torch
     from paper_2312_11819_b200 import ops
-    M, N, K = B * S, a.d_ff, a.d_model
+    M, N, K = B * S, a.d_ff * (2 if a.family == 1 else 1), a.d_model
     x = torch.randn(M, K, device="cuda").bfloat16()
     w = torch.randn(N, K, device="cuda").bfloat16()
     y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
