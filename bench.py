@@ -189,6 +189,7 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--strategy", default="colocated")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--zero", type=int, default=0, choices=[0, 1], help="ZeRO stage of the trainable models")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     rank = int(os.environ.get("RANK", 0))
@@ -213,7 +214,8 @@ def main():
         obj = [Engine.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    eng = Engine(cfg, device=local, rank=rank, world_size=world, strategy=args.strategy, nccl_id=nid)
+    eng = Engine(cfg, device=local, rank=rank, world_size=world, strategy=args.strategy, nccl_id=nid,
+                 zero_stage=args.zero)
     prompts = prompt_tokens(cfg.prompt_seed, B, P, cfg.actor.vocab, sample_offset=rank * B)
 
     for _ in range(args.warmup):
@@ -276,7 +278,7 @@ def main():
         "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded random-init weights, uniform prompt ids)",
         "config": {"workload": wl["name"], "placement": args.strategy, "global_batch": B * world,
-                   "prompt_len": P, "gen_len": R, "parallelism": f"dp{world}",
+                   "prompt_len": P, "gen_len": R, "parallelism": f"dp{world}", "zero_stage": args.zero,
                    "l2": "working set (4 models' weights + activations) >> 126 MB L2 every step"},
         "split_seconds_per_step": stage,
         "split_fraction": {k: v / (dev_s / args.steps) for k, v in stage.items()},

@@ -113,6 +113,11 @@ typedef struct rlhf_engine_options {
   int use_cuda_graph;         /* decode loop: 0 eager kernels, 1 CUDA graph of one step with programmatic
                                  dependent launches (default), 2 graph without PDL, 3 persistent
                                  cooperative decode kernel (rlhf_decode_loop) */
+  int zero_stage;             /* trainable models' AdamW state over their data-parallel group
+                                 (StrategyConfig::zero_level, scenario.hpp:12-26; memory model
+                                 costmodel.hpp:48-50): 0 replicated (gradient all-reduce); 1 fp32
+                                 master/m/v sharded 1/dp per rank (gradient reduce-scatter, AdamW on
+                                 the shard, bf16 weight all-gather) — bit-identical updates */
 } rlhf_engine_options;
 
 int rlhf_nccl_unique_id(uint8_t out[128]);

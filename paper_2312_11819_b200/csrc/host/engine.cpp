@@ -79,6 +79,8 @@ bool in(const std::vector<int>& v, int x) { return std::find(v.begin(), v.end(),
 
 Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg_(cfg), opt_(opt) {
   validate(cfg_);
+  if (opt_.zero_stage < 0 || opt_.zero_stage > 1)
+    throw ConfigError("zero_stage must be 0 or 1 (ZeRO-2/3 are planned, DESIGN.md §8)");
   cfg_.actor.scalar_head = 0;
   cfg_.critic.scalar_head = 1;
   strategy_ = opt.strategy ? opt.strategy : "colocated";
@@ -142,8 +144,8 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
   }
   opt_.nccl_id = nullptr;
 
-  if (hosts_[0]) init_decoder(actor_, fixed(cfg_.actor, 0), rlhf_model_seed(cfg_.seed, 0), true);
-  if (hosts_[1]) init_decoder(critic_, fixed(cfg_.critic, 1), rlhf_model_seed(cfg_.seed, 1), true);
+  if (hosts_[0]) init_decoder(actor_, fixed(cfg_.actor, 0), rlhf_model_seed(cfg_.seed, 0), true, actor_comm_);
+  if (hosts_[1]) init_decoder(critic_, fixed(cfg_.critic, 1), rlhf_model_seed(cfg_.seed, 1), true, critic_comm_);
   if (hosts_[2]) init_decoder(ref_, fixed(cfg_.actor, 0), rlhf_model_seed(cfg_.seed, 2), false);
   if (hosts_[3]) init_decoder(reward_, fixed(cfg_.critic, 1), rlhf_model_seed(cfg_.seed, 3), false);
   // shadows start from the trainers' initial weights (same seeds), then ParamSync
@@ -233,6 +235,12 @@ Engine::~Engine() {
 
 void Engine::allreduce_grads(Decoder& m, ncclComm_t comm) {
   if (!comm) return;
+  if (m.sharded) {  // ZeRO-1: each rank only needs the summed gradient of its own shard
+    NK(nccl().ReduceScatter(m.grad.p, m.grad.as<float>() + m.shard_off, static_cast<size_t>(m.shard), ncclFloat32,
+                            ncclSum, comm, stream_));
+    comm_bytes_ += 4.0 * static_cast<double>(m.npad - m.shard);
+    return;
+  }
   NK(nccl().AllReduce(m.grad.p, m.grad.p, static_cast<size_t>(m.n), ncclFloat32, ncclSum, comm, stream_));
   comm_bytes_ += 2.0 * 4.0 * m.n;
 }
@@ -275,7 +283,7 @@ void Engine::train_actor(Decoder& m, int B, ncclComm_t comm) {
   K(rlhf_scatter_rows_f32(arp_->dhf_resp, arp_->dhf, B, S_, R_, P_ - 1, d, stream_), 1);
   backward(m, tokens_.as<int32_t>(), B, S_);
   allreduce_grads(m, comm);
-  adam(m, cfg_.lr_actor);
+  adam(m, cfg_.lr_actor, comm);
 }
 
 void Engine::train_critic(Decoder& m, int B, ncclComm_t comm) {
@@ -291,7 +299,7 @@ void Engine::train_critic(Decoder& m, int B, ncclComm_t comm) {
                          arp_->ws, stream_), 2);
   backward(m, tokens_.as<int32_t>(), B, S_);
   allreduce_grads(m, comm);
-  adam(m, cfg_.lr_critic);
+  adam(m, cfg_.lr_critic, comm);
 }
 
 // Scoring helpers on tokens `tok` [B, S] -> per-row outputs.
@@ -576,8 +584,10 @@ size_t Engine::tensor_bytes(const std::string& name) const {
   if (name == "score") return static_cast<size_t>(Bcap_) * 4;
   if (name == "sample_ids") return static_cast<size_t>(Bcap_) * 4;
   auto flat = [](const Decoder& m, size_t e) { return static_cast<size_t>(m.n) * e; };
-  if (name == "actor_grad" || name == "actor_master") return flat(actor_, 4);
-  if (name == "critic_grad" || name == "critic_master") return flat(critic_, 4);
+  if (name == "actor_grad") return flat(actor_, 4);
+  if (name == "critic_grad") return flat(critic_, 4);
+  if (name == "actor_master") return static_cast<size_t>(actor_.shard) * 4;  // this rank's slice under ZeRO-1
+  if (name == "critic_master") return static_cast<size_t>(critic_.shard) * 4;
   if (name == "actor_params") return flat(actor_, 2);
   if (name == "critic_params") return flat(critic_, 2);
   if (name == "ref_params") return flat(ref_, 2);

@@ -41,6 +41,10 @@ struct Decoder {
   uint64_t seed = 0;
   bool trainable = false;
   int64_t n = 0;  // flat parameter count (rlhf_param_total)
+  // ZeRO-1: the fp32 master/m/v hold elements [shard_off, shard_off + shard) of the flat
+  // vector (padded to npad = dp * shard); unsharded: shard = npad = n, shard_off = 0
+  int64_t npad = 0, shard = 0, shard_off = 0;
+  bool sharded = false;
   DevBuf w;       // bf16 flat
   DevBuf master, m, v, grad;  // fp32 flat (trainable only)
   int adam_step = 0;
@@ -100,7 +104,7 @@ class Engine {
 
  private:
   // ---- building blocks (engine_model.cpp) ----
-  void init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool trainable);
+  void init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool trainable, ncclComm_t dp_comm = nullptr);
   void forward(const Decoder& m, const int32_t* tokens, int B, int tok_stride, int T, bool save, KVCache* kv);
   void attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd, bool keep_p);
   void attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_t* dov, uint16_t* dqkv, int B, int T, int H, int hd);
@@ -113,7 +117,7 @@ class Engine {
   void lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t* dst);
   void train_actor(Decoder& m, int B, ncclComm_t comm);
   void train_critic(Decoder& m, int B, ncclComm_t comm);
-  void adam(Decoder& m, float lr);
+  void adam(Decoder& m, float lr, ncclComm_t comm);
   void allreduce_grads(Decoder& m, ncclComm_t comm);
   void p2p(const std::vector<std::pair<const void*, size_t>>& sends, const std::vector<std::pair<void*, size_t>>& recvs);
   void score_logp(const Decoder& m, const int32_t* tok, int B, float* logp);

@@ -13,6 +13,7 @@
 
 #include "engine.hpp"
 #include "flexrlhf/errors.hpp"
+#include "nccl_dyn.hpp"
 
 namespace flexrlhf {
 
@@ -40,6 +41,11 @@ void Engine::kcheck(int status, const char* what) {
   }
 }
 
+#define NK(x)                                                                                     \
+  do {                                                                                            \
+    ncclResult_t r_ = (x);                                                                        \
+    if (r_ != ncclSuccess) throw DeviceError(std::string(#x) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
 #define K(call, n)                \
   do {                            \
     kcheck((call), #call);        \
@@ -127,11 +133,23 @@ void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t*
   K(rlhf_gemm_decode(&p, stream_), 1);
 }
 
-void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool trainable) {
+void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool trainable, ncclComm_t dp_comm) {
   m.a = a;
   m.seed = seed;
   m.trainable = trainable;
   m.n = rlhf_param_total(&a);
+  m.npad = m.shard = m.n;
+  m.shard_off = 0;
+  m.sharded = trainable && opt_.zero_stage >= 1 && dp_comm;
+  if (m.sharded) {
+    int dp = 1, r = 0;
+    NK(nccl().CommCount(dp_comm, &dp));
+    NK(nccl().CommUserRank(dp_comm, &r));
+    m.shard = (m.n + dp - 1) / dp;
+    m.shard = (m.shard + 63) / 64 * 64;  // 16-byte vectors in AdamW, aligned NCCL chunks
+    m.npad = m.shard * dp;
+    m.shard_off = m.shard * r;
+  }
   std::vector<uint16_t> host(static_cast<size_t>(m.n), 0);
   struct Piece { int t, l; int64_t i0, i1; };
   std::vector<Piece> pieces;
@@ -154,17 +172,17 @@ void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool tr
       }
     });
   for (auto& t : th) t.join();
-  m.w.alloc(static_cast<size_t>(m.n) * 2);
+  m.w.alloc(static_cast<size_t>(m.npad) * 2);
   if (cudaMemcpy(m.w.p, host.data(), host.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess)
     throw DeviceError("weight upload failed");
   if (trainable) {
-    std::vector<float> f(host.size());
-    for (size_t i = 0; i < host.size(); ++i) f[i] = rlhf_bf16_to_f32(host[i]);
+    std::vector<float> f(static_cast<size_t>(m.shard), 0.0f);  // this rank's slice of the fp32 master
+    for (int64_t i = 0; i < m.shard && m.shard_off + i < m.n; ++i) f[i] = rlhf_bf16_to_f32(host[m.shard_off + i]);
     m.master.alloc(f.size() * 4);
     cudaMemcpy(m.master.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice);
     m.m.alloc(f.size() * 4);
     m.v.alloc(f.size() * 4);
-    m.grad.alloc(f.size() * 4);
+    m.grad.alloc(static_cast<size_t>(m.npad) * 4);
   }
   if (m.llama()) {
     const int hd = a.d_model / a.n_heads, half = hd / 2;
@@ -633,10 +651,18 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   }
 }
 
-void Engine::adam(Decoder& m, float lr) {
+void Engine::adam(Decoder& m, float lr, ncclComm_t comm) {
   m.adam_step += 1;
-  K(rlhf_adamw(m.master.as<float>(), m.m.as<float>(), m.v.as<float>(), m.grad.as<float>(), m.w.p, m.n, lr, cfg_.beta1,
-               cfg_.beta2, cfg_.adam_eps, cfg_.weight_decay, m.adam_step, stream_), 1);
+  // ZeRO-1: the gradient shard was reduce-scattered into grad[shard_off, +shard); AdamW
+  // updates the rank's master slice and its bf16 copy, then the slices are all-gathered
+  K(rlhf_adamw(m.master.as<float>(), m.m.as<float>(), m.v.as<float>(), m.grad.as<float>() + m.shard_off,
+               m.w.as<uint16_t>() + m.shard_off, m.shard, lr, cfg_.beta1, cfg_.beta2, cfg_.adam_eps,
+               cfg_.weight_decay, m.adam_step, stream_), 1);
+  if (m.sharded && comm) {
+    NK(nccl().AllGather(m.w.as<uint16_t>() + m.shard_off, m.w.p, static_cast<size_t>(m.shard), ncclBfloat16, comm,
+                        stream_));
+    comm_bytes_ += 2.0 * static_cast<double>(m.npad - m.shard);
+  }
 }
 
 }  // namespace flexrlhf

@@ -21,6 +21,10 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+      nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -51,6 +55,9 @@ inline const NcclApi& nccl() {
     get(api.CommSplit, "ncclCommSplit");
     get(api.AllReduce, "ncclAllReduce");
     get(api.AllGather, "ncclAllGather");
+    get(api.ReduceScatter, "ncclReduceScatter");
+    get(api.CommCount, "ncclCommCount");
+    get(api.CommUserRank, "ncclCommUserRank");
     get(api.Broadcast, "ncclBroadcast");
     get(api.Send, "ncclSend");
     get(api.Recv, "ncclRecv");

@@ -29,7 +29,7 @@ def _gpus():
         return 0
 
 
-def _rank(rank, strategy, q_id, q_out):
+def _rank(rank, strategy, q_id, q_out, zero=0, arch="tiny"):
     import torch
     torch.cuda.set_device(rank)
     from paper_2312_11819_b200.capi import make_config as mc
@@ -40,8 +40,8 @@ def _rank(rank, strategy, q_id, q_out):
             q_id.put(nid)
     else:
         nid = q_id.get(timeout=120)
-    cfg = mc("tiny", "tiny", BG, P, R, sample_offset=rank * BG, loss_denominator=float(BG * WORLD * R))
-    eng = Engine(cfg, device=rank, rank=rank, world_size=WORLD, strategy=strategy, nccl_id=nid)
+    cfg = mc(arch, arch, BG, P, R, sample_offset=rank * BG, loss_denominator=float(BG * WORLD * R))
+    eng = Engine(cfg, device=rank, rank=rank, world_size=WORLD, strategy=strategy, nccl_id=nid, zero_stage=zero)
     eng.step()
     out = {"rank": rank, "sample_ids": eng.read("sample_ids")}
     for k in ("tokens", "logp_old", "logp_ref", "values", "score", "advantages", "returns", "actor_grad", "critic_grad",
@@ -113,3 +113,38 @@ def test_two_gpu_placement_matches_full_batch_oracle(strategy, oracle):
         inference = next(o for o in outs if "shadow_actor_params" in o)
         np.testing.assert_array_equal(inference["shadow_actor_params"], trainer["actor_params"])
         np.testing.assert_array_equal(inference["shadow_critic_params"], trainer["critic_params"])
+
+
+def _spawn(strategy, zero, arch):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q_id, q_out = ctx.Queue(), ctx.Queue()
+    procs = [ctx.Process(target=_rank, args=(r, strategy, q_id, q_out, zero, arch)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    outs = sorted((q_out.get(timeout=600) for _ in range(WORLD)), key=lambda o: o["rank"])
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    return outs
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("arch", ["tiny", "llama-tiny"])
+def test_zero1_sharded_adamw_is_bit_identical_to_replicated(arch):
+    """ZeRO-1 (reduce-scatter of gradients, AdamW on a 1/dp slice of master/m/v, all-gather of
+    the bf16 weights) against the replicated all-reduce step on the same data-parallel pair:
+    the sum of two addends is order-free, so updated weights and master slices match bit for bit."""
+    from paper_2312_11819_b200.capi import param_total
+    z0, z1 = _spawn("colocated", 0, arch), _spawn("colocated", 1, arch)
+    cfg = make_config(arch, arch, BG, P, R)
+    for tag, a in (("actor", cfg.actor), ("critic", cfg.critic)):
+        n = param_total(a)
+        shard = ((n + WORLD - 1) // WORLD + 63) // 64 * 64
+        for r in range(WORLD):
+            np.testing.assert_array_equal(z1[r][f"{tag}_params"], z0[r][f"{tag}_params"], err_msg=f"{tag} rank {r}")
+            m1 = z1[r][f"{tag}_master"]
+            assert m1.size == shard
+            lo, hi = r * shard, min(n, (r + 1) * shard)
+            np.testing.assert_array_equal(m1[:hi - lo], z0[r][f"{tag}_master"][lo:hi])
+            assert not m1[hi - lo:].any()
