@@ -47,6 +47,10 @@ WORKLOADS = {
     "c4-llama1b": dict(actor="llama-1b", critic="llama-1b", batch=16, prompt=256, gen=256,
                        name="c4 family study: LLaMA-shaped 1B (d 2048, 16 layers, head_dim 128, SwiGLU 5504, "
                             "V 32000) x4, batch 16/GPU, prompt 256 + response 256"),
+    # c4 proper: LLaMA-7B-shaped Actor/Ref + Critic/Reward; needs >= 4 GPUs and ZeRO-1 (--zero 1);
+    # the per-GPU batch is what fits next to the placement's resident models (--batch)
+    "c4": dict(actor="llama-7b", critic="llama-7b", batch=8, prompt=256, gen=256,
+               name="c4: LLaMA-7B-shaped Actor/Ref + Critic/Reward, prompt 256 + response 256"),
     "c5-r1024": dict(actor="opt-1.3b", critic="opt-350m", batch=16, prompt=256, gen=1024,
                      name="c5: OPT-1.3B/350m, batch 16/GPU, prompt 256 + response 1024"),
 }
@@ -189,9 +193,12 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--strategy", default="colocated")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch override (memory studies)")
     ap.add_argument("--zero", type=int, default=0, choices=[0, 1], help="ZeRO stage of the trainable models")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.batch:
+        wl["batch"] = args.batch
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -241,10 +248,12 @@ def main():
     stage = {k: sum(r["per_stage_seconds"][k] for r in reps) / args.steps for k in reps[0]["per_stage_seconds"]}
     dec_s = sum(r["decode_seconds"] for r in reps)
     launches = sum(r["gpu_launches"] for r in reps)
+    free_b, total_b = torch.cuda.mem_get_info()
+    mem_gb = (total_b - free_b) / 1e9
     if world > 1:
-        t = torch.tensor([e2e_s, dev_s, dec_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s, dev_s, dec_s, mem_gb], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s, dev_s, dec_s = t.tolist()
+        e2e_s, dev_s, dec_s, mem_gb = t.tolist()
     if rank != 0:
         dist.destroy_process_group()
         return 0
@@ -290,6 +299,7 @@ def main():
         "cpu_baseline": cpu,
         "clocks": clk,
         "losses": [reps[-1]["actor_loss"], reps[-1]["critic_loss"]],
+        "hbm_used_gb_max_rank": mem_gb,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

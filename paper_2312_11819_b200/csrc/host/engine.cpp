@@ -160,6 +160,11 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
     // when it does not fit (long sequences, large models) the step stays single-stream
     try {
       build_arena(ar_side_, true, true);
+      // keep room for the generation state allocated next (KV cache + decode buffers)
+      const size_t kv = 2ull * cfg_.actor.n_layers * gen_B_ * S_ * cfg_.actor.d_model * 2;
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      if (free_b < kv + (4ull << 30)) throw DeviceError("second-stream arena leaves too little memory");
       CK(cudaStreamCreateWithFlags(&stream_side_, cudaStreamNonBlocking));
     } catch (const DeviceError&) {
       for (DevBuf* b : ar_side_.owned) delete b;
