@@ -194,6 +194,7 @@ def main():
     ap.add_argument("--strategy", default="colocated")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch override (memory studies)")
+    ap.add_argument("--train-mb", type=int, default=0, help="samples per TrainFB micro-batch (0: all)")
     ap.add_argument("--zero", type=int, default=0, choices=[0, 1], help="ZeRO stage of the trainable models")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
@@ -222,7 +223,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     eng = Engine(cfg, device=local, rank=rank, world_size=world, strategy=args.strategy, nccl_id=nid,
-                 zero_stage=args.zero)
+                 zero_stage=args.zero, train_micro_batch=args.train_mb)
     prompts = prompt_tokens(cfg.prompt_seed, B, P, cfg.actor.vocab, sample_offset=rank * B)
 
     for _ in range(args.warmup):
@@ -287,7 +288,7 @@ def main():
         "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded random-init weights, uniform prompt ids)",
         "config": {"workload": wl["name"], "placement": args.strategy, "global_batch": B * world,
-                   "prompt_len": P, "gen_len": R, "parallelism": f"dp{world}", "zero_stage": args.zero,
+                   "prompt_len": P, "gen_len": R, "parallelism": f"dp{world}", "zero_stage": args.zero, "train_micro_batch": args.train_mb,
                    "l2": "working set (4 models' weights + activations) >> 126 MB L2 every step"},
         "split_seconds_per_step": stage,
         "split_fraction": {k: v / (dev_s / args.steps) for k, v in stage.items()},

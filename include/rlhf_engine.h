@@ -118,6 +118,11 @@ typedef struct rlhf_engine_options {
                                  costmodel.hpp:48-50): 0 replicated (gradient all-reduce); 1 fp32
                                  master/m/v sharded 1/dp per rank (gradient reduce-scatter, AdamW on
                                  the shard, bf16 weight all-gather) — bit-identical updates */
+  int train_micro_batch;      /* samples per TrainFB micro-batch (LoopParams::micro_batches,
+                                 workload.hpp:25-40, as a size): forward + backward run per
+                                 micro-batch and the gradients accumulate; only one micro-batch's
+                                 activations are kept, which is what bounds the batch that fits.
+                                 0 = the rank's whole batch */
 } rlhf_engine_options;
 
 int rlhf_nccl_unique_id(uint8_t out[128]);

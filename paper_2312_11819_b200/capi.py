@@ -30,7 +30,8 @@ class PPOConfig(C.Structure):
 
 class EngineOptions(C.Structure):
     _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world_size", C.c_int), ("strategy", C.c_char_p),
-                ("nccl_id", C.POINTER(C.c_uint8)), ("use_cuda_graph", C.c_int), ("zero_stage", C.c_int)]
+                ("nccl_id", C.POINTER(C.c_uint8)), ("use_cuda_graph", C.c_int), ("zero_stage", C.c_int),
+                ("train_micro_batch", C.c_int)]
 
 
 class StepReport(C.Structure):

@@ -118,6 +118,7 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
   }
   const bool pair_batch = tag_ == StrategyTag::Interleaving2 || tag_ == StrategyTag::Disaggregated;
   Bcap_ = (tag_ == StrategyTag::Colocated) ? Bg_ : 2 * Bg_;
+  train_mb_ = opt_.train_micro_batch > 0 ? std::min(opt_.train_micro_batch, Bcap_) : Bcap_;
   gen_B_ = pair_batch ? 2 * Bg_ : Bg_;
 
   CK(cudaSetDevice(opt_.device));
@@ -262,15 +263,27 @@ void Engine::p2p(const std::vector<std::pair<const void*, size_t>>& sends, const
   NK(nccl().GroupEnd());
 }
 
+// TrainFB over micro-batches of train_mb_ samples: each runs forward (activations saved),
+// loss, backward, accumulating into the flat gradient; then one all-reduce and AdamW.
 void Engine::train_actor(Decoder& m, int B, ncclComm_t comm) {
-  const int d = m.a.d_model, V = m.a.vocab, BR = B * R_;
-  const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator : static_cast<float>(BR);
+  const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator : static_cast<float>(B * R_);
   cudaMemsetAsync(m.grad.p, 0, static_cast<size_t>(m.n) * 4, stream_);
-  forward(m, tokens_.as<int32_t>(), B, S_, S_, true, nullptr);
-  lm_logprobs(m, tokens_.as<int32_t>(), B, logp_new_.as<float>(), true);
-  K(rlhf_ppo_actor_loss(logp_new_.as<float>(), logp_old_.as<float>(), adv_.as<float>(), BR, cfg_.cliprange, denom,
-                        gbuf_.as<float>(), loss_.as<float>(), stream_), 1);
-  K(rlhf_logprob_bwd(arp_->logits, arp_->lse, gbuf_.as<float>(), BR, V, tokens_.as<int32_t>(), S_, P_, R_, arp_->dz, stream_), 1);
+  for (int b0 = 0; b0 < B; b0 += train_mb_) train_actor_mb(m, b0, std::min(train_mb_, B - b0), denom);
+  allreduce_grads(m, comm);
+  adam(m, cfg_.lr_actor, comm);
+}
+
+void Engine::train_actor_mb(Decoder& m, int b0, int B, float denom) {
+  const int d = m.a.d_model, V = m.a.vocab, BR = B * R_;
+  const int32_t* tok = tokens_.as<int32_t>() + static_cast<size_t>(b0) * S_;
+  const size_t r0 = static_cast<size_t>(b0) * R_;
+  float* logp = logp_new_.as<float>() + r0;
+  float* g = gbuf_.as<float>() + r0;
+  forward(m, tok, B, S_, S_, true, nullptr);
+  lm_logprobs(m, tok, B, logp, true);
+  K(rlhf_ppo_actor_loss(logp, logp_old_.as<float>() + r0, adv_.as<float>() + r0, BR, cfg_.cliprange, denom, g,
+                        loss_.as<float>(), stream_), 1);
+  K(rlhf_logprob_bwd(arp_->logits, arp_->lse, g, BR, V, tok, S_, P_, R_, arp_->dz, stream_), 1);
   // dhf_resp = dz E ; dE += dz^T hf_resp
   rlhf_gemm_params p{};
   p.M = BR; p.N = d; p.K = V; p.batch = 1; p.batch_h = 1;
@@ -286,25 +299,31 @@ void Engine::train_actor(Decoder& m, int B, ncclComm_t comm) {
   gemm(q);
   cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
   K(rlhf_scatter_rows_f32(arp_->dhf_resp, arp_->dhf, B, S_, R_, P_ - 1, d, stream_), 1);
-  backward(m, tokens_.as<int32_t>(), B, S_);
-  allreduce_grads(m, comm);
-  adam(m, cfg_.lr_actor, comm);
+  backward(m, tok, B, S_);
 }
 
 void Engine::train_critic(Decoder& m, int B, ncclComm_t comm) {
-  const int d = m.a.d_model, BR = B * R_;
-  const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator : static_cast<float>(BR);
+  const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator : static_cast<float>(B * R_);
   cudaMemsetAsync(m.grad.p, 0, static_cast<size_t>(m.n) * 4, stream_);
-  forward(m, tokens_.as<int32_t>(), B, S_, S_, true, nullptr);
-  K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, d, values_new_.as<float>(), stream_), 1);
-  K(rlhf_ppo_critic_loss(values_new_.as<float>(), values_.as<float>(), ret_.as<float>(), BR, cfg_.cliprange_value, denom,
-                         gbuf2_.as<float>(), loss_.as<float>() + 1, stream_), 1);
-  cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
-  K(rlhf_scalar_head_bwd(arp_->hf, m.T(RLHF_T_VHEAD), gbuf2_.as<float>(), B, S_, R_, P_ - 1, d, arp_->dhf, m.G(RLHF_T_VHEAD),
-                         arp_->ws, stream_), 2);
-  backward(m, tokens_.as<int32_t>(), B, S_);
+  for (int b0 = 0; b0 < B; b0 += train_mb_) train_critic_mb(m, b0, std::min(train_mb_, B - b0), denom);
   allreduce_grads(m, comm);
   adam(m, cfg_.lr_critic, comm);
+}
+
+void Engine::train_critic_mb(Decoder& m, int b0, int B, float denom) {
+  const int d = m.a.d_model, BR = B * R_;
+  const int32_t* tok = tokens_.as<int32_t>() + static_cast<size_t>(b0) * S_;
+  const size_t r0 = static_cast<size_t>(b0) * R_;
+  float* v = values_new_.as<float>() + r0;
+  float* g = gbuf2_.as<float>() + r0;
+  forward(m, tok, B, S_, S_, true, nullptr);
+  K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, d, v, stream_), 1);
+  K(rlhf_ppo_critic_loss(v, values_.as<float>() + r0, ret_.as<float>() + r0, BR, cfg_.cliprange_value, denom, g,
+                         loss_.as<float>() + 1, stream_), 1);
+  cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
+  K(rlhf_scalar_head_bwd(arp_->hf, m.T(RLHF_T_VHEAD), g, B, S_, R_, P_ - 1, d, arp_->dhf, m.G(RLHF_T_VHEAD), arp_->ws,
+                         stream_), 2);
+  backward(m, tok, B, S_);
 }
 
 // Scoring helpers on tokens `tok` [B, S] -> per-row outputs.
@@ -338,6 +357,8 @@ void Engine::build_arena(Arena& A, bool trains, bool critic_only) {
   }
   A.T = static_cast<int64_t>(Bcap_) * S_;
   A.Z = static_cast<int64_t>(Bcap_) * A.H;
+  A.Ts = trains ? static_cast<int64_t>(train_mb_) * S_ : A.T;
+  A.Zs = trains ? static_cast<int64_t>(train_mb_) * A.H : A.Z;
   auto mk = [&](size_t bytes) {
     DevBuf* b = new DevBuf(bytes);
     A.owned.push_back(b);
@@ -345,15 +366,21 @@ void Engine::build_arena(Arena& A, bool trains, bool critic_only) {
   };
   const int64_t T = A.T, d = A.d, SS = static_cast<int64_t>(A.S) * A.S, BR = static_cast<int64_t>(Bcap_) * R_;
   const int64_t Ls = trains ? A.L : 1;  // layers of saved activations (inference-only ranks keep one)
-  A.xres = static_cast<float*>(mk((2 * Ls + 1) * T * d * 4));
-  A.mean = static_cast<float*>(mk((2 * Ls + 1) * T * 4));
-  A.rstd = static_cast<float*>(mk((2 * Ls + 1) * T * 4));
-  A.h1 = static_cast<uint16_t*>(mk(Ls * T * d * 2));
-  A.qkv = static_cast<uint16_t*>(mk(Ls * T * 3 * d * 2));
-  A.P = static_cast<uint16_t*>(mk(Ls * A.Z * SS * 2));
-  A.o = static_cast<uint16_t*>(mk(Ls * T * d * 2));
-  A.h2 = static_cast<uint16_t*>(mk(Ls * T * d * 2));
-  A.f = static_cast<uint16_t*>(mk(Ls * T * A.ff * 2));
+  // per-layer saved activations: Ls slots of one training micro-batch (Ts rows), and at
+  // least one slot of a whole Forward stage (T rows, layer buffers reused across layers)
+  const int64_t Ts = A.Ts, Zs = A.Zs;
+  auto cap = [&](int64_t slots, int64_t per_row, int64_t rows_s, int64_t rows_all) {
+    return std::max(slots * rows_s, rows_all) * per_row;
+  };
+  A.xres = static_cast<float*>(mk(cap(2 * Ls + 1, d * 4, Ts, T)));
+  A.mean = static_cast<float*>(mk(cap(2 * Ls + 1, 4, Ts, T)));
+  A.rstd = static_cast<float*>(mk(cap(2 * Ls + 1, 4, Ts, T)));
+  A.h1 = static_cast<uint16_t*>(mk(cap(Ls, d * 2, Ts, T)));
+  A.qkv = static_cast<uint16_t*>(mk(cap(Ls, 3 * d * 2, Ts, T)));
+  A.P = static_cast<uint16_t*>(mk(cap(Ls, SS * 2, Zs, A.Z)));
+  A.o = static_cast<uint16_t*>(mk(cap(Ls, d * 2, Ts, T)));
+  A.h2 = static_cast<uint16_t*>(mk(cap(Ls, d * 2, Ts, T)));
+  A.f = static_cast<uint16_t*>(mk(cap(Ls, A.ff * 2, Ts, T)));
   A.hf = static_cast<uint16_t*>(mk(T * d * 2));
   A.act = static_cast<uint16_t*>(mk(A.ffa ? T * A.ffa * 2 : 16));
   A.scores = static_cast<float*>(mk(A.Z * SS * 4));

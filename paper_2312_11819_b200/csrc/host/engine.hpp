@@ -65,7 +65,8 @@ struct Arena {
   int B = 0, S = 0, R = 0, d = 0, ff = 0, H = 0, V = 0, L = 0;  // capacities (ff: FFN-up width, 2 d_ff for SwiGLU)
   int ffa = 0;                                                     // SwiGLU output width (0: OPT only)
   uint16_t* act = nullptr;                                         // SwiGLU output / its gradient [T, ffa]
-  int64_t T = 0, Z = 0;
+  int64_t T = 0, Z = 0;    // rows / (sample, head) pairs of a whole Forward stage
+  int64_t Ts = 0, Zs = 0;  // the same for one TrainFB micro-batch: stride of the saved layers
   std::vector<DevBuf*> owned;
   float *xres = nullptr, *mean = nullptr, *rstd = nullptr;  // [(2L+1)][T*d], [(2L+1)][T]
   uint16_t *h1 = nullptr, *qkv = nullptr, *P = nullptr, *o = nullptr, *h2 = nullptr, *f = nullptr, *hf = nullptr;
@@ -117,6 +118,8 @@ class Engine {
   void lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t* dst);
   void train_actor(Decoder& m, int B, ncclComm_t comm);
   void train_critic(Decoder& m, int B, ncclComm_t comm);
+  void train_actor_mb(Decoder& m, int b0, int B, float denom);
+  void train_critic_mb(Decoder& m, int b0, int B, float denom);
   void adam(Decoder& m, float lr, ncclComm_t comm);
   void allreduce_grads(Decoder& m, ncclComm_t comm);
   void p2p(const std::vector<std::pair<const void*, size_t>>& sends, const std::vector<std::pair<void*, size_t>>& recvs);
@@ -145,6 +148,7 @@ class Engine {
   int Bg_ = 0;     // samples of this rank's shard (prompts it owns)
   int Bcap_ = 0;   // experience rows this rank may hold (Bg or 2*Bg)
   int gen_B_ = 0;  // sequences this rank generates
+  int train_mb_ = 0;  // samples per TrainFB micro-batch (gradients accumulate over them)
   PlacementPlan plan_;
   StrategyTag tag_ = StrategyTag::Colocated;
   cudaStream_t stream_ = nullptr;

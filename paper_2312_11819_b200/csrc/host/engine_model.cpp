@@ -229,19 +229,21 @@ void Engine::forward(const Decoder& m, const int32_t* tokens, int B, int tok_str
   const int d = a.d_model, H = a.n_heads, hd = d / H, ff = a.d_ff, L = a.n_layers;
   const int rows = B * T;
   const int64_t Td = static_cast<int64_t>(rows) * d;
-  auto X = [&](int k) { return arp_->xres + (save ? static_cast<int64_t>(k) * arp_->T * arp_->d : 0); };
-  auto MEAN = [&](int k) { return save ? arp_->mean + static_cast<int64_t>(k) * arp_->T : nullptr; };
-  auto RSTD = [&](int k) { return save ? arp_->rstd + static_cast<int64_t>(k) * arp_->T : nullptr; };
+  // saved layers are strided by the training micro-batch's rows (Arena::Ts, Zs)
+  if (save && rows > arp_->Ts) throw ConfigError("saved forward exceeds the training micro-batch capacity");
+  auto X = [&](int k) { return arp_->xres + (save ? static_cast<int64_t>(k) * arp_->Ts * arp_->d : 0); };
+  auto MEAN = [&](int k) { return save ? arp_->mean + static_cast<int64_t>(k) * arp_->Ts : nullptr; };
+  auto RSTD = [&](int k) { return save ? arp_->rstd + static_cast<int64_t>(k) * arp_->Ts : nullptr; };
   auto slot = [&](uint16_t* base, int64_t per, int l) { return base + (save ? static_cast<int64_t>(l) * per : 0); };
   (void)Td;
   K(rlhf_embed(tokens, tok_stride, B, T, 0, nullptr, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, X(0), stream_), 1);
   for (int l = 0; l < L; ++l) {
-    uint16_t* h1 = slot(arp_->h1, arp_->T * arp_->d, l);
-    uint16_t* qkv = slot(arp_->qkv, arp_->T * 3 * arp_->d, l);
-    uint16_t* P = slot(arp_->P, arp_->Z * arp_->S * arp_->S, l);
-    uint16_t* o = slot(arp_->o, arp_->T * arp_->d, l);
-    uint16_t* h2 = slot(arp_->h2, arp_->T * arp_->d, l);
-    uint16_t* f = slot(arp_->f, arp_->T * arp_->ff, l);
+    uint16_t* h1 = slot(arp_->h1, arp_->Ts * arp_->d, l);
+    uint16_t* qkv = slot(arp_->qkv, arp_->Ts * 3 * arp_->d, l);
+    uint16_t* P = slot(arp_->P, arp_->Zs * arp_->S * arp_->S, l);
+    uint16_t* o = slot(arp_->o, arp_->Ts * arp_->d, l);
+    uint16_t* h2 = slot(arp_->h2, arp_->Ts * arp_->d, l);
+    uint16_t* f = slot(arp_->f, arp_->Ts * arp_->ff, l);
     float* xin = X(2 * l);
     float* xmid = X(2 * l + 1);
     float* xout = X(2 * l + 2);
@@ -343,9 +345,9 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
   const rlhf_arch& a = m.a;
   const int d = a.d_model, H = a.n_heads, hd = d / H, ff = a.d_ff, L = a.n_layers;
   const int rows = B * S;
-  auto X = [&](int k) { return arp_->xres + static_cast<int64_t>(k) * arp_->T * arp_->d; };
-  auto MEAN = [&](int k) { return arp_->mean + static_cast<int64_t>(k) * arp_->T; };
-  auto RSTD = [&](int k) { return arp_->rstd + static_cast<int64_t>(k) * arp_->T; };
+  auto X = [&](int k) { return arp_->xres + static_cast<int64_t>(k) * arp_->Ts * arp_->d; };
+  auto MEAN = [&](int k) { return arp_->mean + static_cast<int64_t>(k) * arp_->Ts; };
+  auto RSTD = [&](int k) { return arp_->rstd + static_cast<int64_t>(k) * arp_->Ts; };
   cudaMemsetAsync(arp_->dres, 0, static_cast<size_t>(rows) * d * 4, stream_);
   norm_bwd(m, arp_->dhf, X(2 * L), MEAN(2 * L), RSTD(2 * L), RLHF_T_LNF_G, 0, rows);
   auto colsum = [&](const uint16_t* Gm, int N, float* db) {  // bias gradient (absent in LLaMA)
@@ -382,10 +384,10 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
     gemm(p);
   };
   for (int l = L - 1; l >= 0; --l) {
-    const int64_t Tn = arp_->T;
+    const int64_t Tn = arp_->Ts;
     const uint16_t* h1 = arp_->h1 + l * Tn * arp_->d;
     const uint16_t* qkv = arp_->qkv + l * Tn * 3 * arp_->d;
-    const uint16_t* P = arp_->P + l * arp_->Z * arp_->S * arp_->S;
+    const uint16_t* P = arp_->P + l * arp_->Zs * arp_->S * arp_->S;
     const uint16_t* o = arp_->o + l * Tn * arp_->d;
     const uint16_t* h2 = arp_->h2 + l * Tn * arp_->d;
     const uint16_t* f = arp_->f + l * Tn * arp_->ff;

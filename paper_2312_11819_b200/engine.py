@@ -27,7 +27,7 @@ _DTYPES = {"tokens": np.int32, "pred": np.int32, "sample_ids": np.int32, "actor_
 class Engine:
     def __init__(self, cfg: PPOConfig, device: int = 0, rank: int = 0, world_size: int = 1,
                  strategy: str = "colocated", nccl_id: bytes | None = None, cuda_graph: int = 1,
-                 zero_stage: int = 0):
+                 zero_stage: int = 0, train_micro_batch: int = 0):
         L = lib()
         self._cfg = cfg
         self._keep = []
@@ -36,7 +36,8 @@ class Engine:
             buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
             self._keep.append(buf)
             idp = C.cast(buf, C.POINTER(C.c_uint8))
-        opt = EngineOptions(device, rank, world_size, strategy.encode(), idp, int(cuda_graph), int(zero_stage))
+        opt = EngineOptions(device, rank, world_size, strategy.encode(), idp, int(cuda_graph), int(zero_stage),
+                            int(train_micro_batch))
         h = C.c_void_p()
         check(L.rlhf_engine_create(C.byref(cfg), C.byref(opt), C.byref(h)))
         self._h = h

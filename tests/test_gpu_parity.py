@@ -113,3 +113,24 @@ def test_second_step_runs_and_is_finite():
         rep = eng.step()
     assert np.isfinite(rep["actor_loss"]) and np.isfinite(rep["critic_loss"])
     assert rep["gpu_launches"] > 100
+
+
+@pytest.mark.parametrize("arch,mb", [("tiny", 1), ("llama-tiny", 3)])
+def test_micro_batched_training_matches_oracle(arch, mb):
+    """TrainFB in micro-batches of `mb` samples (gradient accumulation; only one micro-batch's
+    activations resident) against the full-batch oracle step: same tolerances as above."""
+    from paper_2312_11819_b200.engine import Engine
+    cfg = make_config(arch, arch, 4, 16, 16)
+    eng = Engine(cfg, train_micro_batch=mb)
+    rep = eng.step()
+    out = {k: eng.read(k) for k in ("tokens", "logp_new", "values_new", "actor_grad", "critic_grad", "actor_master",
+                                    "critic_master")}
+    ora = oracle_lib.ppo_step(cfg, tokens_in=out["tokens"])
+    for key in ("logp_new", "values_new"):
+        np.testing.assert_allclose(out[key], ora[key], atol=2e-2, rtol=1e-3, err_msg=key)
+    np.testing.assert_allclose([rep["actor_loss"], rep["critic_loss"]], [ora["actor_loss"], ora["critic_loss"]], rtol=2e-2)
+    for tag, a, lr in (("actor", cfg.actor, 1e-5), ("critic", cfg.critic, 5e-6)):
+        for name, off, n in named_slices(a):
+            x, y = out[f"{tag}_grad"][off:off + n].astype(np.float64), ora[f"{tag}_grad"][off:off + n].astype(np.float64)
+            assert np.linalg.norm(x - y) / (np.linalg.norm(y) + 1e-12) <= 3e-2, (tag, name)
+        assert np.abs(out[f"{tag}_master"] - ora[f"{tag}_master"]).max() <= 2 * lr + 1e-7
