@@ -20,7 +20,8 @@ ap.add_argument("--graph-mode", type=int, default=1, help="1: graph + PDL, 2: gr
 a = ap.parse_args()
 cfg = {"c2": lambda: make_config("opt-125m", "opt-125m", 32, 256, 256),
        "c3": lambda: make_config("opt-1.3b", "opt-350m", 16, 256, 256),
-       "c1": lambda: make_config("tiny", "tiny", 4, 16, 16)}[a.workload]()
+       "c1": lambda: make_config("tiny", "tiny", 4, 16, 16),
+       "c4-llama1b": lambda: make_config("llama-1b", "llama-1b", 16, 256, 256)}[a.workload]()
 eng = Engine(cfg, cuda_graph=0 if a.no_graph else a.graph_mode)
 for _ in range(a.steps):
     rep = eng.step()
