@@ -261,6 +261,88 @@ __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* 
   }
 }
 
+// RMSNorm backward for d > 2048 (LLaMA-7B: 4096): a row is split between the two warps of a
+// pair (half the columns each, VPLH float4 per lane), so the row arrays stay in registers
+// (the one-warp-per-row kernel spills at VPL 32: 0.7 TB/s).  The pair exchanges its two
+// partial row sums through shared memory (double-buffered slot, named barrier per pair,
+// fixed summation order); gamma is staged in shared memory; dgamma partials per warp half.
+template <int VPLH>
+__global__ void __launch_bounds__(256) rmsnorm_bwd_pair_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+                                                               const float* __restrict__ rstd, const uint16_t* __restrict__ g,
+                                                               float* __restrict__ dx, float* __restrict__ ws, int M, int d,
+                                                               int rpb) {
+  extern __shared__ float red[];  // [8 warps][d] (each warp fills its half), gamma [d], exchange [2][8]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, half = warp & 1;
+  const int q = d / 4, qh = q / 2;
+  float4* gs = reinterpret_cast<float4*>(red + 8 * d);
+  float* xch = red + 9 * d;
+  for (int c = threadIdx.x; c < q; c += blockDim.x) {
+    const uint2 u = reinterpret_cast<const uint2*>(g)[c];
+    gs[c] = make_float4(bf2f(u.x & 0xFFFFu), bf2f(u.x >> 16), bf2f(u.y & 0xFFFFu), bf2f(u.y >> 16));
+  }
+  __syncthreads();
+  const int cb = half * qh;
+  float4 pg[VPLH];
+#pragma unroll
+  for (int k = 0; k < VPLH; ++k) pg[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int r0 = blockIdx.x * rpb;
+  int par = 0;
+  for (int rr = pair; rr < rpb; rr += 4, par ^= 1) {
+    const int row = r0 + rr;
+    if (row >= M) break;
+    const float4* dr = reinterpret_cast<const float4*>(dy + static_cast<int64_t>(row) * d);
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * d);
+    float4* o = reinterpret_cast<float4*>(dx + static_cast<int64_t>(row) * d);
+    const float rs = rstd[row];
+    float4 dyv[VPLH], xh[VPLH];
+#pragma unroll
+    for (int k = 0; k < VPLH; ++k) {
+      const int c = cb + lane + 32 * k;
+      const bool ok = lane + 32 * k < qh;
+      dyv[k] = ok ? dr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      xh[k] = ok ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float cs = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPLH; ++k) {
+      if (lane + 32 * k >= qh) continue;
+      const float4 gv = gs[cb + lane + 32 * k];
+      xh[k] = make_float4(xh[k].x * rs, xh[k].y * rs, xh[k].z * rs, xh[k].w * rs);
+      cs += (dyv[k].x * gv.x * xh[k].x + dyv[k].y * gv.y * xh[k].y) + (dyv[k].z * gv.z * xh[k].z + dyv[k].w * gv.w * xh[k].w);
+      pg[k].x += dyv[k].x * xh[k].x; pg[k].y += dyv[k].y * xh[k].y;
+      pg[k].z += dyv[k].z * xh[k].z; pg[k].w += dyv[k].w * xh[k].w;
+    }
+    cs = warp_sum(cs);
+    if (lane == 0) xch[par * 8 + warp] = cs;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    cs = (xch[par * 8 + 2 * pair] + xch[par * 8 + 2 * pair + 1]) / d;  // fixed order: half 0, half 1
+#pragma unroll
+    for (int k = 0; k < VPLH; ++k) {
+      const int c = cb + lane + 32 * k;
+      if (lane + 32 * k >= qh) continue;
+      const float4 gv = gs[c];
+      float4 r = o[c];
+      r.x += rs * (dyv[k].x * gv.x - xh[k].x * cs);
+      r.y += rs * (dyv[k].y * gv.y - xh[k].y * cs);
+      r.z += rs * (dyv[k].z * gv.z - xh[k].z * cs);
+      r.w += rs * (dyv[k].w * gv.w - xh[k].w * cs);
+      o[c] = r;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < VPLH; ++k)
+    if (lane + 32 * k < qh) reinterpret_cast<float4*>(red + warp * d)[cb + lane + 32 * k] = pg[k];
+  __syncthreads();
+  float* wg = ws + static_cast<int64_t>(blockIdx.x) * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const int h = (j / 4) >= qh ? 1 : 0;
+    float acc = 0.f;
+    for (int p = 0; p < 4; ++p) acc += red[(2 * p + h) * d + j];  // fixed pair order
+    wg[j] = acc;
+  }
+}
+
 __global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblk, int ncol, int64_t blk_stride,
                                        float* __restrict__ out0, float* __restrict__ out1, int split) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -436,9 +518,16 @@ extern "C" int rlhf_rmsnorm_bwd(const float* dy, const float* x, const float* rs
   } else if (d <= 2048) {
     cudaFuncSetAttribute(layernorm_bwd_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2048 * 4);
     layernorm_bwd_kernel<16, true><<<nblk, 256, sm, S(s)>>>(dy, x, nm, rstd, gp, dx, ws, M, d);
-  } else if (d <= 4096) {
-    cudaFuncSetAttribute(layernorm_bwd_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096 * 4);
-    layernorm_bwd_kernel<32, true><<<nblk, 256, sm, S(s)>>>(dy, x, nm, rstd, gp, dx, ws, M, d);
+  } else if (d <= 4096 && d % 8 == 0) {
+    // short micro-batches: 16-row blocks so that M = 1024..4096 still fills the SMs
+    int rpb = M >= 8192 ? kLnBwdRows : 16;
+    if (ws_floats < static_cast<size_t>((M + rpb - 1) / rpb) * d) rpb = kLnBwdRows;  // small workspace
+    const int nb2 = (M + rpb - 1) / rpb;
+    const size_t sm2 = static_cast<size_t>(9) * d * 4 + 16 * 4;
+    cudaFuncSetAttribute(rmsnorm_bwd_pair_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 9 * 4096 * 4 + 64);
+    rmsnorm_bwd_pair_kernel<16><<<nb2, 256, sm2, S(s)>>>(dy, x, rstd, gp, dx, ws, M, d, rpb);
+    reduce_partials_kernel<<<(d + 63) / 64, 64, 0, S(s)>>>(ws, nb2, d, d, dg, dg, d);
+    return cuda_status();
   } else {
     return 2;
   }
