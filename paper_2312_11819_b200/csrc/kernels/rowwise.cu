@@ -261,31 +261,34 @@ __global__ void layernorm_bwd_kernel(const float* __restrict__ dy, const float* 
   }
 }
 
-// RMSNorm backward for d > 2048 (LLaMA-7B: 4096): a row is split between the two warps of a
-// pair (half the columns each, VPLH float4 per lane), so the row arrays stay in registers
-// (the one-warp-per-row kernel spills at VPL 32: 0.7 TB/s).  The pair exchanges its two
-// partial row sums through shared memory (double-buffered slot, named barrier per pair,
-// fixed summation order); gamma is staged in shared memory; dgamma partials per warp half.
-template <int VPLH>
-__global__ void __launch_bounds__(256) rmsnorm_bwd_pair_kernel(const float* __restrict__ dy, const float* __restrict__ x,
-                                                               const float* __restrict__ rstd, const uint16_t* __restrict__ g,
-                                                               float* __restrict__ dx, float* __restrict__ ws, int M, int d,
-                                                               int rpb) {
-  extern __shared__ float red[];  // [8 warps][d] (each warp fills its half), gamma [d], exchange [2][8]
+// Norm backward for wide rows (LayerNorm d = 2048 (OPT-1.3B), RMSNorm d = 2048 / 4096 (LLaMA)):
+// a row is split between the two warps of a pair (half the columns each, VPLH float4 per lane),
+// so the row arrays stay in registers (the one-warp-per-row kernel spills: 0.7 TB/s at
+// d = 4096, 2.1-2.5 TB/s at d = 2048).  The pair exchanges its partial row sums (sum dy*g and,
+// for LayerNorm, sum dy*g*xhat) through shared memory (double-buffered slot, named barrier per
+// pair, fixed summation order: half 0 then half 1); gamma is staged in shared memory; the
+// dgamma (, dbeta) column partials stay in registers per warp half.
+template <int VPLH, bool RMS>
+__global__ void __launch_bounds__(256) norm_bwd_pair_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+                                                            const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                            const uint16_t* __restrict__ g, float* __restrict__ dx,
+                                                            float* __restrict__ ws, int M, int d, int rpb) {
+  constexpr int NP = RMS ? 1 : 2;
+  extern __shared__ float red[];  // [8 warps][NP][d] (each warp fills its half), gamma [d], exchange [2][8][2]
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int pair = warp >> 1, half = warp & 1;
   const int q = d / 4, qh = q / 2;
-  float4* gs = reinterpret_cast<float4*>(red + 8 * d);
-  float* xch = red + 9 * d;
+  float4* gs = reinterpret_cast<float4*>(red + 8 * NP * d);
+  float* xch = red + (8 * NP + 1) * d;
   for (int c = threadIdx.x; c < q; c += blockDim.x) {
     const uint2 u = reinterpret_cast<const uint2*>(g)[c];
     gs[c] = make_float4(bf2f(u.x & 0xFFFFu), bf2f(u.x >> 16), bf2f(u.y & 0xFFFFu), bf2f(u.y >> 16));
   }
   __syncthreads();
   const int cb = half * qh;
-  float4 pg[VPLH];
+  float4 pg[VPLH], pb[VPLH];
 #pragma unroll
-  for (int k = 0; k < VPLH; ++k) pg[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = 0; k < VPLH; ++k) pg[k] = pb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   const int r0 = blockIdx.x * rpb;
   int par = 0;
   for (int rr = pair; rr < rpb; rr += 4, par ^= 1) {
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_pair_kernel(const float* __re
     const float4* dr = reinterpret_cast<const float4*>(dy + static_cast<int64_t>(row) * d);
     const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * d);
     float4* o = reinterpret_cast<float4*>(dx + static_cast<int64_t>(row) * d);
-    const float rs = rstd[row];
+    const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
     float4 dyv[VPLH], xh[VPLH];
 #pragma unroll
     for (int k = 0; k < VPLH; ++k) {
@@ -303,44 +306,74 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_pair_kernel(const float* __re
       dyv[k] = ok ? dr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
       xh[k] = ok ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    float cs = 0.f;
+    float a = 0.f, cs = 0.f;
 #pragma unroll
     for (int k = 0; k < VPLH; ++k) {
       if (lane + 32 * k >= qh) continue;
       const float4 gv = gs[cb + lane + 32 * k];
-      xh[k] = make_float4(xh[k].x * rs, xh[k].y * rs, xh[k].z * rs, xh[k].w * rs);
-      cs += (dyv[k].x * gv.x * xh[k].x + dyv[k].y * gv.y * xh[k].y) + (dyv[k].z * gv.z * xh[k].z + dyv[k].w * gv.w * xh[k].w);
+      xh[k] = make_float4((xh[k].x - mu) * rs, (xh[k].y - mu) * rs, (xh[k].z - mu) * rs, (xh[k].w - mu) * rs);
+      const float t0 = dyv[k].x * gv.x, t1 = dyv[k].y * gv.y, t2 = dyv[k].z * gv.z, t3 = dyv[k].w * gv.w;
+      if (!RMS) a += (t0 + t1) + (t2 + t3);
+      cs += (t0 * xh[k].x + t1 * xh[k].y) + (t2 * xh[k].z + t3 * xh[k].w);
       pg[k].x += dyv[k].x * xh[k].x; pg[k].y += dyv[k].y * xh[k].y;
       pg[k].z += dyv[k].z * xh[k].z; pg[k].w += dyv[k].w * xh[k].w;
+      if (!RMS) { pb[k].x += dyv[k].x; pb[k].y += dyv[k].y; pb[k].z += dyv[k].z; pb[k].w += dyv[k].w; }
     }
     cs = warp_sum(cs);
-    if (lane == 0) xch[par * 8 + warp] = cs;
+    if (!RMS) a = warp_sum(a);
+    if (lane == 0) {
+      xch[(par * 8 + warp) * 2] = cs;
+      xch[(par * 8 + warp) * 2 + 1] = a;
+    }
     asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
-    cs = (xch[par * 8 + 2 * pair] + xch[par * 8 + 2 * pair + 1]) / d;  // fixed order: half 0, half 1
+    const float* xp = xch + (par * 8 + 2 * pair) * 2;
+    cs = (xp[0] + xp[2]) / d;  // fixed order: half 0, half 1
+    a = RMS ? 0.f : (xp[1] + xp[3]) / d;
 #pragma unroll
     for (int k = 0; k < VPLH; ++k) {
       const int c = cb + lane + 32 * k;
       if (lane + 32 * k >= qh) continue;
       const float4 gv = gs[c];
       float4 r = o[c];
-      r.x += rs * (dyv[k].x * gv.x - xh[k].x * cs);
-      r.y += rs * (dyv[k].y * gv.y - xh[k].y * cs);
-      r.z += rs * (dyv[k].z * gv.z - xh[k].z * cs);
-      r.w += rs * (dyv[k].w * gv.w - xh[k].w * cs);
+      r.x += rs * (dyv[k].x * gv.x - a - xh[k].x * cs);
+      r.y += rs * (dyv[k].y * gv.y - a - xh[k].y * cs);
+      r.z += rs * (dyv[k].z * gv.z - a - xh[k].z * cs);
+      r.w += rs * (dyv[k].w * gv.w - a - xh[k].w * cs);
       o[c] = r;
     }
   }
 #pragma unroll
   for (int k = 0; k < VPLH; ++k)
-    if (lane + 32 * k < qh) reinterpret_cast<float4*>(red + warp * d)[cb + lane + 32 * k] = pg[k];
+    if (lane + 32 * k < qh) {
+      reinterpret_cast<float4*>(red + (warp * NP) * d)[cb + lane + 32 * k] = pg[k];
+      if (!RMS) reinterpret_cast<float4*>(red + (warp * NP + 1) * d)[cb + lane + 32 * k] = pb[k];
+    }
   __syncthreads();
-  float* wg = ws + static_cast<int64_t>(blockIdx.x) * d;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    const int h = (j / 4) >= qh ? 1 : 0;
+  float* wg = ws + static_cast<int64_t>(blockIdx.x) * NP * d;
+  for (int j = threadIdx.x; j < NP * d; j += blockDim.x) {
+    const int which = j / d, col = j % d;
+    const int h = (col / 4) >= qh ? 1 : 0;
     float acc = 0.f;
-    for (int p = 0; p < 4; ++p) acc += red[(2 * p + h) * d + j];  // fixed pair order
+    for (int p = 0; p < 4; ++p) acc += red[((2 * p + h) * NP + which) * d + col];  // fixed pair order
     wg[j] = acc;
   }
+}
+
+// rows per block for the pair kernel: 16 for short micro-batches so M = 1024..4096 fills the SMs
+static int pair_rows_per_block(int M, int d, int np, size_t ws_floats) {
+  int rpb = M >= 8192 ? kLnBwdRows : 16;
+  if (ws_floats < static_cast<size_t>((M + rpb - 1) / rpb) * np * d) rpb = kLnBwdRows;  // small workspace
+  return rpb;
+}
+
+template <int VPLH, bool RMS>
+static void launch_norm_bwd_pair(const float* dy, const float* x, const float* mean, const float* rstd, const uint16_t* g,
+                                 float* dx, float* ws, int M, int d, int rpb, cudaStream_t s) {
+  constexpr int NP = RMS ? 1 : 2;
+  const size_t sm = static_cast<size_t>(8 * NP + 1) * d * 4 + 32 * 4;
+  cudaFuncSetAttribute(norm_bwd_pair_kernel<VPLH, RMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (8 * NP + 1) * (VPLH * 256) * 4 + 32 * 4);
+  norm_bwd_pair_kernel<VPLH, RMS><<<(M + rpb - 1) / rpb, 256, sm, s>>>(dy, x, mean, rstd, g, dx, ws, M, d, rpb);
 }
 
 __global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblk, int ncol, int64_t blk_stride,
@@ -515,19 +548,15 @@ extern "C" int rlhf_rmsnorm_bwd(const float* dy, const float* x, const float* rs
   if (d <= 1024) {
     cudaFuncSetAttribute(layernorm_bwd_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 1024 * 4);
     layernorm_bwd_kernel<8, true><<<nblk, 256, sm, S(s)>>>(dy, x, nm, rstd, gp, dx, ws, M, d);
+  } else if (d <= 4096 && d % 8 == 0) {
+    const int rpb = pair_rows_per_block(M, d, 1, ws_floats);
+    if (d <= 2048) launch_norm_bwd_pair<8, true>(dy, x, nm, rstd, gp, dx, ws, M, d, rpb, S(s));
+    else launch_norm_bwd_pair<16, true>(dy, x, nm, rstd, gp, dx, ws, M, d, rpb, S(s));
+    reduce_partials_kernel<<<(d + 63) / 64, 64, 0, S(s)>>>(ws, (M + rpb - 1) / rpb, d, d, dg, dg, d);
+    return cuda_status();
   } else if (d <= 2048) {
     cudaFuncSetAttribute(layernorm_bwd_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2048 * 4);
     layernorm_bwd_kernel<16, true><<<nblk, 256, sm, S(s)>>>(dy, x, nm, rstd, gp, dx, ws, M, d);
-  } else if (d <= 4096 && d % 8 == 0) {
-    // short micro-batches: 16-row blocks so that M = 1024..4096 still fills the SMs
-    int rpb = M >= 8192 ? kLnBwdRows : 16;
-    if (ws_floats < static_cast<size_t>((M + rpb - 1) / rpb) * d) rpb = kLnBwdRows;  // small workspace
-    const int nb2 = (M + rpb - 1) / rpb;
-    const size_t sm2 = static_cast<size_t>(9) * d * 4 + 16 * 4;
-    cudaFuncSetAttribute(rmsnorm_bwd_pair_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 9 * 4096 * 4 + 64);
-    rmsnorm_bwd_pair_kernel<16><<<nb2, 256, sm2, S(s)>>>(dy, x, rstd, gp, dx, ws, M, d, rpb);
-    reduce_partials_kernel<<<(d + 63) / 64, 64, 0, S(s)>>>(ws, nb2, d, d, dg, dg, d);
-    return cuda_status();
   } else {
     return 2;
   }
@@ -545,6 +574,11 @@ extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* 
   if (d <= 1024) {
     cudaFuncSetAttribute(layernorm_bwd_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024 * 4);
     layernorm_bwd_kernel<8, false><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);
+  } else if (d <= 2048 && d % 8 == 0) {
+    const int rpb = pair_rows_per_block(M, d, 2, ws_floats);
+    launch_norm_bwd_pair<8, false>(dy, x, mean, rstd, gp, dx, ws, M, d, rpb, S(s));
+    reduce_partials_kernel<<<(2 * d + 63) / 64, 64, 0, S(s)>>>(ws, (M + rpb - 1) / rpb, 2 * d, 2 * d, dg, db, d);
+    return cuda_status();
   } else if (d <= 2048) {
     cudaFuncSetAttribute(layernorm_bwd_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4);
     layernorm_bwd_kernel<16, false><<<nblk, 256, sm, S(s)>>>(dy, x, mean, rstd, gp, dx, ws, M, d);

@@ -35,7 +35,7 @@ def bf(x):
     return x.to(torch.bfloat16).float()
 
 
-@pytest.mark.parametrize("M,d", [(37, 128), (256, 2048), (64, 4096)])
+@pytest.mark.parametrize("M,d", [(37, 128), (256, 2048), (64, 4096), (2048, 4096), (1000, 1536), (100, 1100)])
 def test_rmsnorm_fwd_bwd(M, d):
     L = lib()
     torch.manual_seed(0)
@@ -52,7 +52,7 @@ def test_rmsnorm_fwd_bwd(M, d):
     dy = torch.randn(M, d, device=dev)
     dx = torch.full((M, d), 0.5, device=dev)
     dg = torch.full((d,), 0.25, device=dev)
-    ws = torch.empty(((M + 63) // 64) * d + 64, device=dev)
+    ws = torch.empty(((M + 15) // 16) * d + 64, device=dev)  # room for 16-row pair blocks
     L.rlhf_rmsnorm_bwd.argtypes = [C.c_void_p] * 6 + [C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
     assert L.rlhf_rmsnorm_bwd(_p(dy), _p(x), _p(rstd), _p(g), _p(dx), _p(dg), M, d, _p(ws), ws.numel(), _s()) == 0
     xr = x.clone().requires_grad_(True)
@@ -61,6 +61,35 @@ def test_rmsnorm_fwd_bwd(M, d):
     out.backward(dy)
     torch.testing.assert_close(dx, 0.5 + xr.grad, rtol=1e-4, atol=1e-4)
     torch.testing.assert_close(dg, 0.25 + gr.grad, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("M,d,ws_rows", [(50, 768, 64), (300, 2048, 16), (300, 2048, 64), (70, 1040, 64),
+                                          (8192, 2048, 16)])
+def test_layernorm_bwd(M, d, ws_rows):
+    """LayerNorm backward (d = 2048 takes the two-warps-per-row pair kernel) vs torch autograd."""
+    L = lib()
+    torch.manual_seed(2)
+    x = torch.randn(M, d, device=dev) * 2 + 0.3
+    g = (1 + 0.1 * torch.randn(d, device=dev)).to(torch.bfloat16)
+    b = (0.1 * torch.randn(d, device=dev)).to(torch.bfloat16)
+    y = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
+    mean, rstd = torch.empty(M, device=dev), torch.empty(M, device=dev)
+    assert L.rlhf_layernorm(_p(x), _p(g), _p(b), _p(y), _p(mean), _p(rstd), M, d, _s()) == 0
+    dy = torch.randn(M, d, device=dev)
+    dx = torch.full((M, d), 0.5, device=dev)
+    dg = torch.full((d,), 0.25, device=dev)
+    db = torch.full((d,), -0.25, device=dev)
+    ws = torch.empty(((M + ws_rows - 1) // ws_rows) * 2 * d + 64, device=dev)
+    L.rlhf_layernorm_bwd.argtypes = [C.c_void_p] * 8 + [C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
+    assert L.rlhf_layernorm_bwd(_p(dy), _p(x), _p(mean), _p(rstd), _p(g), _p(dx), _p(dg), _p(db), M, d, _p(ws),
+                                ws.numel(), _s()) == 0
+    xr = x.clone().requires_grad_(True)
+    gr = g.float().clone().requires_grad_(True)
+    br = b.float().clone().requires_grad_(True)
+    torch.nn.functional.layer_norm(xr, (d,), gr, br, 1e-5).backward(dy)
+    torch.testing.assert_close(dx, 0.5 + xr.grad, rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(dg, 0.25 + gr.grad, rtol=1e-4, atol=2e-3)
+    torch.testing.assert_close(db, -0.25 + br.grad, rtol=1e-4, atol=2e-3)
 
 
 @pytest.mark.parametrize("B,T,H,hd", [(3, 40, 4, 64), (2, 16, 2, 128)])
