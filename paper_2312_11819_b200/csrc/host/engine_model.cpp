@@ -497,17 +497,23 @@ void Engine::decode_step(const Decoder& m, int B) {
   // per layer 7 launches: LN1 (layer 0: fused with the embedding), [QKV GEMM + KV-cache
   // store], attention, [O-proj + residual], LN2, [FFN-up + ReLU], [FFN-down + residual];
   // then final LN, [LM head + per-tile top-2], [merge -> token, *pos += 1]
+  // RLHF_DEC_FUSE_LN=1: LN1 (layers > 0) and LN2 run as the decode GEMM's LayerNorm prologue
+  // (every CTA normalises the B rows into its K-slice of the swizzled operand tiles)
+  static const bool fuse_ln = [] { const char* e = getenv("RLHF_DEC_FUSE_LN"); return e && atoi(e) != 0; }();
+  const bool fl = fuse_ln && B <= 64 && d <= 2048 && d % 64 == 0;
   for (int l = 0; l < a.n_layers; ++l) {
-    if (l > 0 && !(skip & 1))  // layer 0's LN1 ran in rlhf_embed_ln
+    const bool fl1 = fl && l > 0;
+    if (l > 0 && !(skip & 1) && !fl1)  // layer 0's LN1 ran in rlhf_embed_ln
       K(rlhf_layernorm(x, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h, nullptr, nullptr, B, d, stream_), 1);
     if (!(skip & 4))
-      linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr, nullptr, nullptr,
-                    nullptr, l);
+      linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr,
+                    fl1 ? x : nullptr, fl1 ? m.T(RLHF_T_LN1_G, l) : nullptr, fl1 ? m.T(RLHF_T_LN1_B, l) : nullptr, l);
     if (!(skip & 2)) K(rlhf_attn_decode(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o, stream_), 1);
     if (!(skip & 8)) linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, m.T(RLHF_T_BO, l), x, true, false, x);
-    if (!(skip & 1)) K(rlhf_layernorm(x, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h, nullptr, nullptr, B, d, stream_), 1);
+    if (!(skip & 1) && !fl) K(rlhf_layernorm(x, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h, nullptr, nullptr, B, d, stream_), 1);
     if (!(skip & 16)) {
-      linear_decode(m.T(RLHF_T_W1, l), ff, d, h, B, m.T(RLHF_T_B1, l), f, false, true, nullptr);
+      linear_decode(m.T(RLHF_T_W1, l), ff, d, h, B, m.T(RLHF_T_B1, l), f, false, true, nullptr, fl ? x : nullptr,
+                    fl ? m.T(RLHF_T_LN2_G, l) : nullptr, fl ? m.T(RLHF_T_LN2_B, l) : nullptr);
       linear_decode(m.T(RLHF_T_W2, l), d, ff, f, B, m.T(RLHF_T_B2, l), x, true, false, x);
     }
   }

@@ -101,6 +101,78 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 __device__ __forceinline__ float b2f(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
 
+// LayerNorm prologue of the fused decode GEMM: each warp normalises RPW batch rows at a
+// time (their loads in flight together), gamma/beta of this CTA's K-slice are fetched
+// before griddepcontrol.wait (weights do not depend on the predecessor).  Same per-lane
+// element assignment and reduction order as layernorm_kernel (rowwise.cu), so the bf16
+// operand is bit-identical to the unfused LN output.
+template <int VPL, int RPW>
+__device__ __forceinline__ void ln_prologue(const Args& e, uint8_t* btile0, int stage_bytes, int kb0, int kb1,
+                                            uint32_t warp, uint32_t lane) {
+  const int K4 = e.K / 4;
+  uint2 gg[VPL], bb[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = static_cast<int>(lane) + 32 * i, k = 4 * c;
+    const bool in = c < K4 && k >= kb0 * BK && k < kb1 * BK;
+    gg[i] = in ? *reinterpret_cast<const uint2*>(e.ln_g + k) : make_uint2(0u, 0u);
+    bb[i] = in ? *reinterpret_cast<const uint2*>(e.ln_b + k) : make_uint2(0u, 0u);
+  }
+  pdl_wait();
+  for (int n0 = static_cast<int>(warp); n0 < e.N; n0 += RPW * (kThreads / 32)) {
+    float4 v[RPW][VPL];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int n = n0 + r * (kThreads / 32);
+      const float4* xr = reinterpret_cast<const float4*>(e.ln_x + static_cast<int64_t>(n < e.N ? n : 0) * e.K);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = static_cast<int>(lane) + 32 * i;
+        v[r][i] = (c < K4 && n < e.N) ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int n = n0 + r * (kThreads / 32);
+      if (n >= e.N) break;
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i)
+        if (static_cast<int>(lane) + 32 * i < K4) sum += (v[r][i].x + v[r][i].y) + (v[r][i].z + v[r][i].w);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const float mu = sum / e.K;
+      float vs = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        if (static_cast<int>(lane) + 32 * i < K4)
+          vs += (v[r][i].x - mu) * (v[r][i].x - mu) + (v[r][i].y - mu) * (v[r][i].y - mu) +
+                (v[r][i].z - mu) * (v[r][i].z - mu) + (v[r][i].w - mu) * (v[r][i].w - mu);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) vs += __shfl_xor_sync(0xffffffffu, vs, o);
+      const float rs = 1.0f / sqrtf(vs / e.K + 1e-5f);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = static_cast<int>(lane) + 32 * i;
+        const int k = 4 * c;
+        if (c >= K4 || k < kb0 * BK || k >= kb1 * BK) continue;
+        const float y0 = (v[r][i].x - mu) * rs * b2f(static_cast<uint16_t>(gg[i].x & 0xFFFFu)) + b2f(static_cast<uint16_t>(bb[i].x & 0xFFFFu));
+        const float y1 = (v[r][i].y - mu) * rs * b2f(static_cast<uint16_t>(gg[i].x >> 16)) + b2f(static_cast<uint16_t>(bb[i].x >> 16));
+        const float y2 = (v[r][i].z - mu) * rs * b2f(static_cast<uint16_t>(gg[i].y & 0xFFFFu)) + b2f(static_cast<uint16_t>(bb[i].y & 0xFFFFu));
+        const float y3 = (v[r][i].w - mu) * rs * b2f(static_cast<uint16_t>(gg[i].y >> 16)) + b2f(static_cast<uint16_t>(bb[i].y >> 16));
+        const int j = k / BK - kb0, kk = k % BK;
+        uint8_t* dst = btile0 + j * stage_bytes + n * 128 + (((kk >> 3) ^ (n & 7)) << 4) + (kk & 7) * 2;
+        const uint32_t w0 = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y0))) |
+                            (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y1))) << 16);
+        const uint32_t w1 = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y2))) |
+                            (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y3))) << 16);
+        *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+      }
+    }
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -185,52 +257,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // LayerNorm of every batch row (full K for the statistics), written for this
     // CTA's K-slice straight into the SWIZZLE_128B K-major B tiles:
     //   byte(n, kk) = n*128 + ((kk/8) ^ (n%8))*16 + (kk%8)*2   within a 64-wide k block
-    pdl_wait();
-    const int K4 = e.K / 4;
-    for (int n = static_cast<int>(warp); n < e.N; n += kThreads / 32) {
-      const float4* xr = reinterpret_cast<const float4*>(e.ln_x + static_cast<int64_t>(n) * e.K);
-      float4 v[16];
-      float sum = 0.f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int c = static_cast<int>(lane) + 32 * i;
-        v[i] = c < K4 ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-        sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      const float mu = sum / e.K;
-      float vs = 0.f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int c = static_cast<int>(lane) + 32 * i;
-        if (c < K4)
-          vs += (v[i].x - mu) * (v[i].x - mu) + (v[i].y - mu) * (v[i].y - mu) + (v[i].z - mu) * (v[i].z - mu) +
-                (v[i].w - mu) * (v[i].w - mu);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) vs += __shfl_xor_sync(0xffffffffu, vs, o);
-      const float rs = 1.0f / sqrtf(vs / e.K + 1e-5f);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int c = static_cast<int>(lane) + 32 * i;
-        const int k = 4 * c;
-        if (c >= K4 || k < kb0 * BK || k >= kb1 * BK) continue;
-        const uint2 gg = *reinterpret_cast<const uint2*>(e.ln_g + k);
-        const uint2 bb = *reinterpret_cast<const uint2*>(e.ln_b + k);
-        const float y0 = (v[i].x - mu) * rs * b2f(static_cast<uint16_t>(gg.x & 0xFFFFu)) + b2f(static_cast<uint16_t>(bb.x & 0xFFFFu));
-        const float y1 = (v[i].y - mu) * rs * b2f(static_cast<uint16_t>(gg.x >> 16)) + b2f(static_cast<uint16_t>(bb.x >> 16));
-        const float y2 = (v[i].z - mu) * rs * b2f(static_cast<uint16_t>(gg.y & 0xFFFFu)) + b2f(static_cast<uint16_t>(bb.y & 0xFFFFu));
-        const float y3 = (v[i].w - mu) * rs * b2f(static_cast<uint16_t>(gg.y >> 16)) + b2f(static_cast<uint16_t>(bb.y >> 16));
-        const int j = k / BK - kb0, kk = k % BK;
-        uint8_t* dst = smem + j * C::STAGE_BYTES + C::A_BYTES + n * 128 + (((kk >> 3) ^ (n & 7)) << 4) + (kk & 7) * 2;
-        const uint32_t w0 = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y0))) |
-                            (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y1))) << 16);
-        const uint32_t w1 = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y2))) |
-                            (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y3))) << 16);
-        *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
-      }
-    }
+    if (e.K <= 1024) ln_prologue<8, 2>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
+    else ln_prologue<16, 1>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> visible to tcgen05.mma
     __syncthreads();
   }
