@@ -17,12 +17,12 @@ P = lambda t: C.c_void_p(t.data_ptr())
 L.rlhf_rmsnorm_bwd.argtypes = [C.c_void_p] * 6 + [C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
 L.rlhf_layernorm_bwd.argtypes = [C.c_void_p] * 8 + [C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
 for kind, M, d in [("ln", 16384, 768), ("ln", 8192, 2048), ("rms", 8192, 2048), ("rms", 4096, 4096),
-                   ("rms", 1024, 4096), ("rms", 2048, 4096), ("ln", 2048, 2048)]:
+                   ("rms", 1024, 4096), ("rms", 2048, 4096), ("ln", 2048, 2048), ("ln", 4096, 2048), ("rms", 8192, 4096)]:
     x, dy, dx = (torch.randn(M, d, device="cuda") for _ in range(3))
     mean, rstd = torch.randn(M, device="cuda"), torch.rand(M, device="cuda") + 0.5
     g = torch.randn(d, device="cuda").bfloat16()
     dg, db = torch.zeros(d, device="cuda"), torch.zeros(d, device="cuda")
-    ws = torch.empty((M // 8 + 1) * 2 * d + 64, device="cuda")
+    ws = torch.empty((M // 8 + 1) * 2 * d + 64, device="cuda")  # room for any rows-per-block
 
     def run():
         if kind == "rms":
