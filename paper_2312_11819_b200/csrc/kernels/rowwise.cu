@@ -362,10 +362,11 @@ __global__ void __launch_bounds__(256) norm_bwd_pair_kernel(const float* __restr
 
 // rows per block for the pair kernel: shorter blocks for micro-batch-sized M fill the SMs, longer
 // ones keep the dgamma partial reduction small (measured, tools/norm_bwd_bench.py with
-// RLHF_NORM_RPB: M >= 8192 -> 64, 4096 -> 32 (RMS 4096x4096 82 -> 68 us), <= 2048 -> 16)
+// RLHF_NORM_RPB: M >= 8192 -> 64 (32 when the partial row is only np*d <= 2048 floats: RMS
+// 8192x2048 70 -> 62 us), 4096 -> 32 (RMS 4096x4096 82 -> 68 us), <= 2048 -> 16)
 static int pair_rows_per_block(int M, int d, int np, size_t ws_floats) {
   static const int force = [] { const char* e = getenv("RLHF_NORM_RPB"); return e ? atoi(e) : 0; }();  // timing only
-  int rpb = force == 16 || force == 32 || force == 64 ? force : (M >= 8192 ? kLnBwdRows : M >= 4096 ? 32 : 16);
+  int rpb = force == 16 || force == 32 || force == 64 ? force : (M >= 8192 && np * d > 2048 ? kLnBwdRows : M >= 4096 ? 32 : 16);
   if (ws_floats < static_cast<size_t>((M + rpb - 1) / rpb) * np * d) rpb = kLnBwdRows;  // small workspace
   return rpb;
 }
