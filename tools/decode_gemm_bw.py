@@ -13,6 +13,7 @@ from paper_2312_11819_b200 import ops  # noqa: E402
 from paper_2312_11819_b200.capi import lib  # noqa: E402
 
 for name, M, K, N, splits in [("c3 W1", 8192, 2048, 16, 4), ("c3 W2", 2048, 8192, 16, 16), ("c3 W2", 2048, 8192, 16, 8), ("c3 qkv", 6144, 2048, 16, 4), ("c3 qkv", 6144, 2048, 16, 8), ("c3 W1", 8192, 2048, 16, 8),
+                              ("c3 O", 2048, 2048, 16, 8), ("c3 O", 2048, 2048, 16, 16), ("c3 O", 2048, 2048, 16, 4),
                               ("c2 W1", 3072, 768, 32, 8), ("c2 qkv", 2304, 768, 32, 8)]:
     copies = max(2, int(2e9 // (M * K * 2)))
     Ws = [torch.randn(M, K, device="cuda").bfloat16() for _ in range(min(copies, 24))]
