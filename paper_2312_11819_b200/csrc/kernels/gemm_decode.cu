@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     else ln_prologue<16, 1>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> visible to tcgen05.mma
     __syncthreads();
+    DPROBE(3);
   }
   if (warp == 1 && lane == 0) {
     const uint32_t idesc = umma_idesc_bf16(BM, BN, 0, 0);
