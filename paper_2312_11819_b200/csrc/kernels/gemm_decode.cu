@@ -257,7 +257,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // LayerNorm of every batch row (full K for the statistics), written for this
     // CTA's K-slice straight into the SWIZZLE_128B K-major B tiles:
     //   byte(n, kk) = n*128 + ((kk/8) ^ (n%8))*16 + (kk%8)*2   within a 64-wide k block
-    if (e.K <= 1024) ln_prologue<8, 2>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
+    __syncwarp();  // warp 0 arrives diverged (lane 0 issued the weight TMAs alone)
+    if (e.K <= 768) ln_prologue<6, 4>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
+    else if (e.K <= 1024) ln_prologue<8, 2>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
     else ln_prologue<16, 1>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> visible to tcgen05.mma
     __syncthreads();
