@@ -127,7 +127,24 @@ def cpu_oracle_sample(wl, threads=0):
     return time.perf_counter() - t0
 
 
-def reference_arm(args, wl, rank):
+METRIC = "PPO samples/sec per RLHF step (gen/fwd/train split)"  # identical in both arms
+
+
+def arm_config(args, wl, world):
+    """The `config` object both arms print (the driver compares the arms on it)."""
+    B, P, R = wl["batch"], wl["prompt"], wl["gen"]
+    return {"workload": wl["name"], "placement": args.strategy, "global_batch": B * world,
+            "prompt_len": P, "gen_len": R, "parallelism": f"dp{world}", "zero_stage": args.zero,
+            "train_micro_batch": args.train_mb,
+            "l2": "working set (4 models' weights + activations) >> 126 MB L2 every step"}
+
+
+def reference_arm(args, wl, rank, world=1):
+    """The reference's CPU path of the PPO step (the oracle port: the reference itself has no
+    numeric path) on the host cores.  Each timed step is a bounded sample of the
+    workload -- ONE of its samples through the full PPO step (generation, 4 forwards, GAE,
+    Actor + Critic training) -- so K + W steps end in minutes; samples/s = samples / seconds,
+    the same metric the GPU arm reports for the whole batch."""
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
@@ -136,12 +153,14 @@ def reference_arm(args, wl, rank):
     ts = [cpu_oracle_sample(wl, cores) for _ in range(args.steps)]
     total = sum(ts)
     v = args.steps / total
-    line = {"impl": "reference", "metric": "PPO samples/sec per RLHF step", "value": v, "unit": "samples/s",
+    sample = (f"1 of the {wl['batch']} samples per GPU of {wl['name']} per timed step: full PPO step "
+              f"(oracle/ppo_oracle.cpp, fp32, {cores} threads)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16-rounded operands)",
-            "data": "synthetic", "config": {"workload": wl["name"], "placement": "cpu", "sample": "1 sample per step"},
-            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-                             "sample": f"1 sample of {wl['name']} per step (oracle/ppo_oracle.cpp, full PPO step)"},
+            "data": "synthetic (seeded random-init weights, uniform prompt ids)",
+            "config": arm_config(args, wl, world), "sample": sample,
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -162,6 +181,7 @@ def gemm_roofline(a, B, S, tflops_peak):
     import torch
     from paper_2312_11819_b200 import ops
     M, N, K = B * S, a.d_ff * (2 if a.family == 1 else 1), a.d_model
+    kname = ops.gemm_kernel_name(M, N, K)
     x = torch.randn(M, K, device="cuda").bfloat16()
     w = torch.randn(N, K, device="cuda").bfloat16()
     y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
@@ -176,11 +196,12 @@ def gemm_roofline(a, B, S, tflops_peak):
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 1e3 / iters
     fl = 2.0 * M * N * K
-    tr = profile_json("r1_gemm_traffic.json")
-    traffic = tr["dram_bytes_per_launch"] if tr and tr.get("shape") == [M, N, K] else None
-    return {"bound": "tensor", "kernel": "gemm_sm100_kernel (FFN up-proj, forward)", "shape": [M, N, K],
+    tr = profile_json("r2_gemm_traffic.json")
+    ok = tr and tr.get("shape") == [M, N, K] and tr.get("kernel") == kname
+    traffic = tr["dram_bytes_per_launch"] if ok else None
+    return {"bound": "tensor", "kernel": f"{kname} (FFN up-proj, forward)", "shape": [M, N, K],
             "achieved": fl / t / 1e12, "peak": tflops_peak, "unit": "TFLOP/s", "frac": fl / t / 1e12 / tflops_peak,
-            "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write, profiles/r1_gemm_traffic.json)",
+            "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write of this kernel at this shape, profiles/r2_gemm_traffic.json)",
             "ms": t * 1e3}
 
 
@@ -204,7 +225,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
-        return reference_arm(args, wl, rank)
+        return reference_arm(args, wl, rank, world)
 
     import torch
     import torch.distributed as dist
@@ -283,13 +304,11 @@ def main():
     S = P + R
     samples = B * world * args.steps
     line = {
-        "metric": "PPO samples/sec per RLHF step (gen/fwd/train split)",
+        "metric": METRIC,
         "value": samples / dev_s, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded random-init weights, uniform prompt ids)",
-        "config": {"workload": wl["name"], "placement": args.strategy, "global_batch": B * world,
-                   "prompt_len": P, "gen_len": R, "parallelism": f"dp{world}", "zero_stage": args.zero, "train_micro_batch": args.train_mb,
-                   "l2": "working set (4 models' weights + activations) >> 126 MB L2 every step"},
+        "config": arm_config(args, wl, world),
         "split_seconds_per_step": stage,
         "split_fraction": {k: v / (dev_s / args.steps) for k, v in stage.items()},
         "e2e": {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": B * P * 4,

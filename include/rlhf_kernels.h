@@ -131,6 +131,9 @@ typedef struct rlhf_decode_loop_params {
 size_t rlhf_decode_loop_workspace_bytes(const rlhf_decode_loop_params* p);
 int rlhf_decode_loop(const rlhf_decode_loop_params* p, rlhf_stream_t s);
 int rlhf_gemm_block_n(const rlhf_gemm_params* p); /* tile width the dispatcher picks */
+/* Name of the kernel rlhf_gemm(p) dispatches to ("gemm_pair_kernel" or
+ * "gemm_sm100_kernel<BN>"), for labelling timings and ncu captures. */
+const char* rlhf_gemm_kernel_name(const rlhf_gemm_params* p);
 
 /* ---- embedding / norms (all stages) --------------------------------------
  * x[r] = tok_emb[tokens[b*tok_stride + p]] + pos_emb[p],  r = b*T + i,
@@ -226,16 +229,23 @@ int rlhf_scalar_head(const void* hf, const void* w, int B, int S, int R, int off
 int rlhf_scalar_head_bwd(const void* hf, const void* w, const float* g, int B, int S, int R, int off, int d,
                          float* dhf, float* dw, float* ws, rlhf_stream_t s);
 /* Experience buffer: rewards = -kl*(logp-logp_ref) (+clip(score) at the last
- * token); GAE(gamma, lam) -> advantages, returns.  One warp per sample. */
+ * token); GAE(gamma, lam) -> advantages, returns.  One warp per sample: the
+ * reverse recurrence A_t = delta_t + gamma*lam*A_{t+1} as a warp scan of affine
+ * maps over 32 contiguous chunks of the response (deterministic). */
 int rlhf_gae(const float* logp, const float* logp_ref, const float* values, const float* score, int B, int R,
              float kl_ctl, float clip_reward, float gamma, float lam, float* rewards, float* adv, float* ret,
              rlhf_stream_t s);
-/* PPO clipped policy loss: g = dL/dlogp; loss_sum[0] += sum(max(pg1, pg2)). */
+/* PPO clipped policy loss: g = dL/dlogp; loss_sum[0] += sum(max(pg1, pg2))
+ * (one block, fixed-order reduction: bit-reproducible). */
 int rlhf_ppo_actor_loss(const float* logp, const float* logp_old, const float* adv, int n, float clip, float denom,
                         float* g, float* loss_sum, rlhf_stream_t s);
 /* Clipped value loss: g = dL/dv; loss_sum[0] += sum(max(l1, l2)) (x0.5/denom on host). */
 int rlhf_ppo_critic_loss(const float* v, const float* v_old, const float* ret, int n, float clip, float denom,
                          float* g, float* loss_sum, rlhf_stream_t s);
+/* out[0] = sum of score[B], out[1] = sum of (logp - logp_ref)[B,R] (fixed order):
+ * the report's mean_score / mean_kl. */
+int rlhf_experience_stats(const float* logp, const float* logp_ref, const float* score, int B, int R, float* out,
+                          rlhf_stream_t s);
 /* Programmatic dependent launch for the decode-step kernels issued by this host
  * thread (embed, layernorm, kv_store, attn_decode, argmax, add_int; decode GEMM
  * takes its own flag).  Used while recording the decode CUDA graph. */

@@ -51,6 +51,8 @@ ARCHS = {
     # LLaMA family (family 1: RMSNorm, SwiGLU, rotary, no biases, untied head)
     "llama-tiny": dict(family=1, vocab=512, d_model=128, n_layers=2, n_heads=2, d_ff=384),
     "llama-tiny-hd128": dict(family=1, vocab=512, d_model=256, n_layers=2, n_heads=2, d_ff=704),
+    # LLaMA mid shape for end-to-end parity at S = 512 (head_dim 128, the 7B's)
+    "llama-mid": dict(family=1, vocab=32000, d_model=1024, n_layers=4, n_heads=8, d_ff=2816),
     "llama-1b": dict(family=1, vocab=32000, d_model=2048, n_layers=16, n_heads=16, d_ff=5504),
     "llama-7b": dict(family=1, vocab=32000, d_model=4096, n_layers=32, n_heads=32, d_ff=11008),
 }

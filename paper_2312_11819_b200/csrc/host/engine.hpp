@@ -135,7 +135,8 @@ class Engine {
               bool relu, const float* residual);
   void linear_decode(const uint16_t* W, int N_out, int K, const uint16_t* X, int Bg, const uint16_t* bias, void* Y,
                      bool y_f32, bool relu, const float* residual, const float* ln_x = nullptr,
-                     const uint16_t* ln_g = nullptr, const uint16_t* ln_b = nullptr, int kv_layer = -1);
+                     const uint16_t* ln_g = nullptr, const uint16_t* ln_b = nullptr, int kv_layer = -1,
+                     int kv_b0 = 0);
   void gemm(rlhf_gemm_params& p);
   void kcheck(int status, const char* what);
   void event(cudaEvent_t e) { cudaEventRecord(e, stream_); }

@@ -82,14 +82,28 @@ void Engine::linear(const uint16_t* X, int M, int Kd, const uint16_t* W, int N, 
 // dimension); K split over a thread-block cluster so ~2 CTAs per SM stream weights.
 void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t* X, int Bg, const uint16_t* bias,
                            void* Y, bool y_f32, bool relu, const float* residual, const float* ln_x,
-                           const uint16_t* ln_g, const uint16_t* ln_b, int kv_layer) {
+                           const uint16_t* ln_g, const uint16_t* ln_b, int kv_layer, int kv_b0) {
+  // the decode kernel takes at most 64 batch columns: larger batches whose epilogue stores
+  // K/V (or whose operand is LayerNorm-fused) run as 64-column chunks (the cache is indexed
+  // by the chunk-local sample, so its base moves with the chunk)
+  if (Bg > 64 && (ln_x || kv_layer >= 0)) {
+    for (int b0 = 0; b0 < Bg; b0 += 64) {
+      const int nb = std::min(64, Bg - b0);
+      const size_t ey = static_cast<size_t>(b0) * N_out * (y_f32 ? 4 : 2);
+      linear_decode(W, N_out, Kd, X ? X + static_cast<size_t>(b0) * Kd : nullptr, nb, bias,
+                    static_cast<char*>(Y) + ey, y_f32, relu, residual ? residual + static_cast<size_t>(b0) * N_out : nullptr,
+                    ln_x ? ln_x + static_cast<size_t>(b0) * Kd : nullptr, ln_g, ln_b, kv_layer, b0);
+    }
+    return;
+  }
   rlhf_gemm_decode_params p{};
   p.ln_x = ln_x;
   p.ln_g = ln_g;
   p.ln_b = ln_b;
   if (kv_layer >= 0) {
-    p.kcache = kv_.Kc(kv_layer);
-    p.vcache = kv_.Vc(kv_layer);
+    const size_t kv_off = static_cast<size_t>(kv_b0) * kv_.H * kv_.Smax * kv_.hd;
+    p.kcache = kv_.Kc(kv_layer) + kv_off;
+    p.vcache = kv_.Vc(kv_layer) + kv_off;
     p.pos = pos_.as<int>();
     p.kv_d = N_out / 3;
     p.kv_hd = kv_.hd;
@@ -646,8 +660,18 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
       if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         throw DeviceError("decode graph capture begin failed");
       pdl_ = opt_.use_cuda_graph == 2 ? 0 : 1;  // programmatic dependent launches inside the graph
-      rlhf_set_pdl(pdl_);
-      decode_step(m, B);
+      rlhf_set_pdl(pdl_);  // (thread-local: engines on other host threads are unaffected)
+      try {
+        decode_step(m, B);
+      } catch (...) {  // leave the stream usable: end the capture, drop the partial graph
+        rlhf_set_pdl(0);
+        pdl_ = 0;
+        cudaGraph_t partial = nullptr;
+        cudaStreamEndCapture(stream_, &partial);
+        if (partial) cudaGraphDestroy(partial);
+        cudaGetLastError();
+        throw;
+      }
       rlhf_set_pdl(0);
       pdl_ = 0;
       if (cudaStreamEndCapture(stream_, &g) != cudaSuccess) throw DeviceError("decode graph capture failed");

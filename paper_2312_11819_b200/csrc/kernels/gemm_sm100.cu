@@ -1037,6 +1037,18 @@ using namespace rlhf;
 
 extern "C" int rlhf_gemm_block_n(const rlhf_gemm_params* p) { return pick_bn(p); }
 
+extern "C" const char* rlhf_gemm_kernel_name(const rlhf_gemm_params* p) {
+  const int bn = pick_bn(p);
+  const int splits = p->split_k > 1 ? std::min(p->split_k, (p->K + BK - 1) / BK) : 1;
+  if (use_pair(p, bn, splits)) return "gemm_pair_kernel";
+  switch (bn) {
+    case 32: return "gemm_sm100_kernel<32>";
+    case 64: return "gemm_sm100_kernel<64>";
+    case 128: return "gemm_sm100_kernel<128>";
+    default: return "gemm_sm100_kernel<256>";
+  }
+}
+
 extern "C" size_t rlhf_gemm_workspace_bytes(const rlhf_gemm_params* p) {
   if (p->split_k <= 1 || p->causal) return 0;
   const int bn = pick_bn(p);

@@ -260,60 +260,111 @@ __global__ void sum_chunks_kernel(const float* __restrict__ ws, int chunks, int 
   out[e] += s;
 }
 
-// One thread per sample: reverse scan over the response (R sequential steps).
+// Experience buffer, one warp per sample.  A_t = delta_t + c A_{t+1} (c = gamma lam) is a
+// first-order linear recurrence: lane i owns the contiguous chunk [i*n, i*n+n) of the
+// response, reduces it to the affine map A_lo = u + c^n A_hi (one reverse pass over its
+// chunk, fully parallel across lanes), the 32 maps are composed by a reverse warp scan
+// (Kogge-Stone over __shfl_down), and each lane replays its chunk from its exact incoming
+// A_hi.  All loads are lane-contiguous (each lane streams its own chunk), every value is
+// produced in a fixed order, so the result is deterministic.
 __global__ void gae_kernel(const float* __restrict__ logp, const float* __restrict__ logp_ref, const float* __restrict__ val,
                            const float* __restrict__ score, int B, int R, float kl, float clip_r, float gamma, float lam,
                            float* __restrict__ rew, float* __restrict__ adv, float* __restrict__ ret) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= B) return;
   const int64_t o = static_cast<int64_t>(b) * R;
-  for (int j = 0; j < R; ++j) rew[o + j] = -kl * (logp[o + j] - logp_ref[o + j]);
-  rew[o + R - 1] += fminf(fmaxf(score[b], -clip_r), clip_r);
-  float last = 0.f;
-  for (int j = R - 1; j >= 0; --j) {
+  const float c = gamma * lam;
+  const int n = (R + 31) / 32;
+  const int j0 = min(R, lane * n), j1 = min(R, j0 + n);
+  const float sc = fminf(fmaxf(score[b], -clip_r), clip_r);
+  auto delta = [&](int j) {
+    float r = -kl * (logp[o + j] - logp_ref[o + j]);
+    if (j == R - 1) r += sc;
     const float nextv = j < R - 1 ? val[o + j + 1] : 0.0f;
-    const float delta = rew[o + j] + gamma * nextv - val[o + j];
-    last = delta + gamma * lam * last;
-    adv[o + j] = last;
+    return r + gamma * nextv - val[o + j];
+  };
+  // this lane's chunk as an affine map of the advantage just after it: A_{j0} = u + m A_{j1}
+  float u = 0.f, m = 1.f;
+  for (int j = j1 - 1; j >= j0; --j) {
+    u = delta(j) + c * u;
+    m *= c;
   }
-  for (int j = 0; j < R; ++j) ret[o + j] = adv[o + j] + val[o + j];
+  // reverse inclusive scan: lane i composes its map with every map to its right
+  for (int k = 1; k < 32; k <<= 1) {
+    const float u2 = __shfl_down_sync(0xffffffffu, u, k), m2 = __shfl_down_sync(0xffffffffu, m, k);
+    if (lane + k < 32) {
+      u = u + m * u2;
+      m = m * m2;
+    }
+  }
+  // incoming advantage of this chunk = the composed map of the lanes to its right applied to 0
+  float last = __shfl_down_sync(0xffffffffu, u, 1);
+  if (lane == 31) last = 0.f;
+  for (int j = j1 - 1; j >= j0; --j) {
+    float r = -kl * (logp[o + j] - logp_ref[o + j]);
+    if (j == R - 1) r += sc;
+    const float nextv = j < R - 1 ? val[o + j + 1] : 0.0f;
+    last = (r + gamma * nextv - val[o + j]) + c * last;
+    rew[o + j] = r;
+    adv[o + j] = last;
+    ret[o + j] = last + val[o + j];
+  }
 }
 
+// PPO losses: one block, a fixed per-thread stride and a fixed block-reduction tree, so
+// the loss sum is bit-reproducible (no atomics); `loss` accumulates across the TrainFB
+// micro-batches in stream order.
 __global__ void actor_loss_kernel(const float* __restrict__ lp, const float* __restrict__ lpo, const float* __restrict__ A,
                                   int n, float clip, float denom, float* __restrict__ g, float* __restrict__ loss) {
   __shared__ float sh[32];
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
   float l = 0.f;
-  if (k < n) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const float ratio = expf(lp[k] - lpo[k]);
     const float a = A[k];
     const float cl = fminf(fmaxf(ratio, 1.0f - clip), 1.0f + clip);
     const float pg1 = -a * ratio, pg2 = -a * cl;
-    l = fmaxf(pg1, pg2);
+    l += fmaxf(pg1, pg2);
     const bool inside = ratio >= 1.0f - clip && ratio <= 1.0f + clip;
     const float d1 = -a * ratio / denom, d2 = inside ? -a * ratio / denom : 0.0f;
     g[k] = pg1 > pg2 ? d1 : (pg1 < pg2 ? d2 : 0.5f * (d1 + d2));
   }
   l = block_reduce(l, SumOp(), sh);
-  if (threadIdx.x == 0) atomicAdd(loss, l);
+  if (threadIdx.x == 0) *loss += l;
 }
 
 __global__ void critic_loss_kernel(const float* __restrict__ v, const float* __restrict__ vo, const float* __restrict__ ret,
                                    int n, float clip, float denom, float* __restrict__ g, float* __restrict__ loss) {
   __shared__ float sh[32];
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
   float l = 0.f;
-  if (k < n) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const float x = v[k], o = vo[k], R = ret[k];
     const float vc = fminf(fmaxf(x, o - clip), o + clip);
     const float l1 = (x - R) * (x - R), l2 = (vc - R) * (vc - R);
-    l = fmaxf(l1, l2);
+    l += fmaxf(l1, l2);
     const bool inside = x >= o - clip && x <= o + clip;
     const float d1 = (x - R) / denom, d2 = inside ? (vc - R) / denom : 0.0f;
     g[k] = l1 > l2 ? d1 : (l1 < l2 ? d2 : 0.5f * (d1 + d2));
   }
   l = block_reduce(l, SumOp(), sh);
-  if (threadIdx.x == 0) atomicAdd(loss, l);
+  if (threadIdx.x == 0) *loss += l;
+}
+
+// out[0] = sum(score[b]), out[1] = sum(logp - logp_ref) over the experience rows (fixed order).
+__global__ void experience_stats_kernel(const float* __restrict__ lp, const float* __restrict__ lpr,
+                                        const float* __restrict__ score, int B, int R, float* __restrict__ out) {
+  __shared__ float sh[32];
+  float kl = 0.f, sc = 0.f;
+  const int n = B * R;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) kl += lp[k] - lpr[k];
+  for (int k = threadIdx.x; k < B; k += blockDim.x) sc += score[k];
+  kl = block_reduce(kl, SumOp(), sh);
+  __syncthreads();
+  sc = block_reduce(sc, SumOp(), sh);
+  if (threadIdx.x == 0) {
+    out[0] = sc;
+    out[1] = kl;
+  }
 }
 
 }  // namespace rlhf
@@ -362,20 +413,28 @@ extern "C" int rlhf_scalar_head_bwd(const void* hf, const void* w, const float* 
 extern "C" int rlhf_gae(const float* logp, const float* logp_ref, const float* values, const float* score, int B, int R,
                         float kl_ctl, float clip_reward, float gamma, float lam, float* rewards, float* adv, float* ret,
                         rlhf_stream_t s) {
-  gae_kernel<<<(B + 127) / 128, 128, 0, HS(s)>>>(logp, logp_ref, values, score, B, R, kl_ctl, clip_reward, gamma, lam,
-                                                 rewards, adv, ret);
+  if (B < 1 || R < 1) return 2;
+  gae_kernel<<<(B + 3) / 4, 128, 0, HS(s)>>>(logp, logp_ref, values, score, B, R, kl_ctl, clip_reward, gamma, lam,
+                                             rewards, adv, ret);
   return HST();
 }
 
 extern "C" int rlhf_ppo_actor_loss(const float* logp, const float* logp_old, const float* adv, int n, float clip,
                                    float denom, float* g, float* loss_sum, rlhf_stream_t s) {
-  actor_loss_kernel<<<(n + 255) / 256, 256, 0, HS(s)>>>(logp, logp_old, adv, n, clip, denom, g, loss_sum);
+  actor_loss_kernel<<<1, 1024, 0, HS(s)>>>(logp, logp_old, adv, n, clip, denom, g, loss_sum);
   return HST();
 }
 
 extern "C" int rlhf_ppo_critic_loss(const float* v, const float* v_old, const float* ret, int n, float clip, float denom,
                                     float* g, float* loss_sum, rlhf_stream_t s) {
-  critic_loss_kernel<<<(n + 255) / 256, 256, 0, HS(s)>>>(v, v_old, ret, n, clip, denom, g, loss_sum);
+  critic_loss_kernel<<<1, 1024, 0, HS(s)>>>(v, v_old, ret, n, clip, denom, g, loss_sum);
+  return HST();
+}
+
+extern "C" int rlhf_experience_stats(const float* logp, const float* logp_ref, const float* score, int B, int R,
+                                     float* out, rlhf_stream_t s) {
+  if (B < 1 || R < 1) return 2;
+  experience_stats_kernel<<<1, 1024, 0, HS(s)>>>(logp, logp_ref, score, B, R, out);
   return HST();
 }
 

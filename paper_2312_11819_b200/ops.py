@@ -90,6 +90,17 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = F
     return out
 
 
+def gemm_kernel_name(M: int, N: int, K: int) -> str:
+    """Kernel rlhf_gemm dispatches a row-major bf16 Y[M,N] = X[M,K] W[N,K]^T to."""
+    L = lib()
+    L.rlhf_gemm_kernel_name.argtypes = [C.POINTER(GemmParams)]
+    L.rlhf_gemm_kernel_name.restype = C.c_char_p
+    p = GemmParams()
+    p.M, p.N, p.K, p.batch, p.batch_h = M, N, K, 1, 1
+    p.lda, p.ldb, p.c_rs, p.c_cs = K, K, N, 1
+    return L.rlhf_gemm_kernel_name(C.byref(p)).decode()
+
+
 def gemm_batched(params: GemmParams) -> None:
     L = _declare_gemm()
     st = L.rlhf_gemm(C.byref(params), _stream())
@@ -126,6 +137,18 @@ def gemm_decode(W: torch.Tensor, X: torch.Tensor, *, out: torch.Tensor | None = 
     if st != 0:
         raise RuntimeError(f"rlhf_gemm_decode failed with status {st}")
     return out
+
+
+def layernorm(x: torch.Tensor, g: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """bf16(LayerNorm(x) * g + b) of fp32 rows x [N, d] via rlhf_layernorm (eps 1e-5)."""
+    L = lib()
+    L.rlhf_layernorm.argtypes = [C.c_void_p] * 6 + [C.c_int, C.c_int, C.c_void_p]
+    N, d = x.shape
+    y = torch.empty(N, d, device=x.device, dtype=torch.bfloat16)
+    st = L.rlhf_layernorm(x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(), None, None, N, d, _stream())
+    if st != 0:
+        raise RuntimeError(f"rlhf_layernorm failed with status {st}")
+    return y
 
 
 def attn_decode(qkv: torch.Tensor, kcache: torch.Tensor, vcache: torch.Tensor, pos: torch.Tensor) -> torch.Tensor:

@@ -231,31 +231,70 @@ def hf_llama(w, arch):
     return m
 
 
-def decoder(w, tok, arch):
-    """tok [B,S] long -> final-LN hidden [B,S,d] (bf16-rounded)."""
+def hf_opt(w, arch):
+    """The same weights in transformers' OPTForCausalLM (float64).  OPT's learned position
+    table is offset by 2 (OPTLearnedPositionalEmbedding), so row p of ours is its row p + 2;
+    the LM head is tied to the token embedding as in our layout."""
+    from transformers import OPTConfig, OPTForCausalLM
+    d, ff = arch["d"], arch["ff"]
+    cfg = OPTConfig(vocab_size=arch["V"], hidden_size=d, num_hidden_layers=arch["L"], ffn_dim=ff,
+                    num_attention_heads=arch["H"], max_position_embeddings=arch["max_pos"], do_layer_norm_before=True,
+                    word_embed_proj_dim=d, activation_function="relu", dropout=0.0, attention_dropout=0.0,
+                    layerdrop=0.0, enable_bias=True, layer_norm_elementwise_affine=True, tie_word_embeddings=True,
+                    pad_token_id=1, bos_token_id=2, eos_token_id=2)
+    m = OPTForCausalLM(cfg).double().eval()
+    dec = m.model.decoder
+    with torch.no_grad():
+        dec.embed_tokens.weight.copy_(w["tok"])
+        dec.embed_positions.weight.zero_()
+        dec.embed_positions.weight[2:2 + w["pos"].shape[0]].copy_(w["pos"])
+        for lw, L in zip(w["layers"], dec.layers):
+            a = L.self_attn
+            for proj, sl in ((a.q_proj, slice(0, d)), (a.k_proj, slice(d, 2 * d)), (a.v_proj, slice(2 * d, 3 * d))):
+                proj.weight.copy_(lw["wqkv"][sl])
+                proj.bias.copy_(lw["bqkv"][sl])
+            a.out_proj.weight.copy_(lw["wo"])
+            a.out_proj.bias.copy_(lw["bo"])
+            L.self_attn_layer_norm.weight.copy_(lw["ln1_g"])
+            L.self_attn_layer_norm.bias.copy_(lw["ln1_b"])
+            L.final_layer_norm.weight.copy_(lw["ln2_g"])
+            L.final_layer_norm.bias.copy_(lw["ln2_b"])
+            L.fc1.weight.copy_(lw["w1"])
+            L.fc1.bias.copy_(lw["b1"])
+            L.fc2.weight.copy_(lw["w2"])
+            L.fc2.bias.copy_(lw["b2"])
+        dec.final_layer_norm.weight.copy_(w["lnf_g"])
+        dec.final_layer_norm.bias.copy_(w["lnf_b"])
+        m.lm_head.weight.copy_(w["tok"])
+    return m
+
+
+def decoder(w, tok, arch, r=None):
+    """tok [B,S] long -> final-LN hidden [B,S,d] (bf16-rounded; r=identity turns rounding off)."""
     if arch.get("family", 0) == 1:
-        return decoder_llama(w, tok, arch)
+        return decoder_llama(w, tok, arch, r)
+    rb_ = r or rb
     B, S = tok.shape
     d, H = arch["d"], arch["H"]
     hd = d // H
     x = w["tok"][tok] + w["pos"][:S][None]
     mask = torch.ones(S, S, dtype=torch.bool).tril()
     for lw in w["layers"]:
-        h = rb(layernorm(x, lw["ln1_g"], lw["ln1_b"]))
-        qkv = rb(h @ lw["wqkv"].T + lw["bqkv"])
+        h = rb_(layernorm(x, lw["ln1_g"], lw["ln1_b"]))
+        qkv = rb_(h @ lw["wqkv"].T + lw["bqkv"])
         q, k, v = qkv.split(d, -1)
         q = q.view(B, S, H, hd).transpose(1, 2)
         k = k.view(B, S, H, hd).transpose(1, 2)
         v = v.view(B, S, H, hd).transpose(1, 2)
         s = (q @ k.transpose(-1, -2)) * (1.0 / np.sqrt(hd))
         s = s.masked_fill(~mask, float("-inf"))
-        p = rb(torch.softmax(s, -1))
-        o = rb((p @ v).transpose(1, 2).reshape(B, S, d))
+        p = rb_(torch.softmax(s, -1))
+        o = rb_((p @ v).transpose(1, 2).reshape(B, S, d))
         x = x + (o @ lw["wo"].T + lw["bo"])
-        h2 = rb(layernorm(x, lw["ln2_g"], lw["ln2_b"]))
-        f = rb(torch.relu(h2 @ lw["w1"].T + lw["b1"]))
+        h2 = rb_(layernorm(x, lw["ln2_g"], lw["ln2_b"]))
+        f = rb_(torch.relu(h2 @ lw["w1"].T + lw["b1"]))
         x = x + (f @ lw["w2"].T + lw["b2"])
-    return rb(layernorm(x, w["lnf_g"], w["lnf_b"]))
+    return rb_(layernorm(x, w["lnf_g"], w["lnf_b"]))
 
 
 def params_of(w):
@@ -286,6 +325,39 @@ def head_of(w):
 def main():
     run(dict(V=512, d=128, L=2, H=2, ff=512, max_pos=64), "c1_golden.npz")
     run(dict(family=1, V=512, d=128, L=2, H=2, ff=384, max_pos=64), "c1_llama_golden.npz")
+    hf_pins()
+
+
+# OPT shapes pinned against transformers' OPTForCausalLM (teacher-forced logprobs of a fixed
+# sequence under the Actor's seeded weights): the c1 tiny decoder and the OPT-125m shape of
+# BASELINE.json configs[1] at a short sequence (P + R = 32 + 32, max_pos 64).
+HF_PINS = {"tiny": (dict(V=512, d=128, L=2, H=2, ff=512, max_pos=64), 2, 16, 16),
+           "opt-125m": (dict(V=50272, d=768, L=12, H=12, ff=3072, max_pos=64), 1, 32, 32)}
+
+
+def hf_pins(fname="hf_opt_pins.npz"):
+    seed, prompt_seed = 7, 1000
+    fx = {}
+    for name, (arch, B, P, R) in HF_PINS.items():
+        S = P + R
+        actor = make_weights(arch, seed * 16 + 0, False)
+        tok = torch.zeros(B, S, dtype=torch.long)
+        for b in range(B):
+            for t in range(S):  # prompt ids for t < P; the "response" continues the same seeded stream
+                tok[b, t] = prompt_token(prompt_seed, b, t, arch["V"])
+        m = hf_opt(actor, arch)
+        with torch.no_grad():
+            z_hf = m(tok).logits
+            z_me = decoder(actor, tok, arch, r=lambda t: t) @ actor["tok"].T
+            err = (z_hf - z_me).abs().max().item()
+            assert err < 1e-4, f"{name}: OPT restatement differs from transformers by {err}"
+            hf_logp = torch.log_softmax(z_hf[:, P - 1:S - 1], -1).gather(-1, tok[:, P:, None])[..., 0]
+        fx[f"{name}/config"] = np.array([B, P, R, seed, prompt_seed, arch["max_pos"]])
+        fx[f"{name}/tokens"] = tok.numpy().astype(np.int32)
+        fx[f"{name}/hf_logp"] = hf_logp.numpy().astype(np.float32)
+        fx[f"{name}/hf_max_abs_logit_diff"] = np.array(err)
+        print(name, "restatement vs transformers max |dlogit|", err)
+    np.savez_compressed(os.path.join(HERE, fname), **fx)
 
 
 def run(arch, fname):
@@ -387,4 +459,5 @@ def run(arch, fname):
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+    hf_pins() if sys.argv[1:] == ["hf"] else main()

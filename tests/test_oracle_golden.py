@@ -126,3 +126,24 @@ def oracle_params(cfg):
     for (name, off, n), p in zip(named_slices(a), ps):
         flat[off:off + n] = p.detach().numpy().ravel()
     return flat
+
+
+# ---- OPT family pinned against transformers' OPTForCausalLM ------------------------------
+# tests/golden/hf_opt_pins.npz (make_golden.py hf): teacher-forced logprobs under the Actor's
+# seeded weights computed by HF itself in float64; the generator first checks its own torch
+# restatement against HF to < 1e-4 in the logits (stored: hf_max_abs_logit_diff).  The oracle
+# rounds to bf16 at the DESIGN.md §3 points, so it may differ from HF by that rounding spread.
+HF_OPT = os.path.join(GOLD_DIR, "hf_opt_pins.npz")
+
+
+@pytest.mark.parametrize("name,atol", [("tiny", 3e-2), ("opt-125m", 3.5e-2)])
+def test_opt_oracle_matches_transformers(name, atol):
+    pins = np.load(HF_OPT)
+    B, P, R, seed, pseed, mp = (int(x) for x in pins[f"{name}/config"])
+    assert float(pins[f"{name}/hf_max_abs_logit_diff"]) < 1e-4
+    cfg = make_config(name, name, B, P, R, seed=seed, prompt_seed=pseed)
+    assert cfg.actor.max_pos == mp
+    o = oracle_lib.ppo_step(cfg, tokens_in=pins[f"{name}/tokens"], stop_after=1)
+    err = np.abs(o["logp_old"] - pins[f"{name}/hf_logp"])
+    print(f"{name}: oracle vs transformers OPT logprobs max {err.max():.3e} mean {err.mean():.3e}")
+    np.testing.assert_allclose(o["logp_old"], pins[f"{name}/hf_logp"], atol=atol)
