@@ -118,11 +118,23 @@ typedef struct rlhf_engine_options {
                                  costmodel.hpp:48-50): 0 replicated (gradient all-reduce); 1 fp32
                                  master/m/v sharded 1/dp per rank (gradient reduce-scatter, AdamW on
                                  the shard, bf16 weight all-gather) — bit-identical updates */
-  int train_micro_batch;      /* samples per TrainFB micro-batch (LoopParams::micro_batches,
-                                 workload.hpp:25-40, as a size): forward + backward run per
-                                 micro-batch and the gradients accumulate; only one micro-batch's
-                                 activations are kept, which is what bounds the batch that fits.
-                                 0 = the rank's whole batch */
+  int train_micro_batch;      /* samples per TrainFB chunk: forward + backward run per chunk and
+                                 the gradients accumulate; only one chunk's activations are kept,
+                                 which is what bounds the batch that fits.  0 = a whole TrainFB
+                                 micro-batch */
+  /* ---- LoopParams (workload.hpp:25-40) and StrategyConfig (scenario.hpp:12-26) fields;
+   * zero-initialised options mean the reference defaults ---- */
+  int micro_batches;          /* LoopParams::micro_batches: the task DAG's Generation / Forward /
+                                 TrainFB micro-batches (workload.cpp:145-163); 0 -> 1 */
+  int rollout_nums;           /* LoopParams::rollout_nums: Generation+Forward rounds per step, each
+                                 on new prompts (ids r*G + ...); 0 -> 1 */
+  int ppo_epochs;             /* LoopParams::ppo_epochs: TrainFB passes over the experience, one
+                                 AdamW step each; 0 -> 1 */
+  double inference_ratio;     /* DisaggregatedOptions::inference_ratio (placement.hpp:54-58); 0 -> 0.5 */
+  int tp_gen;                 /* DisaggregatedOptions::tp_gen; must be <= 1 (tensor-parallel shadow
+                                 generation is not executed) */
+  double ratios[4];           /* strategy "ratio_vector": PlacementRatioVector fractions of
+                                 {Actor, Critic, Ref, Reward} (placement.hpp:29-46); 0 = omitted */
 } rlhf_engine_options;
 
 int rlhf_nccl_unique_id(uint8_t out[128]);
@@ -141,11 +153,45 @@ typedef struct rlhf_step_report {
   double actor_loss, critic_loss;
   double mean_score, mean_kl;
   int gpu_launches;                    /* kernels this rank launched in the step */
+  /* ---- the remaining SimReport fields, measured on this rank (simulator.hpp:30-44) ---- */
+  double busy_seconds;                 /* union of this rank's compute-lane intervals */
+  double bubble_fraction;              /* 1 - busy_seconds / step_seconds (idle compute lanes) */
+  double comm_seconds;                 /* union of this rank's comm-lane intervals */
+  double mem_peak_bytes;               /* device bytes the engine holds on this rank */
+  int busiest_stage;                   /* argmax stage_seconds */
+  int n_events;                        /* intervals recorded (rlhf_engine_events) */
+  int feasible;                        /* validate_plan of the executed placement with the real
+                                          parameter counts (analytic memory model, 95 % cap) */
 } rlhf_step_report;
 
-/* One PPO iteration (generation -> forward x4 -> GAE -> train -> sync).
- * prompts_host: [batch, prompt_len] int32 for this rank's shard, or NULL to use
- * the seeded synthetic prompts.  stream: cudaStream_t (NULL = engine stream). */
+/* One measured interval of the last step (SimEvent, simulator.hpp:18-28).
+ * kind: 0 Generation, 1 Forward, 2 TrainFB, 3 Collective (exchanges, gradient
+ * sync), 4 ParamSync, 6 experience buffer (rewards + GAE), 7 AdamW.
+ * lane: 0 main compute stream, 1 side compute stream, 2 comm stream.
+ * stage: Stage (0 generation, 1 forward, 2 training, 3 sync). */
+typedef struct rlhf_event {
+  int task, kind, model, micro_batch, rollout, epoch, lane, comm_op, stage;
+  double start, end;      /* seconds from the step's start */
+} rlhf_event;
+
+/* Copy up to max events of the last step; returns the count (or -status). */
+int rlhf_engine_events(rlhf_engine* e, rlhf_event* out, int max);
+
+/* The executed plan (execplan.hpp) as JSON: row sets, model -> set, the task DAG,
+ * the derived comm schedule and every exchange step with its row transfers.
+ * Writes up to out_len bytes (NUL-terminated); *needed = full length + 1. */
+int rlhf_exec_plan_json(const char* strategy, int world, int batch_per_rank, int prompt_len, int gen_len,
+                        int micro_batches, int rollout_nums, int ppo_epochs, double inference_ratio,
+                        const double* ratios4, char* out, int out_len, int* needed);
+
+/* One PPO iteration: the task DAG of task_graph (workload.cpp:109-175) --
+ * rollout_nums x micro_batches of Generation -> Forward per scorer, the
+ * experience barrier (rewards + GAE), ppo_epochs x micro_batches of TrainFB
+ * with one AdamW step per epoch, ParamSync to the shadows -- plus the exchanges
+ * the placement's comm schedule induces.  prompts_host: [rollout_nums * batch,
+ * prompt_len] int32 for this rank's home shard (rollout-major), or NULL to use
+ * the seeded synthetic prompts.  Launches on the engine's streams; returns
+ * after the step completed (rlhf_engine_stream() is the stream that brackets it). */
 int rlhf_engine_step(rlhf_engine* e, const int32_t* prompts_host, rlhf_step_report* rep);
 
 /* Copy a named engine tensor to host (parity tests).  Names: "tokens" int32

@@ -511,8 +511,8 @@ extern "C" int oracle_forward_hidden(const rlhf_arch* arch, uint64_t model_seed,
   return 0;
 }
 
-extern "C" int oracle_ppo_step(const rlhf_ppo_config* cfg_in, const int32_t* tokens_in, int32_t* greedy_pred,
-                               int stop_after, int n_threads, oracle_ppo_outputs* out) {
+extern "C" int oracle_ppo_step_epochs(const rlhf_ppo_config* cfg_in, int ppo_epochs, const int32_t* tokens_in,
+                                      int32_t* greedy_pred, int stop_after, int n_threads, oracle_ppo_outputs* out) {
   if (n_threads > 0) omp_set_num_threads(n_threads);
   rlhf_ppo_config cfg = *cfg_in;
   cfg.actor.scalar_head = 0;
@@ -606,8 +606,12 @@ extern "C" int oracle_ppo_step(const rlhf_ppo_config* cfg_in, const int32_t* tok
 
   const float N = cfg.loss_denominator > 0 ? cfg.loss_denominator : static_cast<float>(B * R);
 
-  // ---- TrainFB(Actor): clipped PPO policy loss ----------------------------
-  {
+  // ---- TrainFB(Actor): clipped PPO policy loss, ppo_epochs passes over the experience
+  // (one AdamW step each; the next pass runs on the bf16 copy of the updated master) ----
+  Vec a_master = actor.w, a_m(a_master.size(), 0.0f), a_v(a_master.size(), 0.0f);
+  for (int epoch = 0; epoch < ppo_epochs; ++epoch) {
+    if (epoch > 0)
+      for (size_t i = 0; i < actor.w.size(); ++i) actor.w[i] = bfr(a_master[i]);
     Saved sv;
     Cache c;
     c.init(actor.a.n_layers, B, S, actor.a.d_model);
@@ -659,13 +663,15 @@ extern "C" int oracle_ppo_step(const rlhf_ppo_config* cfg_in, const int32_t* tok
     }
     backward(actor, tok.data(), B, S, sv, dhf, grad);
     put(out->actor_grad, grad);
-    Vec master = actor.w, m(master.size(), 0.0f), v(master.size(), 0.0f);
-    adamw(master, m, v, grad, cfg.lr_actor, cfg, 1);
-    put(out->actor_master, master);
+    adamw(a_master, a_m, a_v, grad, cfg.lr_actor, cfg, epoch + 1);
+    put(out->actor_master, a_master);
   }
 
-  // ---- TrainFB(Critic): clipped value loss --------------------------------
-  {
+  // ---- TrainFB(Critic): clipped value loss, ppo_epochs passes ------------------
+  Vec c_master = critic.w, c_m(c_master.size(), 0.0f), c_v(c_master.size(), 0.0f);
+  for (int epoch = 0; epoch < ppo_epochs; ++epoch) {
+    if (epoch > 0)
+      for (size_t i = 0; i < critic.w.size(); ++i) critic.w[i] = bfr(c_master[i]);
     Saved sv;
     Cache c;
     c.init(critic.a.n_layers, B, S, critic.a.d_model);
@@ -703,9 +709,13 @@ extern "C" int oracle_ppo_step(const rlhf_ppo_config* cfg_in, const int32_t* tok
       }
     backward(critic, tok.data(), B, S, sv, dhf, grad);
     put(out->critic_grad, grad);
-    Vec master = critic.w, m(master.size(), 0.0f), v(master.size(), 0.0f);
-    adamw(master, m, v, grad, cfg.lr_critic, cfg, 1);
-    put(out->critic_master, master);
+    adamw(c_master, c_m, c_v, grad, cfg.lr_critic, cfg, epoch + 1);
+    put(out->critic_master, c_master);
   }
   return 0;
+}
+
+extern "C" int oracle_ppo_step(const rlhf_ppo_config* cfg, const int32_t* tokens_in, int32_t* greedy_pred,
+                               int stop_after, int n_threads, oracle_ppo_outputs* out) {
+  return oracle_ppo_step_epochs(cfg, 1, tokens_in, greedy_pred, stop_after, n_threads, out);
 }

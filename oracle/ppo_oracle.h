@@ -58,6 +58,14 @@ typedef struct oracle_ppo_outputs {
 int oracle_ppo_step(const rlhf_ppo_config* cfg, const int32_t* tokens_in, int32_t* greedy_pred,
                     int stop_after, int n_threads, oracle_ppo_outputs* out);
 
+/* The same with ppo_epochs TrainFB passes over the experience (one AdamW step per pass,
+ * each pass on the bf16 copy of the previous pass's master): logp_new / values_new /
+ * losses / grads are those of the last pass, masters after it.  A batch of B samples
+ * with prompt ids sample_offset + [0, B) equals rollout_nums rollouts of B / rollout_nums
+ * (the engine's rollout r uses ids r * G + ...). */
+int oracle_ppo_step_epochs(const rlhf_ppo_config* cfg, int ppo_epochs, const int32_t* tokens_in, int32_t* greedy_pred,
+                           int stop_after, int n_threads, oracle_ppo_outputs* out);
+
 /* Teacher-forced forward of one model over tokens [B,S]: final-LN hidden
  * states hf [B,S,d] (bf16-rounded values as fp32) — building block checks. */
 int oracle_forward_hidden(const rlhf_arch* arch, uint64_t model_seed, const int32_t* tokens, int B,

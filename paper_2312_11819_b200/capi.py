@@ -31,7 +31,9 @@ class PPOConfig(C.Structure):
 class EngineOptions(C.Structure):
     _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world_size", C.c_int), ("strategy", C.c_char_p),
                 ("nccl_id", C.POINTER(C.c_uint8)), ("use_cuda_graph", C.c_int), ("zero_stage", C.c_int),
-                ("train_micro_batch", C.c_int)]
+                ("train_micro_batch", C.c_int), ("micro_batches", C.c_int), ("rollout_nums", C.c_int),
+                ("ppo_epochs", C.c_int), ("inference_ratio", C.c_double), ("tp_gen", C.c_int),
+                ("ratios", C.c_double * 4)]
 
 
 class StepReport(C.Structure):
@@ -39,7 +41,16 @@ class StepReport(C.Structure):
                 ("stage_seconds", C.c_double * 4), ("decode_seconds", C.c_double),
                 ("prefill_seconds", C.c_double), ("comm_bytes_total", C.c_double),
                 ("actor_loss", C.c_double), ("critic_loss", C.c_double), ("mean_score", C.c_double),
-                ("mean_kl", C.c_double), ("gpu_launches", C.c_int)]
+                ("mean_kl", C.c_double), ("gpu_launches", C.c_int), ("busy_seconds", C.c_double),
+                ("bubble_fraction", C.c_double), ("comm_seconds", C.c_double), ("mem_peak_bytes", C.c_double),
+                ("busiest_stage", C.c_int), ("n_events", C.c_int), ("feasible", C.c_int)]
+
+
+class Event(C.Structure):
+    """rlhf_event: one measured interval of the last step (SimEvent, simulator.hpp:18-28)."""
+    _fields_ = [("task", C.c_int), ("kind", C.c_int), ("model", C.c_int), ("micro_batch", C.c_int),
+                ("rollout", C.c_int), ("epoch", C.c_int), ("lane", C.c_int), ("comm_op", C.c_int),
+                ("stage", C.c_int), ("start", C.c_double), ("end", C.c_double)]
 
 
 # Named shapes (SURVEY.md §8 model table); max_pos is set per pipeline.
@@ -191,3 +202,21 @@ def prompt_tokens(seed: int, batch: int, prompt_len: int, vocab: int, sample_off
     with np.errstate(over="ignore"):
         z = splitmix(splitmix(np.uint64(seed) ^ np.uint64(0xA5A5A5A5)) + b * np.uint64(1000003) + t)
     return (z % np.uint64(vocab)).astype(np.int32)
+
+
+def exec_plan(strategy: str, world: int, batch_per_rank: int, prompt_len: int, gen_len: int, micro_batches: int = 1,
+              rollout_nums: int = 1, ppo_epochs: int = 1, inference_ratio: float = 0.5, ratios=None) -> dict:
+    """The executed plan (csrc/host/execplan.hpp) the engine walks: row sets, model -> set, the
+    task DAG, the derived comm schedule and every exchange step's row transfers (JSON)."""
+    import json
+    L = lib()
+    L.rlhf_exec_plan_json.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.c_double, C.POINTER(C.c_double), C.c_char_p, C.c_int, C.POINTER(C.c_int)]
+    r4 = (C.c_double * 4)(*ratios) if ratios is not None else None
+    need = C.c_int(0)
+    args = (strategy.encode(), world, batch_per_rank, prompt_len, gen_len, micro_batches, rollout_nums, ppo_epochs,
+            inference_ratio, r4)
+    check(L.rlhf_exec_plan_json(*args, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check(L.rlhf_exec_plan_json(*args, buf, need.value, C.byref(need)))
+    return json.loads(buf.value.decode())

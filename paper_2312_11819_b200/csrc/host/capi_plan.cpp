@@ -1,10 +1,12 @@
 // C-ABI over the host placement / workload API (include/rlhf_engine.h).
 // Pure host logic: no device calls.
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
 
 #include "capi_util.hpp"
+#include "execplan.hpp"
 #include "flexrlhf/placement.hpp"
 #include "rlhf_engine.h"
 
@@ -204,5 +206,32 @@ extern "C" int rlhf_validate_plan(const char* strategy, int n_devices, int zero_
     return 0;
   } catch (const std::exception& e) {
     return capi_status(e);
+  }
+}
+
+extern "C" int rlhf_exec_plan_json(const char* strategy, int world, int batch_per_rank, int prompt_len, int gen_len,
+                                   int micro_batches, int rollout_nums, int ppo_epochs, double inference_ratio,
+                                   const double* ratios4, char* out, int out_len, int* needed) {
+  try {
+    StrategyConfig sc;
+    sc.name = strategy ? strategy : "colocated";
+    sc.inference_ratio = inference_ratio > 0 ? inference_ratio : 0.5;
+    sc.tp_gen = 1;
+    const ModelName order[4] = {ModelName::Actor, ModelName::Critic, ModelName::Ref, ModelName::Reward};
+    if (ratios4)
+      for (int i = 0; i < 4; ++i)
+        if (ratios4[i] > 0) sc.ratios.push_back({order[i], ratios4[i]});
+    const ExecPlan e = build_exec_plan(sc, world, batch_per_rank, prompt_len, gen_len, std::max(1, micro_batches),
+                                       std::max(1, rollout_nums), std::max(1, ppo_epochs));
+    const std::string js = to_json(e);
+    if (needed) *needed = static_cast<int>(js.size()) + 1;
+    if (out && out_len > 0) {
+      const size_t n = std::min(js.size(), static_cast<size_t>(out_len - 1));
+      std::memcpy(out, js.data(), n);
+      out[n] = 0;
+    }
+    return 0;
+  } catch (const std::exception& ex) {
+    return capi_status(ex);
   }
 }

@@ -1,27 +1,21 @@
-// engine.cpp — the PPO iteration driver and its C-ABI (include/rlhf_engine.h).
+// engine.cpp — the PPO iteration executor and its C-ABI (include/rlhf_engine.h).
 //
-// Walks the reference's one-iteration stage DAG (task_graph,
-// /root/reference/proj/src/workload.cpp:109-175): Generation -> Forward for
-// every scorer model -> experience-buffer barrier (GAE) -> TrainFB(Actor),
-// TrainFB(Critic) -> (shadows) ParamSync.  Each stage is timed with CUDA events
-// and reported in the reference's SimReport vocabulary (simulator.hpp:30-44).
+// The executor walks an ExecPlan (execplan.hpp): the reference's one-iteration stage DAG
+// (task_graph, /root/reference/proj/src/workload.cpp:109-175 -- rollout_nums x
+// micro_batches of Generation -> Forward per scorer, the experience-buffer barrier,
+// ppo_epochs x micro_batches of TrainFB, ParamSync + Barrier under shadows) interleaved
+// with the exchanges the placement's comm schedule induces (derive_comm_schedule,
+// placement.hpp:101-102).  Each step runs only on the ranks that take
+// part in it; every rank walks the same list, so NCCL calls pair up.
 //
-// One process per GPU.  The rank's role comes from the placement plan
-// (build_strategy over ClusterTopology::b200_box(world)): which models it hosts,
-// its data-parallel groups, and the partner rank (i <-> i + N/2) it exchanges
-// experience with -- the executed form of derive_comm_schedule
-// (placement.hpp:101-102):
-//   colocated     every model everywhere; gradient all-reduce over the world
-//   interleaving1 Actor/Critic everywhere, Ref on the first half, Reward on the
-//                 second: AllGather of (query,response) within the pair, each
-//                 side scores 2*Bg samples, AlltoAll of the outputs back
-//   interleaving2 {Actor, Ref} on the first half, {Critic, Reward} on the second:
-//                 the Actor side generates the pair's 2*Bg samples, tokens go
-//                 over, outputs are swapped, Actor and Critic train concurrently
-//   disaggregated {Actor, Critic} trainers on the first half, {ShadowActor,
-//                 ShadowCritic, Ref, Reward} on the second: inference side
-//                 generates + scores, sends experience to the trainers, trainers
-//                 send updated weights back (ParamSync) after training.
+// Streams ("lanes"): 0 main compute, 1 side compute (the Critic-shaped models on ranks
+// that also host the Actor-shaped ones, with their own activation arena), 2 comm (every
+// NCCL call and every row exchange, so no two collectives ever run concurrently).  A step
+// waits only for the events of the DAG steps it depends on that ran on another lane of
+// this rank; cross-rank ordering is carried by the exchanges themselves.  Every executed
+// interval is bracketed by CUDA events and reported in SimReport's vocabulary
+// (simulator.hpp:18-44): per-stage seconds with compute-lane attribution, busy time,
+// bubble fraction, the event list.
 #include "engine.hpp"
 
 #include <algorithm>
@@ -53,6 +47,8 @@ namespace flexrlhf {
 
 namespace {
 
+constexpr int kEvExperience = 6, kEvAdam = 7;
+
 rlhf_arch fixed(rlhf_arch a, int scalar_head) {
   a.scalar_head = scalar_head;
   return a;
@@ -73,75 +69,153 @@ void validate(const rlhf_ppo_config& c) {
   if (c.prompt_len % 8 || S % 8) throw ConfigError("prompt_len and prompt_len+gen_len must be multiples of 8");
 }
 
-bool in(const std::vector<int>& v, int x) { return std::find(v.begin(), v.end(), x) != v.end(); }
+bool actor_shaped(ModelName m) { return m == ModelName::Actor || m == ModelName::Ref || m == ModelName::ShadowActor; }
+
+size_t field_row_bytes(Field f, int S, int R) {
+  switch (f) {
+    case Field::Prompt:
+    case Field::Tokens: return static_cast<size_t>(S) * 4;
+    case Field::Score: return 4;
+    default: return static_cast<size_t>(R) * 4;
+  }
+}
 
 }  // namespace
+
+void* RowBufs::field(Field f) const {
+  switch (f) {
+    case Field::Prompt:
+    case Field::Tokens: return tokens.p;
+    case Field::LogpOld: return logp_old.p;
+    case Field::LogpRef: return logp_ref.p;
+    case Field::Values: return values.p;
+    case Field::Score: return score.p;
+  }
+  return nullptr;
+}
+
+Decoder* Engine::model(ModelName m) {
+  switch (m) {
+    case ModelName::Actor: return &actor_;
+    case ModelName::Critic: return &critic_;
+    case ModelName::Ref: return &ref_;
+    case ModelName::Reward: return &reward_;
+    case ModelName::ShadowActor: return &shadow_actor_;
+    case ModelName::ShadowCritic: return &shadow_critic_;
+  }
+  return nullptr;
+}
+
+int Engine::lane_of(ModelName m) const { return side_ && !actor_shaped(m) ? 1 : 0; }
+
+void Engine::use_lane(int l) {
+  cur_lane_ = l;
+  stream_ = lane_[l];
+  arp_ = l == 1 ? &ar_side_ : &ar_main_;
+}
+
+cudaEvent_t Engine::take_event() {
+  if (ev_next_ == ev_pool_.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ev_pool_.push_back(e);
+  }
+  return ev_pool_[ev_next_++];
+}
 
 Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg_(cfg), opt_(opt) {
   validate(cfg_);
   if (opt_.zero_stage < 0 || opt_.zero_stage > 1)
-    throw ConfigError("zero_stage must be 0 or 1 (ZeRO-2/3 are planned, DESIGN.md §8)");
+    throw ConfigError("zero_stage must be 0 or 1 (ZeRO-2/3 are not executed)");
   cfg_.actor.scalar_head = 0;
   cfg_.critic.scalar_head = 1;
   strategy_ = opt.strategy ? opt.strategy : "colocated";
   opt_.strategy = nullptr;
   rank_ = opt_.rank;
   world_n_ = std::max(1, opt_.world_size);
+  if (rank_ < 0 || rank_ >= world_n_) throw ConfigError("rank outside [0, world_size)");
   Bg_ = cfg_.batch;
   P_ = cfg_.prompt_len;
   R_ = cfg_.gen_len;
   S_ = P_ + R_;
 
-  // ---- role of this rank from the placement plan -------------------------------
+  // ---- the executed plan: placement, task DAG, comm schedule, sample ownership ----
   {
-    ModelSizes sz;
-    sz.actor = ArchSpec{}.param_count(false);  // sizes only matter for memory planning
-    sz.critic = sz.ref = sz.reward = sz.actor;
-    LoopParams lp;
-    lp.batch_size = Bg_ * world_n_;
-    lp.prompt_len = P_;
-    lp.gen_len = R_;
     StrategyConfig sc;
     sc.name = strategy_;
-    sc.tp_gen = 1;
-    sc.inference_ratio = 0.5;
-    const BuiltStrategy bs = build_strategy(sc, ClusterTopology::b200_box(world_n_),
-                                            build_pipeline(PipelineStructure::ACNonShare, sz, lp));
-    plan_ = bs.plan;
-    for (int m = 0; m < 6; ++m) {
-      const ModelName mn = static_cast<ModelName>(m);
-      hosts_[m] = plan_.has(mn) && in(plan_.cfg(mn).devices, rank_);
-    }
-    tag_ = plan_.strategy_tag;
-    if (tag_ != StrategyTag::Colocated && world_n_ % 2) throw ConfigError(strategy_ + " needs an even number of GPUs");
-    partner_ = tag_ == StrategyTag::Colocated ? -1 : (rank_ < world_n_ / 2 ? rank_ + world_n_ / 2 : rank_ - world_n_ / 2);
+    sc.zero_level = opt_.zero_stage;
+    sc.inference_ratio = opt_.inference_ratio > 0 ? opt_.inference_ratio : 0.5;
+    sc.tp_gen = opt_.tp_gen > 0 ? opt_.tp_gen : 1;
+    const ModelName order[4] = {ModelName::Actor, ModelName::Critic, ModelName::Ref, ModelName::Reward};
+    for (int i = 0; i < 4; ++i)
+      if (opt_.ratios[i] > 0) sc.ratios.push_back({order[i], opt_.ratios[i]});
+    ModelSizes sz;
+    sz.actor = sz.ref = static_cast<double>(rlhf_param_total(&cfg_.actor));
+    sz.critic = sz.reward = static_cast<double>(rlhf_param_total(&cfg_.critic));
+    xp_ = build_exec_plan(sc, world_n_, Bg_, P_, R_, std::max(1, opt_.micro_batches), std::max(1, opt_.rollout_nums),
+                          std::max(1, opt_.ppo_epochs), sz);
+    tag_ = xp_.tag;
+    for (int m = 0; m < 6; ++m) hosts_[m] = xp_.hosts(rank_, static_cast<ModelName>(m));
   }
-  const bool pair_batch = tag_ == StrategyTag::Interleaving2 || tag_ == StrategyTag::Disaggregated;
-  Bcap_ = (tag_ == StrategyTag::Colocated) ? Bg_ : 2 * Bg_;
-  train_mb_ = opt_.train_micro_batch > 0 ? std::min(opt_.train_micro_batch, Bcap_) : Bcap_;
-  gen_B_ = pair_batch ? 2 * Bg_ : Bg_;
+  int train_per = 0;
+  for (int m = 0; m < 6; ++m) {
+    if (!hosts_[m]) continue;
+    const int per = xp_.sets[xp_.set_of[m]].per;
+    Bcap_ = std::max(Bcap_, per);
+    if (m <= 1) train_per = std::max(train_per, per);
+  }
+  Bcap_ = std::max(Bcap_, 1);
+  gen_B_ = xp_.hosts(rank_, xp_.generator) ? xp_.sets[xp_.set_of[static_cast<int>(xp_.generator)]].per : 0;
+  train_mb_ = std::max(1, opt_.train_micro_batch > 0 ? std::min(opt_.train_micro_batch, std::max(1, train_per))
+                                                      : train_per);
 
   CK(cudaSetDevice(opt_.device));
-  CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  for (auto& e : ev_) CK(cudaEventCreate(&e));
+  for (auto& l : lane_) CK(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking));
+  use_lane(0);
+  CK(cudaEventCreate(&ev_begin_));
+  CK(cudaEventCreate(&ev_end_));
 
-  // ---- communicators: world + one data-parallel group per trainable model -----
+  // ---- communicators: world, the data-parallel group of each trained model, ParamSync pairs
   if (world_n_ > 1) {
     if (!opt_.nccl_id) throw ConfigError("world_size > 1 needs an NCCL unique id");
     ncclUniqueId id;
     std::memcpy(&id, opt_.nccl_id, sizeof(id));
     NK(nccl().CommInitRank(&world_, world_n_, id, rank_));
     auto split = [&](ModelName m, ncclComm_t* out) {
-      const std::vector<int>& g = plan_.cfg(m).devices;
-      const int color = in(g, rank_) ? 1 : NCCL_SPLIT_NOCOLOR;
-      NK(nccl().CommSplit(world_, color, rank_, out, nullptr));
-      if (!in(g, rank_) || g.size() < 2) {  // nothing to all-reduce with
+      *out = nullptr;
+      if (!xp_.plan.has(m)) {  // every rank takes part in every split (collective)
+        ncclComm_t c = nullptr;
+        NK(nccl().CommSplit(world_, NCCL_SPLIT_NOCOLOR, rank_, &c, nullptr));
+        return;
+      }
+      const std::vector<int>& g = xp_.plan.cfg(m).devices;
+      const bool member = std::find(g.begin(), g.end(), rank_) != g.end();
+      NK(nccl().CommSplit(world_, member ? 1 : NCCL_SPLIT_NOCOLOR, rank_, out, nullptr));
+      if (!member || g.size() < 2) {  // nothing to reduce with
         if (*out) nccl().CommDestroy(*out);
         *out = nullptr;
       }
     };
     split(ModelName::Actor, &actor_comm_);
     split(ModelName::Critic, &critic_comm_);
+    // ParamSync (workload.cpp:164-172): shadow member j receives from trainer member
+    // j % |trainers| by broadcast over the {trainer, its shadows} communicator
+    const std::pair<ModelName, ModelName> pairs[2] = {{ModelName::Actor, ModelName::ShadowActor},
+                                                      {ModelName::Critic, ModelName::ShadowCritic}};
+    for (int k = 0; k < 2; ++k) {
+      const auto [src, dst] = pairs[k];
+      int color = NCCL_SPLIT_NOCOLOR, key = rank_;
+      if (xp_.plan.has(dst) && xp_.plan.has(src)) {
+        const std::vector<int>& tg = xp_.plan.cfg(src).devices;
+        const std::vector<int>& sg = xp_.plan.cfg(dst).devices;
+        for (size_t i = 0; i < tg.size(); ++i)
+          if (tg[i] == rank_) color = static_cast<int>(i), key = 0;
+        for (size_t j = 0; j < sg.size(); ++j)
+          if (sg[j] == rank_) color = static_cast<int>(j % tg.size()), key = 1 + static_cast<int>(j);
+      }
+      NK(nccl().CommSplit(world_, color, key, &sync_comm_[k], nullptr));
+      sync_root_[k] = 0;  // the trainer has the lowest key
+    }
   }
   opt_.nccl_id = nullptr;
 
@@ -153,32 +227,30 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
   if (hosts_[4]) init_decoder(shadow_actor_, fixed(cfg_.actor, 0), rlhf_model_seed(cfg_.seed, 0), false);
   if (hosts_[5]) init_decoder(shadow_critic_, fixed(cfg_.critic, 1), rlhf_model_seed(cfg_.seed, 1), false);
 
-  // ---- activation arenas: the main one, plus a forward-only one for the second
-  // stream of the Co-located Forward stage (Critic + Reward beside Actor + Ref)
-  build_arena(ar_main_, hosts_[0] || hosts_[1]);
-  if (tag_ == StrategyTag::Colocated) {
-    // Critic-shaped arena for the second stream (Critic/Reward forwards, Critic training);
-    // when it does not fit (long sequences, large models) the step stays single-stream
+  // ---- activation arenas: main lane, plus a Critic-shaped one for the side lane when this
+  // rank hosts both an Actor-shaped and a Critic-shaped model and it fits
+  const bool trains = hosts_[0] || hosts_[1];
+  build_arena(ar_main_, trains);
+  const bool a_shaped = hosts_[0] || hosts_[2] || hosts_[4], c_shaped = hosts_[1] || hosts_[3] || hosts_[5];
+  if (a_shaped && c_shaped) {
     try {
-      build_arena(ar_side_, true, true);
+      build_arena(ar_side_, hosts_[1], true);
       // keep room for the generation state allocated next (KV cache + decode buffers)
-      const size_t kv = 2ull * cfg_.actor.n_layers * gen_B_ * S_ * cfg_.actor.d_model * 2;
+      const size_t kv = 2ull * cfg_.actor.n_layers * std::max(gen_B_, 1) * S_ * cfg_.actor.d_model * 2;
       size_t free_b = 0, total_b = 0;
       CK(cudaMemGetInfo(&free_b, &total_b));
-      if (free_b < kv + (4ull << 30)) throw DeviceError("second-stream arena leaves too little memory");
-      CK(cudaStreamCreateWithFlags(&stream_side_, cudaStreamNonBlocking));
-    } catch (const DeviceError&) {
+      if (free_b < kv + (4ull << 30)) throw InfeasibleError("side-lane arena leaves too little memory");
+      side_ = true;
+    } catch (const InfeasibleError&) {  // the step stays on one compute lane
       for (DevBuf* b : ar_side_.owned) delete b;
       ar_side_.owned.clear();
       cudaGetLastError();
-      stream_side_ = nullptr;
+      side_ = false;
     }
   }
 
-  // ---- generation state (the generator: Actor or ShadowActor) -----------------
-  if (hosts_[0] && tag_ != StrategyTag::Disaggregated) generator_ = &actor_;
-  if (hosts_[4]) generator_ = &shadow_actor_;
-  if (tag_ == StrategyTag::Interleaving2 && !hosts_[0]) generator_ = nullptr;
+  // ---- generation state (the generator: Actor or ShadowActor) ----
+  if (gen_B_ > 0) generator_ = model(xp_.generator);
   if (generator_) {
     kv_.L = cfg_.actor.n_layers;
     kv_.B = gen_B_;
@@ -200,31 +272,99 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
     dec_logits_.alloc(static_cast<size_t>(gen_B_) * cfg_.actor.vocab * 4);
     dec_top2_.alloc(static_cast<size_t>((cfg_.actor.vocab + 127) / 128) * gen_B_ * 16);
     argmax_ws_.alloc(static_cast<size_t>(gen_B_) * 64 * 4 * 4);
+    gen_tok_.alloc(static_cast<size_t>(gen_B_) * S_ * 4);
+    pred_.alloc(static_cast<size_t>(gen_B_) * S_ * 4);
+    margin_.alloc(static_cast<size_t>(gen_B_) * S_ * 4);
   }
   pos_.alloc(16);
-
-  const size_t bs = static_cast<size_t>(Bcap_) * S_, br = static_cast<size_t>(Bcap_) * R_;
-  tokens_.alloc(bs * 4);
-  tok2_.alloc(bs * 4);
-  pred_.alloc(bs * 4);
-  margin_.alloc(bs * 4);
-  prompt_stage_.alloc(static_cast<size_t>(Bg_) * P_ * 4);
-  for (DevBuf* b : {&logp_old_, &logp_ref_, &values_, &rewards_, &adv_, &ret_, &logp_new_, &values_new_, &gbuf_, &gbuf2_,
-                    &out2_})
-    b->alloc(br * 4);
-  score_.alloc(static_cast<size_t>(Bcap_) * 4);
-  score2_.alloc(static_cast<size_t>(Bcap_) * 4);
   loss_.alloc(16);
 
-  // global sample id of every row this rank holds (experience rows)
-  sample_ids_.assign(static_cast<size_t>(Bcap_), -1);
-  const int lo = std::min(rank_, partner_ < 0 ? rank_ : partner_), hi = std::max(rank_, partner_ < 0 ? rank_ : partner_);
-  if (tag_ == StrategyTag::Colocated || tag_ == StrategyTag::Interleaving1) {
-    for (int b = 0; b < Bg_; ++b) sample_ids_[b] = rank_ * Bg_ + b;
-  } else {
-    for (int b = 0; b < Bg_; ++b) {
-      sample_ids_[b] = lo * Bg_ + b;
-      sample_ids_[Bg_ + b] = hi * Bg_ + b;
+  // ---- row sets this rank belongs to; home prompt rows ----
+  rs_.reset(new RowBufs[xp_.sets.size()]);
+  for (size_t s = 0; s < xp_.sets.size(); ++s) {
+    if (xp_.member_index(static_cast<int>(s), rank_) < 0) continue;
+    RowBufs& b = rs_[s];
+    b.rows = xp_.sets[s].rows;
+    const size_t rr = static_cast<size_t>(b.rows) * R_ * 4;
+    b.tokens.alloc(static_cast<size_t>(b.rows) * S_ * 4);
+    b.logp_old.alloc(rr);
+    b.logp_ref.alloc(rr);
+    b.values.alloc(rr);
+    b.score.alloc(static_cast<size_t>(b.rows) * 4);
+    b.trainer = (hosts_[0] && xp_.set_of[0] == static_cast<int>(s)) || (hosts_[1] && xp_.set_of[1] == static_cast<int>(s));
+    if (b.trainer)
+      for (DevBuf* d : {&b.rewards, &b.adv, &b.ret, &b.logp_new, &b.values_new, &b.gbuf, &b.gbuf2}) d->alloc(rr);
+  }
+  home_.alloc(static_cast<size_t>(xp_.rollouts) * Bg_ * S_ * 4);
+
+  // ---- per-step dependencies (indices into xp_.steps; rank-independent) ----
+  const int ns = static_cast<int>(xp_.steps.size());
+  deps_.assign(ns, {});
+  step_lane_.assign(ns, -1);
+  step_done_.resize(ns);
+  for (auto& e : step_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  std::map<std::pair<int, int>, int> gen_of, before_of;
+  std::map<std::pair<int, int>, std::vector<int>> fwds_of;
+  std::map<std::pair<int, int>, int> prompt_of;
+  std::vector<int> all_fwd, all_after, all_exp;
+  std::map<std::pair<int, int>, std::vector<int>> train_of;  // (model, epoch)
+  std::map<std::pair<int, int>, int> opt_of;
+  for (int i = 0; i < ns; ++i) {
+    const ExecStep& s = xp_.steps[i];
+    const auto key = std::make_pair(s.rollout, s.mb);
+    std::vector<int>& d = deps_[i];
+    if (s.kind == StepKind::Exchange) {
+      const bool prompt = !s.moves.empty() && s.moves[0].field == Field::Prompt;
+      if (prompt) {
+        prompt_of[key] = i;
+      } else if (s.attach == AttachKind::Before) {
+        d.push_back(gen_of[key]);
+        before_of[key] = i;
+      } else {
+        d.push_back(gen_of[key]);
+        d.insert(d.end(), fwds_of[key].begin(), fwds_of[key].end());
+        all_after.push_back(i);
+      }
+      continue;
+    }
+    if (s.kind == StepKind::Experience) {
+      d = all_fwd;
+      d.insert(d.end(), all_after.begin(), all_after.end());
+      for (auto& [k, g] : gen_of) d.push_back(g);
+      all_exp.push_back(i);
+      continue;
+    }
+    if (s.kind == StepKind::OptimizerStep) {
+      d = train_of[{static_cast<int>(s.model), s.epoch}];
+      opt_of[{static_cast<int>(s.model), s.epoch}] = i;
+      continue;
+    }
+    const StageTask& t = xp_.tasks[s.task];
+    switch (t.kind) {
+      case TaskKind::Generation:
+        if (prompt_of.count(key)) d.push_back(prompt_of[key]);
+        gen_of[key] = i;
+        break;
+      case TaskKind::Forward:
+        d.push_back(gen_of[key]);
+        if (before_of.count(key)) d.push_back(before_of[key]);
+        fwds_of[key].push_back(i);
+        all_fwd.push_back(i);
+        break;
+      case TaskKind::TrainFB:
+        d = all_exp;
+        if (t.epoch_index > 0 && opt_of.count({static_cast<int>(t.model), t.epoch_index - 1}))
+          d.push_back(opt_of[{static_cast<int>(t.model), t.epoch_index - 1}]);
+        train_of[{static_cast<int>(t.model), t.epoch_index}].push_back(i);
+        break;
+      case TaskKind::ParamSync: {
+        const int src = t.model == ModelName::ShadowActor ? 0 : 1;
+        const auto it = opt_of.find({src, xp_.epochs - 1});
+        if (it != opt_of.end()) d.push_back(it->second);
+        break;
+      }
+      default:
+        break;
     }
   }
   CK(cudaDeviceSynchronize());
@@ -232,97 +372,137 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
 
 Engine::~Engine() {
   if (decode_graph_) cudaGraphExecDestroy(decode_graph_);
-  for (ncclComm_t c : {actor_comm_, critic_comm_, world_})
+  for (ncclComm_t c : {actor_comm_, critic_comm_, sync_comm_[0], sync_comm_[1], world_})
     if (c) nccl().CommDestroy(c);
-  for (auto& e : ev_) cudaEventDestroy(e);
-  if (stream_) cudaStreamDestroy(stream_);
-  if (stream_side_) cudaStreamDestroy(stream_side_);
+  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  for (cudaEvent_t e : step_done_) cudaEventDestroy(e);
+  for (cudaEvent_t e : {ev_begin_, ev_end_})
+    if (e) cudaEventDestroy(e);
+  for (auto& l : lane_)
+    if (l) cudaStreamDestroy(l);
 }
 
-void Engine::allreduce_grads(Decoder& m, ncclComm_t comm) {
-  if (!comm) return;
-  if (m.sharded) {  // ZeRO-1: each rank only needs the summed gradient of its own shard
-    NK(nccl().ReduceScatter(m.grad.p, m.grad.as<float>() + m.shard_off, static_cast<size_t>(m.shard), ncclFloat32,
-                            ncclSum, comm, stream_));
-    comm_bytes_ += 4.0 * static_cast<double>(m.npad - m.shard);
-    return;
+// ---- events --------------------------------------------------------------------------
+
+void Engine::wait_deps(int i, int lane) {
+  for (int d : deps_[i])
+    if (step_lane_[d] >= 0 && step_lane_[d] != lane) CK(cudaStreamWaitEvent(lane_[lane], step_done_[d], 0));
+}
+
+void Engine::begin_event(int i, const ExecStep& s, int kind, int lane, int stage) {
+  use_lane(lane);
+  wait_deps(i, lane);
+  ExecEvent e;
+  e.step = i;
+  e.task = s.task;
+  e.kind = kind;
+  e.model = static_cast<int>(s.kind == StepKind::Task ? xp_.tasks[s.task].model : s.model);
+  e.mb = s.mb;
+  e.rollout = s.rollout;
+  e.epoch = s.epoch;
+  e.lane = lane;
+  e.comm_op = s.comm_op;
+  e.stage = stage;
+  e.a = take_event();
+  e.b = take_event();
+  CK(cudaEventRecord(e.a, lane_[lane]));
+  evs_.push_back(e);
+}
+
+void Engine::end_event() {
+  ExecEvent& e = evs_.back();
+  CK(cudaEventRecord(e.b, lane_[e.lane]));
+  step_lane_[e.step] = e.lane;
+  CK(cudaEventRecord(step_done_[e.step], lane_[e.lane]));
+}
+
+// ---- exchanges: row transfers over NCCL send/recv on the comm lane --------------------
+
+void Engine::run_exchange(const ExecStep& s) {
+  const int i = static_cast<int>(&s - xp_.steps.data());
+  bool mine = false;
+  for (const Move& m : s.moves)
+    for (const Transfer& t : m.transfers) mine |= t.src_rank == rank_ || t.dst_rank == rank_;
+  if (!mine) return;
+  const bool prompt = s.moves[0].field == Field::Prompt;
+  begin_event(i, s, static_cast<int>(TaskKind::Collective), 2,
+              static_cast<int>(prompt ? Stage::Generation : Stage::Forward));
+  auto src_ptr = [&](const Move& m) -> char* {
+    return static_cast<char*>(m.src_set < 0 ? home_.p : rs_[m.src_set].field(m.field));
+  };
+  // local rows first (plain copies), then one NCCL group for the remote ones
+  bool remote = false;
+  for (const Move& m : s.moves) {
+    const size_t rb = field_row_bytes(m.field, S_, R_);
+    for (const Transfer& t : m.transfers) {
+      if (t.src_rank == rank_ && t.dst_rank == rank_)
+        CK(cudaMemcpyAsync(static_cast<char*>(rs_[m.dst_set].field(m.field)) + t.dst_row * rb, src_ptr(m) + t.src_row * rb,
+                           t.count * rb, cudaMemcpyDeviceToDevice, stream_));
+      else if (t.src_rank == rank_ || t.dst_rank == rank_)
+        remote = true;
+    }
   }
-  NK(nccl().AllReduce(m.grad.p, m.grad.p, static_cast<size_t>(m.n), ncclFloat32, ncclSum, comm, stream_));
-  comm_bytes_ += 2.0 * 4.0 * m.n;
-}
-
-// Paired P2P exchange with the partner rank inside one NCCL group (sends and
-// receives between a pair match in issue order per direction).
-void Engine::p2p(const std::vector<std::pair<const void*, size_t>>& sends, const std::vector<std::pair<void*, size_t>>& recvs) {
-  NK(nccl().GroupStart());
-  for (const auto& [p, n] : sends) {
-    NK(nccl().Send(p, n, ncclInt8, partner_, world_, stream_));
-    comm_bytes_ += static_cast<double>(n);
+  if (remote) {
+    NK(nccl().GroupStart());
+    for (const Move& m : s.moves) {
+      const size_t rb = field_row_bytes(m.field, S_, R_);
+      for (const Transfer& t : m.transfers) {
+        if (t.src_rank == t.dst_rank) continue;
+        if (t.src_rank == rank_) {
+          NK(nccl().Send(src_ptr(m) + t.src_row * rb, t.count * rb, ncclInt8, t.dst_rank, world_, stream_));
+          comm_bytes_ += static_cast<double>(t.count * rb);
+        } else if (t.dst_rank == rank_) {
+          NK(nccl().Recv(static_cast<char*>(rs_[m.dst_set].field(m.field)) + t.dst_row * rb, t.count * rb, ncclInt8,
+                         t.src_rank, world_, stream_));
+        }
+      }
+    }
+    NK(nccl().GroupEnd());
   }
-  for (const auto& [p, n] : recvs) NK(nccl().Recv(p, n, ncclInt8, partner_, world_, stream_));
-  NK(nccl().GroupEnd());
+  end_event();
 }
 
-// TrainFB over micro-batches of train_mb_ samples: each runs forward (activations saved),
-// loss, backward, accumulating into the flat gradient; then one all-reduce and AdamW.
-void Engine::train_actor(Decoder& m, int B, ncclComm_t comm) {
-  const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator : static_cast<float>(B * R_);
-  cudaMemsetAsync(m.grad.p, 0, static_cast<size_t>(m.n) * 4, stream_);
-  for (int b0 = 0; b0 < B; b0 += train_mb_) train_actor_mb(m, b0, std::min(train_mb_, B - b0), denom);
-  allreduce_grads(m, comm);
-  adam(m, cfg_.lr_actor, comm);
-}
+// ---- tasks ----------------------------------------------------------------------------
 
-void Engine::train_actor_mb(Decoder& m, int b0, int B, float denom) {
+// Forward + loss + backward of `B` experience rows starting at row0 of row set rb,
+// accumulating into m's flat gradient.
+void Engine::train_rows(Decoder& m, bool actor, RowBufs& rb, int row0, int B, float denom) {
   const int d = m.a.d_model, V = m.a.vocab, BR = B * R_;
-  const int32_t* tok = tokens_.as<int32_t>() + static_cast<size_t>(b0) * S_;
-  const size_t r0 = static_cast<size_t>(b0) * R_;
-  float* logp = logp_new_.as<float>() + r0;
-  float* g = gbuf_.as<float>() + r0;
+  const int32_t* tok = rb.tokens.as<int32_t>() + static_cast<size_t>(row0) * S_;
+  const size_t r0 = static_cast<size_t>(row0) * R_;
   forward(m, tok, B, S_, S_, true, nullptr);
-  lm_logprobs(m, tok, B, logp, true);
-  K(rlhf_ppo_actor_loss(logp, logp_old_.as<float>() + r0, adv_.as<float>() + r0, BR, cfg_.cliprange, denom, g,
-                        loss_.as<float>(), stream_), 1);
-  K(rlhf_logprob_bwd(arp_->logits, arp_->lse, g, BR, V, tok, S_, P_, R_, arp_->dz, stream_), 1);
-  // dhf_resp = dz E ; dE += dz^T hf_resp
-  rlhf_gemm_params p{};
-  p.M = BR; p.N = d; p.K = V; p.batch = 1; p.batch_h = 1;
-  p.A = arp_->dz; p.lda = V;
-  p.B = m.T(m.head_id()); p.b_mn_major = 1; p.ldb = d;
-  p.C = arp_->dhf_resp; p.c_f32 = 1; p.c_rs = d; p.c_cs = 1; p.alpha = 1.0f;
-  gemm(p);
-  rlhf_gemm_params q{};
-  q.M = V; q.N = d; q.K = BR; q.batch = 1; q.batch_h = 1;
-  q.A = arp_->dz; q.a_mn_major = 1; q.lda = V;
-  q.B = arp_->hf_resp; q.b_mn_major = 1; q.ldb = d;
-  q.C = m.G(m.head_id()); q.c_f32 = 1; q.c_rs = d; q.c_cs = 1; q.alpha = 1.0f; q.accumulate = 1;
-  gemm(q);
-  cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
-  K(rlhf_scatter_rows_f32(arp_->dhf_resp, arp_->dhf, B, S_, R_, P_ - 1, d, stream_), 1);
-  backward(m, tok, B, S_);
-}
-
-void Engine::train_critic(Decoder& m, int B, ncclComm_t comm) {
-  const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator : static_cast<float>(B * R_);
-  cudaMemsetAsync(m.grad.p, 0, static_cast<size_t>(m.n) * 4, stream_);
-  for (int b0 = 0; b0 < B; b0 += train_mb_) train_critic_mb(m, b0, std::min(train_mb_, B - b0), denom);
-  allreduce_grads(m, comm);
-  adam(m, cfg_.lr_critic, comm);
-}
-
-void Engine::train_critic_mb(Decoder& m, int b0, int B, float denom) {
-  const int d = m.a.d_model, BR = B * R_;
-  const int32_t* tok = tokens_.as<int32_t>() + static_cast<size_t>(b0) * S_;
-  const size_t r0 = static_cast<size_t>(b0) * R_;
-  float* v = values_new_.as<float>() + r0;
-  float* g = gbuf2_.as<float>() + r0;
-  forward(m, tok, B, S_, S_, true, nullptr);
-  K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, d, v, stream_), 1);
-  K(rlhf_ppo_critic_loss(v, values_.as<float>() + r0, ret_.as<float>() + r0, BR, cfg_.cliprange_value, denom, g,
-                         loss_.as<float>() + 1, stream_), 1);
-  cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_);
-  K(rlhf_scalar_head_bwd(arp_->hf, m.T(RLHF_T_VHEAD), g, B, S_, R_, P_ - 1, d, arp_->dhf, m.G(RLHF_T_VHEAD), arp_->ws,
-                         stream_), 2);
+  if (actor) {
+    float* logp = rb.logp_new.as<float>() + r0;
+    float* g = rb.gbuf.as<float>() + r0;
+    lm_logprobs(m, tok, B, logp, true);
+    K(rlhf_ppo_actor_loss(logp, rb.logp_old.as<float>() + r0, rb.adv.as<float>() + r0, BR, cfg_.cliprange, denom, g,
+                          loss_.as<float>(), stream_), 1);
+    K(rlhf_logprob_bwd(arp_->logits, arp_->lse, g, BR, V, tok, S_, P_, R_, arp_->dz, stream_), 1);
+    // dhf_resp = dz E ; dE += dz^T hf_resp
+    rlhf_gemm_params p{};
+    p.M = BR; p.N = d; p.K = V; p.batch = 1; p.batch_h = 1;
+    p.A = arp_->dz; p.lda = V;
+    p.B = m.T(m.head_id()); p.b_mn_major = 1; p.ldb = d;
+    p.C = arp_->dhf_resp; p.c_f32 = 1; p.c_rs = d; p.c_cs = 1; p.alpha = 1.0f;
+    gemm(p);
+    rlhf_gemm_params q{};
+    q.M = V; q.N = d; q.K = BR; q.batch = 1; q.batch_h = 1;
+    q.A = arp_->dz; q.a_mn_major = 1; q.lda = V;
+    q.B = arp_->hf_resp; q.b_mn_major = 1; q.ldb = d;
+    q.C = m.G(m.head_id()); q.c_f32 = 1; q.c_rs = d; q.c_cs = 1; q.alpha = 1.0f; q.accumulate = 1;
+    gemm(q);
+    CK(cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_));
+    K(rlhf_scatter_rows_f32(arp_->dhf_resp, arp_->dhf, B, S_, R_, P_ - 1, d, stream_), 1);
+  } else {
+    float* v = rb.values_new.as<float>() + r0;
+    float* g = rb.gbuf2.as<float>() + r0;
+    K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, d, v, stream_), 1);
+    K(rlhf_ppo_critic_loss(v, rb.values.as<float>() + r0, rb.ret.as<float>() + r0, BR, cfg_.cliprange_value, denom, g,
+                           loss_.as<float>() + 1, stream_), 1);
+    CK(cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_));
+    K(rlhf_scalar_head_bwd(arp_->hf, m.T(RLHF_T_VHEAD), g, B, S_, R_, P_ - 1, d, arp_->dhf, m.G(RLHF_T_VHEAD), arp_->ws,
+                           stream_), 2);
+  }
   backward(m, tok, B, S_);
 }
 
@@ -338,6 +518,141 @@ void Engine::score_values(const Decoder& m, const int32_t* tok, int B, float* va
 void Engine::score_reward(const Decoder& m, const int32_t* tok, int B, float* score) {
   forward(m, tok, B, S_, S_, false, nullptr);
   K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, 1, S_ - 1, m.a.d_model, score, stream_), 1);
+}
+
+void Engine::run_task(const ExecStep& s) {
+  const int i = static_cast<int>(&s - xp_.steps.data());
+  const StageTask& t = xp_.tasks[s.task];
+  const int mi = static_cast<int>(t.model);
+  switch (t.kind) {
+    case TaskKind::Generation: {
+      if (!hosts_[mi]) return;
+      RowBufs& rb = rs_[xp_.set_of[mi]];
+      const size_t row0 = static_cast<size_t>(s.rollout * xp_.M + s.mb) * gen_B_;
+      begin_event(i, s, static_cast<int>(TaskKind::Generation), 0, static_cast<int>(Stage::Generation));
+      const size_t bytes = static_cast<size_t>(gen_B_) * S_ * 4;
+      CK(cudaMemcpyAsync(gen_tok_.p, rb.tokens.as<int32_t>() + row0 * S_, bytes, cudaMemcpyDeviceToDevice, stream_));
+      ev_prefill_ = take_event();
+      generate(*generator_, gen_B_, false);
+      CK(cudaMemcpyAsync(rb.tokens.as<int32_t>() + row0 * S_, gen_tok_.p, bytes, cudaMemcpyDeviceToDevice, stream_));
+      end_event();
+      prefill_.push_back({evs_.back().a, ev_prefill_});
+      decode_.push_back({ev_prefill_, evs_.back().b});
+      ev_prefill_ = nullptr;
+      return;
+    }
+    case TaskKind::Forward: {
+      if (!hosts_[mi]) return;
+      RowBufs& rb = rs_[xp_.set_of[mi]];
+      const int per = xp_.sets[xp_.set_of[mi]].per;
+      const size_t row0 = static_cast<size_t>(s.rollout * xp_.M + s.mb) * per;
+      const int32_t* tok = rb.tokens.as<int32_t>() + row0 * S_;
+      begin_event(i, s, static_cast<int>(TaskKind::Forward), lane_of(t.model), static_cast<int>(Stage::Forward));
+      const Decoder& m = *model(t.model);
+      switch (output_field(t.model)) {
+        case Field::LogpOld: score_logp(m, tok, per, rb.logp_old.as<float>() + row0 * R_); break;
+        case Field::LogpRef: score_logp(m, tok, per, rb.logp_ref.as<float>() + row0 * R_); break;
+        case Field::Values: score_values(m, tok, per, rb.values.as<float>() + row0 * R_); break;
+        case Field::Score: score_reward(m, tok, per, rb.score.as<float>() + row0); break;
+        default: break;
+      }
+      end_event();
+      return;
+    }
+    case TaskKind::TrainFB: {
+      if (!hosts_[mi]) return;
+      const bool actor = t.model == ModelName::Actor;
+      Decoder& m = *model(t.model);
+      RowBufs& rb = rs_[xp_.set_of[mi]];
+      const int per = xp_.sets[xp_.set_of[mi]].per;
+      begin_event(i, s, static_cast<int>(TaskKind::TrainFB), lane_of(t.model), static_cast<int>(Stage::Training));
+      if (t.micro_batch_index == 0) {  // a new epoch's gradient and loss sum
+        CK(cudaMemsetAsync(m.grad.p, 0, static_cast<size_t>(m.npad) * 4, stream_));
+        CK(cudaMemsetAsync(loss_.as<float>() + (actor ? 0 : 1), 0, 4, stream_));
+      }
+      // the micro-batch's rows of every rollout (one block per rollout), in chunks of train_mb_
+      const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator * xp_.rollouts
+                                                    : static_cast<float>(xp_.G) * xp_.rollouts * R_;
+      for (int r = 0; r < xp_.rollouts; ++r) {
+        const int row0 = (r * xp_.M + t.micro_batch_index) * per;
+        for (int c = 0; c < per; c += train_mb_) train_rows(m, actor, rb, row0 + c, std::min(train_mb_, per - c), denom);
+      }
+      end_event();
+      return;
+    }
+    case TaskKind::ParamSync: {
+      const int k = t.model == ModelName::ShadowActor ? 0 : 1;
+      if (!sync_comm_[k]) return;  // world 1, or this rank is neither trainer nor shadow
+      Decoder& src = k == 0 ? actor_ : critic_;
+      Decoder& dst = k == 0 ? shadow_actor_ : shadow_critic_;
+      const bool is_src = hosts_[k == 0 ? 0 : 1];
+      begin_event(i, s, static_cast<int>(TaskKind::ParamSync), 2, static_cast<int>(Stage::Sync));
+      const size_t n = static_cast<size_t>(is_src ? src.n : dst.n);
+      NK(nccl().Broadcast(is_src ? src.w.p : dst.w.p, is_src ? src.w.p : dst.w.p, n, ncclBfloat16, sync_root_[k],
+                          sync_comm_[k], stream_));
+      if (is_src) comm_bytes_ += 2.0 * static_cast<double>(n);
+      end_event();
+      return;
+    }
+    default:
+      return;
+  }
+}
+
+// Experience-buffer barrier (workload.cpp:153-163) on one trainer row set: KL-shaped rewards,
+// GAE, returns over every row; the reported score / KL means come from the experience set.
+void Engine::run_experience(const ExecStep& s) {
+  const int i = static_cast<int>(&s - xp_.steps.data());
+  if (xp_.member_index(s.set, rank_) < 0 || !rs_[s.set].trainer) return;
+  RowBufs& rb = rs_[s.set];
+  begin_event(i, s, kEvExperience, 0, static_cast<int>(Stage::Training));
+  K(rlhf_gae(rb.logp_old.as<float>(), rb.logp_ref.as<float>(), rb.values.as<float>(), rb.score.as<float>(), rb.rows, R_,
+             cfg_.kl_ctl, cfg_.clip_reward, cfg_.gamma, cfg_.lam, rb.rewards.as<float>(), rb.adv.as<float>(),
+             rb.ret.as<float>(), stream_), 1);
+  if (s.set == xp_.experience_set(rank_))
+    K(rlhf_experience_stats(rb.logp_old.as<float>(), rb.logp_ref.as<float>(), rb.score.as<float>(), rb.rows, R_,
+                            loss_.as<float>() + 2, stream_), 1);
+  end_event();
+}
+
+// Gradient sync + AdamW closing a TrainFB epoch of one model (costmodel.hpp:59-74): ZeRO-0
+// all-reduce, or ZeRO-1 reduce-scatter -> AdamW on the rank's shard -> all-gather of the
+// bf16 weights.  The collectives run on the comm lane, AdamW on the model's compute lane.
+void Engine::run_optimizer(const ExecStep& s, int i) {
+  const int mi = static_cast<int>(s.model);
+  if (!hosts_[mi]) return;
+  Decoder& m = *model(s.model);
+  ncclComm_t comm = s.model == ModelName::Actor ? actor_comm_ : critic_comm_;
+  const float lr = s.model == ModelName::Actor ? cfg_.lr_actor : cfg_.lr_critic;
+  const int ml = lane_of(s.model);
+  const int st = static_cast<int>(Stage::Training);
+  cudaEvent_t prev = nullptr;
+  if (comm) {
+    begin_event(i, s, static_cast<int>(TaskKind::Collective), 2, st);
+    if (m.sharded) {  // each rank only needs the summed gradient of its own shard
+      NK(nccl().ReduceScatter(m.grad.p, m.grad.as<float>() + m.shard_off, static_cast<size_t>(m.shard), ncclFloat32,
+                              ncclSum, comm, stream_));
+      comm_bytes_ += 4.0 * static_cast<double>(m.npad - m.shard);
+    } else {
+      NK(nccl().AllReduce(m.grad.p, m.grad.p, static_cast<size_t>(m.n), ncclFloat32, ncclSum, comm, stream_));
+      comm_bytes_ += 2.0 * 4.0 * static_cast<double>(m.n);
+    }
+    end_event();
+    prev = evs_.back().b;
+  }
+  begin_event(i, s, kEvAdam, ml, st);
+  if (prev) CK(cudaStreamWaitEvent(stream_, prev, 0));
+  adam(m, lr);
+  end_event();
+  if (m.sharded && comm) {
+    prev = evs_.back().b;
+    begin_event(i, s, static_cast<int>(TaskKind::Collective), 2, st);
+    CK(cudaStreamWaitEvent(stream_, prev, 0));
+    NK(nccl().AllGather(m.w.as<uint16_t>() + m.shard_off, m.w.p, static_cast<size_t>(m.shard), ncclBfloat16, comm,
+                        stream_));
+    comm_bytes_ += 2.0 * static_cast<double>(m.npad - m.shard);
+    end_event();
+  }
 }
 
 // Activation arena: capacities = max over hosted models.  `trains` keeps every layer's
@@ -360,14 +675,15 @@ void Engine::build_arena(Arena& A, bool trains, bool critic_only) {
   A.Ts = trains ? static_cast<int64_t>(train_mb_) * S_ : A.T;
   A.Zs = trains ? static_cast<int64_t>(train_mb_) * A.H : A.Z;
   auto mk = [&](size_t bytes) {
-    DevBuf* b = new DevBuf(bytes);
+    DevBuf* b = new DevBuf();
     A.owned.push_back(b);
+    b->alloc(bytes);
     return b->p;
   };
   const int64_t T = A.T, d = A.d, SS = static_cast<int64_t>(A.S) * A.S, BR = static_cast<int64_t>(Bcap_) * R_;
   const int64_t Ls = trains ? A.L : 1;  // layers of saved activations (inference-only ranks keep one)
-  // per-layer saved activations: Ls slots of one training micro-batch (Ts rows), and at
-  // least one slot of a whole Forward stage (T rows, layer buffers reused across layers)
+  // per-layer saved activations: Ls slots of one training chunk (Ts rows), and at least
+  // one slot of a whole Forward block (T rows, layer buffers reused across layers)
   const int64_t Ts = A.Ts, Zs = A.Zs;
   auto cap = [&](int64_t slots, int64_t per_row, int64_t rows_s, int64_t rows_all) {
     return std::max(slots * rows_s, rows_all) * per_row;
@@ -403,218 +719,137 @@ void Engine::build_arena(Arena& A, bool trains, bool critic_only) {
   A.gemm_ws = static_cast<float*>(mk(A.gemm_ws_bytes));
   A.counters_len = 1 << 16;
   A.counters = static_cast<int*>(mk(A.counters_len * 4));
-
 }
 
-void Engine::gae(int B) {
-  K(rlhf_gae(logp_old_.as<float>(), logp_ref_.as<float>(), values_.as<float>(), score_.as<float>(), B, R_, cfg_.kl_ctl,
-             cfg_.clip_reward, cfg_.gamma, cfg_.lam, rewards_.as<float>(), adv_.as<float>(), ret_.as<float>(), stream_), 1);
-}
-
-// Put this rank's prompts [Bg, P] into rows [row0, row0+Bg) of tokens_.
-void Engine::place_prompts(const int32_t* dev_prompts, int row0) {
-  CK(cudaMemcpy2DAsync(tokens_.as<int32_t>() + static_cast<size_t>(row0) * S_, static_cast<size_t>(S_) * 4, dev_prompts,
-                       static_cast<size_t>(P_) * 4, static_cast<size_t>(P_) * 4, Bg_, cudaMemcpyDeviceToDevice, stream_));
-}
+// ---- the step -------------------------------------------------------------------------
 
 void Engine::step(const int32_t* prompts_host, rlhf_step_report* rep) {
   CK(cudaSetDevice(opt_.device));
   launches_ = 0;
   comm_bytes_ = 0;
-  // this rank's prompt shard (global samples [rank*Bg, rank*Bg + Bg)) -> device
-  std::vector<int32_t> pr(static_cast<size_t>(Bg_) * P_);
-  for (int b = 0; b < Bg_; ++b)
-    for (int t = 0; t < P_; ++t)
-      pr[static_cast<size_t>(b) * P_ + t] =
-          prompts_host ? prompts_host[static_cast<size_t>(b) * P_ + t]
-                       : rlhf_prompt_token(cfg_.prompt_seed, b + cfg_.sample_offset, t, cfg_.actor.vocab);
-  CK(cudaMemcpyAsync(prompt_stage_.p, pr.data(), pr.size() * 4, cudaMemcpyHostToDevice, stream_));
-  cudaMemsetAsync(loss_.p, 0, 16, stream_);
-  cudaEventRecord(ev_[0], stream_);  // device-resident inputs from here on
-  cudaEventRecord(ev_[1], stream_);  // (prefill end; re-recorded by generate)
+  evs_.clear();
+  ev_next_ = 0;
+  prefill_.clear();
+  decode_.clear();
+  std::fill(step_lane_.begin(), step_lane_.end(), -1);
+  // this rank's home prompts: global samples r*G + rank*Bg + [0, Bg) of every rollout,
+  // rows of S int32 (first P columns) so an exchange moves whole token rows
+  const int rows = xp_.rollouts * Bg_;
+  std::vector<int32_t> pr(static_cast<size_t>(rows) * S_, 0);
+  const int64_t id_shift = static_cast<int64_t>(cfg_.sample_offset) - static_cast<int64_t>(rank_) * Bg_;
+  for (int r = 0; r < xp_.rollouts; ++r)
+    for (int b = 0; b < Bg_; ++b) {
+      const size_t row = static_cast<size_t>(r) * Bg_ + b;
+      const int64_t id = static_cast<int64_t>(r) * xp_.G + static_cast<int64_t>(rank_) * Bg_ + b + id_shift;
+      for (int t = 0; t < P_; ++t)
+        pr[row * S_ + t] = prompts_host ? prompts_host[row * P_ + t]
+                                        : rlhf_prompt_token(cfg_.prompt_seed, static_cast<int>(id), t, cfg_.actor.vocab);
+    }
+  CK(cudaEventRecord(ev_begin_, lane_[0]));
+  for (int l = 1; l < 3; ++l) CK(cudaStreamWaitEvent(lane_[l], ev_begin_, 0));
+  // host -> device on the comm lane: the prompt exchanges that follow consume it there
+  CK(cudaMemcpyAsync(home_.p, pr.data(), pr.size() * 4, cudaMemcpyHostToDevice, lane_[2]));
 
-  const int Bg = Bg_;
-  int32_t* tok = tokens_.as<int32_t>();
-  const bool lower = partner_ < 0 || rank_ < partner_;
-  switch (tag_) {
-    case StrategyTag::Colocated: {
-      place_prompts(prompt_stage_.as<int32_t>(), 0);
-      generate(actor_, Bg, false);
-      cudaEventRecord(ev_[2], stream_);
-      // Forward x4 (workload.cpp:119 lists Actor, Critic, Ref, Reward; they are
-      // independent): Critic + Reward on a second stream with their own arena, Actor +
-      // Ref on the main stream, joined before the experience-buffer barrier
-      if (stream_side_) {
-        cudaEventRecord(ev_[6], stream_);
-        CK(cudaStreamWaitEvent(stream_side_, ev_[6], 0));
-        std::swap(stream_, stream_side_);
-        arp_ = &ar_side_;
-      }
-      score_values(critic_, tok, Bg, values_.as<float>());
-      score_reward(reward_, tok, Bg, score_.as<float>());
-      if (stream_side_) {
-        cudaEventRecord(ev_[7], stream_);
-        std::swap(stream_, stream_side_);
-        arp_ = &ar_main_;
-      }
-      score_logp(actor_, tok, Bg, logp_old_.as<float>());
-      score_logp(ref_, tok, Bg, logp_ref_.as<float>());
-      if (stream_side_) CK(cudaStreamWaitEvent(stream_, ev_[7], 0));
-      cudaEventRecord(ev_[3], stream_);
-      gae(Bg);
-      // TrainFB(Actor) and TrainFB(Critic) are independent given the experience buffer:
-      // the Critic trains on the second stream / arena
-      if (stream_side_) {
-        cudaEventRecord(ev_[6], stream_);
-        CK(cudaStreamWaitEvent(stream_side_, ev_[6], 0));
-        std::swap(stream_, stream_side_);
-        arp_ = &ar_side_;
-      }
-      train_critic(critic_, Bg, critic_comm_);
-      if (stream_side_) {
-        cudaEventRecord(ev_[7], stream_);
-        std::swap(stream_, stream_side_);
-        arp_ = &ar_main_;
-      }
-      train_actor(actor_, Bg, actor_comm_);
-      if (stream_side_) CK(cudaStreamWaitEvent(stream_, ev_[7], 0));
-      cudaEventRecord(ev_[4], stream_);
-      break;
+  for (size_t i = 0; i < xp_.steps.size(); ++i) {
+    const ExecStep& s = xp_.steps[i];
+    switch (s.kind) {
+      case StepKind::Exchange: run_exchange(s); break;
+      case StepKind::Task: run_task(s); break;
+      case StepKind::Experience: run_experience(s); break;
+      case StepKind::OptimizerStep: run_optimizer(s, static_cast<int>(i)); break;
     }
-    case StrategyTag::Interleaving1: {
-      place_prompts(prompt_stage_.as<int32_t>(), 0);
-      generate(actor_, Bg, false);
-      cudaEventRecord(ev_[2], stream_);
-      score_logp(actor_, tok, Bg, logp_old_.as<float>());
-      score_values(critic_, tok, Bg, values_.as<float>());
-      // AllGather of (query, response) within the Ref|Reward pair (Alg. 1 line 8)
-      int32_t* t2 = tok2_.as<int32_t>();
-      const size_t sb = static_cast<size_t>(Bg) * S_ * 4;
-      int32_t* mine = t2 + (lower ? 0 : static_cast<size_t>(Bg) * S_);
-      int32_t* theirs = t2 + (lower ? static_cast<size_t>(Bg) * S_ : 0);
-      CK(cudaMemcpyAsync(mine, tok, sb, cudaMemcpyDeviceToDevice, stream_));
-      p2p({{tok, sb}}, {{theirs, sb}});
-      const int own0 = lower ? 0 : Bg, oth0 = lower ? Bg : 0;
-      if (hosts_[2]) {  // Ref side: logprobs of both shards; swap with the Reward side's scores
-        score_logp(ref_, t2, 2 * Bg, out2_.as<float>());
-        const size_t rb = static_cast<size_t>(Bg) * R_ * 4;
-        CK(cudaMemcpyAsync(logp_ref_.p, out2_.as<float>() + static_cast<size_t>(own0) * R_, rb, cudaMemcpyDeviceToDevice,
-                           stream_));
-        p2p({{out2_.as<float>() + static_cast<size_t>(oth0) * R_, rb}}, {{score_.p, static_cast<size_t>(Bg) * 4}});
-      } else {  // Reward side
-        score_reward(reward_, t2, 2 * Bg, score2_.as<float>());
-        CK(cudaMemcpyAsync(score_.p, score2_.as<float>() + own0, static_cast<size_t>(Bg) * 4, cudaMemcpyDeviceToDevice,
-                           stream_));
-        p2p({{score2_.as<float>() + oth0, static_cast<size_t>(Bg) * 4}}, {{logp_ref_.p, static_cast<size_t>(Bg) * R_ * 4}});
-      }
-      cudaEventRecord(ev_[3], stream_);
-      gae(Bg);
-      train_actor(actor_, Bg, actor_comm_);
-      train_critic(critic_, Bg, critic_comm_);
-      cudaEventRecord(ev_[4], stream_);
-      break;
-    }
-    case StrategyTag::Interleaving2:
-    case StrategyTag::Disaggregated: {
-      const bool disagg = tag_ == StrategyTag::Disaggregated;
-      // generator side: Actor ranks (I2) / inference ranks (disaggregated)
-      const bool gen_side = disagg ? hosts_[4] : hosts_[0];
-      const int B2 = 2 * Bg;
-      const size_t rbytes = static_cast<size_t>(B2) * R_ * 4, tbytes = static_cast<size_t>(B2) * S_ * 4;
-      if (gen_side) {
-        place_prompts(prompt_stage_.as<int32_t>(), lower ? 0 : Bg);
-        p2p({}, {{tok2_.p, static_cast<size_t>(Bg) * P_ * 4}});  // the partner's prompt shard
-        place_prompts(tok2_.as<int32_t>(), lower ? Bg : 0);
-        generate(*generator_, B2, false);
-        cudaEventRecord(ev_[2], stream_);
-        if (disagg) {
-          score_logp(shadow_actor_, tok, B2, logp_old_.as<float>());
-          score_values(shadow_critic_, tok, B2, values_.as<float>());
-          score_logp(ref_, tok, B2, logp_ref_.as<float>());
-          score_reward(reward_, tok, B2, score_.as<float>());
-          // Send the experience to the training side (Alg. 2)
-          p2p({{tok, tbytes}, {logp_old_.p, rbytes}, {logp_ref_.p, rbytes}, {values_.p, rbytes},
-               {score_.p, static_cast<size_t>(B2) * 4}},
-              {});
-          cudaEventRecord(ev_[3], stream_);
-          cudaEventRecord(ev_[4], stream_);
-          // ParamSync: trained weights -> shadows, before the next Generation
-          p2p({}, {{shadow_actor_.w.p, static_cast<size_t>(shadow_actor_.n) * 2},
-                   {shadow_critic_.w.p, static_cast<size_t>(shadow_critic_.n) * 2}});
-        } else {
-          p2p({{tok, tbytes}}, {});
-          score_logp(actor_, tok, B2, logp_old_.as<float>());
-          score_logp(ref_, tok, B2, logp_ref_.as<float>());
-          p2p({{logp_old_.p, rbytes}, {logp_ref_.p, rbytes}}, {{values_.p, rbytes}, {score_.p, static_cast<size_t>(B2) * 4}});
-          cudaEventRecord(ev_[3], stream_);
-          gae(B2);
-          train_actor(actor_, B2, actor_comm_);
-          cudaEventRecord(ev_[4], stream_);
-        }
-      } else {
-        p2p({{prompt_stage_.p, static_cast<size_t>(Bg) * P_ * 4}}, {});
-        cudaEventRecord(ev_[1], stream_);
-        cudaEventRecord(ev_[2], stream_);
-        if (disagg) {
-          p2p({}, {{tok, tbytes}, {logp_old_.p, rbytes}, {logp_ref_.p, rbytes}, {values_.p, rbytes},
-                   {score_.p, static_cast<size_t>(B2) * 4}});
-          cudaEventRecord(ev_[3], stream_);
-          gae(B2);
-          train_actor(actor_, B2, actor_comm_);
-          train_critic(critic_, B2, critic_comm_);
-          cudaEventRecord(ev_[4], stream_);
-          p2p({{actor_.w.p, static_cast<size_t>(actor_.n) * 2}, {critic_.w.p, static_cast<size_t>(critic_.n) * 2}}, {});
-        } else {
-          p2p({}, {{tok, tbytes}});
-          score_values(critic_, tok, B2, values_.as<float>());
-          score_reward(reward_, tok, B2, score_.as<float>());
-          p2p({{values_.p, rbytes}, {score_.p, static_cast<size_t>(B2) * 4}}, {{logp_old_.p, rbytes}, {logp_ref_.p, rbytes}});
-          cudaEventRecord(ev_[3], stream_);
-          gae(B2);
-          train_critic(critic_, B2, critic_comm_);
-          cudaEventRecord(ev_[4], stream_);
-        }
-      }
-      break;
-    }
-    default:
-      throw ConfigError("strategy not executable: " + strategy_);
   }
-  cudaEventRecord(ev_[5], stream_);
-  float loss[2];
-  CK(cudaMemcpyAsync(loss, loss_.p, 8, cudaMemcpyDeviceToHost, stream_));
-  CK(cudaStreamSynchronize(stream_));
+  // join every lane into the main one
+  for (int l = 1; l < 3; ++l) {
+    cudaEvent_t j = take_event();
+    CK(cudaEventRecord(j, lane_[l]));
+    CK(cudaStreamWaitEvent(lane_[0], j, 0));
+  }
+  use_lane(0);
+  CK(cudaEventRecord(ev_end_, lane_[0]));
+  float loss[4];
+  CK(cudaMemcpyAsync(loss, loss_.p, 16, cudaMemcpyDeviceToHost, lane_[0]));
+  CK(cudaStreamSynchronize(lane_[0]));
 
-  auto sec = [&](int a, int b) {
+  std::memset(rep, 0, sizeof(*rep));
+  auto since = [&](cudaEvent_t a, cudaEvent_t b) {
     float t = 0;
-    cudaEventElapsedTime(&t, ev_[a], ev_[b]);
+    cudaEventElapsedTime(&t, a, b);
     return static_cast<double>(t) * 1e-3;
   };
-  std::memset(rep, 0, sizeof(*rep));
-  rep->step_seconds = sec(0, 5);
-  const double global_batch = cfg_.loss_denominator > 0 ? cfg_.loss_denominator / R_ : Bg_;
-  rep->throughput_samples_per_sec = global_batch / rep->step_seconds;
-  rep->stage_seconds[0] = sec(0, 2);
-  rep->stage_seconds[1] = sec(2, 3);
-  rep->stage_seconds[2] = sec(3, 4);
-  rep->stage_seconds[3] = sec(4, 5);
-  rep->prefill_seconds = sec(0, 1);
-  rep->decode_seconds = sec(1, 2);
-  const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator : static_cast<float>(Bg_ * R_);
-  rep->actor_loss = loss[0] / denom;
-  rep->critic_loss = 0.5 * loss[1] / denom;
+  rep->step_seconds = since(ev_begin_, ev_end_);
+  rep->throughput_samples_per_sec = static_cast<double>(xp_.G) * xp_.rollouts / rep->step_seconds;
+  for (ExecEvent& e : evs_) {
+    e.start = since(ev_begin_, e.a);
+    e.end = since(ev_begin_, e.b);
+  }
+  for (const auto& [a, b] : prefill_) rep->prefill_seconds += since(a, b);
+  for (const auto& [a, b] : decode_) rep->decode_seconds += since(a, b);
+
+  // SimReport accounting: every instant of the step is attributed to one
+  // stage -- the lowest Stage among the compute-lane intervals active then, else among the
+  // comm-lane ones, else (idle) the stage of the next interval to start
+  std::vector<double> cut{0.0, rep->step_seconds};
+  for (const ExecEvent& e : evs_) {
+    cut.push_back(e.start);
+    cut.push_back(e.end);
+  }
+  std::sort(cut.begin(), cut.end());
+  cut.erase(std::unique(cut.begin(), cut.end()), cut.end());
+  double pending = 0;
+  int last_stage = 0;
+  for (size_t k = 0; k + 1 < cut.size(); ++k) {
+    const double t0 = cut[k], t1 = cut[k + 1], mid = 0.5 * (t0 + t1);
+    if (t1 <= t0 || t0 >= rep->step_seconds) continue;
+    int comp = 99, comm = 99;
+    for (const ExecEvent& e : evs_)
+      if (e.start <= mid && mid < e.end) (e.lane == 2 ? comm : comp) = std::min(e.lane == 2 ? comm : comp, e.stage);
+    if (comp < 99) rep->busy_seconds += t1 - t0;
+    if (comm < 99) rep->comm_seconds += t1 - t0;
+    const int stg = comp < 99 ? comp : comm;
+    if (stg == 99) {
+      pending += t1 - t0;
+      continue;
+    }
+    rep->stage_seconds[stg] += t1 - t0 + pending;
+    pending = 0;
+    last_stage = stg;
+  }
+  rep->stage_seconds[last_stage] += pending;
+  rep->bubble_fraction = rep->step_seconds > 0 ? 1.0 - rep->busy_seconds / rep->step_seconds : 0.0;
+  rep->busiest_stage = static_cast<int>(std::max_element(rep->stage_seconds, rep->stage_seconds + 4) - rep->stage_seconds);
+  rep->mem_peak_bytes = static_cast<double>(g_device_bytes.load());
+  rep->n_events = static_cast<int>(evs_.size());
+  {
+    const FeasibilityReport fr = validate_plan(xp_.plan, xp_.pipeline, CostModel{}, ClusterTopology::b200_box(world_n_));
+    rep->feasible = fr.feasible ? 1 : 0;
+  }
+  const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator * xp_.rollouts
+                                                : static_cast<float>(xp_.G) * xp_.rollouts * R_;
+  rep->actor_loss = hosts_[0] ? loss[0] / denom : 0.0;
+  rep->critic_loss = hosts_[1] ? 0.5 * loss[1] / denom : 0.0;
+  const int es = xp_.experience_set(rank_);
+  if (es >= 0 && rs_[es].trainer) {
+    rep->mean_score = loss[2] / rs_[es].rows;
+    rep->mean_kl = loss[3] / (static_cast<double>(rs_[es].rows) * R_);
+  }
   rep->comm_bytes_total = comm_bytes_;
   rep->gpu_launches = launches_;
 }
 
+// ---- tensors for tests ------------------------------------------------------------------
+
 size_t Engine::tensor_bytes(const std::string& name) const {
-  const size_t br = static_cast<size_t>(Bcap_) * R_ * 4;
-  static const std::map<std::string, int> kBR = {{"logp_old", 0}, {"logp_ref", 0}, {"values", 0}, {"rewards", 0},
-                                                 {"advantages", 0}, {"returns", 0}, {"logp_new", 0}, {"values_new", 0}};
-  if (kBR.count(name)) return br;
-  if (name == "tokens" || name == "pred" || name == "margin") return static_cast<size_t>(Bcap_) * S_ * 4;
-  if (name == "score") return static_cast<size_t>(Bcap_) * 4;
-  if (name == "sample_ids") return static_cast<size_t>(Bcap_) * 4;
+  const int es = xp_.experience_set(rank_);
+  const size_t rows = es >= 0 ? static_cast<size_t>(rs_[es].rows) : 0;
+  static const std::map<std::string, int> kBR = {{"logp_old", 0}, {"logp_ref", 0}, {"values", 0}};
+  static const std::map<std::string, int> kTrain = {{"rewards", 0},  {"advantages", 0}, {"returns", 0},
+                                                    {"logp_new", 0}, {"values_new", 0}};
+  if (kBR.count(name)) return rows * R_ * 4;
+  if (kTrain.count(name)) return es >= 0 && rs_[es].trainer ? rows * R_ * 4 : 0;
+  if (name == "tokens") return rows * S_ * 4;
+  if (name == "pred" || name == "margin") return static_cast<size_t>(gen_B_) * S_ * 4;
+  if (name == "score" || name == "sample_ids") return rows * 4;
   auto flat = [](const Decoder& m, size_t e) { return static_cast<size_t>(m.n) * e; };
   if (name == "actor_grad") return flat(actor_, 4);
   if (name == "critic_grad") return flat(critic_, 4);
@@ -632,29 +867,44 @@ size_t Engine::tensor_bytes(const std::string& name) const {
 void Engine::read(const std::string& name, void* host, size_t bytes) {
   CK(cudaSetDevice(opt_.device));
   if (bytes != tensor_bytes(name) || bytes == 0) throw ConfigError("size mismatch (or tensor absent on this rank): " + name);
+  for (auto& l : lane_) CK(cudaStreamSynchronize(l));
+  const int es = xp_.experience_set(rank_);
   if (name == "sample_ids") {
-    std::memcpy(host, sample_ids_.data(), bytes);
+    std::vector<int32_t> ids(bytes / 4);
+    for (size_t r = 0; r < ids.size(); ++r) ids[r] = static_cast<int32_t>(xp_.sample_id(es, rank_, static_cast<int>(r)));
+    std::memcpy(host, ids.data(), bytes);
     return;
   }
+  const DevBuf* src = nullptr;
+  if (es >= 0) {
+    const RowBufs& b = rs_[es];
+    const std::map<std::string, const DevBuf*> rowf = {
+        {"tokens", &b.tokens}, {"logp_old", &b.logp_old}, {"logp_ref", &b.logp_ref}, {"values", &b.values},
+        {"score", &b.score}, {"rewards", &b.rewards}, {"advantages", &b.adv}, {"returns", &b.ret},
+        {"logp_new", &b.logp_new}, {"values_new", &b.values_new}};
+    auto it = rowf.find(name);
+    if (it != rowf.end()) src = it->second;
+  }
   const std::map<std::string, const DevBuf*> m = {
-      {"tokens", &tokens_}, {"pred", &pred_}, {"margin", &margin_}, {"logp_old", &logp_old_}, {"logp_ref", &logp_ref_},
-      {"values", &values_}, {"score", &score_}, {"rewards", &rewards_}, {"advantages", &adv_}, {"returns", &ret_},
-      {"logp_new", &logp_new_}, {"values_new", &values_new_}, {"actor_grad", &actor_.grad},
-      {"critic_grad", &critic_.grad}, {"actor_master", &actor_.master}, {"critic_master", &critic_.master},
-      {"actor_params", &actor_.w}, {"critic_params", &critic_.w}, {"ref_params", &ref_.w}, {"reward_params", &reward_.w},
+      {"pred", &pred_}, {"margin", &margin_}, {"actor_grad", &actor_.grad}, {"critic_grad", &critic_.grad},
+      {"actor_master", &actor_.master}, {"critic_master", &critic_.master}, {"actor_params", &actor_.w},
+      {"critic_params", &critic_.w}, {"ref_params", &ref_.w}, {"reward_params", &reward_.w},
       {"shadow_actor_params", &shadow_actor_.w}, {"shadow_critic_params", &shadow_critic_.w}};
-  auto it = m.find(name);
-  if (it == m.end()) throw ConfigError("unknown tensor " + name);
-  CK(cudaStreamSynchronize(stream_));
-  CK(cudaMemcpy(host, it->second->p, bytes, cudaMemcpyDeviceToHost));
+  if (!src) {
+    auto it = m.find(name);
+    if (it == m.end()) throw ConfigError("unknown tensor " + name);
+    src = it->second;
+  }
+  CK(cudaMemcpy(host, src->p, bytes, cudaMemcpyDeviceToHost));
 }
 
 void Engine::greedy_check(const int32_t* tokens_host, int32_t* pred_host, float* margin_host) {
   CK(cudaSetDevice(opt_.device));
   if (!generator_) throw ConfigError("this rank does not generate");
+  use_lane(0);
   const int B = gen_B_;
-  CK(cudaMemcpyAsync(tokens_.p, tokens_host, static_cast<size_t>(B) * S_ * 4, cudaMemcpyHostToDevice, stream_));
-  cudaMemsetAsync(pred_.p, 0, static_cast<size_t>(B) * S_ * 4, stream_);
+  CK(cudaMemcpyAsync(gen_tok_.p, tokens_host, static_cast<size_t>(B) * S_ * 4, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemsetAsync(pred_.p, 0, static_cast<size_t>(B) * S_ * 4, stream_));
   generate(*generator_, B, true);
   std::vector<int32_t> pred(static_cast<size_t>(B) * S_);
   std::vector<float> mar(pred.size());
@@ -719,6 +969,16 @@ extern "C" int rlhf_engine_step(rlhf_engine* e, const int32_t* prompts_host, rlh
   } catch (const std::exception& ex) {
     return flexrlhf::capi_status(ex);
   }
+}
+
+extern "C" int rlhf_engine_events(rlhf_engine* e, rlhf_event* out, int max) {
+  const std::vector<flexrlhf::ExecEvent>& ev = e->impl->events();
+  const int n = std::min<int>(max, static_cast<int>(ev.size()));
+  for (int i = 0; i < n; ++i) {
+    const flexrlhf::ExecEvent& x = ev[i];
+    out[i] = rlhf_event{x.task, x.kind, x.model, x.mb, x.rollout, x.epoch, x.lane, x.comm_op, x.stage, x.start, x.end};
+  }
+  return static_cast<int>(ev.size());
 }
 
 extern "C" void* rlhf_engine_stream(rlhf_engine* e) { return e->impl->stream(); }

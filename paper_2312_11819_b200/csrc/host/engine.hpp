@@ -2,25 +2,32 @@
 // clock (simulate(), /root/reference/proj/include/rlhfsim/simulator.hpp:46-47)
 // with real execution of the PPO iteration on one GPU per process.
 //
-// Per rank: the models this rank hosts under its placement (colocated: all
-// four; interleaving: a subset), their bf16 weights (+ fp32 master / Adam state
-// for trainable ones), one activation arena sized for the largest model, the
-// Actor's KV cache, and an NCCL communicator per device group.
+// Per rank: the models this rank hosts under its placement, their bf16 weights
+// (+ fp32 master / Adam state for trainable ones), activation arenas, the
+// generator's KV cache, one row-set buffer per device group it belongs to
+// (execplan.hpp), and NCCL communicators (world, one per trained model's
+// data-parallel group, one per ParamSync pair).  The step walks the ExecPlan --
+// the task DAG plus the exchanges the comm schedule induces -- on three CUDA
+// streams ("lanes": main compute, side compute, comm) joined by per-step events.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <string>
 #include <vector>
 
+#include "execplan.hpp"
 #include "flexrlhf/placement.hpp"
 #include "rlhf_engine.h"
 #include "rlhf_kernels.h"
 
 namespace flexrlhf {
+
+extern std::atomic<int64_t> g_device_bytes;  // bytes held by DevBufs of this process
 
 struct DevBuf {
   void* p = nullptr;
@@ -93,6 +100,24 @@ struct KVCache {
   uint16_t* Vc(int l) const { return v.as<uint16_t>() + static_cast<int64_t>(l) * B * H * Smax * hd; }
 };
 
+// Per row set this rank belongs to (ExecPlan::sets): the experience rows of its samples.
+struct RowBufs {
+  int rows = 0;
+  bool trainer = false;                            // holds a trained model: GAE + training buffers
+  DevBuf tokens;                                   // int32 [rows][S]
+  DevBuf logp_old, logp_ref, values, score;        // f32 [rows][R] ([rows] for score)
+  DevBuf rewards, adv, ret, logp_new, values_new;  // f32 [rows][R] (trainers)
+  DevBuf gbuf, gbuf2;                              // loss gradients wrt logp / values
+  void* field(Field f) const;
+};
+
+// One executed interval of the step (rlhf_event in include/rlhf_engine.h).
+struct ExecEvent {
+  int step = -1, task = -1, kind = 0, model = 0, mb = 0, rollout = 0, epoch = 0, lane = 0, comm_op = -1, stage = 0;
+  cudaEvent_t a = nullptr, b = nullptr;
+  double start = 0, end = 0;
+};
+
 class Engine {
  public:
   Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt);
@@ -101,7 +126,9 @@ class Engine {
   size_t tensor_bytes(const std::string& name) const;
   void read(const std::string& name, void* host, size_t bytes);
   void greedy_check(const int32_t* tokens_host, int32_t* pred_host, float* margin_host);
-  cudaStream_t stream() const { return stream_; }
+  cudaStream_t stream() const { return lane_[0]; }
+  const std::vector<ExecEvent>& events() const { return evs_; }
+  const ExecPlan& exec_plan() const { return xp_; }
 
  private:
   // ---- building blocks (engine_model.cpp) ----
@@ -116,19 +143,25 @@ class Engine {
   void generate(const Decoder& m, int B, bool teacher_forced);
   void decode_step(const Decoder& m, int B);
   void lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t* dst);
-  void train_actor(Decoder& m, int B, ncclComm_t comm);
-  void train_critic(Decoder& m, int B, ncclComm_t comm);
-  void train_actor_mb(Decoder& m, int b0, int B, float denom);
-  void train_critic_mb(Decoder& m, int b0, int B, float denom);
-  void adam(Decoder& m, float lr, ncclComm_t comm);
-  void allreduce_grads(Decoder& m, ncclComm_t comm);
-  void p2p(const std::vector<std::pair<const void*, size_t>>& sends, const std::vector<std::pair<void*, size_t>>& recvs);
+  void adam(Decoder& m, float lr);
   void score_logp(const Decoder& m, const int32_t* tok, int B, float* logp);
   void score_values(const Decoder& m, const int32_t* tok, int B, float* values);
   void score_reward(const Decoder& m, const int32_t* tok, int B, float* score);
-  void gae(int B);
   void build_arena(Arena& A, bool trains, bool critic_only = false);
-  void place_prompts(const int32_t* dev_prompts, int row0);
+
+  // ---- the executor (engine.cpp) ----
+  Decoder* model(ModelName m);
+  int lane_of(ModelName m) const;
+  void use_lane(int l);
+  void run_exchange(const ExecStep& s);
+  void run_task(const ExecStep& s);
+  void run_experience(const ExecStep& s);
+  void run_optimizer(const ExecStep& s, int step_index);
+  void train_rows(Decoder& m, bool actor, RowBufs& rb, int row0, int B, float denom);
+  void begin_event(int step_index, const ExecStep& s, int kind, int lane, int stage);
+  void end_event();
+  void wait_deps(int step_index, int lane);
+  void finish_report(rlhf_step_report* rep, double loss_denom);
 
   // GEMM helpers (all go through rlhf_gemm)
   void linear(const uint16_t* X, int M, int K, const uint16_t* W, int N, const uint16_t* bias, void* Y, bool y_f32,
@@ -139,44 +172,57 @@ class Engine {
                      int kv_b0 = 0);
   void gemm(rlhf_gemm_params& p);
   void kcheck(int status, const char* what);
-  void event(cudaEvent_t e) { cudaEventRecord(e, stream_); }
 
   rlhf_ppo_config cfg_;
   rlhf_engine_options opt_;
   std::string strategy_;
   int P_, R_, S_;
-  int rank_ = 0, world_n_ = 1, partner_ = -1;
-  int Bg_ = 0;     // samples of this rank's shard (prompts it owns)
-  int Bcap_ = 0;   // experience rows this rank may hold (Bg or 2*Bg)
-  int gen_B_ = 0;  // sequences this rank generates
-  int train_mb_ = 0;  // samples per TrainFB micro-batch (gradients accumulate over them)
-  PlacementPlan plan_;
+  int rank_ = 0, world_n_ = 1;
+  int Bg_ = 0;        // prompts of this rank's home shard per rollout
+  int Bcap_ = 0;      // rows of the largest Forward / Generation block this rank runs
+  int gen_B_ = 0;     // sequences per Generation task (the generator row set's per)
+  int train_mb_ = 0;  // samples per TrainFB chunk (gradients accumulate over them)
+  ExecPlan xp_;
   StrategyTag tag_ = StrategyTag::Colocated;
-  cudaStream_t stream_ = nullptr;
-  cudaStream_t stream_side_ = nullptr;  // second stream of the Co-located Forward stage
+  // lanes: 0 main compute, 1 side compute (critic-shaped models, Co-located-style ranks), 2 comm
+  cudaStream_t lane_[3] = {nullptr, nullptr, nullptr};
+  bool side_ = false;
+  cudaStream_t stream_ = nullptr;  // the lane currently enqueued on
+  int cur_lane_ = 0;
   ncclComm_t world_ = nullptr, actor_comm_ = nullptr, critic_comm_ = nullptr;
+  ncclComm_t sync_comm_[2] = {nullptr, nullptr};  // ParamSync: Actor -> ShadowActor, Critic -> ShadowCritic
+  int sync_root_[2] = {0, 0};
   double comm_bytes_ = 0;
-  std::vector<int> sample_ids_;
   int launches_ = 0;
   int pdl_ = 0;  // launch decode kernels as programmatic dependents
   bool hosts_[6] = {false, false, false, false, false, false};
 
   Decoder actor_, critic_, ref_, reward_, shadow_actor_, shadow_critic_;
   Decoder* generator_ = nullptr;
-  Arena ar_main_, ar_side_;   // activation arenas (main stream / second Forward stream)
-  Arena* arp_ = &ar_main_;  // the arena the stream_ currently in use writes
+  Arena ar_main_, ar_side_;  // activation arenas (main lane / side lane)
+  Arena* arp_ = &ar_main_;   // the arena of the lane currently in use
   KVCache kv_;
-  // per-step buffers
-  DevBuf tokens_, tok2_, pred_, margin_, pos_, prompt_stage_;
-  DevBuf logp_old_, logp_ref_, values_, score_, rewards_, adv_, ret_, logp_new_, values_new_, gbuf_, gbuf2_, loss_, out2_,
-      score2_;
-  DevBuf loop_ws_;  // persistent decode loop workspace
+  std::unique_ptr<RowBufs[]> rs_;  // indexed like xp_.sets (empty for sets this rank is not in)
+  DevBuf home_;               // int32 [rollouts * Bg][S]: this rank's prompts (first P columns)
+  DevBuf gen_tok_, pred_, margin_, pos_;  // generation staging [gen_B][S] (the decode graph's fixed rows)
+  DevBuf loss_;                           // f32 [actor_loss, critic_loss, sum score, sum kl]
+  DevBuf loop_ws_;   // persistent decode loop workspace
   DevBuf dec_top2_;  // LM-head per-tile top-2 partials [V/128][B] x float4
   DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_act_, dec_hf_, dec_logits_, argmax_ws_;
   cudaGraphExec_t decode_graph_ = nullptr;
   int graph_launches_ = 0;
   bool graph_for_pred_ = false;
-  cudaEvent_t ev_[8];
+  // per-step timing: events of every executed interval, the step's start/end
+  std::vector<ExecEvent> evs_;
+  std::vector<cudaEvent_t> ev_pool_;
+  size_t ev_next_ = 0;
+  std::vector<std::vector<int>> deps_;   // per ExecPlan step: the steps it waits for
+  std::vector<int> step_lane_;           // per ExecPlan step: lane of its last event on this rank (-1: not run)
+  std::vector<cudaEvent_t> step_done_;   // per ExecPlan step: its completion event on this rank
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prefill_;  // (gen start, prefill end), (prefill end, gen end)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> decode_;
+  cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_prefill_ = nullptr;
+  cudaEvent_t take_event();
 };
 
 }  // namespace flexrlhf

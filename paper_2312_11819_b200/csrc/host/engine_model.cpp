@@ -4,6 +4,7 @@
 // decode loop).  Every launch goes through the C-ABI of include/rlhf_kernels.h.
 // Rounding points follow DESIGN.md §3 and are mirrored by oracle/ppo_oracle.cpp.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <vector>
 #include <cmath>
@@ -17,16 +18,35 @@
 
 namespace flexrlhf {
 
+std::atomic<int64_t> g_device_bytes{0};
+
 DevBuf::~DevBuf() {
-  if (p) cudaFree(p);
+  if (p) {
+    cudaFree(p);
+    g_device_bytes -= static_cast<int64_t>(bytes);
+  }
 }
 
 void DevBuf::alloc(size_t n) {
-  if (p) cudaFree(p);
+  if (p) {
+    cudaFree(p);
+    g_device_bytes -= static_cast<int64_t>(bytes);
+  }
   p = nullptr;
-  bytes = n;
+  bytes = 0;
   if (n == 0) return;
-  if (cudaMalloc(&p, n) != cudaSuccess) throw DeviceError("cudaMalloc of " + std::to_string(n) + " bytes failed");
+  if (cudaMalloc(&p, n) != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    // an allocation the placement cannot hold is an infeasible plan (exit code 3,
+    // reference errors.hpp), not a device fault
+    throw InfeasibleError("device allocation of " + std::to_string(n) + " bytes does not fit (" +
+                          std::to_string(free_b) + " of " + std::to_string(total_b) + " bytes free)");
+  }
+  bytes = n;
+  g_device_bytes += static_cast<int64_t>(n);
   cudaMemset(p, 0, n);
 }
 
@@ -481,7 +501,7 @@ void Engine::decode_step(const Decoder& m, int B) {
   uint16_t* qkv = dec_qkv_.as<uint16_t>();
   uint16_t* o = dec_o_.as<uint16_t>();
   uint16_t* f = dec_f_.as<uint16_t>();
-  const int32_t* tok = tokens_.as<int32_t>();
+  const int32_t* tok = gen_tok_.as<int32_t>();
   // RLHF_DECODE_SKIP (debug timing only, results become wrong): bit 0 LN, 1 attention,
   // 2 qkv GEMM, 3 o-proj, 4 FFN GEMMs, 5 LM head + argmax
   static const int skip = [] { const char* e = getenv("RLHF_DECODE_SKIP"); return e ? atoi(e) : 0; }();
@@ -502,7 +522,7 @@ void Engine::decode_step(const Decoder& m, int B) {
       linear_decode(m.T(RLHF_T_W2, l), d, ff, act, B, nullptr, x, true, false, x);
     }
     K(rlhf_rmsnorm(x, m.T(RLHF_T_LNF_G), dec_hf_.as<uint16_t>(), nullptr, B, d, stream_), 1);
-    lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, graph_for_pred_ ? pred_.as<int32_t>() : tokens_.as<int32_t>());
+    lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, graph_for_pred_ ? pred_.as<int32_t>() : gen_tok_.as<int32_t>());
     return;
   }
   K(rlhf_embed_ln(tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x, m.T(RLHF_T_LN1_G, 0),
@@ -536,7 +556,7 @@ void Engine::decode_step(const Decoder& m, int B) {
     return;
   }
   K(rlhf_layernorm(x, m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), dec_hf_.as<uint16_t>(), nullptr, nullptr, B, d, stream_), 1);
-  int32_t* dst = graph_for_pred_ ? pred_.as<int32_t>() : tokens_.as<int32_t>();
+  int32_t* dst = graph_for_pred_ ? pred_.as<int32_t>() : gen_tok_.as<int32_t>();
   lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);  // also advances *pos
 }
 
@@ -558,18 +578,19 @@ void Engine::lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t
     1);
 }
 
-// Greedy generation of R tokens for the B prompts already in tokens_[:, :P].
-// teacher_forced: tokens_ already holds full sequences; predictions go to pred_.
+// Greedy generation of R tokens for the B prompts already in gen_tok_[:, :P] (the fixed
+// staging rows the decode graph was captured on).  teacher_forced: gen_tok_ already holds
+// full sequences; predictions go to pred_.
 void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   const int d = m.a.d_model, V = m.a.vocab;
   // prefill: forward over the prompt, K/V stored for every prompt position
-  forward(m, tokens_.as<int32_t>(), B, S_, P_, false, &kv_);
+  forward(m, gen_tok_.as<int32_t>(), B, S_, P_, false, &kv_);
   K(rlhf_gather_rows(arp_->hf, dec_hf_.p, B, P_, 1, P_ - 1, d, 2, stream_), 1);
   const int start = P_ - 1;
   cudaMemcpyAsync(pos_.p, &start, sizeof(int), cudaMemcpyHostToDevice, stream_);
-  int32_t* dst = teacher_forced ? pred_.as<int32_t>() : tokens_.as<int32_t>();
+  int32_t* dst = teacher_forced ? pred_.as<int32_t>() : gen_tok_.as<int32_t>();
   lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);  // also advances *pos
-  cudaEventRecord(ev_[1], stream_);  // prefill done
+  if (ev_prefill_) cudaEventRecord(ev_prefill_, stream_);  // prefill done (per Generation task)
   if (R_ <= 1) return;
   if (opt_.use_cuda_graph == 3 && !m.llama()) {  // the persistent loop implements the OPT family
     // persistent decode loop: all R-1 steps in one cooperative kernel (opt-in;
@@ -578,7 +599,7 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
     lp.arch = &m.a;
     lp.weights = m.w.p;
     lp.B = B;
-    lp.tokens = tokens_.as<int32_t>();
+    lp.tokens = gen_tok_.as<int32_t>();
     lp.tok_stride = S_;
     lp.pred = teacher_forced ? pred_.as<int32_t>() : nullptr;
     lp.margin = margin_.as<float>();
@@ -690,18 +711,13 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   }
 }
 
-void Engine::adam(Decoder& m, float lr, ncclComm_t comm) {
+// Fused AdamW on this rank's master slice (ZeRO-1: the reduce-scattered gradient shard at
+// grad[shard_off, +shard); unsharded: the whole vector), writing the bf16 compute copy.
+void Engine::adam(Decoder& m, float lr) {
   m.adam_step += 1;
-  // ZeRO-1: the gradient shard was reduce-scattered into grad[shard_off, +shard); AdamW
-  // updates the rank's master slice and its bf16 copy, then the slices are all-gathered
   K(rlhf_adamw(m.master.as<float>(), m.m.as<float>(), m.v.as<float>(), m.grad.as<float>() + m.shard_off,
                m.w.as<uint16_t>() + m.shard_off, m.shard, lr, cfg_.beta1, cfg_.beta2, cfg_.adam_eps,
                cfg_.weight_decay, m.adam_step, stream_), 1);
-  if (m.sharded && comm) {
-    NK(nccl().AllGather(m.w.as<uint16_t>() + m.shard_off, m.w.p, static_cast<size_t>(m.shard), ncclBfloat16, comm,
-                        stream_));
-    comm_bytes_ += 2.0 * static_cast<double>(m.npad - m.shard);
-  }
 }
 
 }  // namespace flexrlhf

@@ -15,9 +15,12 @@ import ctypes as C
 
 import numpy as np
 
-from .capi import EngineOptions, PPOConfig, StepReport, check, lib
+from .capi import EngineOptions, Event, PPOConfig, StepReport, check, lib
 
 STAGES = ("generation", "forward", "training", "sync")
+MODELS = ("Actor", "Critic", "Ref", "Reward", "ShadowActor", "ShadowCritic")
+EVENT_KINDS = {0: "Generation", 1: "Forward", 2: "TrainFB", 3: "Collective", 4: "ParamSync", 6: "Experience",
+               7: "AdamW"}
 
 _DTYPES = {"tokens": np.int32, "pred": np.int32, "sample_ids": np.int32, "actor_params": np.uint16,
            "critic_params": np.uint16, "ref_params": np.uint16, "reward_params": np.uint16,
@@ -27,7 +30,8 @@ _DTYPES = {"tokens": np.int32, "pred": np.int32, "sample_ids": np.int32, "actor_
 class Engine:
     def __init__(self, cfg: PPOConfig, device: int = 0, rank: int = 0, world_size: int = 1,
                  strategy: str = "colocated", nccl_id: bytes | None = None, cuda_graph: int = 1,
-                 zero_stage: int = 0, train_micro_batch: int = 0):
+                 zero_stage: int = 0, train_micro_batch: int = 0, micro_batches: int = 1, rollout_nums: int = 1,
+                 ppo_epochs: int = 1, inference_ratio: float = 0.5, ratios=None):
         L = lib()
         self._cfg = cfg
         self._keep = []
@@ -37,7 +41,9 @@ class Engine:
             self._keep.append(buf)
             idp = C.cast(buf, C.POINTER(C.c_uint8))
         opt = EngineOptions(device, rank, world_size, strategy.encode(), idp, int(cuda_graph), int(zero_stage),
-                            int(train_micro_batch))
+                            int(train_micro_batch), int(micro_batches), int(rollout_nums), int(ppo_epochs),
+                            float(inference_ratio), 1, (C.c_double * 4)(*(ratios or (0, 0, 0, 0))))
+        self.rollouts = int(rollout_nums)
         h = C.c_void_p()
         check(L.rlhf_engine_create(C.byref(cfg), C.byref(opt), C.byref(h)))
         self._h = h
@@ -59,7 +65,21 @@ class Engine:
                 "per_stage_seconds": dict(zip(STAGES, list(rep.stage_seconds))),
                 "decode_seconds": rep.decode_seconds, "prefill_seconds": rep.prefill_seconds,
                 "comm_bytes_total": rep.comm_bytes_total, "actor_loss": rep.actor_loss,
-                "critic_loss": rep.critic_loss, "gpu_launches": rep.gpu_launches}
+                "critic_loss": rep.critic_loss, "gpu_launches": rep.gpu_launches, "mean_score": rep.mean_score,
+                "mean_kl": rep.mean_kl, "busy_seconds": rep.busy_seconds, "bubble_fraction": rep.bubble_fraction,
+                "comm_seconds": rep.comm_seconds, "mem_peak_bytes": rep.mem_peak_bytes,
+                "busiest_stage": STAGES[rep.busiest_stage], "n_events": rep.n_events, "feasible": bool(rep.feasible)}
+
+    def events(self) -> list[dict]:
+        """Measured intervals of the last step (SimEvent fields; seconds from the step start)."""
+        L = lib()
+        L.rlhf_engine_events.argtypes = [C.c_void_p, C.POINTER(Event), C.c_int]
+        n = L.rlhf_engine_events(self._h, None, 0)
+        buf = (Event * max(1, n))()
+        n = L.rlhf_engine_events(self._h, buf, n)
+        return [{"task": e.task, "kind": EVENT_KINDS.get(e.kind, str(e.kind)), "model": MODELS[e.model],
+                 "micro_batch": e.micro_batch, "rollout": e.rollout, "epoch": e.epoch, "lane": e.lane,
+                 "comm_op": e.comm_op, "stage": STAGES[e.stage], "start": e.start, "end": e.end} for e in buf[:n]]
 
     @property
     def stream_handle(self) -> int:
@@ -80,12 +100,16 @@ class Engine:
             return out
         if out.size == rows * R and "params" not in name and "grad" not in name and "master" not in name:
             return out.reshape(rows, R)
-        if out.size == rows * S and name in ("tokens", "pred", "margin"):
+        if name in ("pred", "margin"):
+            return out.reshape(-1, S)
+        if out.size == rows * S and name == "tokens":
             return out.reshape(rows, S)
         return out
 
     def greedy_check(self, tokens: np.ndarray):
-        B, R = self._cfg.batch, self._cfg.gen_len
+        """Teacher-forced decode of `tokens` [B, S] (B = sequences per Generation task)."""
+        R, S = self._cfg.gen_len, self._cfg.prompt_len + self._cfg.gen_len
+        B = lib().rlhf_engine_tensor_bytes(self._h, b"pred") // (4 * S)
         tokens = np.ascontiguousarray(tokens, dtype=np.int32)
         pred = np.zeros((B, R), np.int32)
         margin = np.zeros((B, R), np.float32)

@@ -38,6 +38,8 @@ def lib():
         _lib = C.CDLL(ORACLE_SO)
         _lib.oracle_ppo_step.argtypes = [C.POINTER(PPOConfig), C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                          C.POINTER(Outputs)]
+        _lib.oracle_ppo_step_epochs.argtypes = [C.POINTER(PPOConfig), C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                                C.c_int, C.POINTER(Outputs)]
         _lib.oracle_forward_hidden.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                                C.c_void_p]
     return _lib
@@ -47,7 +49,7 @@ def ptr(a):
     return a.ctypes.data_as(C.c_void_p) if a is not None else None
 
 
-def ppo_step(cfg: PPOConfig, tokens_in=None, stop_after=0, threads=0, want_grads=True):
+def ppo_step(cfg: PPOConfig, tokens_in=None, stop_after=0, threads=0, want_grads=True, ppo_epochs=1):
     B, P, R = cfg.batch, cfg.prompt_len, cfg.gen_len
     S = P + R
     f = lambda *s: np.zeros(s, np.float32)
@@ -60,7 +62,7 @@ def ppo_step(cfg: PPOConfig, tokens_in=None, stop_after=0, threads=0, want_grads
     pred = np.zeros((B, R), np.int32)
     out = Outputs(**{k: ptr(v) for k, v in o.items()})
     tin = None if tokens_in is None else np.ascontiguousarray(tokens_in, np.int32)
-    st = lib().oracle_ppo_step(C.byref(cfg), ptr(tin), ptr(pred), stop_after, threads, C.byref(out))
+    st = lib().oracle_ppo_step_epochs(C.byref(cfg), ppo_epochs, ptr(tin), ptr(pred), stop_after, threads, C.byref(out))
     if st != 0:
         raise RuntimeError(f"oracle_ppo_step failed: {st}")
     o["greedy_pred"] = pred

@@ -1,0 +1,104 @@
+"""The executor walks the reference's task DAG (task_graph, workload.cpp:109-175) with the
+LoopParams the reference defines (workload.hpp:33-41): micro_batches > 1 (Generation /
+Forward / TrainFB micro-batches), rollout_nums > 1 (Generation + Forward rounds on new
+prompts into one experience buffer) and ppo_epochs > 1 (TrainFB passes, one AdamW step
+each).  One GPU, against the oracle run on the same samples (a batch of G * rollout_nums
+samples whose prompt ids are the engine's r * G + b) with the same number of epochs.
+
+Tolerances as tests/test_gpu_parity.py; after two AdamW steps an updated weight may differ
+by up to two sign-like steps (4 lr) where a gradient sign flipped under bf16 rounding.
+"""
+import numpy as np
+import pytest
+
+from paper_2312_11819_b200.capi import make_config, named_slices
+from tests import oracle_lib
+
+pytestmark = pytest.mark.gpu
+
+B, P, R = 4, 16, 16
+
+
+@pytest.fixture(scope="module", params=[("tiny", 2, 2, 2), ("llama-tiny", 2, 2, 2), ("tiny", 4, 1, 3)],
+                ids=lambda p: f"{p[0]}-mb{p[1]}-ro{p[2]}-ep{p[3]}")
+def run(request):
+    from paper_2312_11819_b200.engine import Engine
+    arch, mb, ro, ep = request.param
+    cfg = make_config(arch, arch, B, P, R)
+    eng = Engine(cfg, micro_batches=mb, rollout_nums=ro, ppo_epochs=ep)
+    rep = eng.step()
+    ids = eng.read("sample_ids")
+    out = {k: eng.read(k) for k in ("tokens", "logp_old", "logp_ref", "values", "score", "advantages", "returns",
+                                    "logp_new", "values_new", "actor_grad", "critic_grad", "actor_master",
+                                    "critic_master")}
+    order = np.argsort(ids)
+    for k in ("tokens", "logp_old", "logp_ref", "values", "score", "advantages", "returns", "logp_new", "values_new"):
+        out[k] = out[k][order]
+    ocfg = make_config(arch, arch, B * ro, P, R)
+    ora = oracle_lib.ppo_step(ocfg, tokens_in=out["tokens"], ppo_epochs=ep)
+    return request.param, cfg, eng, rep, np.sort(ids), out, ora
+
+
+def test_every_sample_once(run):
+    (_, _, ro, _), _, _, _, ids, _, _ = run
+    np.testing.assert_array_equal(ids, np.arange(B * ro))
+
+
+def test_greedy_tokens(run):
+    _, _, _, _, _, out, ora = run
+    np.testing.assert_array_equal(out["tokens"][:, :P], ora["tokens"][:, :P])  # prompt ids r * G + b
+    m = ora["greedy_margin"] > 1e-2
+    np.testing.assert_array_equal(out["tokens"][:, P:][m], ora["greedy_pred"][m])
+
+
+@pytest.mark.parametrize("key,atol", [("logp_old", 2e-2), ("logp_ref", 2e-2), ("values", 2e-2), ("score", 2e-2),
+                                      ("advantages", 5e-2), ("returns", 5e-2), ("logp_new", 2e-2),
+                                      ("values_new", 2e-2)])
+def test_experience_and_last_epoch_forward(run, key, atol):
+    _, _, _, _, _, out, ora = run
+    np.testing.assert_allclose(out[key], ora[key], atol=atol, rtol=1e-3)
+
+
+def test_losses_and_report(run):
+    _, _, _, rep, _, out, ora = run
+    np.testing.assert_allclose([rep["actor_loss"], rep["critic_loss"]], [ora["actor_loss"], ora["critic_loss"]],
+                               rtol=2e-2)
+    np.testing.assert_allclose(rep["mean_score"], out["score"].mean(), rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(rep["mean_kl"], (out["logp_old"] - out["logp_ref"]).mean(), rtol=1e-3, atol=1e-6)
+
+
+@pytest.mark.parametrize("tag", ["actor", "critic"])
+def test_last_epoch_gradients(run, tag):
+    _, cfg, _, _, _, out, ora = run
+    arch = cfg.actor if tag == "actor" else cfg.critic
+    for name, off, n in named_slices(arch):
+        a, b = out[f"{tag}_grad"][off:off + n].astype(np.float64), ora[f"{tag}_grad"][off:off + n].astype(np.float64)
+        assert np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-12) <= 3e-2, name
+
+
+@pytest.mark.parametrize("tag,lr", [("actor", 1e-5), ("critic", 5e-6)])
+def test_masters_after_all_epochs(run, tag, lr):
+    (_, _, _, ep), _, _, _, _, out, ora = run
+    mine, ref = out[f"{tag}_master"], ora[f"{tag}_master"]
+    assert np.abs(mine - ref).max() <= 2 * ep * lr + 1e-7
+    moved = np.abs(ref - mine) > lr
+    assert moved.mean() <= 0.02, moved.mean()
+
+
+def test_events_cover_the_dag(run):
+    """Measured SimEvents: one Generation per (rollout, micro-batch), one Forward per scorer
+    and block, one TrainFB per (trainee, micro-batch, epoch); stage seconds partition the step."""
+    (_, mb, ro, ep), _, eng, rep, _, _, _ = run
+    ev = eng.events()
+    kinds = [e["kind"] for e in ev]
+    assert kinds.count("Generation") == mb * ro
+    assert kinds.count("Forward") == 4 * mb * ro
+    assert kinds.count("TrainFB") == 2 * mb * ep
+    assert kinds.count("AdamW") == 2 * ep
+    for e in ev:
+        assert 0 <= e["start"] <= e["end"] <= rep["step_seconds"] + 1e-6
+    stages = sum(rep["per_stage_seconds"].values())
+    assert abs(stages - rep["step_seconds"]) <= 1e-3 * rep["step_seconds"] + 1e-6
+    assert 0.0 <= rep["bubble_fraction"] < 1.0
+    assert rep["busy_seconds"] <= rep["step_seconds"] + 1e-6
+    assert rep["mem_peak_bytes"] > 0 and rep["n_events"] == len(ev)
