@@ -99,6 +99,16 @@ int rlhf_comm_schedule(const char* strategy, int n_devices, int batch, int promp
                        int micro_batches, int max_ops, int* n_ops, int* kind, int* attach,
                        int* anchor, double* payload, uint32_t* group_mask);
 
+/* The planner/simulator front end (the reference's simulate / emit_trace /
+ * compare_strategies / max_batch_search / recommend / exhaustive_search /
+ * calibrate, simulator.hpp:46-54, scenario.hpp:52, planner.hpp:18-37,
+ * costmodel.hpp:89; CLI subcommands SPEC.md:547).  command: "simulate" |
+ * "trace" | "compare" | "maxbatch" | "plan" | "search" take a scenario JSON;
+ * "calibrate" takes {"scenario": ..., "observations": [...]} (measured engine
+ * steps).  Result JSON in out (NUL-terminated, up to out_len bytes); *needed =
+ * its full length + 1.  Status 2 config, 3 infeasible, 4 search cap. */
+int rlhf_sim_run(const char* command, const char* json, char* out, int out_len, int* needed);
+
 /* ---- engine --------------------------------------------------------------- */
 
 typedef struct rlhf_engine rlhf_engine;

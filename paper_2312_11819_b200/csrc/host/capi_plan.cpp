@@ -7,6 +7,7 @@
 
 #include "capi_util.hpp"
 #include "execplan.hpp"
+#include "flexrlhf/simulator.hpp"
 #include "flexrlhf/placement.hpp"
 #include "rlhf_engine.h"
 
@@ -228,6 +229,21 @@ extern "C" int rlhf_exec_plan_json(const char* strategy, int world, int batch_pe
     if (out && out_len > 0) {
       const size_t n = std::min(js.size(), static_cast<size_t>(out_len - 1));
       std::memcpy(out, js.data(), n);
+      out[n] = 0;
+    }
+    return 0;
+  } catch (const std::exception& ex) {
+    return capi_status(ex);
+  }
+}
+
+extern "C" int rlhf_sim_run(const char* command, const char* json, char* out, int out_len, int* needed) {
+  try {
+    const std::string r = run_command(command ? command : "", json ? json : "");
+    if (needed) *needed = static_cast<int>(r.size()) + 1;
+    if (out && out_len > 0) {
+      const size_t n = std::min(r.size(), static_cast<size_t>(out_len - 1));
+      std::memcpy(out, r.data(), n);
       out[n] = 0;
     }
     return 0;
