@@ -220,3 +220,18 @@ def exec_plan(strategy: str, world: int, batch_per_rank: int, prompt_len: int, g
     buf = C.create_string_buffer(need.value)
     check(L.rlhf_exec_plan_json(*args, buf, need.value, C.byref(need)))
     return json.loads(buf.value.decode())
+
+
+def sim_run(command: str, payload) -> object:
+    """The planner/simulator front end (rlhf_sim_run): command in simulate | trace | compare |
+    maxbatch | plan | search | calibrate; payload a scenario dict (calibrate: {"scenario",
+    "observations"}) or its JSON text.  Returns the parsed JSON result."""
+    import json
+    L = lib()
+    L.rlhf_sim_run.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_int)]
+    text = payload if isinstance(payload, str) else json.dumps(payload)
+    need = C.c_int(0)
+    check(L.rlhf_sim_run(command.encode(), text.encode(), None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check(L.rlhf_sim_run(command.encode(), text.encode(), buf, need.value, C.byref(need)))
+    return json.loads(buf.value.decode())

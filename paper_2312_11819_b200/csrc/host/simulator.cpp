@@ -604,12 +604,11 @@ Scenario parse_scenario(const JVal& root) {
     throw ConfigError("scenario: missing workload");
   }
   if (const JVal* sv = r.get("strategies")) {
-    if (sv->type != JVal::Arr || sv->a.empty()) throw ConfigError("scenario: strategies must be a non-empty array");
+    if (sv->type != JVal::Arr) throw ConfigError("scenario: strategies must be an array");
     for (size_t i = 0; i < sv->a.size(); ++i)
       s.strategies.push_back(parse_strategy(sv->a[i], "strategies[" + std::to_string(i) + "]"));
-  } else {
-    s.strategies.push_back(ScenarioStrategy{});
   }
+  if (s.strategies.empty()) s.strategies.push_back(ScenarioStrategy{});  // (plan / search ignore it)
   if (const JVal* cv = r.get("cost_model")) {
     Obj c(*cv, "cost_model");
     CommConstants& k = s.cost.comm;
@@ -995,8 +994,13 @@ std::string run_command(const std::string& cmd, const std::string& json) {
       if (!stv) throw ConfigError("calibrate: observation without strategy");
       const ScenarioStrategy ss = parse_strategy(*stv, "observations[].strategy");
       x.name = ss.cfg.name;
-      x.devices = o.integer("devices", 1);
-      x.topo = ClusterTopology::b200_box(x.devices);
+      // the scenario's device kind at the observation's device count (one node)
+      TopologySpec ts = sc.topology;
+      x.devices = o.integer("devices", ClusterTopology::build(ts).device_count());
+      ts.groups.resize(1);
+      ts.groups[0].nodes = 1;
+      ts.groups[0].devices_per_node = x.devices;
+      x.topo = ClusterTopology::build(ts);
       LoopParams lp = sc.loop;
       lp.batch_size = o.integer("batch", lp.batch_size);
       lp.micro_batches = o.integer("micro_batches", lp.micro_batches);
