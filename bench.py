@@ -24,6 +24,8 @@ from __future__ import annotations
 
 import argparse
 import json
+
+import numpy as np
 import os
 import statistics
 import subprocess
@@ -133,9 +135,10 @@ METRIC = "PPO samples/sec per RLHF step (gen/fwd/train split)"  # identical in b
 def arm_config(args, wl, world):
     """The `config` object both arms print (the driver compares the arms on it)."""
     B, P, R = wl["batch"], wl["prompt"], wl["gen"]
-    return {"workload": wl["name"], "placement": args.strategy, "global_batch": B * world,
+    return {"workload": wl["name"], "placement": args.strategy, "global_batch": B * world * args.rollouts,
             "prompt_len": P, "gen_len": R, "parallelism": f"dp{world}", "zero_stage": args.zero,
-            "train_micro_batch": args.train_mb,
+            "train_micro_batch": args.train_mb, "micro_batches": args.micro_batches, "rollout_nums": args.rollouts,
+            "ppo_epochs": args.epochs,
             "l2": "working set (4 models' weights + activations) >> 126 MB L2 every step"}
 
 
@@ -164,6 +167,23 @@ def reference_arm(args, wl, rank, world=1):
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def write_trace(path, per_rank_events):
+    """Chrome trace of the measured step: one process per rank, threads = lanes (0 main
+    compute, 1 side compute, 2 comm); names "<stage>:<model>:mb<i>" as emit_trace."""
+    ev = []
+    for rank, events in enumerate(per_rank_events):
+        ev.append({"ph": "M", "name": "process_name", "pid": rank, "args": {"name": f"rank {rank} (B200)"}})
+        for lane, name in enumerate(("compute", "compute (side)", "comm")):
+            ev.append({"ph": "M", "name": "thread_name", "pid": rank, "tid": lane, "args": {"name": name}})
+        for e in events:
+            ev.append({"ph": "X", "pid": rank, "tid": e["lane"], "cat": e["kind"],
+                       "name": f"{e['stage']}:{e['model']}:mb{e['micro_batch']}",
+                       "ts": round(e["start"] * 1e6, 3), "dur": round((e["end"] - e["start"]) * 1e6, 3),
+                       "args": {"task": e["task"], "rollout": e["rollout"], "epoch": e["epoch"]}})
+    with open(path, "w") as f:
+        json.dump({"displayTimeUnit": "ms", "traceEvents": ev}, f)
 
 
 def profile_json(name):
@@ -217,6 +237,10 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch override (memory studies)")
     ap.add_argument("--train-mb", type=int, default=0, help="samples per TrainFB micro-batch (0: all)")
     ap.add_argument("--zero", type=int, default=0, choices=[0, 1], help="ZeRO stage of the trainable models")
+    ap.add_argument("--micro-batches", type=int, default=1, help="LoopParams::micro_batches (task-DAG micro-batches)")
+    ap.add_argument("--rollouts", type=int, default=1, help="LoopParams::rollout_nums")
+    ap.add_argument("--epochs", type=int, default=1, help="LoopParams::ppo_epochs")
+    ap.add_argument("--trace", default="", help="write a Chrome trace of the last step's measured events (all ranks)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
     if args.batch:
@@ -244,8 +268,11 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     eng = Engine(cfg, device=local, rank=rank, world_size=world, strategy=args.strategy, nccl_id=nid,
-                 zero_stage=args.zero, train_micro_batch=args.train_mb)
-    prompts = prompt_tokens(cfg.prompt_seed, B, P, cfg.actor.vocab, sample_offset=rank * B)
+                 zero_stage=args.zero, train_micro_batch=args.train_mb, micro_batches=args.micro_batches,
+                 rollout_nums=args.rollouts, ppo_epochs=args.epochs)
+    # this rank's home prompts, rollout-major ([rollouts * B, P]; rollout r = global ids r*G + ...)
+    prompts = np.concatenate([prompt_tokens(cfg.prompt_seed, B, P, cfg.actor.vocab, sample_offset=r * B * world + rank * B)
+                              for r in range(args.rollouts)])
 
     for _ in range(args.warmup):
         eng.step(prompts)
@@ -267,21 +294,47 @@ def main():
     clk = clocks.stop() if rank == 0 else None
     e2e_s = e0.elapsed_time(e1) / 1e3
     dev_s = sum(r["step_seconds"] for r in reps)
-    stage = {k: sum(r["per_stage_seconds"][k] for r in reps) / args.steps for k in reps[0]["per_stage_seconds"]}
-    dec_s = sum(r["decode_seconds"] for r in reps)
-    launches = sum(r["gpu_launches"] for r in reps)
     free_b, total_b = torch.cuda.mem_get_info()
-    mem_gb = (total_b - free_b) / 1e9
+    # this rank's measured SimReport fields (per step): its own compute-lane stage attribution,
+    # busy / bubble, and the sequences its Generation tasks decode
+    gen_rows = eng.generation_rows
+    mine = {"rank": rank, "stage": {k: sum(r["per_stage_seconds"][k] for r in reps) / args.steps
+                                    for k in reps[0]["per_stage_seconds"]},
+            "busy_s": sum(r["busy_seconds"] for r in reps) / args.steps,
+            "bubble_fraction": sum(r["bubble_fraction"] for r in reps) / args.steps,
+            "comm_s": sum(r["comm_seconds"] for r in reps) / args.steps,
+            "decode_s": sum(r["decode_seconds"] for r in reps), "gen_rows": gen_rows,
+            "launches": sum(r["gpu_launches"] for r in reps), "mem_gb": (total_b - free_b) / 1e9,
+            "engine_mem_gb": reps[-1]["mem_peak_bytes"] / 1e9}
+    events = eng.events() if args.trace else None
+    ranks = [mine]
     if world > 1:
-        t = torch.tensor([e2e_s, dev_s, dec_s, mem_gb], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s, dev_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s, dev_s, dec_s, mem_gb = t.tolist()
+        e2e_s, dev_s = t.tolist()
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
+        if args.trace:
+            evs = [None] * world
+            dist.all_gather_object(evs, events)
+            events = evs
+    elif args.trace:
+        events = [events]
     if rank != 0:
         dist.destroy_process_group()
         return 0
+    if args.trace:
+        write_trace(args.trace, events)
+    launches = sum(r["launches"] for r in ranks)
+    mem_gb = max(r["mem_gb"] for r in ranks)
+    # stage split: each stage's seconds on the rank where it is longest (a rank's idle time
+    # goes to the stage it waits for); the per-rank splits are reported beside it
+    stage = {k: max(r["stage"][k] for r in ranks) for k in ranks[0]["stage"]}
+    gen_rank = max(ranks, key=lambda r: (r["gen_rows"], r["decode_s"]))  # the generating rank(s)
 
     hbm, tf_burst, tf_sus, src = peaks()
-    dbytes = decode_bytes_per_step(cfg.actor, B, P, R)
+    dbytes = decode_bytes_per_step(cfg.actor, gen_rank["gen_rows"], P, R)
+    dec_s = gen_rank["decode_s"] / (args.rollouts * args.micro_batches)  # per Generation task
     dec_per_launch = dec_s / (args.steps * max(1, R - 1))
     tr = profile_json("r1_decode_traffic.json") if args.workload == "c2" else None
     roof_decode = {"bound": "hbm", "kernel": "decode step (CUDA graph: swap-AB tcgen05 GEMMs + decode attention)",
@@ -302,7 +355,7 @@ def main():
         cpu = {"value": 1.0 / t, "unit": "samples/s", "cores": cores, "kind": "port",
                "sample": f"1 sample of {wl['name']}: full PPO step in oracle/ppo_oracle.cpp ({t:.1f} s)"}
     S = P + R
-    samples = B * world * args.steps
+    samples = B * world * args.rollouts * args.steps
     line = {
         "metric": METRIC,
         "value": samples / dev_s, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -311,8 +364,12 @@ def main():
         "config": arm_config(args, wl, world),
         "split_seconds_per_step": stage,
         "split_fraction": {k: v / (dev_s / args.steps) for k, v in stage.items()},
-        "e2e": {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": B * P * 4,
-                "d2h_bytes_per_step": 8},
+        "split_by_rank": [{"rank": r["rank"], **{k: round(v, 6) for k, v in r["stage"].items()},
+                           "busy_s": round(r["busy_s"], 6), "bubble_fraction": round(r["bubble_fraction"], 4),
+                           "comm_s": round(r["comm_s"], 6), "generation_rows": r["gen_rows"],
+                           "engine_mem_gb": round(r["engine_mem_gb"], 2)} for r in ranks],
+        "e2e": {"value": samples / e2e_s, "unit": "samples/s",
+                "h2d_bytes_per_step": B * args.rollouts * (P + R) * 4, "d2h_bytes_per_step": 16},
         "gpu_launches": launches,
         "roofline": roof_decode,
         "roofline_gemm": roof_gemm,

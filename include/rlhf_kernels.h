@@ -208,6 +208,13 @@ int rlhf_kv_store(const void* qkv, int B, int T, int p0, const int* p0_dev, int 
 /* Decode attention: one query per sample at position p (= *pos_dev), keys 0..p. */
 int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax, const void* kcache, const void* vcache,
                      const int* pos_dev, void* out, rlhf_stream_t s);
+/* The same, then pulls the (sample, head) rows [0, pos] of the NEXT attention's K/V cache
+ * (kcache_next / vcache_next: layer l+1, or layer 0 of the next decode step) into L2 with
+ * cp.async.bulk.prefetch.L2 -- those rows do not change before that attention runs, and
+ * the latency-bound GEMMs in between leave HBM idle. */
+int rlhf_attn_decode_prefetch(const void* qkv, int B, int H, int hd, int Smax, const void* kcache, const void* vcache,
+                              const int* pos_dev, void* out, const void* kcache_next, const void* vcache_next,
+                              rlhf_stream_t s);
 
 /* ---- heads, experience, PPO (Generation, Forward, TrainFB) ---------------- */
 /* logp[r] = z[r, y_r] - logsumexp(z[r, :]), y_r = tokens[b*S + P + j] for r = b*R + j; lse saved. */

@@ -505,6 +505,9 @@ void Engine::decode_step(const Decoder& m, int B) {
   // RLHF_DECODE_SKIP (debug timing only, results become wrong): bit 0 LN, 1 attention,
   // 2 qkv GEMM, 3 o-proj, 4 FFN GEMMs, 5 LM head + argmax
   static const int skip = [] { const char* e = getenv("RLHF_DECODE_SKIP"); return e ? atoi(e) : 0; }();
+  // next-attention K/V pulled into L2 by each decode attention: measured SLOWER (c2 decode step 492 -> 512 us,
+  // c3 1547 -> 1664 us), so off unless RLHF_DEC_KV_PREFETCH=1
+  static const bool pf_kv = [] { const char* e = getenv("RLHF_DEC_KV_PREFETCH"); return e && atoi(e) != 0; }();
   if (m.llama()) {
     // LLaMA: RMSNorm, [QKV GEMM], rotary q/k + KV-cache store, attention, [O-proj + residual],
     // RMSNorm, [gate|up GEMM], SwiGLU, [down + residual]; final RMSNorm, untied head
@@ -514,7 +517,9 @@ void Engine::decode_step(const Decoder& m, int B) {
       if (l > 0) K(rlhf_rmsnorm(x, m.T(RLHF_T_LN1_G, l), h, nullptr, B, d, stream_), 1);
       linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, nullptr, qkv, false, false, nullptr);
       K(rlhf_rope_qkv(qkv, B, 1, 0, pos, H, hd, m.rope.as<float>(), 0, kv_.Kc(l), kv_.Vc(l), kv_.Smax, stream_), 1);
-      K(rlhf_attn_decode(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o, stream_), 1);
+      K(rlhf_attn_decode_prefetch(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o,
+                                  pf_kv ? kv_.Kc((l + 1) % a.n_layers) : nullptr,
+                                  pf_kv ? kv_.Vc((l + 1) % a.n_layers) : nullptr, stream_), 1);
       linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, nullptr, x, true, false, x);
       K(rlhf_rmsnorm(x, m.T(RLHF_T_LN2_G, l), h, nullptr, B, d, stream_), 1);
       linear_decode(m.T(RLHF_T_W1, l), 2 * ff, d, h, B, nullptr, f, false, false, nullptr);
@@ -542,7 +547,10 @@ void Engine::decode_step(const Decoder& m, int B) {
     if (!(skip & 4))
       linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr,
                     fl1 ? x : nullptr, fl1 ? m.T(RLHF_T_LN1_G, l) : nullptr, fl1 ? m.T(RLHF_T_LN1_B, l) : nullptr, l);
-    if (!(skip & 2)) K(rlhf_attn_decode(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o, stream_), 1);
+    if (!(skip & 2))
+      K(rlhf_attn_decode_prefetch(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o,
+                                  pf_kv ? kv_.Kc((l + 1) % a.n_layers) : nullptr,
+                                  pf_kv ? kv_.Vc((l + 1) % a.n_layers) : nullptr, stream_), 1);
     if (!(skip & 8)) linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, m.T(RLHF_T_BO, l), x, true, false, x);
     if (!(skip & 1) && !fl) K(rlhf_layernorm(x, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h, nullptr, nullptr, B, d, stream_), 1);
     if (!(skip & 16)) {

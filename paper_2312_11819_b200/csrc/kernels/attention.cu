@@ -175,12 +175,18 @@ __device__ __forceinline__ void dec_issue(uint16_t* ring, const uint16_t* src, i
            &bars[slot]);
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 template <int HD, int NS_>
 __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t* __restrict__ qkv, int H, int Smax,
                                                                   const uint16_t* __restrict__ kc,
                                                                   const uint16_t* __restrict__ vc,
                                                                   const int* __restrict__ pos_dev,
-                                                                  uint16_t* __restrict__ out) {
+                                                                  uint16_t* __restrict__ out,
+                                                                  const uint16_t* __restrict__ kc_next,
+                                                                  const uint16_t* __restrict__ vc_next) {
   using Cf = DecCfg<HD, NS_>;
   constexpr int RB = Cf::RB, NS = Cf::NS, LPR = Cf::LPR, RPW = Cf::RPW, NW = kDecThreads / 32;
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -326,6 +332,17 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
     for (int g2 = 0; g2 < G; ++g2) o += part[g2 * HD + e];
     out[static_cast<int64_t>(b) * d + h * HD + e] = f2bf_a(o);
   }
+  // The next attention of the step chain (layer l+1, or layer 0 of the next step) reads this
+  // (sample, head)'s cached rows [0, ctx) of its own layer: nothing computed in between
+  // changes them, so they are pulled into L2 now, while the latency-bound O-proj / FFN /
+  // QKV kernels leave HBM mostly idle, and that attention streams them from L2.
+  if (kc_next && threadIdx.x < 2) {
+    const uint16_t* src = (threadIdx.x == 0 ? kc_next : vc_next) + static_cast<int64_t>(bh) * Smax * HD;
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int rows = min(RB, ctx - blk * RB);
+      prefetch_l2(src + static_cast<int64_t>(blk) * RB * HD, static_cast<uint32_t>(rows * HD * 2));
+    }
+  }
 }
 
 }  // namespace rlhf
@@ -373,7 +390,7 @@ extern "C" int rlhf_kv_store(const void* qkv, int B, int T, int p0, const int* p
 
 template <int HD, int NS>
 static int launch_dec_ns(int grid, cudaStream_t st, const uint16_t* q, int H, int Smax, const uint16_t* k,
-                         const uint16_t* v, const int* pos_dev, uint16_t* o) {
+                         const uint16_t* v, const int* pos_dev, uint16_t* o, const uint16_t* kn, const uint16_t* vn) {
   const size_t smem = DecCfg<HD, NS>::smem(Smax);
   static size_t configured = 0;  // per-instantiation opt-in to > 48 KB dynamic shared memory
   if (smem > configured) {
@@ -382,19 +399,20 @@ static int launch_dec_ns(int grid, cudaStream_t st, const uint16_t* q, int H, in
       return 5;
     configured = smem;
   }
-  return launch_k(attn_decode_kernel<HD, NS>, dim3(grid), dim3(kDecThreads), smem, st, q, H, Smax, k, v, pos_dev, o);
+  return launch_k(attn_decode_kernel<HD, NS>, dim3(grid), dim3(kDecThreads), smem, st, q, H, Smax, k, v, pos_dev, o, kn,
+                  vn);
 }
 
 template <int HD>
 static int launch_dec(int grid, cudaStream_t st, const uint16_t* q, int H, int Smax, const uint16_t* k, const uint16_t* v,
-                      const int* pos_dev, uint16_t* o) {
+                      const int* pos_dev, uint16_t* o, const uint16_t* kn, const uint16_t* vn) {
   // RLHF_ATTN_NS: ring depth override (timing experiments only)
   static const int ns = [] { const char* e = getenv("RLHF_ATTN_NS"); return e ? atoi(e) : 0; }();
   switch (ns) {
-    case 1: return launch_dec_ns<HD, 1>(grid, st, q, H, Smax, k, v, pos_dev, o);
-    case 2: return launch_dec_ns<HD, 2>(grid, st, q, H, Smax, k, v, pos_dev, o);
-    case 4: return launch_dec_ns<HD, 4>(grid, st, q, H, Smax, k, v, pos_dev, o);
-    case 8: return launch_dec_ns<HD, 8>(grid, st, q, H, Smax, k, v, pos_dev, o);
+    case 1: return launch_dec_ns<HD, 1>(grid, st, q, H, Smax, k, v, pos_dev, o, kn, vn);
+    case 2: return launch_dec_ns<HD, 2>(grid, st, q, H, Smax, k, v, pos_dev, o, kn, vn);
+    case 4: return launch_dec_ns<HD, 4>(grid, st, q, H, Smax, k, v, pos_dev, o, kn, vn);
+    case 8: return launch_dec_ns<HD, 8>(grid, st, q, H, Smax, k, v, pos_dev, o, kn, vn);
     default: break;
   }
   // one wave: 4 ring slots (3 CTAs / SM) while the (sample, head) grid fits, else 3 slots
@@ -405,21 +423,30 @@ static int launch_dec(int grid, cudaStream_t st, const uint16_t* q, int H, int S
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  if (HD == 128 || grid <= 3 * sms) return launch_dec_ns<HD, DecCfg<HD>::NS>(grid, st, q, H, Smax, k, v, pos_dev, o);
-  if (grid <= 4 * sms) return launch_dec_ns<HD, 3>(grid, st, q, H, Smax, k, v, pos_dev, o);
-  return launch_dec_ns<HD, 2>(grid, st, q, H, Smax, k, v, pos_dev, o);
+  if (HD == 128 || grid <= 3 * sms) return launch_dec_ns<HD, DecCfg<HD>::NS>(grid, st, q, H, Smax, k, v, pos_dev, o, kn, vn);
+  if (grid <= 4 * sms) return launch_dec_ns<HD, 3>(grid, st, q, H, Smax, k, v, pos_dev, o, kn, vn);
+  return launch_dec_ns<HD, 2>(grid, st, q, H, Smax, k, v, pos_dev, o, kn, vn);
+}
+
+extern "C" int rlhf_attn_decode_prefetch(const void* qkv, int B, int H, int hd, int Smax, const void* kcache,
+                                         const void* vcache, const int* pos_dev, void* out, const void* kcache_next,
+                                         const void* vcache_next, rlhf_stream_t s) {
+  if (Smax > kDecMaxCtx) return 2;
+  if (!kcache_next != !vcache_next) return 2;
+  const auto* q = static_cast<const uint16_t*>(qkv);
+  const auto* k = static_cast<const uint16_t*>(kcache);
+  const auto* v = static_cast<const uint16_t*>(vcache);
+  const auto* kn = static_cast<const uint16_t*>(kcache_next);
+  const auto* vn = static_cast<const uint16_t*>(vcache_next);
+  auto* o = static_cast<uint16_t*>(out);
+  switch (hd) {
+    case 64: return launch_dec<64>(B * H, AS(s), q, H, Smax, k, v, pos_dev, o, kn, vn);
+    case 128: return launch_dec<128>(B * H, AS(s), q, H, Smax, k, v, pos_dev, o, kn, vn);
+    default: return 2;
+  }
 }
 
 extern "C" int rlhf_attn_decode(const void* qkv, int B, int H, int hd, int Smax, const void* kcache, const void* vcache,
                                 const int* pos_dev, void* out, rlhf_stream_t s) {
-  if (Smax > kDecMaxCtx) return 2;
-  const auto* q = static_cast<const uint16_t*>(qkv);
-  const auto* k = static_cast<const uint16_t*>(kcache);
-  const auto* v = static_cast<const uint16_t*>(vcache);
-  auto* o = static_cast<uint16_t*>(out);
-  switch (hd) {
-    case 64: return launch_dec<64>(B * H, AS(s), q, H, Smax, k, v, pos_dev, o);
-    case 128: return launch_dec<128>(B * H, AS(s), q, H, Smax, k, v, pos_dev, o);
-    default: return 2;
-  }
+  return rlhf_attn_decode_prefetch(qkv, B, H, hd, Smax, kcache, vcache, pos_dev, out, nullptr, nullptr, s);
 }

@@ -82,6 +82,12 @@ class Engine:
                  "comm_op": e.comm_op, "stage": STAGES[e.stage], "start": e.start, "end": e.end} for e in buf[:n]]
 
     @property
+    def generation_rows(self) -> int:
+        """Sequences each Generation task of this rank decodes (0: the rank does not generate)."""
+        S = self._cfg.prompt_len + self._cfg.gen_len
+        return lib().rlhf_engine_tensor_bytes(self._h, b"pred") // (4 * S)
+
+    @property
     def stream_handle(self) -> int:
         """cudaStream_t the engine launches on (for CUDA-event timing)."""
         return lib().rlhf_engine_stream(self._h)
