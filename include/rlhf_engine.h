@@ -184,6 +184,12 @@ typedef struct rlhf_event {
   double start, end;      /* seconds from the step's start */
 } rlhf_event;
 
+/* max_batch_search (simulator.hpp:53-54) against the real allocator: the largest per-rank
+ * batch (a multiple of opt->micro_batches, <= cap) whose single-GPU engine allocates (and,
+ * with run_step, runs one PPO step); 0 when batch 1 does not fit. */
+int rlhf_engine_max_batch(const rlhf_ppo_config* cfg, const rlhf_engine_options* opt, int cap, int run_step,
+                          int* best);
+
 /* Copy up to max events of the last step; returns the count (or -status). */
 int rlhf_engine_events(rlhf_engine* e, rlhf_event* out, int max);
 

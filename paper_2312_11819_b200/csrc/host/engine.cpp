@@ -971,6 +971,54 @@ extern "C" int rlhf_engine_step(rlhf_engine* e, const int32_t* prompts_host, rlh
   }
 }
 
+// Largest per-rank batch whose engine fits the device (max_batch_search, simulator.hpp:53-54,
+// against the real allocator instead of the analytic memory model): doubling then bisection
+// over engine constructions; an allocation that does not fit surfaces as InfeasibleError.
+extern "C" int rlhf_engine_max_batch(const rlhf_ppo_config* cfg, const rlhf_engine_options* opt, int cap, int run_step,
+                                     int* best) {
+  try {
+    if (!best || cap < 1) throw flexrlhf::ConfigError("rlhf_engine_max_batch: cap >= 1 and an output are required");
+    if (opt->world_size > 1) throw flexrlhf::ConfigError("rlhf_engine_max_batch: single-GPU engines only");
+    const int mb = std::max(1, opt->micro_batches);
+    auto fits = [&](int k) {
+      rlhf_ppo_config c = *cfg;
+      c.batch = k * mb;
+      try {
+        Engine e(c, *opt);
+        if (run_step) {
+          rlhf_step_report r;
+          e.step(nullptr, &r);
+        }
+        return true;
+      } catch (const flexrlhf::InfeasibleError&) {
+        cudaGetLastError();
+        return false;
+      }
+    };
+    *best = 0;
+    const int kmax = cap / mb;
+    if (kmax < 1 || !fits(1)) return 0;
+    int lo = 1, hi = 1;
+    while (hi < kmax) {  // doubling: lo fits, hi + 1 .. unknown
+      const int nxt = std::min(kmax, hi * 2);
+      if (!fits(nxt)) {
+        hi = nxt - 1;
+        break;
+      }
+      lo = hi = nxt;
+    }
+    while (lo < hi) {
+      const int m = lo + (hi - lo + 1) / 2;
+      if (fits(m)) lo = m;
+      else hi = m - 1;
+    }
+    *best = lo * mb;
+    return 0;
+  } catch (const std::exception& ex) {
+    return flexrlhf::capi_status(ex);
+  }
+}
+
 extern "C" int rlhf_engine_events(rlhf_engine* e, rlhf_event* out, int max) {
   const std::vector<flexrlhf::ExecEvent>& ev = e->impl->events();
   const int n = std::min<int>(max, static_cast<int>(ev.size()));

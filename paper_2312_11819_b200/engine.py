@@ -49,6 +49,19 @@ class Engine:
         self._h = h
 
     @staticmethod
+    def max_batch(cfg: PPOConfig, cap: int, run_step: bool = False, device: int = 0, **kw) -> int:
+        """max_batch_search against the real allocator (rlhf_engine_max_batch, one GPU)."""
+        L = lib()
+        L.rlhf_engine_max_batch.argtypes = [C.POINTER(PPOConfig), C.POINTER(EngineOptions), C.c_int, C.c_int,
+                                            C.POINTER(C.c_int)]
+        opt = EngineOptions(device, 0, 1, kw.get("strategy", "colocated").encode(), None, 1,
+                            int(kw.get("zero_stage", 0)), int(kw.get("train_micro_batch", 0)),
+                            int(kw.get("micro_batches", 1)), 1, 1, 0.5, 1, (C.c_double * 4)(0, 0, 0, 0))
+        best = C.c_int(0)
+        check(L.rlhf_engine_max_batch(C.byref(cfg), C.byref(opt), int(cap), int(run_step), C.byref(best)))
+        return best.value
+
+    @staticmethod
     def nccl_unique_id() -> bytes:
         buf = (C.c_uint8 * 128)()
         check(lib().rlhf_nccl_unique_id(buf))

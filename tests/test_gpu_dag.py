@@ -104,3 +104,16 @@ def test_events_cover_the_dag(run):
     assert 0.0 <= rep["bubble_fraction"] < 1.0
     assert rep["busy_seconds"] <= rep["step_seconds"] + 1e-6
     assert rep["mem_peak_bytes"] > 0 and rep["n_events"] == len(ev)
+
+
+def test_max_batch_against_the_real_allocator():
+    """max_batch_search (simulator.hpp:53-54) on the device: OPT-1.3B Actor/Ref + OPT-350m
+    Critic/Reward with S = 512 -- the largest batch whose engine allocates; one more does not."""
+    from paper_2312_11819_b200.engine import Engine
+    cfg = make_config("opt-1.3b", "opt-350m", 1, 256, 256)
+    best = Engine.max_batch(cfg, cap=1024)
+    assert 16 <= best < 1024, best
+    cfg.batch = best
+    rep = Engine(cfg).step()  # the found batch runs a full PPO step
+    assert rep["throughput_samples_per_sec"] > 0
+    print("max batch (c3 pair, one B200):", best)
