@@ -918,6 +918,39 @@ void Engine::greedy_check(const int32_t* tokens_host, int32_t* pred_host, float*
     }
 }
 
+SimReport execute(Engine& engine, const int32_t* prompts_host) {
+  rlhf_step_report rep;
+  engine.step(prompts_host, &rep);
+  SimReport r;
+  r.step_seconds = rep.step_seconds;
+  r.throughput_samples_per_sec = rep.throughput_samples_per_sec;
+  for (const ExecEvent& x : engine.events()) {
+    SimEvent e;
+    e.task_id = x.task;
+    // the experience barrier (GAE) and AdamW intervals are TrainFB-stage work in SimEvent terms
+    e.kind = x.kind <= static_cast<int>(TaskKind::Barrier) ? static_cast<TaskKind>(x.kind) : TaskKind::TrainFB;
+    e.model = static_cast<ModelName>(x.model);
+    e.micro_batch = x.mb;
+    e.stage = static_cast<Stage>(x.stage);
+    e.comm_lane = x.lane == 2;
+    e.start = x.start;
+    e.end = x.end;
+    e.devices = {engine.rank()};
+    r.events.push_back(e);
+  }
+  for (int k = 0; k < 4; ++k) {
+    r.per_stage_seconds[static_cast<Stage>(k)] = rep.stage_seconds[k];
+    r.per_stage_fraction[static_cast<Stage>(k)] = rep.step_seconds > 0 ? rep.stage_seconds[k] / rep.step_seconds : 0;
+  }
+  r.per_device_busy_seconds[engine.rank()] = rep.busy_seconds;
+  r.per_device_mem_peak[engine.rank()] = rep.mem_peak_bytes;
+  r.comm_bytes_total = rep.comm_bytes_total;
+  r.bubble_fraction = rep.bubble_fraction;
+  r.busiest_stage = static_cast<Stage>(rep.busiest_stage);
+  r.feasible = rep.feasible != 0;
+  return r;
+}
+
 }  // namespace flexrlhf
 
 // ---- C-ABI ---------------------------------------------------------------------

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "execplan.hpp"
+#include "flexrlhf/simulator.hpp"
 #include "flexrlhf/placement.hpp"
 #include "rlhf_engine.h"
 #include "rlhf_kernels.h"
@@ -129,6 +130,7 @@ class Engine {
   cudaStream_t stream() const { return lane_[0]; }
   const std::vector<ExecEvent>& events() const { return evs_; }
   const ExecPlan& exec_plan() const { return xp_; }
+  int rank() const { return rank_; }
 
  private:
   // ---- building blocks (engine_model.cpp) ----
@@ -224,5 +226,11 @@ class Engine {
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_prefill_ = nullptr;
   cudaEvent_t take_event();
 };
+
+// The measured counterpart of simulate() (simulator.hpp:46-47) in the same vocabulary: one
+// PPO iteration on this rank's device, returned as a SimReport whose events are this rank's
+// measured intervals (devices = {rank}, comm_lane for lane 2), per-stage seconds / fractions
+// with the same compute-lane attribution, busy seconds, bubble fraction and memory.
+SimReport execute(Engine& engine, const int32_t* prompts_host = nullptr);
 
 }  // namespace flexrlhf
