@@ -312,12 +312,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   DPROBE(5);
-  mbar_wait(recv_bar, 0);  // all slices' rows of this CTA's share have landed
-  DPROBE(6);
-
   // ---- reduce rows [split*rows_per, +rows_per) over the slices in slice order.
   // Work unit = (row r, 4 consecutive columns); consecutive threads -> consecutive m.
   const int units = rows_per * (BN / 4);
+  // the first unit's residual (the common case: one unit per thread) is loaded while the
+  // peers' partial rows are still in flight
+  float res0[4] = {0.f, 0.f, 0.f, 0.f};
+  if (e.residual && static_cast<int>(threadIdx.x) < units) {
+    const int u = threadIdx.x, m = m0 + split * rows_per + u % rows_per, c4 = (u / rows_per) * 4;
+    if (m < e.M) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (c4 + t < e.N) res0[t] = e.residual[static_cast<int64_t>(c4 + t) * e.ldy + m];
+    }
+  }
+  mbar_wait(recv_bar, 0);  // all slices' rows of this CTA's share have landed
+  DPROBE(6);
+
 #pragma unroll 1
   for (int u = threadIdx.x; u < units; u += kThreads) {
     const int rl = u % rows_per;
@@ -325,8 +336,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int c4 = (u / rows_per) * 4;
     const int m = m0 + r;
     const bool mok = m < e.M;
-    float res[4] = {0.f, 0.f, 0.f, 0.f};
-    if (e.residual && mok) {
+    float res[4] = {res0[0], res0[1], res0[2], res0[3]};
+    if (e.residual && mok && u >= kThreads) {
 #pragma unroll
       for (int t = 0; t < 4; ++t)
         if (c4 + t < e.N) res[t] = e.residual[static_cast<int64_t>(c4 + t) * e.ldy + m];
