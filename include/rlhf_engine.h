@@ -127,7 +127,9 @@ typedef struct rlhf_engine_options {
                                  (StrategyConfig::zero_level, scenario.hpp:12-26; memory model
                                  costmodel.hpp:48-50): 0 replicated (gradient all-reduce); 1 fp32
                                  master/m/v sharded 1/dp per rank (gradient reduce-scatter, AdamW on
-                                 the shard, bf16 weight all-gather) — bit-identical updates */
+                                 the shard, bf16 weight all-gather) -- bit-identical updates; 2 also
+                                 the gradients: per-layer buckets reduce-scattered on the comm stream
+                                 as the backward finishes each layer, no full fp32 gradient resident */
   int train_micro_batch;      /* samples per TrainFB chunk: forward + backward run per chunk and
                                  the gradients accumulate; only one chunk's activations are kept,
                                  which is what bounds the batch that fits.  0 = a whole TrainFB

@@ -180,6 +180,8 @@ int rlhf_swiglu_bwd(const void* gu, const void* dact, void* dgu, int rows, int f
 
 /* out_bf16 = bf16(x) elementwise (n elements). */
 int rlhf_round_bf16(const float* x, void* out, int64_t n, rlhf_stream_t s);
+/* y[i] += x[i] (fp32, 16-byte aligned): ZeRO-2 accumulation of reduce-scattered gradient shards. */
+int rlhf_add_f32(float* y, const float* x, int64_t n, rlhf_stream_t s);
 /* db[n] += sum_m G[m, n] (bf16 G, fp32 sums, fixed order).  ws >= 64*N floats. */
 int rlhf_colsum_bf16(const void* G, int M, int N, float* db, float* ws, rlhf_stream_t s);
 /* Row gather/scatter between [B*S, d] and response rows [B*R, d]: row (b, j) <-> b*S + off + j. */

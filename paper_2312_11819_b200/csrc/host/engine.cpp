@@ -125,8 +125,8 @@ cudaEvent_t Engine::take_event() {
 
 Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg_(cfg), opt_(opt) {
   validate(cfg_);
-  if (opt_.zero_stage < 0 || opt_.zero_stage > 1)
-    throw ConfigError("zero_stage must be 0 or 1 (ZeRO-2/3 are not executed)");
+  if (opt_.zero_stage < 0 || opt_.zero_stage > 2)
+    throw ConfigError("zero_stage must be 0, 1 or 2 (ZeRO-3 is not executed)");
   cfg_.actor.scalar_head = 0;
   cfg_.critic.scalar_head = 1;
   strategy_ = opt.strategy ? opt.strategy : "colocated";
@@ -372,6 +372,9 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
 
 Engine::~Engine() {
   if (decode_graph_) cudaGraphExecDestroy(decode_graph_);
+  for (Decoder* d : {&actor_, &critic_})
+    for (cudaEvent_t e : d->rs_done)
+      if (e) cudaEventDestroy(e);
   for (ncclComm_t c : {actor_comm_, critic_comm_, sync_comm_[0], sync_comm_[1], world_})
     if (c) nccl().CommDestroy(c);
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
@@ -567,7 +570,15 @@ void Engine::run_task(const ExecStep& s) {
       const int per = xp_.sets[xp_.set_of[mi]].per;
       begin_event(i, s, static_cast<int>(TaskKind::TrainFB), lane_of(t.model), static_cast<int>(Stage::Training));
       if (t.micro_batch_index == 0) {  // a new epoch's gradient and loss sum
-        CK(cudaMemsetAsync(m.grad.p, 0, static_cast<size_t>(m.npad) * 4, stream_));
+        if (m.zero2) {
+          CK(cudaMemsetAsync(m.gpre.p, 0, m.gpre.bytes, stream_));
+          CK(cudaMemsetAsync(m.gpost.p, 0, m.gpost.bytes, stream_));
+          // the shard accumulator is also written by the comm lane: order after its last use
+          for (cudaEvent_t e : m.rs_done) CK(cudaStreamWaitEvent(stream_, e, 0));
+          CK(cudaMemsetAsync(m.gshard.p, 0, m.gshard.bytes, stream_));
+        } else {
+          CK(cudaMemsetAsync(m.grad.p, 0, static_cast<size_t>(m.npad) * 4, stream_));
+        }
         CK(cudaMemsetAsync(loss_.as<float>() + (actor ? 0 : 1), 0, 4, stream_));
       }
       // the micro-batch's rows of every rollout (one block per rollout), in chunks of train_mb_
@@ -626,6 +637,11 @@ void Engine::run_optimizer(const ExecStep& s, int i) {
   const float lr = s.model == ModelName::Actor ? cfg_.lr_actor : cfg_.lr_critic;
   const int ml = lane_of(s.model);
   const int st = static_cast<int>(Stage::Training);
+  if (m.zero2) {
+    // the comm lane must also have finished the per-layer reduce-scatters of the last chunk
+    zero2_optimizer(m, comm, lr, i);
+    return;
+  }
   cudaEvent_t prev = nullptr;
   if (comm) {
     begin_event(i, s, static_cast<int>(TaskKind::Collective), 2, st);
@@ -851,8 +867,8 @@ size_t Engine::tensor_bytes(const std::string& name) const {
   if (name == "pred" || name == "margin") return static_cast<size_t>(gen_B_) * S_ * 4;
   if (name == "score" || name == "sample_ids") return rows * 4;
   auto flat = [](const Decoder& m, size_t e) { return static_cast<size_t>(m.n) * e; };
-  if (name == "actor_grad") return flat(actor_, 4);
-  if (name == "critic_grad") return flat(critic_, 4);
+  if (name == "actor_grad") return actor_.zero2 ? 0 : flat(actor_, 4);
+  if (name == "critic_grad") return critic_.zero2 ? 0 : flat(critic_, 4);
   if (name == "actor_master") return static_cast<size_t>(actor_.shard) * 4;  // this rank's slice under ZeRO-1
   if (name == "critic_master") return static_cast<size_t>(critic_.shard) * 4;
   if (name == "actor_params") return flat(actor_, 2);

@@ -43,6 +43,14 @@ struct DevBuf {
   T* as() const { return static_cast<T*>(p); }
 };
 
+// ZeRO-2 gradient bucket: a contiguous range of the flat parameter vector (the embeddings,
+// one decoder layer, or the final norm + heads), reduce-scattered as a unit.  Rank r owns
+// elements [start + r * slice, start + (r + 1) * slice) of it (padded: slice * dp >= len),
+// stored at [soff, soff + slice) of the rank's concatenated shard arrays.
+struct GradBucket {
+  int64_t start = 0, len = 0, slice = 0, soff = 0;
+};
+
 // One decoder (OPT or LLaMA family) resident on this device.
 struct Decoder {
   rlhf_arch a{};
@@ -50,20 +58,36 @@ struct Decoder {
   bool trainable = false;
   int64_t n = 0;  // flat parameter count (rlhf_param_total)
   // ZeRO-1: the fp32 master/m/v hold elements [shard_off, shard_off + shard) of the flat
-  // vector (padded to npad = dp * shard); unsharded: shard = npad = n, shard_off = 0
+  // vector (padded to npad = dp * shard); unsharded: shard = npad = n, shard_off = 0.
+  // ZeRO-2: master/m/v/gshard hold the rank's slice of every GradBucket (shard = their sum).
   int64_t npad = 0, shard = 0, shard_off = 0;
   bool sharded = false;
   DevBuf w;       // bf16 flat
-  DevBuf master, m, v, grad;  // fp32 flat (trainable only)
+  DevBuf master, m, v, grad;  // fp32 flat (trainable only; grad unused under ZeRO-2)
   int adam_step = 0;
   DevBuf rope;    // LLaMA: float2 (cos, sin) [max_pos][hd/2] (rlhf_rope_cos_sin)
+  // ---- ZeRO-2 (bucket-sharded gradients): no full-size gradient is ever resident.  Layer
+  // l's gradients accumulate in working bucket l % 2 (reduce-scattered into gshard after
+  // the layer's backward), the embedding / head groups in full-size buffers that are
+  // reduce-scattered once per optimizer step (the tied LM head adds into the embedding).
+  bool zero2 = false;
+  int dp = 1, dp_rank = 0;
+  std::vector<GradBucket> buckets;  // [pre, layer 0 .. L-1, post]
+  int64_t layers_start = 0, layer_len = 0, post_start = 0, work_len = 0;
+  DevBuf gpre, gpost, gwork[2], gshard, rs_tmp, wshard, ag_stage;
+  cudaEvent_t rs_done[2] = {nullptr, nullptr};  // working bucket free again (comm lane)
   bool llama() const { return a.family == 1; }
   // tensors absent from the family's layout (size 0) are NULL
   const uint16_t* T(int t, int l = 0) const {
     return rlhf_tensor_numel(&a, t) ? w.as<uint16_t>() + rlhf_tensor_offset(&a, t, l) : nullptr;
   }
   float* G(int t, int l = 0) const {
-    return rlhf_tensor_numel(&a, t) ? grad.as<float>() + rlhf_tensor_offset(&a, t, l) : nullptr;
+    if (!rlhf_tensor_numel(&a, t)) return nullptr;
+    const int64_t off = rlhf_tensor_offset(&a, t, l);
+    if (!zero2) return grad.as<float>() + off;
+    if (off < layers_start) return gpre.as<float>() + off;
+    if (off >= post_start) return gpost.as<float>() + (off - post_start);
+    return gwork[l & 1].as<float>() + (off - layers_start - static_cast<int64_t>(l) * layer_len);
   }
   int head_id() const { return llama() ? RLHF_T_LM_HEAD : RLHF_T_TOK_EMB; }  // LM head (tied for OPT)
 };
@@ -139,6 +163,10 @@ class Engine {
   void attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* o, int B, int T, int H, int hd, bool keep_p);
   void attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_t* dov, uint16_t* dqkv, int B, int T, int H, int hd);
   void backward(Decoder& m, const int32_t* tokens, int B, int S);
+  void zero2_layer_begin(Decoder& m, int l);   // working bucket l % 2 free -> zeroed
+  void zero2_layer_end(Decoder& m, int l);     // reduce-scatter + accumulate its shard (comm lane)
+  void zero2_optimizer(Decoder& m, ncclComm_t comm, float lr, int step_index);
+  ncclComm_t dp_comm(const Decoder& m) const { return &m == &actor_ ? actor_comm_ : critic_comm_; }
   void norm(const Decoder& m, const float* x, int g, int l, uint16_t* y, float* mean, float* rstd, int rows);
   void norm_bwd(Decoder& m, const float* dy, const float* x, const float* mean, const float* rstd, int g, int l, int rows);
   void lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits);

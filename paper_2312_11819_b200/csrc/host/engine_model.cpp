@@ -66,6 +66,11 @@ void Engine::kcheck(int status, const char* what) {
     ncclResult_t r_ = (x);                                                                        \
     if (r_ != ncclSuccess) throw DeviceError(std::string(#x) + ": " + nccl().GetErrorString(r_)); \
   } while (0)
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) throw DeviceError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
 #define K(call, n)                \
   do {                            \
     kcheck((call), #call);        \
@@ -181,7 +186,33 @@ void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool tr
   m.n = rlhf_param_total(&a);
   m.npad = m.shard = m.n;
   m.shard_off = 0;
-  m.sharded = trainable && opt_.zero_stage >= 1 && dp_comm;
+  m.sharded = trainable && opt_.zero_stage == 1 && dp_comm;
+  m.zero2 = trainable && opt_.zero_stage == 2;
+  if (m.zero2) {
+    // buckets: embeddings | layer 0 .. L-1 | final norm + heads; each rank owns a
+    // 64-aligned slice of every bucket (costmodel.hpp:48-50 ZeRO-2: 2 + 14/dp B/param)
+    if (dp_comm) {
+      NK(nccl().CommCount(dp_comm, &m.dp));
+      NK(nccl().CommUserRank(dp_comm, &m.dp_rank));
+    }
+    m.layers_start = rlhf_tensor_offset(&a, RLHF_LAYER_FIRST, 0);
+    m.layer_len = a.n_layers > 1 ? rlhf_tensor_offset(&a, RLHF_LAYER_FIRST, 1) - m.layers_start
+                                 : rlhf_tensor_offset(&a, RLHF_T_LNF_G, 0) - m.layers_start;
+    m.post_start = rlhf_tensor_offset(&a, RLHF_T_LNF_G, 0);
+    auto add = [&](int64_t start, int64_t len) {
+      GradBucket g;
+      g.start = start;
+      g.len = len;
+      g.slice = ((len + m.dp - 1) / m.dp + 63) / 64 * 64;
+      g.soff = m.buckets.empty() ? 0 : m.buckets.back().soff + m.buckets.back().slice;
+      m.buckets.push_back(g);
+    };
+    add(0, m.layers_start);
+    for (int l = 0; l < a.n_layers; ++l) add(m.layers_start + static_cast<int64_t>(l) * m.layer_len, m.layer_len);
+    add(m.post_start, m.n - m.post_start);
+    m.shard = m.buckets.back().soff + m.buckets.back().slice;
+    m.work_len = m.buckets[1].slice * m.dp;  // a layer bucket padded to dp slices
+  }
   if (m.sharded) {
     int dp = 1, r = 0;
     NK(nccl().CommCount(dp_comm, &dp));
@@ -218,12 +249,37 @@ void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool tr
     throw DeviceError("weight upload failed");
   if (trainable) {
     std::vector<float> f(static_cast<size_t>(m.shard), 0.0f);  // this rank's slice of the fp32 master
-    for (int64_t i = 0; i < m.shard && m.shard_off + i < m.n; ++i) f[i] = rlhf_bf16_to_f32(host[m.shard_off + i]);
+    if (m.zero2) {
+      for (const GradBucket& g : m.buckets)
+        for (int64_t i = 0; i < g.slice; ++i) {
+          const int64_t e = static_cast<int64_t>(m.dp_rank) * g.slice + i;
+          if (e < g.len) f[g.soff + i] = rlhf_bf16_to_f32(host[g.start + e]);
+        }
+    } else {
+      for (int64_t i = 0; i < m.shard && m.shard_off + i < m.n; ++i) f[i] = rlhf_bf16_to_f32(host[m.shard_off + i]);
+    }
     m.master.alloc(f.size() * 4);
     cudaMemcpy(m.master.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice);
     m.m.alloc(f.size() * 4);
     m.v.alloc(f.size() * 4);
-    m.grad.alloc(static_cast<size_t>(m.npad) * 4);
+    if (m.zero2) {
+      const GradBucket &pre = m.buckets.front(), &post = m.buckets.back();
+      m.gpre.alloc(static_cast<size_t>(pre.slice * m.dp) * 4);
+      m.gpost.alloc(static_cast<size_t>(post.slice * m.dp) * 4);
+      for (DevBuf& b : m.gwork) b.alloc(static_cast<size_t>(m.work_len) * 4);
+      m.gshard.alloc(static_cast<size_t>(m.shard) * 4);
+      int64_t smax = 0;
+      for (const GradBucket& g : m.buckets) smax = std::max(smax, g.slice);
+      m.rs_tmp.alloc(static_cast<size_t>(smax) * 4);
+      m.wshard.alloc(static_cast<size_t>(m.shard) * 2);
+      m.ag_stage.alloc(static_cast<size_t>(smax * m.dp) * 2);
+      for (auto& e : m.rs_done) {
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) throw DeviceError("event create failed");
+        cudaEventRecord(e, stream_);  // both working buckets start free
+      }
+    } else {
+      m.grad.alloc(static_cast<size_t>(m.npad) * 4);
+    }
   }
   if (m.llama()) {
     const int hd = a.d_model / a.n_heads, half = hd / 2;
@@ -418,6 +474,7 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
     gemm(p);
   };
   for (int l = L - 1; l >= 0; --l) {
+    if (m.zero2) zero2_layer_begin(m, l);
     const int64_t Tn = arp_->Ts;
     const uint16_t* h1 = arp_->h1 + l * Tn * arp_->d;
     const uint16_t* qkv = arp_->qkv + l * Tn * 3 * arp_->d;
@@ -457,6 +514,7 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
     wgrad(arp_->dqkv, 3 * d, h1, d, m.G(RLHF_T_WQKV, l));
     dgrad(arp_->dqkv, 3 * d, m.T(RLHF_T_WQKV, l), d, arp_->dh, true, nullptr);
     norm_bwd(m, arp_->dh, X(2 * l), MEAN(2 * l), RSTD(2 * l), RLHF_T_LN1_G, l, rows);
+    if (m.zero2) zero2_layer_end(m, l);
   }
   K(rlhf_embed_bwd(tokens, S, B, S, arp_->dres, d, m.G(RLHF_T_TOK_EMB), m.G(RLHF_T_POS_EMB), stream_), 1);
 }
@@ -717,6 +775,78 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
     graph_for_pred_ = teacher_forced;
     for (int s = 1; s < R_; ++s) decode_step(m, B);
   }
+}
+
+// ---- ZeRO-2: per-layer reduce-scatter of the working gradient bucket (comm lane) ----------
+
+void Engine::zero2_layer_begin(Decoder& m, int l) {
+  // the bucket's previous reduce-scatter (layer l + 2, or the previous chunk) has read it
+  CK(cudaStreamWaitEvent(stream_, m.rs_done[l & 1], 0));
+  CK(cudaMemsetAsync(m.gwork[l & 1].p, 0, static_cast<size_t>(m.work_len) * 4, stream_));
+}
+
+void Engine::zero2_layer_end(Decoder& m, int l) {
+  const GradBucket& g = m.buckets[static_cast<size_t>(l) + 1];
+  cudaEvent_t ready = take_event();
+  CK(cudaEventRecord(ready, stream_));
+  cudaStream_t cs = lane_[2];
+  CK(cudaStreamWaitEvent(cs, ready, 0));
+  float* src = m.gwork[l & 1].as<float>();
+  ncclComm_t comm = dp_comm(m);
+  if (comm) {
+    NK(nccl().ReduceScatter(src, m.rs_tmp.p, static_cast<size_t>(g.slice), ncclFloat32, ncclSum, comm, cs));
+    comm_bytes_ += 4.0 * static_cast<double>(g.slice) * (m.dp - 1);
+    kcheck(rlhf_add_f32(m.gshard.as<float>() + g.soff, m.rs_tmp.as<float>(), g.slice, cs), "rlhf_add_f32");
+  } else {  // one rank: the slice is the whole bucket
+    kcheck(rlhf_add_f32(m.gshard.as<float>() + g.soff, src, g.slice, cs), "rlhf_add_f32");
+  }
+  ++launches_;
+  CK(cudaEventRecord(m.rs_done[l & 1], cs));
+}
+
+// Optimizer step under ZeRO-2: the embedding / head buckets (accumulated over the whole epoch
+// in full) are reduce-scattered into their slices, AdamW updates the rank's slices of every
+// bucket, and each bucket's bf16 slices are all-gathered back into the flat weights.
+void Engine::zero2_optimizer(Decoder& m, ncclComm_t comm, float lr, int i) {
+  const ExecStep& s = xp_.steps[static_cast<size_t>(i)];
+  const int st = static_cast<int>(Stage::Training);
+  const int ml = lane_of(s.model);
+  begin_event(i, s, static_cast<int>(TaskKind::Collective), 2, st);
+  for (int k : {0, static_cast<int>(m.buckets.size()) - 1}) {
+    const GradBucket& g = m.buckets[static_cast<size_t>(k)];
+    float* full = (k == 0 ? m.gpre : m.gpost).as<float>();
+    if (comm) {
+      NK(nccl().ReduceScatter(full, m.rs_tmp.p, static_cast<size_t>(g.slice), ncclFloat32, ncclSum, comm, stream_));
+      comm_bytes_ += 4.0 * static_cast<double>(g.slice) * (m.dp - 1);
+      K(rlhf_add_f32(m.gshard.as<float>() + g.soff, m.rs_tmp.as<float>(), g.slice, stream_), 1);
+    } else {
+      K(rlhf_add_f32(m.gshard.as<float>() + g.soff, full, g.slice, stream_), 1);
+    }
+  }
+  end_event();
+  cudaEvent_t prev = evs_.back().b;
+  begin_event(i, s, 7, ml, st);
+  CK(cudaStreamWaitEvent(stream_, prev, 0));
+  m.adam_step += 1;
+  K(rlhf_adamw(m.master.as<float>(), m.m.as<float>(), m.v.as<float>(), m.gshard.as<float>(), m.wshard.p, m.shard, lr,
+               cfg_.beta1, cfg_.beta2, cfg_.adam_eps, cfg_.weight_decay, m.adam_step, stream_), 1);
+  end_event();
+  prev = evs_.back().b;
+  begin_event(i, s, static_cast<int>(TaskKind::Collective), 2, st);
+  CK(cudaStreamWaitEvent(stream_, prev, 0));
+  for (const GradBucket& g : m.buckets) {
+    const uint16_t* mine = m.wshard.as<uint16_t>() + g.soff;
+    if (comm) {
+      NK(nccl().AllGather(mine, m.ag_stage.p, static_cast<size_t>(g.slice), ncclBfloat16, comm, stream_));
+      comm_bytes_ += 2.0 * static_cast<double>(g.slice) * (m.dp - 1);
+      CK(cudaMemcpyAsync(m.w.as<uint16_t>() + g.start, m.ag_stage.p, static_cast<size_t>(g.len) * 2,
+                         cudaMemcpyDeviceToDevice, stream_));
+    } else {
+      CK(cudaMemcpyAsync(m.w.as<uint16_t>() + g.start, mine, static_cast<size_t>(g.len) * 2, cudaMemcpyDeviceToDevice,
+                         stream_));
+    }
+  }
+  end_event();
 }
 
 // Fused AdamW on this rank's master slice (ZeRO-1: the reduce-scattered gradient shard at

@@ -594,6 +594,26 @@ extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* 
   return cuda_status();
 }
 
+__global__ void add_f32_kernel(float* __restrict__ y, const float* __restrict__ x, int64_t n) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (i + 3 < n) {
+    float4 a = *reinterpret_cast<float4*>(y + i);
+    const float4 b = *reinterpret_cast<const float4*>(x + i);
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    *reinterpret_cast<float4*>(y + i) = a;
+  } else {
+    for (int64_t k = i; k < n; ++k) y[k] += x[k];
+  }
+}
+
+extern "C" int rlhf_add_f32(float* y, const float* x, int64_t n, rlhf_stream_t s) {
+  if (n <= 0) return 0;
+  if ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(x)) & 15) return 2;
+  const int64_t q = (n + 3) / 4;
+  add_f32_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, S(s)>>>(y, x, n);
+  return cuda_status();
+}
+
 extern "C" int rlhf_round_bf16(const float* x, void* out, int64_t n, rlhf_stream_t s) {
   const int64_t q = (n + 3) / 4;
   round_bf16_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, S(s)>>>(x, static_cast<uint16_t*>(out), n);
