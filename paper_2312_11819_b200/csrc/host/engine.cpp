@@ -125,8 +125,7 @@ cudaEvent_t Engine::take_event() {
 
 Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg_(cfg), opt_(opt) {
   validate(cfg_);
-  if (opt_.zero_stage < 0 || opt_.zero_stage > 2)
-    throw ConfigError("zero_stage must be 0, 1 or 2 (ZeRO-3 is not executed)");
+  if (opt_.zero_stage < 0 || opt_.zero_stage > 3) throw ConfigError("zero_stage must be 0..3");
   cfg_.actor.scalar_head = 0;
   cfg_.critic.scalar_head = 1;
   strategy_ = opt.strategy ? opt.strategy : "colocated";
@@ -157,6 +156,9 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
     tag_ = xp_.tag;
     for (int m = 0; m < 6; ++m) hosts_[m] = xp_.hosts(rank_, static_cast<ModelName>(m));
   }
+  if (opt_.zero_stage == 3 && hosts_[0] && xp_.generator == ModelName::Actor)
+    throw ConfigError("ZeRO-3 shards the trainers' weights per layer: the generating Actor needs them whole every "
+                      "decode step (use the Disaggregated placement, whose shadow generates, or zero_stage <= 2)");
   int train_per = 0;
   for (int m = 0; m < 6; ++m) {
     if (!hosts_[m]) continue;
@@ -372,9 +374,12 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
 
 Engine::~Engine() {
   if (decode_graph_) cudaGraphExecDestroy(decode_graph_);
-  for (Decoder* d : {&actor_, &critic_})
+  for (Decoder* d : {&actor_, &critic_}) {
     for (cudaEvent_t e : d->rs_done)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : d->wgather_done)
+      if (e) cudaEventDestroy(e);
+  }
   for (ncclComm_t c : {actor_comm_, critic_comm_, sync_comm_[0], sync_comm_[1], world_})
     if (c) nccl().CommDestroy(c);
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
@@ -598,10 +603,35 @@ void Engine::run_task(const ExecStep& s) {
       Decoder& dst = k == 0 ? shadow_actor_ : shadow_critic_;
       const bool is_src = hosts_[k == 0 ? 0 : 1];
       begin_event(i, s, static_cast<int>(TaskKind::ParamSync), 2, static_cast<int>(Stage::Sync));
-      const size_t n = static_cast<size_t>(is_src ? src.n : dst.n);
-      NK(nccl().Broadcast(is_src ? src.w.p : dst.w.p, is_src ? src.w.p : dst.w.p, n, ncclBfloat16, sync_root_[k],
-                          sync_comm_[k], stream_));
-      if (is_src) comm_bytes_ += 2.0 * static_cast<double>(n);
+      if (opt_.zero_stage == 3) {
+        // the trainers hold bucket slices: per bucket, all-gather among the trainers, then
+        // broadcast the whole bucket to the shadows (same bucket order on every rank)
+        const rlhf_arch& a = is_src ? src.a : dst.a;
+        const int64_t ls = rlhf_tensor_offset(&a, RLHF_LAYER_FIRST, 0), ps = rlhf_tensor_offset(&a, RLHF_T_LNF_G, 0);
+        const int64_t ll = (ps - ls) / a.n_layers, n = rlhf_param_total(&a);
+        std::vector<std::pair<int64_t, int64_t>> rng{{0, ls}};
+        for (int l = 0; l < a.n_layers; ++l) rng.push_back({ls + l * ll, ll});
+        rng.push_back({ps, n - ps});
+        ncclComm_t tcomm = dp_comm(src);
+        for (size_t bk = 0; bk < rng.size(); ++bk) {
+          const auto [start, len] = rng[bk];
+          void* buf = dst.w.p ? static_cast<void*>(dst.w.as<uint16_t>() + start) : nullptr;
+          if (is_src) {
+            const GradBucket& g = src.buckets[bk];
+            const uint16_t* mine = src.wshard.as<uint16_t>() + g.soff;
+            if (tcomm) NK(nccl().AllGather(mine, src.ag_stage.p, static_cast<size_t>(g.slice), ncclBfloat16, tcomm, stream_));
+            else CK(cudaMemcpyAsync(src.ag_stage.p, mine, static_cast<size_t>(g.len) * 2, cudaMemcpyDeviceToDevice, stream_));
+            buf = src.ag_stage.p;
+            comm_bytes_ += 2.0 * static_cast<double>(len);
+          }
+          NK(nccl().Broadcast(buf, buf, static_cast<size_t>(len), ncclBfloat16, sync_root_[k], sync_comm_[k], stream_));
+        }
+      } else {
+        const size_t n = static_cast<size_t>(is_src ? src.n : dst.n);
+        NK(nccl().Broadcast(is_src ? src.w.p : dst.w.p, is_src ? src.w.p : dst.w.p, n, ncclBfloat16, sync_root_[k],
+                            sync_comm_[k], stream_));
+        if (is_src) comm_bytes_ += 2.0 * static_cast<double>(n);
+      }
       end_event();
       return;
     }
@@ -871,8 +901,9 @@ size_t Engine::tensor_bytes(const std::string& name) const {
   if (name == "critic_grad") return critic_.zero2 ? 0 : flat(critic_, 4);
   if (name == "actor_master") return static_cast<size_t>(actor_.shard) * 4;  // this rank's slice under ZeRO-1
   if (name == "critic_master") return static_cast<size_t>(critic_.shard) * 4;
-  if (name == "actor_params") return flat(actor_, 2);
-  if (name == "critic_params") return flat(critic_, 2);
+  // ZeRO-3: this rank's bf16 slices of every bucket (the full weights are never resident)
+  if (name == "actor_params") return actor_.zero3 ? static_cast<size_t>(actor_.shard) * 2 : flat(actor_, 2);
+  if (name == "critic_params") return critic_.zero3 ? static_cast<size_t>(critic_.shard) * 2 : flat(critic_, 2);
   if (name == "ref_params") return flat(ref_, 2);
   if (name == "reward_params") return flat(reward_, 2);
   if (name == "shadow_actor_params") return flat(shadow_actor_, 2);
@@ -903,8 +934,9 @@ void Engine::read(const std::string& name, void* host, size_t bytes) {
   }
   const std::map<std::string, const DevBuf*> m = {
       {"pred", &pred_}, {"margin", &margin_}, {"actor_grad", &actor_.grad}, {"critic_grad", &critic_.grad},
-      {"actor_master", &actor_.master}, {"critic_master", &critic_.master}, {"actor_params", &actor_.w},
-      {"critic_params", &critic_.w}, {"ref_params", &ref_.w}, {"reward_params", &reward_.w},
+      {"actor_master", &actor_.master}, {"critic_master", &critic_.master},
+      {"actor_params", actor_.zero3 ? &actor_.wshard : &actor_.w},
+      {"critic_params", critic_.zero3 ? &critic_.wshard : &critic_.w}, {"ref_params", &ref_.w}, {"reward_params", &reward_.w},
       {"shadow_actor_params", &shadow_actor_.w}, {"shadow_critic_params", &shadow_critic_.w}};
   if (!src) {
     auto it = m.find(name);

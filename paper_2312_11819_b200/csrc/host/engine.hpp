@@ -76,10 +76,23 @@ struct Decoder {
   int64_t layers_start = 0, layer_len = 0, post_start = 0, work_len = 0;
   DevBuf gpre, gpost, gwork[2], gshard, rs_tmp, wshard, ag_stage;
   cudaEvent_t rs_done[2] = {nullptr, nullptr};  // working bucket free again (comm lane)
+  // ---- ZeRO-3 (also the bf16 weights sharded): wshard holds the rank's slices of every
+  // bucket; the embedding / head buckets stay whole in wpre / wpost, a decoder layer's
+  // weights are all-gathered on the comm stream into working buffer l % 2 just before the
+  // layer runs (the next layer's gather overlaps this one's compute).
+  bool zero3 = false;
+  DevBuf wpre, wpost, wwork[2];
+  mutable int wwork_layer[2] = {-1, -1};
+  cudaEvent_t wgather_done[2] = {nullptr, nullptr};
   bool llama() const { return a.family == 1; }
   // tensors absent from the family's layout (size 0) are NULL
   const uint16_t* T(int t, int l = 0) const {
-    return rlhf_tensor_numel(&a, t) ? w.as<uint16_t>() + rlhf_tensor_offset(&a, t, l) : nullptr;
+    if (!rlhf_tensor_numel(&a, t)) return nullptr;
+    const int64_t off = rlhf_tensor_offset(&a, t, l);
+    if (!zero3) return w.as<uint16_t>() + off;
+    if (off < layers_start) return wpre.as<uint16_t>() + off;
+    if (off >= post_start) return wpost.as<uint16_t>() + (off - post_start);
+    return wwork[l & 1].as<uint16_t>() + (off - layers_start - static_cast<int64_t>(l) * layer_len);
   }
   float* G(int t, int l = 0) const {
     if (!rlhf_tensor_numel(&a, t)) return nullptr;
@@ -166,6 +179,7 @@ class Engine {
   void zero2_layer_begin(Decoder& m, int l);   // working bucket l % 2 free -> zeroed
   void zero2_layer_end(Decoder& m, int l);     // reduce-scatter + accumulate its shard (comm lane)
   void zero2_optimizer(Decoder& m, ncclComm_t comm, float lr, int step_index);
+  void zero3_fetch(const Decoder& m, int l, int next);  // layer l's weights resident (+ prefetch next)
   ncclComm_t dp_comm(const Decoder& m) const { return &m == &actor_ ? actor_comm_ : critic_comm_; }
   void norm(const Decoder& m, const float* x, int g, int l, uint16_t* y, float* mean, float* rstd, int rows);
   void norm_bwd(Decoder& m, const float* dy, const float* x, const float* mean, const float* rstd, int g, int l, int rows);

@@ -187,7 +187,8 @@ void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool tr
   m.npad = m.shard = m.n;
   m.shard_off = 0;
   m.sharded = trainable && opt_.zero_stage == 1 && dp_comm;
-  m.zero2 = trainable && opt_.zero_stage == 2;
+  m.zero2 = trainable && opt_.zero_stage >= 2;
+  m.zero3 = trainable && opt_.zero_stage == 3;
   if (m.zero2) {
     // buckets: embeddings | layer 0 .. L-1 | final norm + heads; each rank owns a
     // 64-aligned slice of every bucket (costmodel.hpp:48-50 ZeRO-2: 2 + 14/dp B/param)
@@ -244,9 +245,29 @@ void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool tr
       }
     });
   for (auto& t : th) t.join();
-  m.w.alloc(static_cast<size_t>(m.npad) * 2);
-  if (cudaMemcpy(m.w.p, host.data(), host.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess)
-    throw DeviceError("weight upload failed");
+  if (m.zero3) {  // only the embedding / head buckets whole; the layers as this rank's slices
+    const GradBucket &pre = m.buckets.front(), &post = m.buckets.back();
+    m.wpre.alloc(static_cast<size_t>(pre.len) * 2);
+    m.wpost.alloc(static_cast<size_t>(post.len) * 2);
+    for (DevBuf& b : m.wwork) b.alloc(static_cast<size_t>(m.work_len) * 2);
+    std::vector<uint16_t> sl(static_cast<size_t>(m.shard), 0);
+    for (const GradBucket& g : m.buckets)
+      for (int64_t i = 0; i < g.slice; ++i) {
+        const int64_t e = static_cast<int64_t>(m.dp_rank) * g.slice + i;
+        if (e < g.len) sl[g.soff + i] = host[g.start + e];
+      }
+    m.wshard.alloc(sl.size() * 2);
+    bool ok = cudaMemcpy(m.wpre.p, host.data(), pre.len * 2, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= cudaMemcpy(m.wpost.p, host.data() + post.start, post.len * 2, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= cudaMemcpy(m.wshard.p, sl.data(), sl.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) throw DeviceError("weight upload failed");
+    for (auto& e : m.wgather_done)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) throw DeviceError("event create failed");
+  } else {
+    m.w.alloc(static_cast<size_t>(m.npad) * 2);
+    if (cudaMemcpy(m.w.p, host.data(), host.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess)
+      throw DeviceError("weight upload failed");
+  }
   if (trainable) {
     std::vector<float> f(static_cast<size_t>(m.shard), 0.0f);  // this rank's slice of the fp32 master
     if (m.zero2) {
@@ -271,7 +292,7 @@ void Engine::init_decoder(Decoder& m, const rlhf_arch& a, uint64_t seed, bool tr
       int64_t smax = 0;
       for (const GradBucket& g : m.buckets) smax = std::max(smax, g.slice);
       m.rs_tmp.alloc(static_cast<size_t>(smax) * 4);
-      m.wshard.alloc(static_cast<size_t>(m.shard) * 2);
+      if (!m.zero3) m.wshard.alloc(static_cast<size_t>(m.shard) * 2);
       m.ag_stage.alloc(static_cast<size_t>(smax * m.dp) * 2);
       for (auto& e : m.rs_done) {
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) throw DeviceError("event create failed");
@@ -328,6 +349,7 @@ void Engine::forward(const Decoder& m, const int32_t* tokens, int B, int tok_str
   (void)Td;
   K(rlhf_embed(tokens, tok_stride, B, T, 0, nullptr, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, X(0), stream_), 1);
   for (int l = 0; l < L; ++l) {
+    if (m.zero3) zero3_fetch(m, l, l + 1 < L ? l + 1 : -1);
     uint16_t* h1 = slot(arp_->h1, arp_->Ts * arp_->d, l);
     uint16_t* qkv = slot(arp_->qkv, arp_->Ts * 3 * arp_->d, l);
     uint16_t* P = slot(arp_->P, arp_->Zs * arp_->S * arp_->S, l);
@@ -474,6 +496,7 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
     gemm(p);
   };
   for (int l = L - 1; l >= 0; --l) {
+    if (m.zero3) zero3_fetch(m, l, l > 0 ? l - 1 : -1);
     if (m.zero2) zero2_layer_begin(m, l);
     const int64_t Tn = arp_->Ts;
     const uint16_t* h1 = arp_->h1 + l * Tn * arp_->d;
@@ -804,6 +827,32 @@ void Engine::zero2_layer_end(Decoder& m, int l) {
   CK(cudaEventRecord(m.rs_done[l & 1], cs));
 }
 
+// ZeRO-3: layer l's bf16 weights all-gathered (comm stream) into working buffer l % 2 unless
+// already there; `next` is gathered into the other buffer ahead of its use.
+void Engine::zero3_fetch(const Decoder& m, int l, int next) {
+  auto gather = [&](int layer) {
+    const int b = layer & 1;
+    if (m.wwork_layer[b] == layer) return;
+    cudaEvent_t free_ev = take_event();  // the compute stream's earlier kernels used buffer b
+    CK(cudaEventRecord(free_ev, stream_));
+    cudaStream_t cs = lane_[2];
+    CK(cudaStreamWaitEvent(cs, free_ev, 0));
+    const GradBucket& g = m.buckets[static_cast<size_t>(layer) + 1];
+    const uint16_t* mine = m.wshard.as<uint16_t>() + g.soff;
+    if (ncclComm_t comm = dp_comm(m)) {
+      NK(nccl().AllGather(mine, m.wwork[b].p, static_cast<size_t>(g.slice), ncclBfloat16, comm, cs));
+      comm_bytes_ += 2.0 * static_cast<double>(g.slice) * (m.dp - 1);
+    } else {
+      CK(cudaMemcpyAsync(m.wwork[b].p, mine, static_cast<size_t>(g.len) * 2, cudaMemcpyDeviceToDevice, cs));
+    }
+    CK(cudaEventRecord(m.wgather_done[b], cs));
+    m.wwork_layer[b] = layer;
+  };
+  gather(l);
+  CK(cudaStreamWaitEvent(stream_, m.wgather_done[l & 1], 0));
+  if (next >= 0) gather(next);
+}
+
 // Optimizer step under ZeRO-2: the embedding / head buckets (accumulated over the whole epoch
 // in full) are reduce-scattered into their slices, AdamW updates the rank's slices of every
 // bucket, and each bucket's bf16 slices are all-gathered back into the flat weights.
@@ -834,18 +883,22 @@ void Engine::zero2_optimizer(Decoder& m, ncclComm_t comm, float lr, int i) {
   prev = evs_.back().b;
   begin_event(i, s, static_cast<int>(TaskKind::Collective), 2, st);
   CK(cudaStreamWaitEvent(stream_, prev, 0));
-  for (const GradBucket& g : m.buckets) {
+  // ZeRO-2: every bucket back into the flat weights; ZeRO-3: only the embedding / head
+  // buckets (the layers are gathered when they run; the gathered copies are stale now)
+  for (size_t k = 0; k < m.buckets.size(); ++k) {
+    if (m.zero3 && k != 0 && k + 1 != m.buckets.size()) continue;
+    const GradBucket& g = m.buckets[k];
     const uint16_t* mine = m.wshard.as<uint16_t>() + g.soff;
+    uint16_t* dst = !m.zero3 ? m.w.as<uint16_t>() + g.start : (k == 0 ? m.wpre : m.wpost).as<uint16_t>();
     if (comm) {
       NK(nccl().AllGather(mine, m.ag_stage.p, static_cast<size_t>(g.slice), ncclBfloat16, comm, stream_));
       comm_bytes_ += 2.0 * static_cast<double>(g.slice) * (m.dp - 1);
-      CK(cudaMemcpyAsync(m.w.as<uint16_t>() + g.start, m.ag_stage.p, static_cast<size_t>(g.len) * 2,
-                         cudaMemcpyDeviceToDevice, stream_));
+      CK(cudaMemcpyAsync(dst, m.ag_stage.p, static_cast<size_t>(g.len) * 2, cudaMemcpyDeviceToDevice, stream_));
     } else {
-      CK(cudaMemcpyAsync(m.w.as<uint16_t>() + g.start, mine, static_cast<size_t>(g.len) * 2, cudaMemcpyDeviceToDevice,
-                         stream_));
+      CK(cudaMemcpyAsync(dst, mine, static_cast<size_t>(g.len) * 2, cudaMemcpyDeviceToDevice, stream_));
     }
   }
+  m.wwork_layer[0] = m.wwork_layer[1] = -1;
   end_event();
 }
 

@@ -166,3 +166,19 @@ def test_zero2_bucket_sharded_gradients_match_replicated(arch):
             assert (np.abs(fa - fb) <= 2 * lr + np.abs(fa) * 2 ** -7).all(), tag  # a flip or one bf16 ulp
             assert np.mean(fa != fb) <= 1e-3, (tag, np.mean(fa != fb))
         np.testing.assert_array_equal(z2[0][f"{tag}_params"], z2[1][f"{tag}_params"])  # replicas agree
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("zero", [2, 3])
+def test_disaggregated_zero23_paramsync_matches_replicated(zero):
+    """Disaggregated trainers under ZeRO-2 (bucket-sharded gradients) and ZeRO-3 (weights
+    sharded too: each decoder layer all-gathered on the comm stream as it runs, ParamSync
+    all-gathers bucket by bucket and broadcasts to the shadows) against ZeRO-0: the shadows
+    receive the same updated weights (one trainer per group here, so the bucket slices are
+    whole buckets and the arithmetic is the replicated one)."""
+    z0, zz = _spawn("disaggregated", 0, "tiny"), _spawn("disaggregated", zero, "tiny")
+    inf0 = next(o for o in z0 if "shadow_actor_params" in o)
+    infz = next(o for o in zz if "shadow_actor_params" in o)
+    for key in ("shadow_actor_params", "shadow_critic_params"):
+        a, b = inf0[key], infz[key]
+        assert np.mean(a != b) <= 1e-4, (key, np.mean(a != b))
