@@ -55,6 +55,9 @@ WORKLOADS = {
                name="c4: LLaMA-7B-shaped Actor/Ref + Critic/Reward, prompt 256 + response 256"),
     "c5-r1024": dict(actor="opt-1.3b", critic="opt-350m", batch=16, prompt=256, gen=1024,
                      name="c5: OPT-1.3B/350m, batch 16/GPU, prompt 256 + response 1024"),
+    # the rest of BASELINE.json configs[4]'s generation-heavy sweep (global batch 64 = --batch 64/N)
+    **{f"c5-r{r}": dict(actor="opt-1.3b", critic="opt-350m", batch=16, prompt=256, gen=r,
+                        name=f"c5: OPT-1.3B/350m, prompt 256 + response {r}") for r in (128, 256, 512)},
 }
 
 
