@@ -241,7 +241,10 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
       const size_t kv = 2ull * cfg_.actor.n_layers * std::max(gen_B_, 1) * S_ * cfg_.actor.d_model * 2;
       size_t free_b = 0, total_b = 0;
       CK(cudaMemGetInfo(&free_b, &total_b));
-      if (free_b < kv + (4ull << 30)) throw InfeasibleError("side-lane arena leaves too little memory");
+      // the side lane is a speed-up, not a necessity: keep a quarter of the device free for
+      // memory-bound placements (e.g. Disaggregated 7B trainers), which then run one lane
+      if (free_b < kv + (4ull << 30) || free_b < total_b / 4)
+        throw InfeasibleError("side-lane arena leaves too little memory");
       side_ = true;
     } catch (const InfeasibleError&) {  // the step stays on one compute lane
       for (DevBuf* b : ar_side_.owned) delete b;

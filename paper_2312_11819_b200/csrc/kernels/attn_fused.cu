@@ -7,11 +7,11 @@
 // (up to 512 x 64) arrive by TMA (SWIZZLE_128B), tcgen05.mma writes the 128 x (m0+128)
 // fp32 score tile into TMEM (<= 512 columns), and four epilogue warps (one TMEM lane
 // quarter each, thread = query row) run an online max / sum pass and a second pass that
-// writes P = bf16(exp(s - max) / sum) (zeros above the diagonal) through a shared-memory
-// transpose as coalesced row segments (training only), and into a shared-memory P tile
-// (SW128, K-major) from which tcgen05.mma accumulates O = P V in TMEM (columns [0, 64),
-// reused once key tile 0 has been consumed; V overwrites K in shared memory after the
-// QK^T MMAs).  Inference forwards never write P to HBM.  Eight epilogue
+// writes P = bf16(exp(s - max) / sum) (zeros above the diagonal) as 64-byte row segments
+// (training only), and into one of two shared-memory P tiles (SW128, K-major; the softmax
+// warps fill tile t+1 while tcgen05.mma accumulates O += P_t V_t in TMEM, columns [0, 64),
+// reused once key tile 0 has been consumed).  V has its own shared-memory tiles, loaded
+// together with K.  Inference forwards never write P to HBM.  Eight epilogue
 // warps (two per lane quarter) split the column chunks; exponentials use ex2.approx
 // (__expf, ~2 ulp).
 //
@@ -34,13 +34,13 @@ namespace af {
 constexpr int BMq = 128, HD = 64, kEpi = 8, kThreads = 64 + 32 * kEpi, kMaxS = 512;
 constexpr int Q_BYTES = BMq * HD * 2;   // 16 KB
 constexpr int KT_BYTES = BMq * HD * 2;  // one 128-key tile, 16 KB
-constexpr int STG_PITCH = 40;           // bf16 staging row pitch (80 B: conflict-light)
 constexpr int PB_BYTES = BMq * BMq * 2;  // one 128 x 128 bf16 P tile (two SW128 64-key blocks)
-constexpr int STG_BYTES = kEpi * 32 * STG_PITCH * 2;
-// dynamic shared memory by mode: the P tile only when O is produced, the P staging only
-// when P is stored (so the P-only and O-only kernels fit two CTAs per SM)
+// dynamic shared memory by mode: when O is produced, V tiles of their own (loaded with K,
+// not after the QK^T MMAs) and a double-buffered P tile (the softmax warps write tile t+1
+// while the tensor core multiplies tile t)
 __host__ __device__ constexpr int smem_bytes(bool want_p, bool want_o) {
-  return Q_BYTES + (kMaxS / BMq) * KT_BYTES + (want_o ? PB_BYTES : 0) + (want_p ? STG_BYTES : 0) + 4 * BMq * 4 + 1024 + 256;
+  return Q_BYTES + (kMaxS / BMq) * KT_BYTES * (want_o ? 2 : 1) + (want_o ? 2 * PB_BYTES : 0) + 4 * BMq * 4 + 1024 +
+         256 + 0 * want_p;
 }
 constexpr int SMEM = smem_bytes(true, true);
 
@@ -53,17 +53,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sq = smem;
-  uint8_t* skv = smem + Q_BYTES;                      // K tiles, then (after the QK MMAs) V tiles
+  uint8_t* skv = smem + Q_BYTES;                      // K tiles
   const bool want_o = O != nullptr, want_p = P != nullptr;
-  uint8_t* spb = skv + (kMaxS / BMq) * KT_BYTES;      // P tile (A operand of P.V)
-  uint16_t* stg = reinterpret_cast<uint16_t*>(spb + (want_o ? PB_BYTES : 0));
-  float* rowst = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(stg) + (want_p ? STG_BYTES : 0));  // [2][2][128]
+  uint8_t* svv = skv + (kMaxS / BMq) * KT_BYTES;      // V tiles (want_o)
+  uint8_t* spb = svv + (want_o ? (kMaxS / BMq) * KT_BYTES : 0);  // 2 P tiles (A operand of P.V)
+  float* rowst = reinterpret_cast<float*>(spb + (want_o ? 2 * PB_BYTES : 0));  // [2][2][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(rowst + 4 * BMq);
   uint64_t* done = full + 1;   // QK^T MMAs complete
   uint64_t* vfull = done + 1;  // V tiles landed
-  uint64_t* pfull = vfull + 1;  // P tile written by the epilogue warps
-  uint64_t* pfree = pfull + 1;  // P.V MMAs done with the P tile
-  uint64_t* ofull = pfree + 1;  // O accumulated
+  uint64_t* pfull = vfull + 1;  // [2] P tile written by the epilogue warps
+  uint64_t* pfree = pfull + 2;  // [2] P.V MMAs done with the P tile
+  uint64_t* ofull = pfree + 2;  // O accumulated
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 1);
 
   const int mb = blockIdx.x, z = blockIdx.y, b = z / H, h = z % H;
@@ -74,8 +74,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(full, 1);
     mbar_init(done, 1);
     mbar_init(vfull, 1);
-    mbar_init(pfull, kEpi);
-    mbar_init(pfree, 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&pfull[k], kEpi);
+      mbar_init(&pfree[k], 1);
+    }
     mbar_init(ofull, 1);
     mbar_fence_init();
     tma_prefetch(&tmQ);
@@ -95,10 +97,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive_expect_tx(full, Q_BYTES + nkt * KT_BYTES);
       tma_load_4d(sq, &tmQ, full, 0, h, m0, b);
       for (int t = 0; t < nkt; ++t) tma_load_4d(skv + t * KT_BYTES, &tmK, full, 0, h, t * BMq, b);
-      if (want_o) {  // V tiles overwrite K once the QK^T MMAs have read it
-        mbar_wait(done, 0);
+      if (want_o) {  // V tiles into their own buffers, streaming while QK^T and the softmax run
         mbar_arrive_expect_tx(vfull, nkt * KT_BYTES);
-        for (int t = 0; t < nkt; ++t) tma_load_4d(skv + t * KT_BYTES, &tmV, vfull, 0, h, t * BMq, b);
+        for (int t = 0; t < nkt; ++t) tma_load_4d(svv + t * KT_BYTES, &tmV, vfull, 0, h, t * BMq, b);
       }
     }
   } else if (warp == 1) {
@@ -120,9 +121,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t idv = umma_idesc_bf16(BMq, HD, 0, 1);
         mbar_wait(vfull, 0);
         for (int t = 0; t < nkt; ++t) {
-          mbar_wait(pfull, t & 1);
+          mbar_wait(&pfull[t & 1], (t >> 1) & 1);
           tc_fence_after();
-          const uint32_t pa = smem_u32(spb), vb = smem_u32(skv + t * KT_BYTES);
+          const uint32_t pa = smem_u32(spb + (t & 1) * PB_BYTES), vb = smem_u32(svv + t * KT_BYTES);
 #pragma unroll
           for (int kb2 = 0; kb2 < 2; ++kb2)
 #pragma unroll
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_bf16(tmem, umma_desc_sw128(pa + kb2 * (PB_BYTES / 2) + k * 32, 16, 1024),
                         umma_desc_sw128(vb + (kb2 * 4 + k) * 2048, 8192, 1024), idv,
                         (t > 0 || kb2 > 0 || k > 0) ? 1u : 0u);
-          umma_commit(pfree);
+          umma_commit(&pfree[t & 1]);
         }
         umma_commit(ofull);
       }
@@ -174,11 +175,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       sum = (ma == -FLT_MAX ? 0.f : sa * __expf(ma - mx)) + (mb2 == -FLT_MAX ? 0.f : sb * __expf(mb2 - mx));
     }
     const float inv = 1.0f / sum;
-    uint16_t* st = stg + (warp - 2) * 32 * STG_PITCH;
-    uint16_t* prow0 = want_p ? P + (static_cast<int64_t>(z) * S + m0 + q * 32) * S : nullptr;
+    uint16_t* prow = want_p ? P + (static_cast<int64_t>(z) * S + i) * S : nullptr;
     for (int t = 0; t < nkt; ++t) {
-      if (want_o && t >= 1) mbar_wait(pfree, (t - 1) & 1);  // the MMA has read tile t-1
-      uint8_t* pbuf = spb;
+      if (want_o && t >= 2) mbar_wait(&pfree[t & 1], ((t >> 1) - 1) & 1);  // the MMA has read tile t-2
+      uint8_t* pbuf = spb + (t & 1) * PB_BYTES;
       for (int cc = half; cc < 4; cc += 2) {
         const int c = t * 4 + cc;
         uint32_t pk[16];
@@ -205,25 +205,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
           }
         }
-        if (want_p) {  // probabilities for backward: transpose through smem, row segments
-          uint32_t* srow = reinterpret_cast<uint32_t*>(st + lane * STG_PITCH);
+        if (want_p) {  // probabilities for backward: this row's 32 values of chunk c (64 B)
+          uint4* dst = reinterpret_cast<uint4*>(prow + c * 32);
 #pragma unroll
-          for (int u = 0; u < 16; ++u) srow[u] = pk[u];
-          __syncwarp();
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int row = static_cast<int>(lane >> 2) + 8 * r, seg = static_cast<int>(lane & 3);
-            const uint4 val = *reinterpret_cast<const uint4*>(st + row * STG_PITCH + seg * 8);
-            *reinterpret_cast<uint4*>(prow0 + static_cast<int64_t>(row) * S + c * 32 + seg * 8) = val;
-          }
-          __syncwarp();
+          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       }
       if (want_o) {  // P tile t visible to the tensor core; this warp's score reads are done
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(pfull);
+        if (lane == 0) mbar_arrive(&pfull[t & 1]);
       }
     }
     if (want_o && half == 0) {  // O rows of this quarter: TMEM columns [0, 64) -> bf16
