@@ -97,6 +97,14 @@ typedef struct rlhf_gemm_decode_params {
   const float* ln_x; const void* ln_g; const void* ln_b;
   /* fused KV-cache store (Y = packed qkv [N, 3*kv_d] bf16): k/v -> cache[n][h][*pos][e] */
   void* kcache; void* vcache; const int* pos; int kv_d, kv_hd, kv_H, kv_Smax;
+  /* LayerNorm statistics carried between decode GEMMs (no LayerNorm launch):
+   * ln_stats_out (producer, fp32 output): this GEMM's CTAs write per-CTA partial
+   *   (sum, sum of squares) of their output rows for every batch column n:
+   *   [gridDim][N][2] (gridDim = ceil(M/128) * splits, written to the HOST int *ln_stats_parts_out);
+   * ln_stats_in (consumer, with ln_x / ln_g / ln_b): X = bf16((ln_x - mean) * rstd * g + b)
+   *   with mean / var combined from ln_stats_parts such partials (var = E[x^2] - mean^2). */
+  float* ln_stats_out; int* ln_stats_parts_out;
+  const float* ln_stats_in; int ln_stats_parts;
 } rlhf_gemm_decode_params;
 int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t s);
 size_t rlhf_gemm_workspace_bytes(const rlhf_gemm_params* p);

@@ -277,6 +277,7 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
     dec_logits_.alloc(static_cast<size_t>(gen_B_) * cfg_.actor.vocab * 4);
     dec_top2_.alloc(static_cast<size_t>((cfg_.actor.vocab + 127) / 128) * gen_B_ * 16);
     argmax_ws_.alloc(static_cast<size_t>(gen_B_) * 64 * 4 * 4);
+    for (DevBuf& b : dec_st_) b.alloc(static_cast<size_t>(512) * std::min(gen_B_, 64) * 2 * 4);
     gen_tok_.alloc(static_cast<size_t>(gen_B_) * S_ * 4);
     pred_.alloc(static_cast<size_t>(gen_B_) * S_ * 4);
     margin_.alloc(static_cast<size_t>(gen_B_) * S_ * 4);

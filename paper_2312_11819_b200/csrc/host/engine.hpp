@@ -213,7 +213,8 @@ class Engine {
   void linear_decode(const uint16_t* W, int N_out, int K, const uint16_t* X, int Bg, const uint16_t* bias, void* Y,
                      bool y_f32, bool relu, const float* residual, const float* ln_x = nullptr,
                      const uint16_t* ln_g = nullptr, const uint16_t* ln_b = nullptr, int kv_layer = -1,
-                     int kv_b0 = 0);
+                     int kv_b0 = 0, const float* st_in = nullptr, int st_parts = 0, float* st_out = nullptr,
+                     int* parts_out = nullptr);
   void gemm(rlhf_gemm_params& p);
   void kcheck(int status, const char* what);
 
@@ -253,6 +254,7 @@ class Engine {
   DevBuf loop_ws_;   // persistent decode loop workspace
   DevBuf dec_top2_;  // LM-head per-tile top-2 partials [V/128][B] x float4
   DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_act_, dec_hf_, dec_logits_, argmax_ws_;
+  DevBuf dec_st_[2];  // LayerNorm (sum, sum sq) partials of the O-proj / FFN-down outputs [CTAs][B][2]
   cudaGraphExec_t decode_graph_ = nullptr;
   int graph_launches_ = 0;
   bool graph_for_pred_ = false;

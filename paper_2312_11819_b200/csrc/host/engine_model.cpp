@@ -107,7 +107,8 @@ void Engine::linear(const uint16_t* X, int M, int Kd, const uint16_t* W, int N, 
 // dimension); K split over a thread-block cluster so ~2 CTAs per SM stream weights.
 void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t* X, int Bg, const uint16_t* bias,
                            void* Y, bool y_f32, bool relu, const float* residual, const float* ln_x,
-                           const uint16_t* ln_g, const uint16_t* ln_b, int kv_layer, int kv_b0) {
+                           const uint16_t* ln_g, const uint16_t* ln_b, int kv_layer, int kv_b0, const float* st_in,
+                           int st_parts, float* st_out, int* parts_out) {
   // the decode kernel takes at most 64 batch columns: larger batches whose epilogue stores
   // K/V (or whose operand is LayerNorm-fused) run as 64-column chunks (the cache is indexed
   // by the chunk-local sample, so its base moves with the chunk)
@@ -176,6 +177,22 @@ void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t*
     while (split < 16 && tiles * split * 2 <= 2 * 148 && kb / (split * 2) >= 8) split *= 2;
   p.splits = split;
   p.pdl = pdl_;
+  p.ln_stats_out = st_out;
+  p.ln_stats_parts_out = parts_out;
+  if (st_in) {
+    // LayerNorm from the producer's statistics in the prologue, when every B tile of the
+    // K-slice fits the ring; otherwise the LayerNorm kernel writes the operand X first
+    const int max_kb = Bg <= 32 ? 8 : 6;
+    if ((kb + split - 1) / split <= max_kb) {
+      p.X = nullptr;
+      p.ln_stats_in = st_in;
+      p.ln_stats_parts = st_parts;
+    } else {
+      K(rlhf_layernorm(ln_x, ln_g, ln_b, const_cast<uint16_t*>(X), nullptr, nullptr, Bg, Kd, stream_), 1);
+      p.ln_x = nullptr;
+      p.ln_g = p.ln_b = nullptr;
+    }
+  }
   K(rlhf_gemm_decode(&p, stream_), 1);
 }
 
@@ -617,27 +634,38 @@ void Engine::decode_step(const Decoder& m, int B) {
   // per layer 7 launches: LN1 (layer 0: fused with the embedding), [QKV GEMM + KV-cache
   // store], attention, [O-proj + residual], LN2, [FFN-up + ReLU], [FFN-down + residual];
   // then final LN, [LM head + per-tile top-2], [merge -> token, *pos += 1]
-  // RLHF_DEC_FUSE_LN=1: LN1 (layers > 0) and LN2 run as the decode GEMM's LayerNorm prologue
-  // (every CTA normalises the B rows into its K-slice of the swizzled operand tiles)
-  static const bool fuse_ln = [] { const char* e = getenv("RLHF_DEC_FUSE_LN"); return e && atoi(e) != 0; }();
-  const bool fl = fuse_ln && B <= 64 && d <= 2048 && d % 64 == 0;
+  // LayerNorm statistics carried between the decode GEMMs (RLHF_DEC_LN_STATS=0: LayerNorm
+  // kernels): the O-proj / FFN-down epilogues write per-CTA (sum, sum sq) partials of the
+  // residual rows they produce, and the next GEMM (FFN-up / QKV of the next layer) normalises
+  // its own K-slice of the residual in its prologue -- 23 fewer launches per decode step
+  static const bool ln_stats_env = [] { const char* e = getenv("RLHF_DEC_LN_STATS"); return !e || atoi(e) != 0; }();
+  const bool fs = ln_stats_env && B <= 64 && d % 64 == 0 && d <= 2048;
+  float* st_a = dec_st_[0].as<float>();
+  float* st_b = dec_st_[1].as<float>();
+  int parts_a = 0, parts_b = 0;
   for (int l = 0; l < a.n_layers; ++l) {
-    const bool fl1 = fl && l > 0;
-    if (l > 0 && !(skip & 1) && !fl1)  // layer 0's LN1 ran in rlhf_embed_ln
+    const bool fs1 = fs && l > 0;  // layer 0's LN1 ran in rlhf_embed_ln
+    if (l > 0 && !(skip & 1) && !fs1)
       K(rlhf_layernorm(x, m.T(RLHF_T_LN1_G, l), m.T(RLHF_T_LN1_B, l), h, nullptr, nullptr, B, d, stream_), 1);
     if (!(skip & 4))
       linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, m.T(RLHF_T_BQKV, l), qkv, false, false, nullptr,
-                    fl1 ? x : nullptr, fl1 ? m.T(RLHF_T_LN1_G, l) : nullptr, fl1 ? m.T(RLHF_T_LN1_B, l) : nullptr, l);
+                    fs1 ? x : nullptr, fs1 ? m.T(RLHF_T_LN1_G, l) : nullptr, fs1 ? m.T(RLHF_T_LN1_B, l) : nullptr, l, 0,
+                    fs1 ? st_b : nullptr, parts_b);
     if (!(skip & 2))
       K(rlhf_attn_decode_prefetch(qkv, B, H, hd, kv_.Smax, kv_.Kc(l), kv_.Vc(l), pos, o,
                                   pf_kv ? kv_.Kc((l + 1) % a.n_layers) : nullptr,
                                   pf_kv ? kv_.Vc((l + 1) % a.n_layers) : nullptr, stream_), 1);
-    if (!(skip & 8)) linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, m.T(RLHF_T_BO, l), x, true, false, x);
-    if (!(skip & 1) && !fl) K(rlhf_layernorm(x, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h, nullptr, nullptr, B, d, stream_), 1);
+    if (!(skip & 8))
+      linear_decode(m.T(RLHF_T_WO, l), d, d, o, B, m.T(RLHF_T_BO, l), x, true, false, x, nullptr, nullptr, nullptr, -1, 0,
+                    nullptr, 0, fs ? st_a : nullptr, &parts_a);
+    if (!(skip & 1) && !fs) K(rlhf_layernorm(x, m.T(RLHF_T_LN2_G, l), m.T(RLHF_T_LN2_B, l), h, nullptr, nullptr, B, d, stream_), 1);
     if (!(skip & 16)) {
-      linear_decode(m.T(RLHF_T_W1, l), ff, d, h, B, m.T(RLHF_T_B1, l), f, false, true, nullptr, fl ? x : nullptr,
-                    fl ? m.T(RLHF_T_LN2_G, l) : nullptr, fl ? m.T(RLHF_T_LN2_B, l) : nullptr);
-      linear_decode(m.T(RLHF_T_W2, l), d, ff, f, B, m.T(RLHF_T_B2, l), x, true, false, x);
+      linear_decode(m.T(RLHF_T_W1, l), ff, d, h, B, m.T(RLHF_T_B1, l), f, false, true, nullptr, fs ? x : nullptr,
+                    fs ? m.T(RLHF_T_LN2_G, l) : nullptr, fs ? m.T(RLHF_T_LN2_B, l) : nullptr, -1, 0,
+                    fs ? st_a : nullptr, parts_a);
+      const bool prod = fs && l + 1 < a.n_layers;
+      linear_decode(m.T(RLHF_T_W2, l), d, ff, f, B, m.T(RLHF_T_B2, l), x, true, false, x, nullptr, nullptr, nullptr, -1, 0,
+                    nullptr, 0, prod ? st_b : nullptr, &parts_b);
     }
   }
   if (skip & 32) {

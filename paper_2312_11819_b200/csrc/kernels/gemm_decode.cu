@@ -32,8 +32,9 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int MAX_KB = BN <= 32 ? 8 : 6;
   static constexpr int PART_BYTES = BM * BN * 4;  // receive buffer: [slice][row of this CTA][BN] fp32
-  static constexpr int SMEM = MAX_KB * STAGE_BYTES + PART_BYTES + 1024 + 512;
-  static int smem_for(int stages) { return stages * STAGE_BYTES + PART_BYTES + 1024 + 512; }
+  static constexpr int TAIL = 1024;               // barriers (<= 256 B) + per-row (mean, rstd) (512 B)
+  static constexpr int SMEM = MAX_KB * STAGE_BYTES + PART_BYTES + TAIL + 1024;
+  static int smem_for(int stages) { return stages * STAGE_BYTES + PART_BYTES + TAIL + 1024; }
 };
 
 struct Args {
@@ -54,6 +55,10 @@ struct Args {
   uint16_t* vc;
   const int* pos;
   int kv_d, kv_hd, kv_H, kv_Smax;
+  // LayerNorm statistics between decode GEMMs: partial (sum, sum sq) out / in
+  float* st_out;
+  const float* st_in;
+  int st_parts;
 };
 __device__ __forceinline__ unsigned long long dclk() {
   unsigned long long c;
@@ -173,6 +178,54 @@ __device__ __forceinline__ void ln_prologue(const Args& e, uint8_t* btile0, int 
   }
 }
 
+// LayerNorm prologue from the producer's partial statistics (no row re-reduction): per batch
+// row, mean and rstd from the st_parts (sum, sum sq) partials (one warp per row, lanes over the
+// partials, fixed order), then this CTA's K-slice normalised into the swizzled B tiles.
+__device__ __forceinline__ void ln_stats_prologue(const Args& e, uint8_t* btile0, int stage_bytes, int kb0, int kb1,
+                                                  uint32_t warp, uint32_t lane, float* stat) {
+  const int k0 = kb0 * BK, k1 = min(kb1 * BK, e.K);
+  pdl_wait();  // the partials and ln_x come from the previous kernels
+  for (int n = static_cast<int>(warp); n < e.N; n += kThreads / 32) {
+    float s1 = 0.f, s2 = 0.f;
+    for (int q = static_cast<int>(lane); q < e.st_parts; q += 32) {
+      const float2 v = *reinterpret_cast<const float2*>(e.st_in + (static_cast<int64_t>(q) * e.N + n) * 2);
+      s1 += v.x;
+      s2 += v.y;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      const float mu = s1 / e.K;
+      const float var = fmaxf(s2 / e.K - mu * mu, 0.f);
+      stat[2 * n] = mu;
+      stat[2 * n + 1] = 1.0f / sqrtf(var + 1e-5f);
+    }
+  }
+  __syncthreads();
+  // (n, 4 consecutive k of the slice): float4 of x, 4 gamma / beta
+  const int kq = (k1 - k0) / 4;
+  for (int u = threadIdx.x; u < e.N * kq; u += kThreads) {
+    const int n = u / kq, k = k0 + 4 * (u % kq);
+    const float4 v = *reinterpret_cast<const float4*>(e.ln_x + static_cast<int64_t>(n) * e.K + k);
+    const uint2 gg = *reinterpret_cast<const uint2*>(e.ln_g + k), bb = *reinterpret_cast<const uint2*>(e.ln_b + k);
+    const float mu = stat[2 * n], rs = stat[2 * n + 1];
+    const float y0 = (v.x - mu) * rs * b2f(static_cast<uint16_t>(gg.x & 0xFFFFu)) + b2f(static_cast<uint16_t>(bb.x & 0xFFFFu));
+    const float y1 = (v.y - mu) * rs * b2f(static_cast<uint16_t>(gg.x >> 16)) + b2f(static_cast<uint16_t>(bb.x >> 16));
+    const float y2 = (v.z - mu) * rs * b2f(static_cast<uint16_t>(gg.y & 0xFFFFu)) + b2f(static_cast<uint16_t>(bb.y & 0xFFFFu));
+    const float y3 = (v.w - mu) * rs * b2f(static_cast<uint16_t>(gg.y >> 16)) + b2f(static_cast<uint16_t>(bb.y >> 16));
+    const int j = k / BK - kb0, kk = k % BK;
+    uint8_t* dst = btile0 + j * stage_bytes + n * 128 + (((kk >> 3) ^ (n & 7)) << 4) + (kk & 7) * 2;
+    const uint32_t w0 = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y0))) |
+                        (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y1))) << 16);
+    const uint32_t w1 = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y2))) |
+                        (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(y3))) << 16);
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -181,7 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* part = reinterpret_cast<float*>(smem + e.stages * C::STAGE_BYTES);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + e.stages * C::STAGE_BYTES + C::PART_BYTES);
+  uint8_t* tail = smem + e.stages * C::STAGE_BYTES + C::PART_BYTES;
+  float* stat = reinterpret_cast<float*>(tail + 256);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(tail);
   uint64_t* empty_bar = full_bar + e.stages;
   uint64_t* acc_bar = empty_bar + e.stages;
   uint64_t* recv_bar = acc_bar + 1;
@@ -258,7 +313,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // CTA's K-slice straight into the SWIZZLE_128B K-major B tiles:
     //   byte(n, kk) = n*128 + ((kk/8) ^ (n%8))*16 + (kk%8)*2   within a 64-wide k block
     __syncwarp();  // warp 0 arrives diverged (lane 0 issued the weight TMAs alone)
-    if (e.K <= 768) ln_prologue<6, 4>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
+    if (e.st_in) ln_stats_prologue(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane, stat);
+    else if (e.K <= 768) ln_prologue<6, 4>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
     else if (e.K <= 1024) ln_prologue<8, 2>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
     else ln_prologue<16, 1>(e, smem + C::A_BYTES, C::STAGE_BYTES, kb0, kb1, warp, lane);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> visible to tcgen05.mma
@@ -370,6 +426,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           (which == 0 ? e.kc : e.vc)[dst] = hb;
         }
       }
+    }
+  }
+  if (e.st_out) {
+    // this CTA's partial LayerNorm statistics of the output rows it just stored, per batch
+    // column: one warp per column, lanes over the rows (read back from Y, visible to the CTA
+    // after the barrier; rows past M count 0)
+    __syncthreads();
+    const float* yf = static_cast<const float*>(e.Y);
+    for (int n = static_cast<int>(warp); n < e.N; n += kThreads / 32) {
+      float s1 = 0.f, s2 = 0.f;
+      for (int r = static_cast<int>(lane); r < rows_per; r += 32) {
+        const int m = m0 + split * rows_per + r;
+        const float v = m < e.M ? yf[static_cast<int64_t>(n) * e.ldy + m] : 0.f;
+        s1 += v;
+        s2 += v * v;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (lane == 0)
+        *reinterpret_cast<float2*>(e.st_out + (static_cast<int64_t>(blockIdx.x) * e.N + n) * 2) = make_float2(s1, s2);
     }
   }
   DPROBE(7);
@@ -485,9 +564,15 @@ extern "C" int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t 
   a.kv_hd = p->kv_hd;
   a.kv_H = p->kv_H;
   a.kv_Smax = p->kv_Smax;
+  a.st_out = p->ln_stats_out;
+  a.st_in = p->ln_stats_in;
+  a.st_parts = p->ln_stats_parts;
+  if (a.st_in && (!a.ln_x || a.st_parts < 1)) return 2;
+  if (a.st_out && !p->y_f32) return 2;  // statistics of the fp32 residual stream
   if (a.ln_x && (p->K > 2048 || p->K % 4 || p->N > 64)) return 2;
   if (a.kc && (p->y_f32 || !p->pos || p->M != 3 * p->kv_d)) return 2;
   const int tiles = (p->M + dec::BM - 1) / dec::BM;
+  if (p->ln_stats_parts_out) *p->ln_stats_parts_out = tiles * splits;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return bn == 32 ? dec::launch<32>(tw, tx, a, tiles, p->pdl, s) : dec::launch<64>(tw, tx, a, tiles, p->pdl, s);
 }

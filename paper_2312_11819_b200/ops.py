@@ -114,11 +114,14 @@ class GemmDecodeParams(C.Structure):
                 ("bias", C.c_void_p), ("relu", C.c_int), ("residual", C.c_void_p), ("splits", C.c_int),
                 ("pdl", C.c_int), ("probe", C.c_void_p), ("ln_x", C.c_void_p), ("ln_g", C.c_void_p),
                 ("ln_b", C.c_void_p), ("kcache", C.c_void_p), ("vcache", C.c_void_p), ("pos", C.c_void_p),
-                ("kv_d", C.c_int), ("kv_hd", C.c_int), ("kv_H", C.c_int), ("kv_Smax", C.c_int)]
+                ("kv_d", C.c_int), ("kv_hd", C.c_int), ("kv_H", C.c_int), ("kv_Smax", C.c_int),
+                ("ln_stats_out", C.c_void_p), ("ln_stats_parts_out", C.c_void_p), ("ln_stats_in", C.c_void_p),
+                ("ln_stats_parts", C.c_int)]
 
 
 def gemm_decode(W: torch.Tensor, X: torch.Tensor, *, out: torch.Tensor | None = None, bias=None, relu=False,
-                residual=None, splits: int = 1, out_f32: bool = True, probe=None, ln=None) -> torch.Tensor:
+                residual=None, splits: int = 1, out_f32: bool = True, probe=None, ln=None, stats_out=None,
+                stats_in=None) -> torch.Tensor:
     """Y[N, M] = X[N, K] . W[M, K]^T (+bias[M]) (relu) (+residual) via rlhf_gemm_decode."""
     L = lib()
     L.rlhf_gemm_decode.argtypes = [C.POINTER(GemmDecodeParams), C.c_void_p]
@@ -133,10 +136,15 @@ def gemm_decode(W: torch.Tensor, X: torch.Tensor, *, out: torch.Tensor | None = 
                          probe.data_ptr() if probe is not None else None)
     if ln is not None:  # (x fp32 [N, K], gamma bf16 [K], beta bf16 [K])
         p.ln_x, p.ln_g, p.ln_b = ln[0].data_ptr(), ln[1].data_ptr(), ln[2].data_ptr()
+    parts = C.c_int(0)
+    if stats_out is not None:  # partials fp32 [>= CTAs * N * 2]; the CTA count comes back on the host
+        p.ln_stats_out, p.ln_stats_parts_out = stats_out.data_ptr(), C.cast(C.pointer(parts), C.c_void_p)
+    if stats_in is not None:  # (partials, count)
+        p.ln_stats_in, p.ln_stats_parts = stats_in[0].data_ptr(), int(stats_in[1])
     st = L.rlhf_gemm_decode(C.byref(p), _stream())
     if st != 0:
         raise RuntimeError(f"rlhf_gemm_decode failed with status {st}")
-    return out
+    return (out, parts.value) if stats_out is not None else out
 
 
 def layernorm(x: torch.Tensor, g: torch.Tensor, b: torch.Tensor) -> torch.Tensor:

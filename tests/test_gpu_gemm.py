@@ -284,3 +284,30 @@ def test_gemm_pair_lse_epilogue_logprobs():
     ref = torch.log_softmax(z, -1).gather(1, y[:, None])[:, 0]
     torch.cuda.synchronize()
     assert (logp - ref).abs().max().item() < 2e-3
+
+
+@pytest.mark.parametrize("Mp,Kp,Mc,N,sp,sc", [(768, 768, 2304, 32, 4, 4), (768, 3072, 3072, 32, 8, 4),
+                                              (2048, 8192, 6144, 16, 16, 4), (1024, 1024, 4096, 48, 4, 4)])
+def test_gemm_decode_layernorm_statistics_chain(Mp, Kp, Mc, N, sp, sc):
+    """Decode LayerNorm without a LayerNorm launch: the producer (O-proj / FFN-down shaped,
+    fp32 residual output) writes per-CTA (sum, sum sq) partials of its rows, the consumer
+    normalises its K-slice of that output in its prologue.  Against torch: x = X W^T + r,
+    y = LN(x) W2^T (bf16 LN output, fp32 GEMM)."""
+    from paper_2312_11819_b200 import ops
+    torch.manual_seed(Mp + N)
+    W = torch.randn(Mp, Kp, device="cuda").bfloat16() * 0.05
+    X = torch.randn(N, Kp, device="cuda").bfloat16()
+    res = torch.randn(N, Mp, device="cuda") * 2 + 0.5
+    x = res.clone()
+    parts_buf = torch.zeros(512 * 64 * 2, device="cuda")
+    x, parts = ops.gemm_decode(W, X, out=x, residual=x, splits=sp, stats_out=parts_buf)
+    exp_x = X.float() @ W.float().t() + res
+    torch.cuda.synchronize()
+    close(x, exp_x, 1e-4)
+    g = (1 + 0.1 * torch.randn(Mp, device="cuda")).bfloat16()
+    b = (0.1 * torch.randn(Mp, device="cuda")).bfloat16()
+    W2 = torch.randn(Mc, Mp, device="cuda").bfloat16()
+    y = ops.gemm_decode(W2, None, ln=(x, g, b), stats_in=(parts_buf, parts), splits=sc)
+    h = torch.nn.functional.layer_norm(x, (Mp,), g.float(), b.float(), eps=1e-5).bfloat16()
+    torch.cuda.synchronize()
+    close(y, h.float() @ W2.float().t(), 2e-2)  # one-pass variance: bf16 flips of h at most
