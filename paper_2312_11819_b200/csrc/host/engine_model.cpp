@@ -634,11 +634,12 @@ void Engine::decode_step(const Decoder& m, int B) {
   // per layer 7 launches: LN1 (layer 0: fused with the embedding), [QKV GEMM + KV-cache
   // store], attention, [O-proj + residual], LN2, [FFN-up + ReLU], [FFN-down + residual];
   // then final LN, [LM head + per-tile top-2], [merge -> token, *pos += 1]
-  // LayerNorm statistics carried between the decode GEMMs (RLHF_DEC_LN_STATS=0: LayerNorm
-  // kernels): the O-proj / FFN-down epilogues write per-CTA (sum, sum sq) partials of the
-  // residual rows they produce, and the next GEMM (FFN-up / QKV of the next layer) normalises
-  // its own K-slice of the residual in its prologue -- 23 fewer launches per decode step
-  static const bool ln_stats_env = [] { const char* e = getenv("RLHF_DEC_LN_STATS"); return !e || atoi(e) != 0; }();
+  // RLHF_DEC_LN_STATS=1: LayerNorm statistics carried between the decode GEMMs instead of
+  // LayerNorm kernels -- the O-proj / FFN-down epilogues write per-CTA (sum, sum sq) partials
+  // of the residual rows they produce, the next GEMM (FFN-up / QKV of the next layer)
+  // normalises its K-slice in its prologue: 23 fewer launches per c2 step, parity-green, but
+  // measured SLOWER (c2 decode step 498 -> 716 us, c3 1558 -> 2567 us), so off
+  static const bool ln_stats_env = [] { const char* e = getenv("RLHF_DEC_LN_STATS"); return e && atoi(e) != 0; }();
   const bool fs = ln_stats_env && B <= 64 && d % 64 == 0 && d <= 2048;
   float* st_a = dec_st_[0].as<float>();
   float* st_b = dec_st_[1].as<float>();
