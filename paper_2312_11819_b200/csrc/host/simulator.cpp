@@ -1004,6 +1004,8 @@ std::string run_command(const std::string& cmd, const std::string& json) {
       LoopParams lp = sc.loop;
       lp.batch_size = o.integer("batch", lp.batch_size);
       lp.micro_batches = o.integer("micro_batches", lp.micro_batches);
+      lp.prompt_len = o.integer("prompt_len", lp.prompt_len);
+      lp.gen_len = o.integer("gen_len", lp.gen_len);
       x.bs = build_strategy(ss.cfg, x.topo, build_pipeline(sc.structure, sc.sizes, lp));
       x.measured = o.num("measured_step_seconds", 0);
       x.frac = o.num("generation_fraction", -1);

@@ -36,8 +36,9 @@ def params(name, scalar_head):
 # workload family -> (actor arch, critic arch, bench-line glob, per-GPU batch at 8 GPUs, zero level, train micro-batch)
 FAMILIES = {
     "c2 (OPT-125m x4, 256+256)": ("opt-125m", "opt-125m", "r[12]_bench_c2_n*.json", 32, 0),
-    "c3 (OPT-1.3B / OPT-350m, 256+256)": ("opt-1.3b", "opt-350m", "r[12]_bench_c3_n*.json", 16, 0),
-    "c4 (LLaMA-7B x4, 256+256)": ("llama-7b", "llama-7b", "r1_bench_c4_llama7b_n4_*.json", 32, 1),
+    "c3 / c5 (OPT-1.3B / OPT-350m, prompt 256, response 128..1024)":
+        ("opt-1.3b", "opt-350m", "r[12]_bench_c[35]*_n*.json|r2_sweeps/r2_sweep_c*.json", 8, 0),
+    "c4 (LLaMA-7B x4, 256+256)": ("llama-7b", "llama-7b", "r1_bench_c4_llama7b_n4_*.json|r2_bench_c4_*.json", 32, 1),
 }
 
 
@@ -47,7 +48,7 @@ def main():
         sizes = {"actor": params(actor, 0), "critic": params(critic, 1), "ref": params(actor, 0),
                  "reward": params(critic, 1)}
         obs = []
-        for path in sorted(glob.glob(os.path.join(ROOT, "profiles", pat))):
+        for path in sorted(sum((glob.glob(os.path.join(ROOT, "profiles", p)) for p in pat.split("|")), [])):
             d = line(path)
             if not d or "split_seconds_per_step" not in d:
                 continue
@@ -60,6 +61,7 @@ def main():
             obs.append({"strategy": {"name": cfg.get("placement", "colocated"), "zero_level": cfg.get("zero_stage", 0),
                                      "tp_gen": 1},
                         "devices": d["n_gpus"], "batch": cfg["global_batch"], "measured_step_seconds": step,
+                        "prompt_len": cfg.get("prompt_len", 256), "gen_len": cfg.get("gen_len", 256),
                         "generation_fraction": frac, "source": os.path.basename(path)})
         if not obs:
             continue
