@@ -378,6 +378,7 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
 
 Engine::~Engine() {
   if (decode_graph_) cudaGraphExecDestroy(decode_graph_);
+  if (decode_graph1_) cudaGraphExecDestroy(decode_graph1_);
   for (Decoder* d : {&actor_, &critic_}) {
     for (cudaEvent_t e : d->rs_done)
       if (e) cudaEventDestroy(e);

@@ -255,8 +255,8 @@ class Engine {
   DevBuf dec_top2_;  // LM-head per-tile top-2 partials [V/128][B] x float4
   DevBuf dec_x_, dec_h_, dec_qkv_, dec_o_, dec_f_, dec_act_, dec_hf_, dec_logits_, argmax_ws_;
   DevBuf dec_st_[2];  // LayerNorm (sum, sum sq) partials of the O-proj / FFN-down outputs [CTAs][B][2]
-  cudaGraphExec_t decode_graph_ = nullptr;
-  int graph_launches_ = 0;
+  cudaGraphExec_t decode_graph_ = nullptr, decode_graph1_ = nullptr;  // k decode steps / one step
+  int graph_launches_ = 0, graph1_launches_ = 0, graph_steps_ = 0;
   bool graph_for_pred_ = false;
   // per-step timing: events of every executed interval, the step's start/end
   std::vector<ExecEvent> evs_;

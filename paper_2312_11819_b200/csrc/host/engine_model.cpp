@@ -790,10 +790,12 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   }
   const bool use_graph = opt_.use_cuda_graph != 0;
   if (use_graph) {
-    if (!decode_graph_ || graph_for_pred_ != teacher_forced) {
-      if (decode_graph_) cudaGraphExecDestroy(decode_graph_);
-      decode_graph_ = nullptr;
-      graph_for_pred_ = teacher_forced;
+    // k decode steps per CUDA graph (RLHF_DEC_GRAPH_STEPS, default 8): the PDL chain then also
+    // runs across step boundaries inside a graph; the R-1 steps are floor((R-1)/k) launches of
+    // the k-step graph plus the rest as launches of a one-step graph
+    static const int ksteps = [] { const char* e = getenv("RLHF_DEC_GRAPH_STEPS"); return e ? std::max(1, atoi(e)) : 8; }();
+    const int k = std::max(1, std::min(ksteps, R_ - 1));
+    auto capture = [&](int nsteps, cudaGraphExec_t* out, int* nlaunch) {
       cudaGraph_t g;
       const int before = launches_;
       if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
@@ -801,7 +803,7 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
       pdl_ = opt_.use_cuda_graph == 2 ? 0 : 1;  // programmatic dependent launches inside the graph
       rlhf_set_pdl(pdl_);  // (thread-local: engines on other host threads are unaffected)
       try {
-        decode_step(m, B);
+        for (int st = 0; st < nsteps; ++st) decode_step(m, B);
       } catch (...) {  // leave the stream usable: end the capture, drop the partial graph
         rlhf_set_pdl(0);
         pdl_ = 0;
@@ -814,14 +816,27 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
       rlhf_set_pdl(0);
       pdl_ = 0;
       if (cudaStreamEndCapture(stream_, &g) != cudaSuccess) throw DeviceError("decode graph capture failed");
-      if (cudaGraphInstantiate(&decode_graph_, g, 0) != cudaSuccess) throw DeviceError("decode graph instantiate failed");
+      if (cudaGraphInstantiate(out, g, 0) != cudaSuccess) throw DeviceError("decode graph instantiate failed");
       cudaGraphDestroy(g);
-      graph_launches_ = launches_ - before;
+      *nlaunch = launches_ - before;
       launches_ = before;
+    };
+    if (!decode_graph_ || graph_for_pred_ != teacher_forced || graph_steps_ != k) {
+      for (cudaGraphExec_t* gp : {&decode_graph_, &decode_graph1_})
+        if (*gp) cudaGraphExecDestroy(*gp), *gp = nullptr;
+      graph_for_pred_ = teacher_forced;
+      graph_steps_ = k;
+      capture(k, &decode_graph_, &graph_launches_);
+      if (k > 1) capture(1, &decode_graph1_, &graph1_launches_);
     }
-    for (int s = 1; s < R_; ++s) {
+    const int reps = (R_ - 1) / k, rest = (R_ - 1) % k;
+    for (int r = 0; r < reps; ++r) {
       if (cudaGraphLaunch(decode_graph_, stream_) != cudaSuccess) throw DeviceError("decode graph launch failed");
       launches_ += graph_launches_;
+    }
+    for (int r = 0; r < rest; ++r) {
+      if (cudaGraphLaunch(decode_graph1_, stream_) != cudaSuccess) throw DeviceError("decode graph launch failed");
+      launches_ += graph1_launches_;
     }
   } else {
     graph_for_pred_ = teacher_forced;
