@@ -239,7 +239,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch override (memory studies)")
     ap.add_argument("--train-mb", type=int, default=0, help="samples per TrainFB micro-batch (0: all)")
-    ap.add_argument("--zero", type=int, default=0, choices=[0, 1, 2], help="ZeRO stage of the trainable models")
+    ap.add_argument("--zero", type=int, default=0, choices=[0, 1, 2, 3], help="ZeRO stage of the trainable models")
     ap.add_argument("--micro-batches", type=int, default=1, help="LoopParams::micro_batches (task-DAG micro-batches)")
     ap.add_argument("--rollouts", type=int, default=1, help="LoopParams::rollout_nums")
     ap.add_argument("--epochs", type=int, default=1, help="LoopParams::ppo_epochs")
