@@ -254,6 +254,26 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
     }
   }
 
+  // ---- epoch-0 forward reuse: the experience Forward of a trained model runs with the training
+  // forward (activations saved, LM-head logits kept) and its TrainFB of PPO epoch 0 -- same
+  // weights, same tokens, so the same activations -- backpropagates through them instead of
+  // recomputing the forward.  Needs the Forward block to be the whole TrainFB chunk (one
+  // rollout, one micro-batch, train chunk >= block) and an arena of its own per trained model
+  // (RLHF_REUSE_FWD=0 disables).
+  {
+    static const bool env = [] { const char* e = getenv("RLHF_REUSE_FWD"); return !e || atoi(e) != 0; }();
+    const bool shape_ok = env && xp_.rollouts == 1 && xp_.M == 1;
+    for (int mi : {0, 1}) {
+      const ModelName mn = static_cast<ModelName>(mi);
+      if (!shape_ok || !hosts_[mi]) continue;
+      bool scores = false;  // does this rank run the model's experience Forward?
+      for (const StageTask& t : xp_.tasks) scores |= t.kind == TaskKind::Forward && t.model == mn;
+      const int per = xp_.sets[xp_.set_of[mi]].per;
+      const bool own_arena = side_ || !(hosts_[0] && hosts_[1]);
+      reuse_fwd_[mi] = scores && own_arena && train_mb_ >= per;
+    }
+  }
+
   // ---- generation state (the generator: Actor or ShadowActor) ----
   if (gen_B_ > 0) generator_ = model(xp_.generator);
   if (generator_) {
@@ -479,15 +499,21 @@ void Engine::run_exchange(const ExecStep& s) {
 
 // Forward + loss + backward of `B` experience rows starting at row0 of row set rb,
 // accumulating into m's flat gradient.
-void Engine::train_rows(Decoder& m, bool actor, RowBufs& rb, int row0, int B, float denom) {
+void Engine::train_rows(Decoder& m, bool actor, RowBufs& rb, int row0, int B, float denom, bool reuse) {
   const int d = m.a.d_model, V = m.a.vocab, BR = B * R_;
   const int32_t* tok = rb.tokens.as<int32_t>() + static_cast<size_t>(row0) * S_;
   const size_t r0 = static_cast<size_t>(row0) * R_;
-  forward(m, tok, B, S_, S_, true, nullptr);
+  // reuse: the experience Forward left this block's training activations (and, for the Actor,
+  // its logits / lse / response rows) in the arena; the epoch-0 forward would recompute them
+  if (!reuse) forward(m, tok, B, S_, S_, true, nullptr);
   if (actor) {
     float* logp = rb.logp_new.as<float>() + r0;
     float* g = rb.gbuf.as<float>() + r0;
-    lm_logprobs(m, tok, B, logp, true);
+    if (reuse)
+      CK(cudaMemcpyAsync(logp, rb.logp_old.as<float>() + r0, static_cast<size_t>(BR) * 4, cudaMemcpyDeviceToDevice,
+                         stream_));
+    else
+      lm_logprobs(m, tok, B, logp, true);
     K(rlhf_ppo_actor_loss(logp, rb.logp_old.as<float>() + r0, rb.adv.as<float>() + r0, BR, cfg_.cliprange, denom, g,
                           loss_.as<float>(), stream_), 1);
     K(rlhf_logprob_bwd(arp_->logits, arp_->lse, g, BR, V, tok, S_, P_, R_, arp_->dz, stream_), 1);
@@ -509,7 +535,10 @@ void Engine::train_rows(Decoder& m, bool actor, RowBufs& rb, int row0, int B, fl
   } else {
     float* v = rb.values_new.as<float>() + r0;
     float* g = rb.gbuf2.as<float>() + r0;
-    K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, d, v, stream_), 1);
+    if (reuse)
+      CK(cudaMemcpyAsync(v, rb.values.as<float>() + r0, static_cast<size_t>(BR) * 4, cudaMemcpyDeviceToDevice, stream_));
+    else
+      K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), B, S_, R_, P_ - 1, d, v, stream_), 1);
     K(rlhf_ppo_critic_loss(v, rb.values.as<float>() + r0, rb.ret.as<float>() + r0, BR, cfg_.cliprange_value, denom, g,
                            loss_.as<float>() + 1, stream_), 1);
     CK(cudaMemsetAsync(arp_->dhf, 0, static_cast<size_t>(B) * S_ * d * 4, stream_));
@@ -562,6 +591,14 @@ void Engine::run_task(const ExecStep& s) {
       const int32_t* tok = rb.tokens.as<int32_t>() + row0 * S_;
       begin_event(i, s, static_cast<int>(TaskKind::Forward), lane_of(t.model), static_cast<int>(Stage::Forward));
       const Decoder& m = *model(t.model);
+      if (mi <= 1 && reuse_fwd_[mi]) {  // the training forward, kept for TrainFB epoch 0
+        forward(m, tok, per, S_, S_, true, nullptr);
+        if (mi == 0) lm_logprobs(m, tok, per, rb.logp_old.as<float>() + row0 * R_, true);
+        else K(rlhf_scalar_head(arp_->hf, m.T(RLHF_T_VHEAD), per, S_, R_, P_ - 1, m.a.d_model,
+                                rb.values.as<float>() + row0 * R_, stream_), 1);
+        end_event();
+        return;
+      }
       switch (output_field(t.model)) {
         case Field::LogpOld: score_logp(m, tok, per, rb.logp_old.as<float>() + row0 * R_); break;
         case Field::LogpRef: score_logp(m, tok, per, rb.logp_ref.as<float>() + row0 * R_); break;
@@ -594,9 +631,11 @@ void Engine::run_task(const ExecStep& s) {
       // the micro-batch's rows of every rollout (one block per rollout), in chunks of train_mb_
       const float denom = cfg_.loss_denominator > 0 ? cfg_.loss_denominator * xp_.rollouts
                                                     : static_cast<float>(xp_.G) * xp_.rollouts * R_;
+      const bool reuse = reuse_fwd_[mi] && t.epoch_index == 0;
       for (int r = 0; r < xp_.rollouts; ++r) {
         const int row0 = (r * xp_.M + t.micro_batch_index) * per;
-        for (int c = 0; c < per; c += train_mb_) train_rows(m, actor, rb, row0 + c, std::min(train_mb_, per - c), denom);
+        for (int c = 0; c < per; c += train_mb_)
+          train_rows(m, actor, rb, row0 + c, std::min(train_mb_, per - c), denom, reuse);
       }
       end_event();
       return;
@@ -801,8 +840,26 @@ void Engine::step(const int32_t* prompts_host, rlhf_step_report* rep) {
   // host -> device on the comm lane: the prompt exchanges that follow consume it there
   CK(cudaMemcpyAsync(home_.p, pr.data(), pr.size() * 4, cudaMemcpyHostToDevice, lane_[2]));
 
+  auto is_fwd = [&](size_t i) {
+    const ExecStep& s = xp_.steps[i];
+    return s.kind == StepKind::Task && xp_.tasks[s.task].kind == TaskKind::Forward;
+  };
   for (size_t i = 0; i < xp_.steps.size(); ++i) {
     const ExecStep& s = xp_.steps[i];
+    if (is_fwd(i) && (reuse_fwd_[0] || reuse_fwd_[1])) {
+      // a run of independent Forward tasks (one generation's scorers): the ones whose
+      // activations TrainFB reuses go last on their lane, after the forwards that would
+      // overwrite the arena
+      size_t j = i;
+      while (j < xp_.steps.size() && is_fwd(j)) ++j;
+      for (int pass = 0; pass < 2; ++pass)
+        for (size_t k = i; k < j; ++k) {
+          const int mk = static_cast<int>(xp_.tasks[xp_.steps[k].task].model);
+          if ((mk <= 1 && reuse_fwd_[mk]) == (pass == 1)) run_task(xp_.steps[k]);
+        }
+      i = j - 1;
+      continue;
+    }
     switch (s.kind) {
       case StepKind::Exchange: run_exchange(s); break;
       case StepKind::Task: run_task(s); break;

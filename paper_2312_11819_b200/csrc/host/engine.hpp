@@ -201,7 +201,7 @@ class Engine {
   void run_task(const ExecStep& s);
   void run_experience(const ExecStep& s);
   void run_optimizer(const ExecStep& s, int step_index);
-  void train_rows(Decoder& m, bool actor, RowBufs& rb, int row0, int B, float denom);
+  void train_rows(Decoder& m, bool actor, RowBufs& rb, int row0, int B, float denom, bool reuse = false);
   void begin_event(int step_index, const ExecStep& s, int kind, int lane, int stage);
   void end_event();
   void wait_deps(int step_index, int lane);
@@ -232,6 +232,7 @@ class Engine {
   // lanes: 0 main compute, 1 side compute (critic-shaped models, Co-located-style ranks), 2 comm
   cudaStream_t lane_[3] = {nullptr, nullptr, nullptr};
   bool side_ = false;
+  bool reuse_fwd_[2] = {false, false};  // Actor / Critic: epoch-0 TrainFB reuses the experience Forward
   cudaStream_t stream_ = nullptr;  // the lane currently enqueued on
   int cur_lane_ = 0;
   ncclComm_t world_ = nullptr, actor_comm_ = nullptr, critic_comm_ = nullptr;
