@@ -148,23 +148,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(done, 0);
     tc_fence_after();
     float mx = -FLT_MAX, sum = 0.f;
-    for (int c = half; c < nch; c += 2) {
+    // online (max, sum) over one 32-column chunk of scores already in registers
+    auto absorb = [&](const uint32_t (&r)[32], int c) {
       float v[32];
-      tmem_ld32(tq + c * 32, v);
       float cm = -FLT_MAX;
 #pragma unroll
       for (int t = 0; t < 32; ++t) {
-        v[t] *= alpha;
+        v[t] = __uint_as_float(r[t]) * alpha;
         if (c * 32 + t <= i) cm = fmaxf(cm, v[t]);
       }
       const float nm = fmaxf(mx, cm);
-      if (nm == -FLT_MAX) continue;  // whole chunk above this row's diagonal
+      if (nm == -FLT_MAX) return;  // whole chunk above this row's diagonal
       float cs = 0.f;
 #pragma unroll
       for (int t = 0; t < 32; ++t)
         if (c * 32 + t <= i) cs += __expf(v[t] - nm);
       sum = (mx == -FLT_MAX ? 0.f : sum * __expf(mx - nm)) + cs;
       mx = nm;
+    };
+    // two TMEM loads in flight per wait (chunks c and c + 2 of this warp's parity)
+    for (int c = half; c < nch; c += 4) {
+      uint32_t ra[32], rb[32];
+      tmem_ld32_nowait(tq + c * 32, ra);
+      const bool two = c + 2 < nch;
+      if (two) tmem_ld32_nowait(tq + (c + 2) * 32, rb);
+      tmem_ld_wait32x2(ra, rb);
+      absorb(ra, c);
+      if (two) absorb(rb, c + 2);
     }
     rowst[(half * 2) * BMq + il] = mx;
     rowst[(half * 2 + 1) * BMq + il] = sum;
@@ -179,17 +189,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < nkt; ++t) {
       if (want_o && t >= 2) mbar_wait(&pfree[t & 1], ((t >> 1) - 1) & 1);  // the MMA has read tile t-2
       uint8_t* pbuf = spb + (t & 1) * PB_BYTES;
-      for (int cc = half; cc < 4; cc += 2) {
+      uint32_t ra[32], rb[32];
+      {
+        const int c0 = t * 4 + half;
+        if (c0 < nch) tmem_ld32_nowait(tq + c0 * 32, ra);
+        if (c0 + 2 < nch) tmem_ld32_nowait(tq + (c0 + 2) * 32, rb);
+        if (c0 < nch) tmem_ld_wait32x2(ra, rb);
+      }
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const int cc = half + 2 * k2;
         const int c = t * 4 + cc;
         uint32_t pk[16];
         if (c < nch) {
-          float v[32];
-          tmem_ld32(tq + c * 32, v);
+          const uint32_t(&r)[32] = k2 == 0 ? ra : rb;
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             const int j = c * 32 + 2 * u;
-            const float p0 = j <= i ? __expf(v[2 * u] * alpha - mx) * inv : 0.f;
-            const float p1 = j + 1 <= i ? __expf(v[2 * u + 1] * alpha - mx) * inv : 0.f;
+            const float p0 = j <= i ? __expf(__uint_as_float(r[2 * u]) * alpha - mx) * inv : 0.f;
+            const float p1 = j + 1 <= i ? __expf(__uint_as_float(r[2 * u + 1]) * alpha - mx) * inv : 0.f;
             pk[u] = static_cast<uint32_t>(f2b(p0)) | (static_cast<uint32_t>(f2b(p1)) << 16);
           }
         } else {
