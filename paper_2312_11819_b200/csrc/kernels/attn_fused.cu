@@ -45,6 +45,15 @@ __host__ __device__ constexpr int smem_bytes(bool want_p, bool want_o) {
 constexpr int SMEM = smem_bytes(true, true);
 
 __device__ __forceinline__ uint16_t f2b(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {  // one cvt.rn.bf16x2
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+__device__ __forceinline__ float ex2f(float x) {  // 2^x, flushes subnormal results to 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -147,24 +156,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nch = (m0 + q * 32 + 32) / 32;  // chunks holding any j <= (this warp's last row)
     mbar_wait(done, 0);
     tc_fence_after();
+    // Scores in log2 units (a2 = alpha * log2 e): every exponential is one FFMA + one
+    // ex2.approx.ftz.  Only the chunk holding this quarter's diagonal (c == nch - 1) is
+    // masked; chunks left of it are entirely causal-visible for all 32 rows of the warp.
+    const float a2 = alpha * 1.4426950408889634f;
     float mx = -FLT_MAX, sum = 0.f;
-    // online (max, sum) over one 32-column chunk of scores already in registers
     auto absorb = [&](const uint32_t (&r)[32], int c) {
-      float v[32];
-      float cm = -FLT_MAX;
+      float cm = -FLT_MAX, cs = 0.f;
+      if (c != nch - 1) {
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        v[t] = __uint_as_float(r[t]) * alpha;
-        if (c * 32 + t <= i) cm = fmaxf(cm, v[t]);
+        for (int t = 0; t < 32; ++t) cm = fmaxf(cm, __uint_as_float(r[t]));
+        const float nm = fmaxf(mx, cm * a2);
+#pragma unroll
+        for (int t = 0; t < 32; ++t) cs += ex2f(fmaf(__uint_as_float(r[t]), a2, -nm));
+        sum = sum * ex2f(mx - nm) + cs;
+        mx = nm;
+      } else {
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+          if (c * 32 + t <= i) cm = fmaxf(cm, __uint_as_float(r[t]));
+        const float nm = fmaxf(mx, cm * a2);
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+          if (c * 32 + t <= i) cs += ex2f(fmaf(__uint_as_float(r[t]), a2, -nm));
+        sum = sum * ex2f(mx - nm) + cs;
+        mx = nm;
       }
-      const float nm = fmaxf(mx, cm);
-      if (nm == -FLT_MAX) return;  // whole chunk above this row's diagonal
-      float cs = 0.f;
-#pragma unroll
-      for (int t = 0; t < 32; ++t)
-        if (c * 32 + t <= i) cs += __expf(v[t] - nm);
-      sum = (mx == -FLT_MAX ? 0.f : sum * __expf(mx - nm)) + cs;
-      mx = nm;
     };
     // two TMEM loads in flight per wait (chunks c and c + 2 of this warp's parity)
     for (int c = half; c < nch; c += 4) {
@@ -179,10 +196,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     rowst[(half * 2) * BMq + il] = mx;
     rowst[(half * 2 + 1) * BMq + il] = sum;
     named_bar_sync(1, 32 * kEpi);
-    {
+    {  // an empty half has (-FLT_MAX, 0): its weight ex2(-huge) * 0 is 0
       const float ma = rowst[il], sa = rowst[BMq + il], mb2 = rowst[2 * BMq + il], sb = rowst[3 * BMq + il];
       mx = fmaxf(ma, mb2);
-      sum = (ma == -FLT_MAX ? 0.f : sa * __expf(ma - mx)) + (mb2 == -FLT_MAX ? 0.f : sb * __expf(mb2 - mx));
+      sum = sa * ex2f(ma - mx) + sb * ex2f(mb2 - mx);
     }
     const float inv = 1.0f / sum;
     uint16_t* prow = want_p ? P + (static_cast<int64_t>(z) * S + i) * S : nullptr;
@@ -201,14 +218,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cc = half + 2 * k2;
         const int c = t * 4 + cc;
         uint32_t pk[16];
-        if (c < nch) {
+        if (c < nch - 1) {
+          const uint32_t(&r)[32] = k2 == 0 ? ra : rb;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const float p0 = ex2f(fmaf(__uint_as_float(r[2 * u]), a2, -mx)) * inv;
+            const float p1 = ex2f(fmaf(__uint_as_float(r[2 * u + 1]), a2, -mx)) * inv;
+            pk[u] = pack_bf16(p0, p1);
+          }
+        } else if (c == nch - 1) {
           const uint32_t(&r)[32] = k2 == 0 ? ra : rb;
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             const int j = c * 32 + 2 * u;
-            const float p0 = j <= i ? __expf(__uint_as_float(r[2 * u]) * alpha - mx) * inv : 0.f;
-            const float p1 = j + 1 <= i ? __expf(__uint_as_float(r[2 * u + 1]) * alpha - mx) * inv : 0.f;
-            pk[u] = static_cast<uint32_t>(f2b(p0)) | (static_cast<uint32_t>(f2b(p1)) << 16);
+            const float p0 = j <= i ? ex2f(fmaf(__uint_as_float(r[2 * u]), a2, -mx)) * inv : 0.f;
+            const float p1 = j + 1 <= i ? ex2f(fmaf(__uint_as_float(r[2 * u + 1]), a2, -mx)) * inv : 0.f;
+            pk[u] = pack_bf16(p0, p1);
           }
         } else {
 #pragma unroll
