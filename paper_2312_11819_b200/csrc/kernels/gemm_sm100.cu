@@ -867,19 +867,29 @@ __global__ void __launch_bounds__(pair::THREADS, 1)
           tc_fence_before();
           if (lane == 0) arrive_remote(mapa(smem_u32(&tempty[acc]), 0));
         }
-        if (e.lse_part) {
+        if (e.lse_part) {  // (max, sum) in natural units; exponentials as 2^(v*a2 - m*log2e)
           const int nc0 = w.n0 + c * 32;
-          float cm = -FLT_MAX;
+          const float a2 = e.alpha * 1.4426950408889634f;
+          float cm = -FLT_MAX, cs = 0.f;
+          if (nc0 + 32 <= e.N) {  // every column valid (alpha > 0: max commutes with the scale)
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (nc0 + j < e.N) cm = fmaxf(cm, v[j] * e.alpha);
-          const float nm = fmaxf(lm, cm);
-          float cs = 0.f;
+            for (int j = 0; j < 32; ++j) cm = fmaxf(cm, v[j]);
+            const float nm = fmaxf(lm, cm * e.alpha), nm2 = nm * 1.4426950408889634f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (nc0 + j < e.N) cs += __expf(v[j] * e.alpha - nm);
-          ls = (lm == -FLT_MAX ? 0.f : ls * __expf(lm - nm)) + cs;
-          lm = nm;
+            for (int j = 0; j < 32; ++j) cs += ex2_ftz(fmaf(v[j], a2, -nm2));
+            ls = ls * ex2_ftz((lm - nm) * 1.4426950408889634f) + cs;
+            lm = nm;
+          } else if (nc0 < e.N) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nc0 + j < e.N) cm = fmaxf(cm, v[j]);
+            const float nm = fmaxf(lm, cm * e.alpha), nm2 = nm * 1.4426950408889634f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nc0 + j < e.N) cs += ex2_ftz(fmaf(v[j], a2, -nm2));
+            ls = ls * ex2_ftz((lm - nm) * 1.4426950408889634f) + cs;
+            lm = nm;
+          }
           if (tgt >= nc0 && tgt < nc0 + 32) {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -1115,7 +1125,7 @@ extern "C" int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t stream) {
   a.lse_S = p->lse_S;
   a.lse_P = p->lse_P;
   a.lse_R = p->lse_R;
-  if (a.lse_part && (!p->lse_tgt || !p->lse_tokens || p->lse_R < 1 || p->batch != 1)) return 2;
+  if (a.lse_part && (!p->lse_tgt || !p->lse_tokens || p->lse_R < 1 || p->batch != 1 || !(p->alpha > 0.f))) return 2;
   if (a.top2 && (p->c_cs == 1 || p->split_k > 1 || p->batch != 1 || bn != 32 && bn != 64 && bn != 128 && bn != 256))
     return 2;
   {

@@ -128,6 +128,13 @@ __device__ __forceinline__ void tmem_ld_wait32x2(uint32_t (&a)[32], uint32_t (&b
                : "memory");
 }
 
+// 2^x on the SFU with subnormal results flushed to 0 (no range fix-up around MUFU.EX2)
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits.
 //   K-major tile : rows of 64 bf16 (128 B), 8-row atoms 1024 B apart  -> lbo 16, sbo 1024
 //   MN-major tile: 64-element MN blocks of (BK rows x 128 B), lbo = block stride, sbo 1024
