@@ -31,7 +31,12 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int MAX_KB = BN <= 32 ? 8 : 6;
-  static constexpr int PART_BYTES = BM * BN * 4;  // receive buffer: [slice][row of this CTA][BN] fp32
+  // receive buffer: [slice][row of this CTA][PITCH] fp32.  The 16-byte row padding puts the
+  // rows read by one quarter-warp (consecutive rows, same 4 columns) on distinct banks: with
+  // an unpadded 128-byte row every reduction load was an 8-way bank conflict (0.5 us per
+  // epilogue unit, clock64 probes)
+  static constexpr int PITCH = BN + 4;
+  static constexpr int PART_BYTES = BM * PITCH * 4;
   static constexpr int TAIL = 1024;               // barriers (<= 256 B) + per-row (mean, rstd) (512 B)
   static constexpr int SMEM = MAX_KB * STAGE_BYTES + PART_BYTES + TAIL + 1024;
   static int smem_for(int stages) { return stages * STAGE_BYTES + PART_BYTES + TAIL + 1024; }
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = static_cast<int>(warp) * 32 + static_cast<int>(lane);
     const uint32_t tb = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const int owner = row / rows_per, rl = row % rows_per;
-    const uint32_t dst = map_rank(smem_u32(part) + static_cast<uint32_t>(((split * rows_per + rl) * BN) * 4),
+    const uint32_t dst = map_rank(smem_u32(part) + static_cast<uint32_t>(((split * rows_per + rl) * C::PITCH) * 4),
                                   static_cast<uint32_t>(owner));
     const uint32_t rbar = map_rank(smem_u32(recv_bar), static_cast<uint32_t>(owner));
 #pragma unroll
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
     for (int s2 = 0; s2 < e.splits; ++s2) {  // fixed slice order
-      const float4 v = *reinterpret_cast<const float4*>(part + (s2 * rows_per + rl) * BN + c4);
+      const float4 v = *reinterpret_cast<const float4*>(part + (s2 * rows_per + rl) * C::PITCH + c4);
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
     const float a4[4] = {acc.x, acc.y, acc.z, acc.w};

@@ -11,7 +11,7 @@ for name, M, K, splits in [("Wo", 768, 768, 4), ("W2", 768, 3072, 8), ("qkv", 23
     for it in range(3):
         probe.zero_(); torch.cuda.synchronize()
         ops.gemm_decode(W, X, splits=splits, probe=probe if it == 2 else None); torch.cuda.synchronize()
-    pr = probe.view(-1, 16).cpu().numpy()[:, :9].astype(np.int64)
+    pr = probe.view(-1, 16).cpu().numpy()[:, :13].astype(np.int64)
     pr = pr[pr[:, 0] > 0]
     d = (pr - pr[:, :1]) / 1.9e3
     print(f"{name:4s} ctas={len(pr):3d} median:", " ".join(f"{v:6.2f}" for v in np.median(d, 0)))
