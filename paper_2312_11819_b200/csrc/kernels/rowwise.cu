@@ -125,11 +125,11 @@ template <int VPL, bool RMS>  // float4 vectors per lane; RMS: RMSNorm (no centr
 __global__ void layernorm_kernel(const float* __restrict__ x, const uint16_t* __restrict__ g,
                                  const uint16_t* __restrict__ bta, uint16_t* __restrict__ y, float* __restrict__ mean,
                                  float* __restrict__ rstd, int M, int d) {
-  pdl_entry_early();
+  // gamma / beta are weights: requested before griddepcontrol.wait, only x waits for the
+  // predecessor (the dependents are triggered first, as in pdl_entry_early)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (row >= M) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * d);
   const uint2* g2 = reinterpret_cast<const uint2*>(g);
   const uint2* b2 = reinterpret_cast<const uint2*>(bta);
   const int q = d / 4;
@@ -139,10 +139,17 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const uint16_t* __
   for (int k = 0; k < VPL; ++k) {
     const int c = lane + 32 * k;
     if (c < q) {
-      v[k] = xr[c];
       gg[k] = g2[c];
       bb[k] = RMS ? make_uint2(0u, 0u) : b2[c];
     }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (row >= M) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * d);
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c = lane + 32 * k;
+    if (c < q) v[k] = xr[c];
   }
   float s = 0.f;
   if (!RMS) {
