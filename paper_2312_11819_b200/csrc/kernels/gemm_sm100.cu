@@ -693,7 +693,7 @@ __device__ __forceinline__ void commit_pair(uint64_t* bar) {
       : "memory");
 }
 __device__ __forceinline__ void arrive_remote(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
 // pair unit u -> (batch z, 256-row m tile, 256-col n tile)
