@@ -498,6 +498,16 @@ void Engine::backward(Decoder& m, const int32_t* tokens, int B, int S) {
     int split = 1;
     if (tiles * 4 <= 148)
       while (split < 8 && tiles * split * 2 <= 148 && rows / 64 / (split * 2) >= 8) split *= 2;
+    // default: 128 x 256 tiles (87 FLOP per operand byte against 64 for 128 x 128) with
+    // deterministic split-K filling the SMs (c2 TrainFB 27.3 -> 26.0 ms); RLHF_WGRAD=0: the
+    // previous 128 x 128 unsplit tiles
+    static const int wmode = [] { const char* e = getenv("RLHF_WGRAD"); return e ? atoi(e) : 1; }();
+    if (wmode == 1) {
+      p.block_n = 256;
+      const int t2 = ((N_out + 127) / 128) * ((K_in + 255) / 256);
+      split = 1;
+      while (split < 8 && t2 * split * 2 <= 148 && rows / 64 / (split * 2) >= 8) split *= 2;
+    }
     p.split_k = split;
     gemm(p);
   };
