@@ -175,22 +175,6 @@ __device__ __forceinline__ void dec_issue(uint16_t* ring, const uint16_t* src, i
            &bars[slot]);
 }
 
-// block g of the unified stream K_0 .. K_{n-1}, V_0 .. V_{n-1} -> ring slot g % (2 NS): one
-// ring of 2 NS slots, so value blocks are requested as soon as key blocks free their slots
-// (during the score pass) instead of after the first value blocks are consumed
-template <int HD, int NS>
-__device__ __forceinline__ void dec_issue_kv(uint16_t* ring, const uint16_t* K, const uint16_t* V, int g, int n, int ctx,
-                                             uint64_t* bars) {
-  using Cf = DecCfg<HD, NS>;
-  const int blk = g < n ? g : g - n;
-  const int rows = min(Cf::RB, ctx - blk * Cf::RB);
-  if (g >= 2 * n || rows <= 0) return;
-  const int slot = g % (2 * Cf::NS);
-  mbar_arrive_expect_tx(&bars[slot], static_cast<uint32_t>(rows * HD * 2));
-  bulk_g2s(ring + slot * Cf::RB * HD, (g < n ? K : V) + static_cast<int64_t>(blk) * Cf::RB * HD,
-           static_cast<uint32_t>(rows * HD * 2), &bars[slot]);
-}
-
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -206,11 +190,12 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
   using Cf = DecCfg<HD, NS_>;
   constexpr int RB = Cf::RB, NS = Cf::NS, LPR = Cf::LPR, RPW = Cf::RPW, NW = kDecThreads / 32;
   extern __shared__ __align__(128) uint8_t dsm[];
-  uint16_t* ring = reinterpret_cast<uint16_t*>(dsm);  // 2 NS slots of RB rows
-  float* sc = reinterpret_cast<float*>(ring + 2 * NS * RB * HD);
+  uint16_t* Ks = reinterpret_cast<uint16_t*>(dsm);
+  uint16_t* Vs = Ks + NS * RB * HD;
+  float* sc = reinterpret_cast<float*>(Vs + NS * RB * HD);
   float* q = sc + (Smax + 3) / 4 * 4;
   __shared__ float red[NW];
-  __shared__ uint64_t bar[2 * NS];
+  __shared__ uint64_t kbar[NS], vbar[NS];
   // Programmatic dependent launch: only the new row `pos` (K/V written by the QKV GEMM's
   // epilogue) and q depend on the predecessor.  The position counter and the cached rows
   // [0, pos) were final before the predecessor started (every earlier kernel of the step
@@ -224,20 +209,25 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
   const int nblk = (ctx + RB - 1) / RB;
   const uint16_t* K = kc + static_cast<int64_t>(bh) * Smax * HD;
   const uint16_t* V = vc + static_cast<int64_t>(bh) * Smax * HD;
-  const int ncached = pos / RB;  // leading blocks made only of cached rows
-  const int nfirst = min(2 * NS, 2 * nblk);
-  auto cached = [&](int g) { return (g < nblk ? g : g - nblk) < ncached; };
+  const int npre = min(NS, pos / RB);  // leading blocks made only of cached rows
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < 2 * NS; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kbar[i], 1);
+      mbar_init(&vbar[i], 1);
+    }
     mbar_fence_init();
-    for (int g = 0; g < nfirst; ++g)
-      if (cached(g)) dec_issue_kv<HD, NS>(ring, K, V, g, nblk, ctx, bar);
+    for (int i = 0; i < npre; ++i) {
+      dec_issue<HD, NS>(Ks, K, i, ctx, kbar);
+      dec_issue<HD, NS>(Vs, V, i, ctx, vbar);
+    }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) {
-    for (int g = 0; g < nfirst; ++g)
-      if (!cached(g)) dec_issue_kv<HD, NS>(ring, K, V, g, nblk, ctx, bar);
+    for (int i = npre; i < NS; ++i) {
+      dec_issue<HD, NS>(Ks, K, i, ctx, kbar);
+      dec_issue<HD, NS>(Vs, V, i, ctx, vbar);
+    }
   }
   const float scale = rsqrtf(static_cast<float>(HD));
   const uint16_t* qsrc = qkv + static_cast<int64_t>(b) * 3 * d + h * HD;
@@ -248,22 +238,12 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
   float qr[8];
 #pragma unroll
   for (int t = 0; t < 8; ++t) qr[t] = q[sub * 8 + t];
-  // consumed block g: once every warp is done with its slot, request block g + 2 NS
-  auto release = [&](int g) {
-    if (g + 2 * NS < 2 * nblk) {
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        fence_proxy_async_smem();
-        dec_issue_kv<HD, NS>(ring, K, V, g + 2 * NS, nblk, ctx, bar);
-      }
-    }
-  };
   float mx = -FLT_MAX;
   for (int blk = 0; blk < nblk; ++blk) {
-    const int slot = blk % (2 * NS);
-    mbar_wait(&bar[slot], (blk / (2 * NS)) & 1);
+    const int slot = blk % NS;
+    mbar_wait(&kbar[slot], (blk / NS) & 1);
     const int rows = min(RB, ctx - blk * RB);
-    const uint16_t* Kb = ring + slot * RB * HD;
+    const uint16_t* Kb = Ks + slot * RB * HD;
     for (int r0 = warp * RPW; r0 < rows; r0 += NW * RPW) {  // warp-uniform trip count
       const int r = r0 + rsub;
       float s = 0.f;
@@ -284,7 +264,13 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
         mx = fmaxf(mx, s);
       }
     }
-    release(blk);
+    if (blk + NS < nblk) {
+      __syncthreads();  // every warp is done with this slot
+      if (threadIdx.x == 0) {
+        fence_proxy_async_smem();
+        dec_issue<HD, NS>(Ks, K, blk + NS, ctx, kbar);
+      }
+    }
   }
   mx = wmax(mx);
   if (lane == 0) red[warp] = mx;
@@ -312,10 +298,10 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
   const int cc = threadIdx.x % CH, grp = threadIdx.x / CH;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (int blk = 0; blk < nblk; ++blk) {
-    const int g = nblk + blk, slot = g % (2 * NS);
-    mbar_wait(&bar[slot], (g / (2 * NS)) & 1);
+    const int slot = blk % NS;
+    mbar_wait(&vbar[slot], (blk / NS) & 1);
     const int rows = min(RB, ctx - blk * RB);
-    const uint16_t* Vb = ring + slot * RB * HD;
+    const uint16_t* Vb = Vs + slot * RB * HD;
 #pragma unroll
     for (int r = grp; r < RB; r += G) {
       if (r >= rows) break;
@@ -328,9 +314,15 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(const uint16_t
         acc[2 * t + 1] += pj * bf2f_a(static_cast<uint16_t>(w[t] >> 16));
       }
     }
-    release(g);
+    if (blk + NS < nblk) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_proxy_async_smem();
+        dec_issue<HD, NS>(Vs, V, blk + NS, ctx, vbar);
+      }
+    }
   }
-  float* part = reinterpret_cast<float*>(ring);  // [G][HD] partials (every ring slot consumed)
+  float* part = reinterpret_cast<float*>(Ks);  // [G][HD] partials (key ring no longer needed)
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < 8; ++t) part[grp * HD + cc * 8 + t] = acc[t];
