@@ -388,15 +388,32 @@ static void launch_norm_bwd_pair(const float* dy, const float* x, const float* m
   norm_bwd_pair_kernel<VPLH, RMS><<<(M + rpb - 1) / rpb, 256, sm, s>>>(dy, x, mean, rstd, g, dx, ws, M, d, rpb);
 }
 
+// out[j] += sum_k ws[k][j], fixed order: a block holds 32 columns x 8 row slices; slice t
+// sums rows t, t+8, ... (loads of 8 slices in flight instead of one serial chain per
+// column), then slice 0 adds the 8 slice sums in slice order.
 __global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblk, int ncol, int64_t blk_stride,
                                        float* __restrict__ out0, float* __restrict__ out1, int split) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= ncol) return;
+  __shared__ float red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + tx;
   float s = 0.f;
-#pragma unroll 8
-  for (int k = 0; k < nblk; ++k) s += ws[k * blk_stride + j];  // fixed order; loads run ahead
-  if (j < split) out0[j] += s;
-  else out1[j - split] += s;
+  if (j < ncol) {
+#pragma unroll 4
+    for (int k = ty; k < nblk; k += 8) s += ws[k * blk_stride + j];
+  }
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && j < ncol) {
+    float t = red[0][tx];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += red[q][tx];
+    if (j < split) out0[j] += t;
+    else out1[j - split] += t;
+  }
+}
+static void reduce_partials(const float* ws, int nblk, int ncol, int64_t blk_stride, float* out0, float* out1, int split,
+                            cudaStream_t s) {
+  reduce_partials_kernel<<<(ncol + 31) / 32, 256, 0, s>>>(ws, nblk, ncol, blk_stride, out0, out1, split);
 }
 
 __global__ void round_bf16_kernel(const float* __restrict__ x, uint16_t* __restrict__ y, int64_t n) {
@@ -564,7 +581,7 @@ extern "C" int rlhf_rmsnorm_bwd(const float* dy, const float* x, const float* rs
     const int rpb = pair_rows_per_block(M, d, 1, ws_floats);
     if (d <= 2048) launch_norm_bwd_pair<8, true>(dy, x, nm, rstd, gp, dx, ws, M, d, rpb, S(s));
     else launch_norm_bwd_pair<16, true>(dy, x, nm, rstd, gp, dx, ws, M, d, rpb, S(s));
-    reduce_partials_kernel<<<(d + 63) / 64, 64, 0, S(s)>>>(ws, (M + rpb - 1) / rpb, d, d, dg, dg, d);
+    reduce_partials(ws, (M + rpb - 1) / rpb, d, d, dg, dg, d, S(s));
     return cuda_status();
   } else if (d <= 2048) {
     cudaFuncSetAttribute(layernorm_bwd_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2048 * 4);
@@ -572,7 +589,7 @@ extern "C" int rlhf_rmsnorm_bwd(const float* dy, const float* x, const float* rs
   } else {
     return 2;
   }
-  reduce_partials_kernel<<<(d + 63) / 64, 64, 0, S(s)>>>(ws, nblk, d, d, dg, dg, d);
+  reduce_partials(ws, nblk, d, d, dg, dg, d, S(s));
   return cuda_status();
 }
 
@@ -589,7 +606,7 @@ extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* 
   } else if (d <= 2048 && d % 8 == 0) {
     const int rpb = pair_rows_per_block(M, d, 2, ws_floats);
     launch_norm_bwd_pair<8, false>(dy, x, mean, rstd, gp, dx, ws, M, d, rpb, S(s));
-    reduce_partials_kernel<<<(2 * d + 63) / 64, 64, 0, S(s)>>>(ws, (M + rpb - 1) / rpb, 2 * d, 2 * d, dg, db, d);
+    reduce_partials(ws, (M + rpb - 1) / rpb, 2 * d, 2 * d, dg, db, d, S(s));
     return cuda_status();
   } else if (d <= 2048) {
     cudaFuncSetAttribute(layernorm_bwd_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4);
@@ -597,7 +614,7 @@ extern "C" int rlhf_layernorm_bwd(const float* dy, const float* x, const float* 
   } else {
     return 2;
   }
-  reduce_partials_kernel<<<(2 * d + 63) / 64, 64, 0, S(s)>>>(ws, nblk, 2 * d, 2 * d, dg, db, d);
+  reduce_partials(ws, nblk, 2 * d, 2 * d, dg, db, d, S(s));
   return cuda_status();
 }
 
@@ -631,7 +648,7 @@ extern "C" int rlhf_colsum_bf16(const void* G, int M, int N, float* db, float* w
   if (N % 8) return 2;
   dim3 grid((N + 255) / 256, kColsumChunks);
   colsum_bf16_kernel<<<grid, 256, 0, S(s)>>>(static_cast<const uint16_t*>(G), M, N, ws);
-  reduce_partials_kernel<<<(N + 255) / 256, 256, 0, S(s)>>>(ws, kColsumChunks, N, N, db, db, N);
+  reduce_partials(ws, kColsumChunks, N, N, db, db, N, S(s));
   return cuda_status();
 }
 
