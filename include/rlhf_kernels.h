@@ -204,6 +204,13 @@ int rlhf_scatter_rows_f32(const float* src, float* dst, int B, int S, int R, int
  * up to the end of each 128-row block).  q / k / v come from packed qkv rows [B*S, 3*H*hd].
  * Replaces QK^T GEMM + rlhf_attn_softmax (+ the P.V GEMM when O != NULL). */
 int rlhf_attn_fwd_fused(const void* qkv, int B, int H, int hd, int S, float alpha, void* P, void* O, rlhf_stream_t s);
+/* Attention backward, score-gradient part (S % 128 == 0, S <= 512, hd 64), one tcgen05 kernel:
+ * dP = dO V^T in TMEM, D_i = sum_j P_ij dP_ij, dS = bf16(P (dP - D) * scale) with zeros above the
+ * diagonal, written for key columns < (query block + 1) * 128 (what the dQ / dK GEMMs read).
+ * dO [B, S, H*hd] bf16, qkv packed [B, S, 3*H*hd] (V at offset 2*H*hd), P / dS [B*H, S, S] bf16.
+ * Replaces the dO V^T GEMM (fp32 dP) + rlhf_attn_softmax_bwd pair. */
+int rlhf_attn_bwd_ds_fused(const void* dO, const void* qkv, const void* P, void* dS, int B, int H, int hd, int S,
+                           float scale, rlhf_stream_t s);
 
 /* ---- attention (Generation prefill, Forward, TrainFB) ---------------------
  * Row-wise causal softmax of scores [Z, S, S] (f32) -> probs bf16 (zeros above

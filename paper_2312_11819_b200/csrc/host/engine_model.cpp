@@ -434,15 +434,21 @@ void Engine::attention_bwd(const uint16_t* qkv, const uint16_t* P, const uint16_
   const int d = H * hd;
   const int64_t TT = static_cast<int64_t>(T) * T;
   const int64_t qb = static_cast<int64_t>(T) * 3 * d, ob = static_cast<int64_t>(T) * d;
-  // dP = dO V^T (fp32, causal tiles)
-  rlhf_gemm_params dp{};
-  dp.M = T; dp.N = T; dp.K = hd; dp.batch = B * H; dp.batch_h = H;
-  dp.A = dov; dp.lda = d; dp.a_stride_h = hd; dp.a_stride_b = ob;
-  dp.B = qkv + 2 * d; dp.ldb = 3 * d; dp.b_stride_h = hd; dp.b_stride_b = qb;
-  dp.C = arp_->scores; dp.c_f32 = 1; dp.c_rs = T; dp.c_cs = 1; dp.c_stride_h = TT; dp.c_stride_b = H * TT;
-  dp.alpha = 1.0f; dp.causal = 1;
-  gemm(dp);
-  K(rlhf_attn_softmax_bwd(P, arp_->scores, arp_->dS, B * H, T, 1.0f / std::sqrt(static_cast<float>(hd)), stream_), 1);
+  static const bool unfused = getenv("RLHF_ATTN_BWD_UNFUSED") != nullptr;  // A/B switch for timing
+  if (!unfused && !getenv("RLHF_ATTN_UNFUSED") && hd == 64 && T % 128 == 0 && T <= 512) {
+    // dP = dO V^T, D and dS in one kernel: fp32 dP never leaves TMEM
+    K(rlhf_attn_bwd_ds_fused(dov, qkv, P, arp_->dS, B, H, hd, T, 1.0f / std::sqrt(static_cast<float>(hd)), stream_), 1);
+  } else {
+    // dP = dO V^T (fp32, causal tiles)
+    rlhf_gemm_params dp{};
+    dp.M = T; dp.N = T; dp.K = hd; dp.batch = B * H; dp.batch_h = H;
+    dp.A = dov; dp.lda = d; dp.a_stride_h = hd; dp.a_stride_b = ob;
+    dp.B = qkv + 2 * d; dp.ldb = 3 * d; dp.b_stride_h = hd; dp.b_stride_b = qb;
+    dp.C = arp_->scores; dp.c_f32 = 1; dp.c_rs = T; dp.c_cs = 1; dp.c_stride_h = TT; dp.c_stride_b = H * TT;
+    dp.alpha = 1.0f; dp.causal = 1;
+    gemm(dp);
+    K(rlhf_attn_softmax_bwd(P, arp_->scores, arp_->dS, B * H, T, 1.0f / std::sqrt(static_cast<float>(hd)), stream_), 1);
+  }
   // dQ = dS K
   rlhf_gemm_params dq{};
   dq.M = T; dq.N = hd; dq.K = T; dq.batch = B * H; dq.batch_h = H;

@@ -284,6 +284,162 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Attention backward, score-gradient part, in one tcgen05 kernel (S <= 512, hd 64):
+//   dP = dO V^T (fp32, TMEM, causal key tiles), D_i = sum_j P_ij dP_ij,
+//   dS_ij = bf16(P_ij (dP_ij - D_i) scale)  (0 above the diagonal)
+// replacing the dO V^T GEMM (which wrote fp32 dP, 4 B per score) and the separate softmax
+// backward (which read it back): per score only P is read (2 B, twice, the second time
+// mostly from L2) and dS written (2 B).  CTA = (sample, head, 128 query rows); dO (128 x 64)
+// and V (up to 512 x 64) arrive by TMA; the eight epilogue warps (thread = query row, two
+// warps per TMEM lane quarter splitting the 32-column chunks) run D in pass 1 and dS in pass
+// 2.  dS is written for key columns < m0 + 128 (every column the dQ / dK GEMMs read).
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_ds_kernel(const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmV, int H, int S,
+                       float scale, const uint16_t* __restrict__ P, uint16_t* __restrict__ dS) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* so = smem;
+  uint8_t* sv = smem + Q_BYTES;
+  float* rowst = reinterpret_cast<float*>(sv + (kMaxS / BMq) * KT_BYTES);  // [2 halves][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowst + 2 * BMq);
+  uint64_t* done = full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int mb = blockIdx.x, z = blockIdx.y, b = z / H, h = z % H;
+  const int m0 = mb * BMq, nkt = mb + 1;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    mbar_init(full, 1);
+    mbar_init(done, 1);
+    mbar_fence_init();
+    tma_prefetch(&tmO);
+    tma_prefetch(&tmV);
+  }
+  int tcols = 128;
+  while (tcols < nkt * BMq) tcols *= 2;
+  if (warp == 1) tmem_alloc(tmem_slot, tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(full, Q_BYTES + nkt * KT_BYTES);
+      tma_load_4d(so, &tmO, full, 0, h, m0, b);
+      for (int t = 0; t < nkt; ++t) tma_load_4d(sv + t * KT_BYTES, &tmV, full, 0, h, t * BMq, b);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(BMq, BMq, 0, 0);
+      mbar_wait(full, 0);
+      tc_fence_after();
+      const uint32_t a = smem_u32(so);
+      for (int t = 0; t < nkt; ++t) {
+        const uint32_t bv = smem_u32(sv + t * KT_BYTES);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16(tmem + t * BMq, umma_desc_sw128(a + k * 32, 16, 1024), umma_desc_sw128(bv + k * 32, 16, 1024), idesc,
+                    k > 0 ? 1u : 0u);
+      }
+      umma_commit(done);
+    }
+    __syncwarp();
+  } else {
+    const int q = static_cast<int>(warp & 3u), half = static_cast<int>(warp - 2) >> 2;
+    const int il = q * 32 + static_cast<int>(lane);
+    const int i = m0 + il;
+    const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const int nch = (m0 + q * 32 + 32) / 32;  // chunks holding any j <= (this warp's last row)
+    const uint16_t* prow = P + (static_cast<int64_t>(z) * S + i) * S;
+    uint16_t* drow = dS + (static_cast<int64_t>(z) * S + i) * S;
+    auto pload = [&](int c, uint32_t (&pw)[16]) {
+      const uint4* src = reinterpret_cast<const uint4*>(prow + c * 32);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint4 x = src[u];
+        pw[4 * u] = x.x; pw[4 * u + 1] = x.y; pw[4 * u + 2] = x.z; pw[4 * u + 3] = x.w;
+      }
+    };
+    auto plo = [](uint32_t w) { return __uint_as_float(w << 16); };
+    auto phi = [](uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); };
+    mbar_wait(done, 0);
+    tc_fence_after();
+    // pass 1: D over this warp's chunks (P is 0 above the diagonal; the diagonal chunk is
+    // masked anyway so stale dP never enters)
+    float D = 0.f;
+    auto absorb = [&](const uint32_t (&r)[32], const uint32_t (&pw)[16], int c) {
+      if (c != nch - 1) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          D = fmaf(plo(pw[u]), __uint_as_float(r[2 * u]), D);
+          D = fmaf(phi(pw[u]), __uint_as_float(r[2 * u + 1]), D);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int j = c * 32 + 2 * u;
+          if (j <= i) D = fmaf(plo(pw[u]), __uint_as_float(r[2 * u]), D);
+          if (j + 1 <= i) D = fmaf(phi(pw[u]), __uint_as_float(r[2 * u + 1]), D);
+        }
+      }
+    };
+    for (int c = half; c < nch; c += 4) {
+      uint32_t ra[32], rb[32], pa[16], pb[16];
+      tmem_ld32_nowait(tq + c * 32, ra);
+      const bool two = c + 2 < nch;
+      if (two) tmem_ld32_nowait(tq + (c + 2) * 32, rb);
+      pload(c, pa);
+      if (two) pload(c + 2, pb);
+      tmem_ld_wait32x2(ra, rb);
+      absorb(ra, pa, c);
+      if (two) absorb(rb, pb, c + 2);
+    }
+    rowst[half * BMq + il] = D;
+    named_bar_sync(1, 32 * kEpi);
+    D = rowst[il] + rowst[BMq + il];
+    // pass 2: dS for every chunk left of the diagonal tile's end (zeros past the diagonal)
+    for (int t = 0; t < nkt; ++t) {
+      uint32_t ra[32], rb[32], pa[16], pb[16];
+      const int c0 = t * 4 + half;
+      if (c0 < nch) {
+        tmem_ld32_nowait(tq + c0 * 32, ra);
+        if (c0 + 2 < nch) tmem_ld32_nowait(tq + (c0 + 2) * 32, rb);
+        pload(c0, pa);
+        if (c0 + 2 < nch) pload(c0 + 2, pb);
+        tmem_ld_wait32x2(ra, rb);
+      }
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const int c = c0 + 2 * k2;
+        uint32_t o[16];
+        if (c < nch) {
+          const uint32_t(&r)[32] = k2 == 0 ? ra : rb;
+          const uint32_t(&pw)[16] = k2 == 0 ? pa : pb;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int j = c * 32 + 2 * u;
+            const float g0 = plo(pw[u]) * (__uint_as_float(r[2 * u]) - D) * scale;
+            const float g1 = phi(pw[u]) * (__uint_as_float(r[2 * u + 1]) - D) * scale;
+            o[u] = pack_bf16(j <= i ? g0 : 0.f, j + 1 <= i ? g1 : 0.f);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) o[u] = 0u;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(drow + c * 32);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dst[u] = make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tcols);
+  }
+}
+constexpr int BWD_SMEM = Q_BYTES + (kMaxS / BMq) * KT_BYTES + 2 * BMq * 4 + 64 + 1024;
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -337,5 +493,25 @@ extern "C" int rlhf_attn_fwd_fused(const void* qkv, int B, int H, int hd, int S,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   af::attn_fwd_kernel<<<dim3(S / af::BMq, B * H), af::kThreads, af::smem_bytes(P != nullptr, O != nullptr), s>>>(
       tq, tk, tv, H, S, alpha, static_cast<uint16_t*>(P), static_cast<uint16_t*>(O), static_cast<int64_t>(d));
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+extern "C" int rlhf_attn_bwd_ds_fused(const void* dO, const void* qkv, const void* P, void* dS, int B, int H, int hd,
+                                      int S, float scale, rlhf_stream_t stream) {
+  if (hd != af::HD || S % af::BMq || S > af::kMaxS || B < 1 || H < 1 || !P || !dS) return 2;
+  const int d = H * hd;
+  CUtensorMap to, tv;
+  if (af::qkv_map(&to, dO, H, S, B, d) || af::qkv_map(&tv, static_cast<const uint16_t*>(qkv) + 2 * d, H, S, B, 3 * d))
+    return 2;
+  static bool init = false;
+  if (!init) {
+    if (cudaFuncSetAttribute(af::attn_bwd_ds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, af::BWD_SMEM) !=
+        cudaSuccess)
+      return 5;
+    init = true;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  af::attn_bwd_ds_kernel<<<dim3(S / af::BMq, B * H), af::kThreads, af::BWD_SMEM, s>>>(
+      to, tv, H, S, scale, static_cast<const uint16_t*>(P), static_cast<uint16_t*>(dS));
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }

@@ -177,6 +177,22 @@ def attn_decode(qkv: torch.Tensor, kcache: torch.Tensor, vcache: torch.Tensor, p
     return out
 
 
+def attn_bwd_ds_fused(dO: torch.Tensor, qkv: torch.Tensor, P: torch.Tensor, B: int, H: int, S: int,
+                      scale: float) -> torch.Tensor:
+    """Score gradient of causal attention (rlhf_attn_bwd_ds_fused): dS = bf16(P (dO V^T - D) scale),
+    D = rowsum(P * dO V^T); dS bf16 [B, H, S, S], columns past the query block's diagonal tile
+    left 0 (the buffer is zero-initialised here)."""
+    L = lib()
+    L.rlhf_attn_bwd_ds_fused.argtypes = [C.c_void_p] * 4 + [C.c_int] * 4 + [C.c_float, C.c_void_p]
+    hd = qkv.shape[1] // (3 * H)
+    dS = torch.zeros(B, H, S, S, device=qkv.device, dtype=torch.bfloat16)
+    rc = L.rlhf_attn_bwd_ds_fused(dO.data_ptr(), qkv.data_ptr(), P.data_ptr(), dS.data_ptr(), B, H, hd, S, scale,
+                                  _stream())
+    if rc:
+        raise RuntimeError(f"rlhf_attn_bwd_ds_fused failed ({rc})")
+    return dS
+
+
 def attn_fwd_fused(qkv: torch.Tensor, B: int, H: int, S: int, alpha: float, want_p: bool = True, want_o: bool = True):
     """Fused causal attention forward (rlhf_attn_fwd_fused) from packed qkv rows:
     returns (P bf16 [B, H, S, S] or None, O bf16 [B*S, H*hd] or None)."""

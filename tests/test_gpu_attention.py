@@ -79,3 +79,43 @@ def test_attn_fwd_fused_matches_torch(B, H, S):
     _, O2 = ops.attn_fwd_fused(qkv, B, H, S, 0.125, want_p=False)
     torch.cuda.synchronize()
     assert torch.equal(P2, P) and torch.equal(O2, O)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,H,S", [(2, 3, 128), (2, 4, 256), (1, 2, 384), (3, 2, 512)])
+def test_attn_bwd_ds_fused_matches_torch(B, H, S):
+    """Fused score gradient (dO V^T in TMEM, D = rowsum(P dP), dS = bf16(P (dP - D) scale)) against
+    fp32 torch on the kernel's own bf16 P, and against the unfused GEMM + softmax-backward pair."""
+    import ctypes as C
+    import torch
+    from paper_2312_11819_b200 import ops
+    from paper_2312_11819_b200.capi import lib
+    torch.manual_seed(B * S + H)
+    hd, d, scale = 64, H * 64, 0.125
+    qkv = (torch.randn(B * S, 3 * d, device="cuda") * 1.5).bfloat16()
+    dO = torch.randn(B * S, d, device="cuda").bfloat16()
+    P, _ = ops.attn_fwd_fused(qkv, B, H, S, scale)
+    dS = ops.attn_bwd_ds_fused(dO, qkv, P, B, H, S, scale)
+    v = qkv[:, 2 * d:].float().view(B, S, H, hd).transpose(1, 2)
+    g = dO.float().view(B, S, H, hd).transpose(1, 2)
+    dP = g @ v.transpose(-1, -2)
+    Pf = P.float()
+    D = (Pf * dP).sum(-1, keepdim=True)
+    ref = Pf * (dP - D) * scale
+    mask = torch.ones(S, S, device="cuda", dtype=torch.bool).tril()
+    torch.cuda.synchronize()
+    got = dS.float()
+    assert (got[..., ~mask] == 0).all()
+    err = (got - ref).abs().max().item()
+    assert err <= 1e-2 * ref.abs().max().item() + 1e-4, err
+    # the unfused pair: fp32 dP from the batched GEMM path, then rlhf_attn_softmax_bwd
+    L = lib()
+    L.rlhf_attn_softmax_bwd.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_void_p]
+    dPc = dP.contiguous()
+    dS2 = torch.zeros_like(dS)
+    assert L.rlhf_attn_softmax_bwd(P.data_ptr(), dPc.data_ptr(), dS2.data_ptr(), B * H, S, scale, ops._stream()) == 0
+    torch.cuda.synchronize()
+    # same inputs up to the fp32 summation order of dP and D: bf16 results within one rounding step
+    diff = (got - dS2.float()).abs()
+    assert diff.max().item() <= 2e-2 * ref.abs().max().item() + 1e-4
+    assert (diff > 0).float().mean().item() < 0.05
