@@ -63,9 +63,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* svv = skv + (kMaxS / BMq) * KT_BYTES;      // V tiles (want_o)
   uint8_t* spb = svv + (want_o ? (kMaxS / BMq) * KT_BYTES : 0);  // 2 P tiles (A operand of P.V)
   float* rowst = reinterpret_cast<float*>(spb + (want_o ? 2 * PB_BYTES : 0));  // [2][2][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(rowst + 4 * BMq);
-  uint64_t* done = full + 1;   // QK^T MMAs complete
-  uint64_t* vfull = done + 1;  // V tiles landed
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowst + 4 * BMq);  // [4] Q + key tile 0, key tiles 1..3 landed
+  uint64_t* done = full + 4;   // [4] QK^T MMAs of key tile t complete
+  uint64_t* vfull = done + 4;  // V tiles landed
   uint64_t* pfull = vfull + 1;  // [2] P tile written by the epilogue warps
   uint64_t* pfree = pfull + 2;  // [2] P.V MMAs done with the P tile
   uint64_t* ofull = pfree + 2;  // O accumulated
@@ -76,8 +76,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkt = mb + 1;  // causal key tiles
   const uint32_t warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
-    mbar_init(full, 1);
-    mbar_init(done, 1);
+    for (int t = 0; t < kMaxS / BMq; ++t) {
+      mbar_init(&full[t], 1);
+      mbar_init(&done[t], 1);
+    }
     mbar_init(vfull, 1);
     for (int k = 0; k < 2; ++k) {
       mbar_init(&pfull[k], kEpi);
@@ -99,9 +101,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(full, Q_BYTES + nkt * KT_BYTES);
-      tma_load_4d(sq, &tmQ, full, 0, h, m0, b);
-      for (int t = 0; t < nkt; ++t) tma_load_4d(skv + t * KT_BYTES, &tmK, full, 0, h, t * BMq, b);
+      // per-key-tile barriers: the MMA of tile t and the softmax of its columns start as soon
+      // as that tile has landed, not after the whole key range
+      mbar_arrive_expect_tx(&full[0], Q_BYTES + KT_BYTES);
+      tma_load_4d(sq, &tmQ, &full[0], 0, h, m0, b);
+      for (int t = 0; t < nkt; ++t) {
+        if (t > 0) mbar_arrive_expect_tx(&full[t], KT_BYTES);
+        tma_load_4d(skv + t * KT_BYTES, &tmK, &full[t], 0, h, t * BMq, b);
+      }
       if (want_o) {  // V tiles into their own buffers, streaming while QK^T and the softmax run
         mbar_arrive_expect_tx(vfull, nkt * KT_BYTES);
         for (int t = 0; t < nkt; ++t) tma_load_4d(svv + t * KT_BYTES, &tmV, vfull, 0, h, t * BMq, b);
@@ -110,17 +117,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_bf16(BMq, BMq, 0, 0);
-      mbar_wait(full, 0);
-      tc_fence_after();
       const uint32_t a = smem_u32(sq);
       for (int t = 0; t < nkt; ++t) {
+        mbar_wait(&full[t], 0);
+        tc_fence_after();
         const uint32_t bk = smem_u32(skv + t * KT_BYTES);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
           umma_bf16(tmem + t * BMq, umma_desc_sw128(a + k * 32, 16, 1024), umma_desc_sw128(bk + k * 32, 16, 1024), idesc,
                     k > 0 ? 1u : 0u);
+        umma_commit(&done[t]);
       }
-      umma_commit(done);
       if (want_o) {
         // O[128 x 64] += P_t[128 x 128 keys] . V_t[128 keys x 64], key tiles in order
         const uint32_t idv = umma_idesc_bf16(BMq, HD, 0, 1);
@@ -150,8 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int i = m0 + il;
     const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const int nch = (m0 + q * 32 + 32) / 32;  // chunks holding any j <= (this warp's last row)
-    mbar_wait(done, 0);
-    tc_fence_after();
+    int tdone = -1;  // key tiles whose scores this warp has seen complete
     // Scores in log2 units (a2 = alpha * log2 e): every exponential is one FFMA + one
     // ex2.approx.ftz.  Only the chunk holding this quarter's diagonal (c == nch - 1) is
     // masked; chunks left of it are entirely causal-visible for all 32 rows of the warp.
@@ -181,6 +187,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     // two TMEM loads in flight per wait (chunks c and c + 2 of this warp's parity)
     for (int c = half; c < nch; c += 4) {
+      if (c / 4 > tdone) {  // chunks c and c + 2 lie in key tile c / 4
+        tdone = c / 4;
+        mbar_wait(&done[tdone], 0);
+        tc_fence_after();
+      }
       uint32_t ra[32], rb[32];
       tmem_ld32_nowait(tq + c * 32, ra);
       const bool two = c + 2 < nch;
