@@ -64,6 +64,9 @@ struct Args {
   float* st_out;
   const float* st_in;
   int st_parts;
+  // split-K partials staged in the (consumed) operand ring and sent to their owners with one
+  // bulk DSMEM copy per owner instead of per-thread st.async stores
+  int bulk;
 };
 __device__ __forceinline__ unsigned long long dclk() {
   unsigned long long c;
@@ -264,8 +267,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(acc_bar, 1);
     mbar_init(recv_bar, 1);
-    // every slice pushes its rows_per x BN fp32 rows of this CTA's share here
-    mbar_arrive_expect_tx(recv_bar, static_cast<uint32_t>(e.splits * rows_per * BN * 4));
+    // every slice pushes its rows_per x BN fp32 rows of this CTA's share here (bulk mode:
+    // rows_per padded rows, PITCH floats each)
+    mbar_arrive_expect_tx(recv_bar, static_cast<uint32_t>(e.splits * rows_per * (e.bulk ? C::PITCH : BN) * 4));
     mbar_fence_init();
     tma_prefetch(&tmW);
     tma_prefetch(&tmX);
@@ -350,7 +354,42 @@ __global__ void __launch_bounds__(kThreads, 1)
   mbar_wait(acc_bar, 0);
   DPROBE(4);
   tc_fence_after();
-  {
+  if (e.bulk) {
+    // thread = accumulator row -> staging row (padded pitch: conflict-free 16-byte stores),
+    // then one cp.async.bulk per owner CTA: rows [o * rows_per, +rows_per) land in slot `split`
+    // of its receive buffer and complete on its receive barrier
+    const int row = static_cast<int>(warp) * 32 + static_cast<int>(lane);
+    const uint32_t tb = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const uint32_t stg = smem_u32(smem) + static_cast<uint32_t>(row * C::PITCH * 4);
+#pragma unroll
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      if (nkb > 0) tmem_ld32(tb + c * 32, v);
+      else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + static_cast<uint32_t>((c * 32 + 4 * q) * 4)),
+                     "f"(v[4 * q]), "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                     : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < static_cast<unsigned>(e.splits)) {
+      const uint32_t o = threadIdx.x;
+      const uint32_t bytes = static_cast<uint32_t>(rows_per * C::PITCH * 4);
+      const uint32_t src = smem_u32(smem) + o * bytes;
+      const uint32_t dst = map_rank(smem_u32(part) + static_cast<uint32_t>(split) * bytes, o);
+      const uint32_t rbar = map_rank(smem_u32(recv_bar), o);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+          "r"(src), "r"(bytes), "r"(rbar)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  } else {
     const int row = static_cast<int>(warp) * 32 + static_cast<int>(lane);
     const uint32_t tb = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const int owner = row / rows_per, rl = row % rows_per;
@@ -458,6 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   DPROBE(7);
   DPROBE(8);
+  if (e.bulk && threadIdx.x < static_cast<unsigned>(e.splits))
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging rows read out before exit
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, BN);
@@ -552,6 +593,10 @@ extern "C" int rlhf_gemm_decode(const rlhf_gemm_decode_params* p, rlhf_stream_t 
   a.splits = splits;
   a.kb_per = kb_per;
   a.stages = stages;
+  static const int bulk_env = [] { const char* v = getenv("RLHF_DEC_BULK_PUSH"); return v ? atoi(v) : 1; }();
+  const int pitch = bn == 32 ? dec::Cfg<32>::PITCH : dec::Cfg<64>::PITCH;
+  const int stage_bytes = bn == 32 ? dec::Cfg<32>::STAGE_BYTES : dec::Cfg<64>::STAGE_BYTES;
+  a.bulk = bulk_env && splits > 1 && stages * stage_bytes >= dec::BM * pitch * 4;
   a.Y = p->Y;
   a.y_f32 = p->y_f32;
   a.ldy = p->ldy;
