@@ -249,7 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_bar = empty_bar + e.stages;
   uint64_t* recv_bar = acc_bar + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
-  const int rows_per = BM / e.splits;
+  const int rows_per = BM / e.splits;  // a power of two: index arithmetic by shift / mask
+  const int rp_shift = __ffs(rows_per) - 1, rp_mask = rows_per - 1;
 
   const int split = static_cast<int>(cluster_rank());
   const int tile = blockIdx.x / e.splits;
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_trigger();  // the next kernel may start its (independent) prologue
   // the bias does not depend on the predecessor: fetch it now (every unit of this thread
   // has the same row, since rows_per divides the thread count)
-  const int m_own = m0 + split * rows_per + static_cast<int>(threadIdx.x) % rows_per;
+  const int m_own = m0 + split * rows_per + (static_cast<int>(threadIdx.x) & rp_mask);
   const float bias_own = (e.bias && m_own < e.M) ? b2f(e.bias[m_own]) : 0.0f;
   // announce "receive barrier initialised" to the cluster now (non-blocking); the
   // matching wait sits right before the partial pushes, so a producer thread that
@@ -419,21 +420,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   // peers' partial rows are still in flight
   float res0[4] = {0.f, 0.f, 0.f, 0.f};
   if (e.residual && static_cast<int>(threadIdx.x) < units) {
-    const int u = threadIdx.x, m = m0 + split * rows_per + u % rows_per, c4 = (u / rows_per) * 4;
+    const int u = threadIdx.x, m = m0 + split * rows_per + (u & rp_mask), c4 = (u >> rp_shift) * 4;
     if (m < e.M) {
 #pragma unroll
       for (int t = 0; t < 4; ++t)
         if (c4 + t < e.N) res0[t] = e.residual[static_cast<int64_t>(c4 + t) * e.ldy + m];
     }
   }
+  // KV-cache destination of this thread's output row (loop-invariant: every unit of the
+  // thread has m == m_own): cache element (n, h, *pos, ee) = kv_row + n * H * Smax * hd
+  uint16_t* kv_row = nullptr;
+  if (e.kc && m_own < e.M && m_own >= e.kv_d) {
+    const int mm = m_own - e.kv_d, which = mm / e.kv_d, within = mm % e.kv_d;
+    const int h = within / e.kv_hd, ee = within % e.kv_hd;
+    kv_row = (which == 0 ? e.kc : e.vc) + (static_cast<int64_t>(h) * e.kv_Smax + *e.pos) * e.kv_hd + ee;
+  }
+  const int64_t kv_nstride = static_cast<int64_t>(e.kv_H) * e.kv_Smax * e.kv_hd;
   mbar_wait(recv_bar, 0);  // all slices' rows of this CTA's share have landed
   DPROBE(6);
 
 #pragma unroll 1
   for (int u = threadIdx.x; u < units; u += kThreads) {
-    const int rl = u % rows_per;
+    const int rl = u & rp_mask;
     const int r = split * rows_per + rl;
-    const int c4 = (u / rows_per) * 4;
+    const int c4 = (u >> rp_shift) * 4;
     const int m = m0 + r;
     const bool mok = m < e.M;
     float res[4] = {res0[0], res0[1], res0[2], res0[3]};
@@ -463,12 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         const uint16_t hb = __bfloat16_as_ushort(__float2bfloat16_rn(x));
         static_cast<uint16_t*>(e.Y)[o] = hb;
-        if (e.kc && m >= e.kv_d) {  // k / v columns of qkv -> KV cache [n][h][pos][e]
-          const int mm = m - e.kv_d, which = mm / e.kv_d, within = mm % e.kv_d;
-          const int h = within / e.kv_hd, ee = within % e.kv_hd;
-          const int64_t dst = ((static_cast<int64_t>(n) * e.kv_H + h) * e.kv_Smax + *e.pos) * e.kv_hd + ee;
-          (which == 0 ? e.kc : e.vc)[dst] = hb;
-        }
+        if (kv_row) kv_row[n * kv_nstride] = hb;  // k / v columns of qkv -> KV cache [n][h][pos][e]
       }
     }
   }
