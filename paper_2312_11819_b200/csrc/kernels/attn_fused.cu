@@ -312,15 +312,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* so = smem;
   uint8_t* sv = smem + Q_BYTES;
   float* rowst = reinterpret_cast<float*>(sv + (kMaxS / BMq) * KT_BYTES);  // [2 halves][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(rowst + 2 * BMq);
-  uint64_t* done = full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowst + 2 * BMq);  // [4] dO + V tile 0, V tiles 1..3 landed
+  uint64_t* done = full + 4;                                      // [4] dO V_t^T complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 4);
   const int mb = blockIdx.x, z = blockIdx.y, b = z / H, h = z % H;
   const int m0 = mb * BMq, nkt = mb + 1;
   const uint32_t warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
-    mbar_init(full, 1);
-    mbar_init(done, 1);
+    for (int t = 0; t < kMaxS / BMq; ++t) {
+      mbar_init(&full[t], 1);
+      mbar_init(&done[t], 1);
+    }
     mbar_fence_init();
     tma_prefetch(&tmO);
     tma_prefetch(&tmV);
@@ -334,24 +336,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(full, Q_BYTES + nkt * KT_BYTES);
-      tma_load_4d(so, &tmO, full, 0, h, m0, b);
-      for (int t = 0; t < nkt; ++t) tma_load_4d(sv + t * KT_BYTES, &tmV, full, 0, h, t * BMq, b);
+      mbar_arrive_expect_tx(&full[0], Q_BYTES + KT_BYTES);
+      tma_load_4d(so, &tmO, &full[0], 0, h, m0, b);
+      for (int t = 0; t < nkt; ++t) {
+        if (t > 0) mbar_arrive_expect_tx(&full[t], KT_BYTES);
+        tma_load_4d(sv + t * KT_BYTES, &tmV, &full[t], 0, h, t * BMq, b);
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_bf16(BMq, BMq, 0, 0);
-      mbar_wait(full, 0);
-      tc_fence_after();
       const uint32_t a = smem_u32(so);
       for (int t = 0; t < nkt; ++t) {
+        mbar_wait(&full[t], 0);
+        tc_fence_after();
         const uint32_t bv = smem_u32(sv + t * KT_BYTES);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
           umma_bf16(tmem + t * BMq, umma_desc_sw128(a + k * 32, 16, 1024), umma_desc_sw128(bv + k * 32, 16, 1024), idesc,
                     k > 0 ? 1u : 0u);
+        umma_commit(&done[t]);
       }
-      umma_commit(done);
     }
     __syncwarp();
   } else {
@@ -372,8 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     auto plo = [](uint32_t w) { return __uint_as_float(w << 16); };
     auto phi = [](uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); };
-    mbar_wait(done, 0);
-    tc_fence_after();
+    int tdone = -1;  // key tiles whose dP this warp has seen complete
     // pass 1: D over this warp's chunks (P is 0 above the diagonal; the diagonal chunk is
     // masked anyway so stale dP never enters)
     float D = 0.f;
@@ -394,6 +398,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     for (int c = half; c < nch; c += 4) {
+      if (c / 4 > tdone) {  // chunks c and c + 2 lie in key tile c / 4
+        tdone = c / 4;
+        mbar_wait(&done[tdone], 0);
+        tc_fence_after();
+      }
       uint32_t ra[32], rb[32], pa[16], pb[16];
       tmem_ld32_nowait(tq + c * 32, ra);
       const bool two = c + 2 < nch;
@@ -449,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_dealloc(tmem, tcols);
   }
 }
-constexpr int BWD_SMEM = Q_BYTES + (kMaxS / BMq) * KT_BYTES + 2 * BMq * 4 + 64 + 1024;
+constexpr int BWD_SMEM = Q_BYTES + (kMaxS / BMq) * KT_BYTES + 2 * BMq * 4 + 128 + 1024;
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
