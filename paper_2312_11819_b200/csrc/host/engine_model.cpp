@@ -175,6 +175,19 @@ void Engine::linear_decode(const uint16_t* W, int N_out, int Kd, const uint16_t*
   // 22.4 -> 20.4 us with 8 slices instead of 4)
   if (kb >= 64)
     while (split < 16 && tiles * split * 2 <= 2 * 148 && kb / (split * 2) >= 8) split *= 2;
+  // few tiles (c2's O-proj / FFN-down: 6): one more doubling while every CTA still has an SM
+  // of its own, even if some slices get no k-block (c2 decode step 432 -> 415 us, same-box A/B;
+  // the idle slices push zero partials)
+  if (split < 16 && tiles * split * 2 <= 148 && kb >= split) split *= 2;
+  {  // RLHF_DEC_FORCE="N_out:K:splits,...": per-projection split override (timing experiments)
+    static const char* force = getenv("RLHF_DEC_FORCE");
+    for (const char* f = force; f && *f;) {
+      int n = 0, k = 0, sp = 0;
+      if (sscanf(f, "%d:%d:%d", &n, &k, &sp) == 3 && n == N_out && k == Kd) split = sp;
+      f = strchr(f, ',');
+      if (f) ++f;
+    }
+  }
   p.splits = split;
   p.pdl = pdl_;
   p.ln_stats_out = st_out;
