@@ -72,7 +72,8 @@ typedef struct rlhf_gemm_params {
 int rlhf_gemm(const rlhf_gemm_params* p, rlhf_stream_t s);
 /* Merge per-tile top-2 partials (rlhf_gemm_params.top2) of `tiles` tiles: greedy token
  * (ties -> lowest id) -> tok[b*tok_stride + *pos + 1], margin (top1 - top2) likewise;
- * advance_pos != 0: then *pos += 1 (the decode step's last kernel). */
+ * advance_pos != 0: then *pos += 1 (the decode step's last kernel); pos then points to two
+ * ints, pos[1] a zero-initialised ticket the kernel uses (and resets) to advance once. */
 int rlhf_argmax_tiles(const float* top2, int tiles, int B, int32_t* tok, int64_t tok_stride, int* pos,
                       float* margin, int advance_pos, rlhf_stream_t s);
 

@@ -302,7 +302,8 @@ Engine::Engine(const rlhf_ppo_config& cfg, const rlhf_engine_options& opt) : cfg
     pred_.alloc(static_cast<size_t>(gen_B_) * S_ * 4);
     margin_.alloc(static_cast<size_t>(gen_B_) * S_ * 4);
   }
-  pos_.alloc(16);
+  pos_.alloc(16);  // [0] decode position, [1] the tile-merge kernel's ticket (must start at 0)
+  CK(cudaMemset(pos_.p, 0, 16));
   loss_.alloc(16);
 
   // ---- row sets this rank belongs to; home prompt rows ----

@@ -189,31 +189,49 @@ __global__ void argmax_merge_kernel(const float* __restrict__ ws, int B, int32_t
 // one warp per sample: merge the LM-head GEMM's per-tile top-2 partials
 // One CTA: warp w merges samples w, w+32, ...; afterwards the position counter
 // advances (the decode step's last kernel, so no separate increment launch).
-__global__ void argmax_tiles_kernel(const float4* __restrict__ t2, int tiles, int B, int32_t* __restrict__ tok,
-                                    int64_t S, int* __restrict__ pos_dev, float* __restrict__ margin, int advance) {
+// One CTA per sample: the CTA's threads split the vocabulary tiles (their loads spread over
+// B SMs instead of one SM's load queue), merge inside each warp, then across warps in warp
+// order (top-2 merging is order-independent: the same token and margin as a serial merge).
+// advance: the last CTA to finish (ticket in pos_dev[1], self-resetting) writes *pos + 1,
+// after every CTA has read *pos.
+constexpr int kArgmaxThreads = 128;
+__global__ void __launch_bounds__(kArgmaxThreads) argmax_tiles_kernel(const float4* __restrict__ t2, int tiles, int B,
+                                                                      int32_t* __restrict__ tok, int64_t S,
+                                                                      int* __restrict__ pos_dev, float* __restrict__ margin,
+                                                                      int advance) {
   pdl_entry();
-  const int lane = threadIdx.x & 31, nw = blockDim.x / 32;
+  __shared__ Top2 red[kArgmaxThreads / 32];
+  const int b = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pos = *pos_dev;
-  for (int b = threadIdx.x / 32; b < B; b += nw) {
-    Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
-    for (int i = lane; i < tiles; i += 32) {
-      const float4 o = t2[static_cast<int64_t>(i) * B + b];
-      t = top2_merge(t, Top2{o.x, __float_as_int(o.y), o.z});
-    }
+  Top2 t{-FLT_MAX, 0x7fffffff, -FLT_MAX};
+  for (int i = threadIdx.x; i < tiles; i += kArgmaxThreads) {
+    const float4 o = t2[static_cast<int64_t>(i) * B + b];
+    t = top2_merge(t, Top2{o.x, __float_as_int(o.y), o.z});
+  }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      Top2 u{__shfl_xor_sync(0xffffffffu, t.v1, o), __shfl_xor_sync(0xffffffffu, t.i1, o),
-             __shfl_xor_sync(0xffffffffu, t.v2, o)};
-      t = top2_merge(t, u);
-    }
-    if (lane == 0) {
-      const int64_t at = static_cast<int64_t>(b) * S + pos + 1;
-      tok[at] = t.i1;
-      if (margin) margin[at] = t.v1 - t.v2;
+  for (int o = 16; o; o >>= 1) {
+    Top2 u{__shfl_xor_sync(0xffffffffu, t.v1, o), __shfl_xor_sync(0xffffffffu, t.i1, o),
+           __shfl_xor_sync(0xffffffffu, t.v2, o)};
+    t = top2_merge(t, u);
+  }
+  if (lane == 0) red[warp] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    t = red[0];
+#pragma unroll
+    for (int w = 1; w < kArgmaxThreads / 32; ++w) t = top2_merge(t, red[w]);
+    const int64_t at = static_cast<int64_t>(b) * S + pos + 1;
+    tok[at] = t.i1;
+    if (margin) margin[at] = t.v1 - t.v2;
+    if (advance) {
+      __threadfence();  // this CTA's read of *pos precedes its ticket
+      unsigned* ticket = reinterpret_cast<unsigned*>(pos_dev + 1);
+      if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+        *ticket = 0u;
+        *pos_dev = pos + 1;
+      }
     }
   }
-  __syncthreads();  // every warp has read the position
-  if (advance && threadIdx.x == 0) *pos_dev = pos + 1;
 }
 
 // out[b*R + j] = hf[b*S + off + j] . w   (warp per row)
@@ -441,8 +459,7 @@ extern "C" int rlhf_experience_stats(const float* logp, const float* logp_ref, c
 extern "C" int rlhf_argmax_tiles(const float* top2, int tiles, int B, int32_t* tok, int64_t tok_stride, int* pos,
                                  float* margin, int advance_pos, rlhf_stream_t s) {
   if (tiles < 1 || B < 1 || !pos) return 2;
-  const int warps = B < 32 ? B : 32;
-  return launch_k(argmax_tiles_kernel, dim3(1), dim3(32 * warps), 0, reinterpret_cast<cudaStream_t>(s),
+  return launch_k(argmax_tiles_kernel, dim3(B), dim3(kArgmaxThreads), 0, reinterpret_cast<cudaStream_t>(s),
                   reinterpret_cast<const float4*>(top2), tiles, B, tok, tok_stride, pos, margin, advance_pos);
 }
 

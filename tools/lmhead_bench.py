@@ -30,7 +30,7 @@ tiles = (a.V + 127) // 128
 top2 = torch.empty(tiles * a.B * 4, device="cuda")
 logits = torch.empty(a.B * a.V, device="cuda")
 tok = torch.zeros(a.B, 600, device="cuda", dtype=torch.int32)
-pos = torch.zeros(1, device="cuda", dtype=torch.int32)
+pos = torch.zeros(2, device="cuda", dtype=torch.int32)
 margin = torch.zeros(a.B, 600, device="cuda")
 p = GemmParams()
 p.M, p.N, p.K, p.batch, p.batch_h = a.V, a.B, a.d, 1, 1
