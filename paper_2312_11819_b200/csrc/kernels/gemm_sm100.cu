@@ -37,15 +37,17 @@ constexpr int kThreads = 64 + 32 * 4 * 1;  // warp 0 TMA, warp 1 MMA, 4 epilogue
 constexpr int kEpiWarps = 4;
 constexpr int kStagePitch = 33;  // fp32 epilogue staging pitch (conflict-free transpose)
 
-template <int BN>
+template <int BN, int DEEP = 0>
 struct TileCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES = kEpiWarps * 32 * kStagePitch * 4;  // per-epilogue-warp transpose tiles
-  // narrow tiles serve decode (few k-blocks per unit): 3 stages -> 2 CTAs/SM
-  static constexpr int RAW_STAGES = BN <= 32 ? 3 : (218 * 1024 - EPI_BYTES) / STAGE_BYTES;
-  static constexpr int STAGES = RAW_STAGES > 8 ? 8 : RAW_STAGES;
+  // narrow tiles serve decode (few k-blocks per unit): 3 stages -> 2 CTAs/SM.  DEEP (the
+  // decode LM head): one CTA per SM with the full ring, so the 393 c2 vocabulary tiles split
+  // 3/2 per SM instead of up to 4 on an SM whose two CTAs both drew a second tile
+  static constexpr int RAW_STAGES = BN <= 32 && !DEEP ? 3 : (218 * 1024 - EPI_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = RAW_STAGES > (DEEP ? 10 : 8) ? (DEEP ? 10 : 8) : RAW_STAGES;
   static constexpr int TOP2_BYTES = 4 * 32 * 16;  // per-quarter top-2 of a 32-column chunk
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + TOP2_BYTES + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * BN;
@@ -366,11 +368,11 @@ __device__ __forceinline__ void reduce_partials(const GemmArgs& e, size_t tile_i
   }
 }
 
-template <int BN, int COLMAJOR>
+template <int BN, int COLMAJOR, int DEEP = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ GemmArgs e) {
-  using Cfg = TileCfg<BN>;
+  using Cfg = TileCfg<BN, DEEP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -988,19 +990,27 @@ static int sm_count() {
   return n;
 }
 
-template <int BN, int COLMAJOR>
+template <int BN, int COLMAJOR, int DEEP = 0>
 static int launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t s) {
-  using Cfg = TileCfg<BN>;
+  using Cfg = TileCfg<BN, DEEP>;
   static int per_sm = 0;
   if (!per_sm) {
-    if (cudaFuncSetAttribute(gemm_sm100_kernel<BN, COLMAJOR>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(gemm_sm100_kernel<BN, COLMAJOR, DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
       return 5;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_sm100_kernel<BN, COLMAJOR>, kThreads, Cfg::SMEM) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_sm100_kernel<BN, COLMAJOR, DEEP>, kThreads, Cfg::SMEM) != cudaSuccess)
       per_sm = 1;
     per_sm = std::max(1, std::min(per_sm, 512 / Cfg::TMEM_COLS));
   }
-  const int grid = std::min(a.units, per_sm * sm_count());
-  return launch_k(gemm_sm100_kernel<BN, COLMAJOR>, dim3(grid), dim3(kThreads), Cfg::SMEM, s, ta, tb, a);
+  int grid = std::min(a.units, per_sm * sm_count());
+  if (DEEP) {
+    // as few CTAs as keep the same tiles-per-CTA maximum (393 c2 tiles: 131 CTAs x 3, not
+    // 97 x 3 + 51 x 2): same makespan, fewer CTAs contending for HBM at the tail
+    static int g = -1;
+    if (g < 0) g = getenv("RLHF_LMHEAD_GRID") ? atoi(getenv("RLHF_LMHEAD_GRID")) : 0;
+    const int per = (a.units + grid - 1) / grid;
+    grid = g > 0 ? std::min(a.units, g) : (a.units + per - 1) / per;
+  }
+  return launch_k(gemm_sm100_kernel<BN, COLMAJOR, DEEP>, dim3(grid), dim3(kThreads), Cfg::SMEM, s, ta, tb, a);
 }
 
 static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t s) {
@@ -1038,6 +1048,11 @@ static bool use_pair(const rlhf_gemm_params* p, int bn, int splits) {
 
 template <int BN>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t s) {
+  if constexpr (BN == 32) {
+    static int deep = -1;
+    if (deep < 0) deep = getenv("RLHF_LMHEAD_DEEP") ? atoi(getenv("RLHF_LMHEAD_DEEP")) : 1;
+    if (a.c_cs != 1 && a.top2 && deep) return launch_mode<32, 1, 1>(ta, tb, a, s);
+  }
   return a.c_cs == 1 ? launch_mode<BN, 0>(ta, tb, a, s) : launch_mode<BN, 1>(ta, tb, a, s);
 }
 

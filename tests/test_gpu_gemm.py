@@ -311,3 +311,58 @@ def test_gemm_decode_layernorm_statistics_chain(Mp, Kp, Mc, N, sp, sc):
     h = torch.nn.functional.layer_norm(x, (Mp,), g.float(), b.float(), eps=1e-5).bfloat16()
     torch.cuda.synchronize()
     close(y, h.float() @ W2.float().t(), 2e-2)  # one-pass variance: bf16 flips of h at most
+
+
+@pytest.mark.parametrize("V,N", [(50272, 32), (1000, 8), (32000, 17)])
+def test_gemm_lm_head_top2_and_tile_merge(V, N):
+    """Decode LM head: swap-AB GEMM with the per-tile top-2 epilogue (the one-CTA-per-SM ring
+    variant, gemm_sm100.cu TileCfg<32, 1>) and rlhf_argmax_tiles, vs torch fp32 logits.
+    Per (128-row tile, column): max, its row id (ties -> lowest), second max; tolerance is
+    fp32 accumulation order (1e-4 of the logit scale); ids compared where the tile's top-2 gap
+    exceeds it.  The merge must give the full-vocabulary argmax and margin."""
+    import ctypes as C
+    from paper_2312_11819_b200.capi import lib
+    from paper_2312_11819_b200.ops import GemmParams
+    L = lib()
+    L.rlhf_gemm.argtypes = [C.POINTER(GemmParams), C.c_void_p]
+    L.rlhf_argmax_tiles.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                    C.c_int, C.c_void_p]
+    d = 768
+    W = (torch.randn(V, d, device="cuda") * 0.05).bfloat16()
+    hf = torch.randn(N, d, device="cuda").bfloat16()
+    tiles = (V + 127) // 128
+    top2 = torch.full((tiles, N, 4), float("nan"), device="cuda")
+    p = GemmParams()
+    p.M, p.N, p.K, p.batch, p.batch_h = V, N, d, 1, 1
+    p.A, p.lda, p.B, p.ldb = W.data_ptr(), d, hf.data_ptr(), d
+    sink = torch.empty(N, V, device="cuda")  # the top-2 epilogue never stores logits
+    p.C, p.c_f32, p.c_rs, p.c_cs, p.alpha = sink.data_ptr(), 1, 1, V, 1.0
+    p.top2 = top2.data_ptr()
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.rlhf_gemm(C.byref(p), C.c_void_p(s)) == 0
+    logits = hf.float() @ W.float().t()  # [N, V]
+    pad = torch.full((N, tiles * 128), -float("inf"), device="cuda")
+    pad[:, :V] = logits
+    t = pad.view(N, tiles, 128)
+    v2, i2 = t.topk(2, dim=2)
+    tol = 1e-4 * logits.abs().max().item()
+    got = top2.permute(1, 0, 2)  # [N, tiles, 4]
+    assert (got[..., 0] - v2[..., 0]).abs().max().item() <= tol
+    assert (got[..., 2] - v2[..., 1]).abs().max().item() <= tol
+    ids = got[..., 1].contiguous().view(torch.int32)
+    exp_ids = i2[..., 0] + torch.arange(tiles, device="cuda").view(1, -1) * 128
+    clear = (v2[..., 0] - v2[..., 1]) > 2 * tol
+    assert torch.equal(ids[clear], exp_ids[clear].int())
+    # merge: token at tok[b*S + pos + 1], margin likewise
+    S = 8
+    tok = torch.full((N, S), -1, device="cuda", dtype=torch.int32)
+    margin = torch.zeros(N, S, device="cuda")
+    pos = torch.tensor([2, 0], device="cuda", dtype=torch.int32)
+    assert L.rlhf_argmax_tiles(top2.data_ptr(), tiles, N, tok.data_ptr(), S, pos.data_ptr(), margin.data_ptr(), 1,
+                               C.c_void_p(s)) == 0
+    torch.cuda.synchronize()
+    fv, fi = logits.topk(2, dim=1)
+    ok = (fv[:, 0] - fv[:, 1]) > 2 * tol
+    assert torch.equal(tok[:, 3][ok], fi[:, 0][ok].int())
+    assert (margin[:, 3] - (fv[:, 0] - fv[:, 1])).abs().max().item() <= 2 * tol
+    assert pos[0].item() == 3
