@@ -153,6 +153,16 @@ int rlhf_embed(const int32_t* tokens, int64_t tok_stride, int B, int T, int p0, 
  * y[b] = bf16(LN(x[b]) * ln_g + ln_b) (layer 0's LN1), one launch. */
 int rlhf_embed_ln(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev, const void* tok_emb,
                   const void* pos_emb, int d, float* x, const void* ln_g, const void* ln_b, void* y, rlhf_stream_t s);
+/* Decode step entry fused with the previous step's greedy sampler: merges the LM-head
+ * per-tile top-2 partials (as rlhf_argmax_tiles: ties -> lowest id) into dst[b*tok_stride +
+ * *pos + 1] and margin, advances *pos by one (pos points to two ints, pos[1] a zero ticket),
+ * then embeds position *pos + 1 as rlhf_embed_ln: the merged token when dst == tokens
+ * (free-running), else tokens[b*tok_stride + *pos + 1] (teacher forcing).  One launch replaces
+ * the merge + embed pair of the decode step chain (reference: the Generation term of
+ * stage_compute_time, /root/reference/proj/include/rlhfsim/costmodel.hpp:63-64). */
+int rlhf_argmax_embed_ln(const float* top2, int tiles, int32_t* dst, float* margin, const int32_t* tokens,
+                         int64_t tok_stride, int B, int* pos, const void* tok_emb, const void* pos_emb, int d,
+                         float* x, const void* ln_g, const void* ln_b, void* y, rlhf_stream_t s);
 /* tok_emb grad (+ pos grad) scatter-add of dx [B*T, d] (TrainFB). */
 int rlhf_embed_bwd(const int32_t* tokens, int64_t tok_stride, int B, int T, const float* dx, int d,
                    float* dtok_emb, float* dpos_emb, rlhf_stream_t s);
@@ -176,6 +186,10 @@ int rlhf_rmsnorm_bwd(const float* dy, const float* x, const float* rstd, const v
 /* Decode step entry of the LLaMA family: x[b] = tok_emb[tokens[b*stride + *pos]], y = RMSNorm(x). */
 int rlhf_embed_rmsnorm(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev, const void* tok_emb,
                        int d, float* x, const void* g, void* y, rlhf_stream_t s);
+/* rlhf_argmax_embed_ln for the LLaMA family (no learned positions, RMSNorm). */
+int rlhf_argmax_embed_rmsnorm(const float* top2, int tiles, int32_t* dst, float* margin, const int32_t* tokens,
+                              int64_t tok_stride, int B, int* pos, const void* tok_emb, int d, float* x, const void* g,
+                              void* y, rlhf_stream_t s);
 /* Rotary embedding in place on the q and k parts of packed qkv rows [B*T, 3*H*hd] (bf16),
  * row b*T + i at position p0 + i (p0 = *p0_dev when given); table: float2 (cos, sin)
  * [positions][hd/2] from rlhf_rope_cos_sin.  inverse: the transpose (backward of dq, dk).

@@ -186,7 +186,8 @@ class Engine {
   void lm_logprobs(const Decoder& m, const int32_t* tokens, int B, float* logp, bool keep_logits);
   void generate(const Decoder& m, int B, bool teacher_forced);
   void decode_step(const Decoder& m, int B);
-  void lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t* dst);
+  void lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t* dst, bool merge = true);
+  bool fuse_merge_ = false;  // decode: greedy merge folded into the next step's embed (generate())
   void adam(Decoder& m, float lr);
   void score_logp(const Decoder& m, const int32_t* tok, int B, float* logp);
   void score_values(const Decoder& m, const int32_t* tok, int B, float* values);

@@ -639,7 +639,13 @@ void Engine::decode_step(const Decoder& m, int B) {
     // LLaMA: RMSNorm, [QKV GEMM], rotary q/k + KV-cache store, attention, [O-proj + residual],
     // RMSNorm, [gate|up GEMM], SwiGLU, [down + residual]; final RMSNorm, untied head
     uint16_t* act = dec_act_.as<uint16_t>();
-    K(rlhf_embed_rmsnorm(tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), d, x, m.T(RLHF_T_LN1_G, 0), h, stream_), 1);
+    if (fuse_merge_)
+      K(rlhf_argmax_embed_rmsnorm(dec_top2_.as<float>(), (V + 127) / 128, graph_for_pred_ ? pred_.as<int32_t>() : gen_tok_.as<int32_t>(),
+                                  margin_.as<float>(), tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), d, x, m.T(RLHF_T_LN1_G, 0), h,
+                                  stream_),
+        1);
+    else
+      K(rlhf_embed_rmsnorm(tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), d, x, m.T(RLHF_T_LN1_G, 0), h, stream_), 1);
     for (int l = 0; l < a.n_layers; ++l) {
       if (l > 0) K(rlhf_rmsnorm(x, m.T(RLHF_T_LN1_G, l), h, nullptr, B, d, stream_), 1);
       linear_decode(m.T(RLHF_T_WQKV, l), 3 * d, d, h, B, nullptr, qkv, false, false, nullptr);
@@ -654,12 +660,21 @@ void Engine::decode_step(const Decoder& m, int B) {
       linear_decode(m.T(RLHF_T_W2, l), d, ff, act, B, nullptr, x, true, false, x);
     }
     K(rlhf_rmsnorm(x, m.T(RLHF_T_LNF_G), dec_hf_.as<uint16_t>(), nullptr, B, d, stream_), 1);
-    lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, graph_for_pred_ ? pred_.as<int32_t>() : gen_tok_.as<int32_t>());
+    lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, graph_for_pred_ ? pred_.as<int32_t>() : gen_tok_.as<int32_t>(),
+                   !fuse_merge_);
     return;
   }
-  K(rlhf_embed_ln(tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x, m.T(RLHF_T_LN1_G, 0),
-                  m.T(RLHF_T_LN1_B, 0), h, stream_),
-    1);
+  // fuse_merge_: the previous LM head's greedy merge (token, margin, *pos += 1) runs inside
+  // this entry kernel -- one launch, one PDL link fewer per step
+  if (fuse_merge_)
+    K(rlhf_argmax_embed_ln(dec_top2_.as<float>(), (V + 127) / 128, graph_for_pred_ ? pred_.as<int32_t>() : gen_tok_.as<int32_t>(),
+                           margin_.as<float>(), tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x,
+                           m.T(RLHF_T_LN1_G, 0), m.T(RLHF_T_LN1_B, 0), h, stream_),
+      1);
+  else
+    K(rlhf_embed_ln(tok, S_, B, pos, m.T(RLHF_T_TOK_EMB), m.T(RLHF_T_POS_EMB), d, x, m.T(RLHF_T_LN1_G, 0),
+                    m.T(RLHF_T_LN1_B, 0), h, stream_),
+      1);
   // per layer 7 launches: LN1 (layer 0: fused with the embedding), [QKV GEMM + KV-cache
   // store], attention, [O-proj + residual], LN2, [FFN-up + ReLU], [FFN-down + residual];
   // then final LN, [LM head + per-tile top-2], [merge -> token, *pos += 1]
@@ -704,13 +719,13 @@ void Engine::decode_step(const Decoder& m, int B) {
   }
   K(rlhf_layernorm(x, m.T(RLHF_T_LNF_G), m.T(RLHF_T_LNF_B), dec_hf_.as<uint16_t>(), nullptr, nullptr, B, d, stream_), 1);
   int32_t* dst = graph_for_pred_ ? pred_.as<int32_t>() : gen_tok_.as<int32_t>();
-  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);  // also advances *pos
+  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst, !fuse_merge_);  // the merge also advances *pos
 }
 
 // Tied LM head of the final hidden rows hf [B, d] fused with the greedy sampler: the
 // swap-AB GEMM keeps only each 128-token tile's top-2 per sample (logits never stored),
 // then one warp per sample merges the tiles -> dst[b*S + *pos + 1] and the margin.
-void Engine::lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t* dst) {
+void Engine::lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t* dst, bool merge) {
   const int d = m.a.d_model, V = m.a.vocab;
   rlhf_gemm_params q{};
   q.M = V; q.N = B; q.K = d; q.batch = 1; q.batch_h = 1;
@@ -720,9 +735,10 @@ void Engine::lm_head_argmax(const Decoder& m, const uint16_t* hf, int B, int32_t
   q.alpha = 1.0f;
   q.top2 = dec_top2_.as<float>();
   gemm(q);
-  K(rlhf_argmax_tiles(dec_top2_.as<float>(), (V + 127) / 128, B, dst, S_, pos_.as<int>(), margin_.as<float>(), 1,
-                      stream_),
-    1);
+  if (merge)
+    K(rlhf_argmax_tiles(dec_top2_.as<float>(), (V + 127) / 128, B, dst, S_, pos_.as<int>(), margin_.as<float>(), 1,
+                        stream_),
+      1);
 }
 
 // Greedy generation of R tokens for the B prompts already in gen_tok_[:, :P] (the fixed
@@ -736,7 +752,13 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   const int start = P_ - 1;
   cudaMemcpyAsync(pos_.p, &start, sizeof(int), cudaMemcpyHostToDevice, stream_);
   int32_t* dst = teacher_forced ? pred_.as<int32_t>() : gen_tok_.as<int32_t>();
-  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst);  // also advances *pos
+  // RLHF_DEC_FUSE_MERGE=0: the greedy merge as its own launch after every LM head (timing A/B)
+  static const bool fuse_env = [] { const char* e = getenv("RLHF_DEC_FUSE_MERGE"); return !e || atoi(e) != 0; }();
+  static const bool skip_env = getenv("RLHF_DECODE_SKIP") != nullptr;
+  fuse_merge_ = fuse_env && !skip_env && R_ > 1 && !(opt_.use_cuda_graph == 3 && !m.llama());
+  // with the fused merge, each decode step's entry kernel merges the previous LM head; the
+  // last step's LM head is merged after the loop
+  lm_head_argmax(m, dec_hf_.as<uint16_t>(), B, dst, !fuse_merge_);  // the merge also advances *pos
   if (ev_prefill_) cudaEventRecord(ev_prefill_, stream_);  // prefill done (per Generation task)
   if (R_ <= 1) return;
   if (opt_.use_cuda_graph == 3 && !m.llama()) {  // the persistent loop implements the OPT family
@@ -870,6 +892,12 @@ void Engine::generate(const Decoder& m, int B, bool teacher_forced) {
   } else {
     graph_for_pred_ = teacher_forced;
     for (int s = 1; s < R_; ++s) decode_step(m, B);
+  }
+  if (fuse_merge_) {
+    K(rlhf_argmax_tiles(dec_top2_.as<float>(), (V + 127) / 128, B, dst, S_, pos_.as<int>(), margin_.as<float>(), 1,
+                        stream_),
+      1);
+    fuse_merge_ = false;
   }
 }
 

@@ -2,6 +2,7 @@
 // (fwd + scatter-add bwd), LayerNorm (fwd + bwd), bf16 rounding, bias-gradient
 // column sums, response-row gather/scatter, fused AdamW.
 // All follow the rounding contract in DESIGN.md §3 (mirrored by oracle/ppo_oracle.cpp).
+#include <cfloat>
 #include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -61,17 +62,74 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tokens, int64_t tok
 // Decode step entry: x[b] = tok_emb[tokens[b*stride + *pos]] + pos_emb[*pos] (fp32, the
 // residual stream) and y[b] = bf16(LN1_layer0(x[b])), one warp per sample.  Waits on its
 // predecessor before triggering dependents (the step chain relies on it, see attention.cu).
+//
+// Fused greedy sampler (t2 != null): the previous step's LM-head per-tile top-2 partials
+// t2 [tiles][B] are merged first (the argmax_tiles_kernel reduction: max, ties -> lowest
+// id, second max -- order-independent, so the same token and margin), written to
+// dst[b*stride + *pos + 1] / margin, *pos advanced by one, and the step then embeds position
+// *pos + 1: the merged token itself (dst == tokens, free-running) or tokens[...] (teacher
+// forcing, dst = predictions).  The position is advanced BEFORE dependents are triggered
+// (per-CTA ticket right after the wait; the last CTA writes it): later kernels of the step
+// read *pos before their own griddepcontrol.wait.
+__device__ __forceinline__ void top2_fold(float& v1, int& i1, float& v2, float bv1, int bi1, float bv2) {
+  if (bv1 > v1 || (bv1 == v1 && bi1 < i1)) {
+    v2 = fmaxf(v1, bv2);
+    v1 = bv1;
+    i1 = bi1;
+  } else {
+    v2 = fmaxf(v2, bv1);
+  }
+}
+
 template <int VPL, bool RMS>
 __global__ void embed_ln_kernel(const int32_t* __restrict__ tokens, int64_t tok_stride, const int* __restrict__ pos_dev,
                                 const uint16_t* __restrict__ E, const uint16_t* __restrict__ Pm, int d,
                                 float* __restrict__ x, const uint16_t* __restrict__ g, const uint16_t* __restrict__ bta,
-                                uint16_t* __restrict__ y, int B) {
-  pdl_entry();
+                                uint16_t* __restrict__ y, int B, const float4* __restrict__ t2, int tiles,
+                                int32_t* __restrict__ dst, float* __restrict__ margin) {
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  int p = *pos_dev;
+  if (t2) {
+    __syncthreads();  // every thread of this CTA has read *pos
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned* ticket = reinterpret_cast<unsigned*>(const_cast<int*>(pos_dev) + 1);
+      if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+        *ticket = 0u;
+        *const_cast<int*>(pos_dev) = p + 1;
+        __threadfence();
+      }
+    }
+    __syncthreads();
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (row >= B) return;
-  const int p = *pos_dev;
-  const int id = tokens[static_cast<int64_t>(row) * tok_stride + p];
+  int id;
+  if (t2) {
+    float v1 = -FLT_MAX, v2 = -FLT_MAX;
+    int i1 = 0x7fffffff;
+    for (int i = lane; i < tiles; i += 32) {
+      const float4 o = t2[static_cast<int64_t>(i) * B + row];
+      top2_fold(v1, i1, v2, o.x, __float_as_int(o.y), o.z);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float bv1 = __shfl_xor_sync(0xffffffffu, v1, o), bv2 = __shfl_xor_sync(0xffffffffu, v2, o);
+      const int bi1 = __shfl_xor_sync(0xffffffffu, i1, o);
+      top2_fold(v1, i1, v2, bv1, bi1, bv2);
+    }
+    const int64_t at = static_cast<int64_t>(row) * tok_stride + p + 1;
+    if (lane == 0) {
+      dst[at] = i1;
+      if (margin) margin[at] = v1 - v2;
+    }
+    p += 1;
+    id = dst == tokens ? i1 : tokens[at];
+  } else {
+    id = tokens[static_cast<int64_t>(row) * tok_stride + p];
+  }
   const uint2* e2 = reinterpret_cast<const uint2*>(E + static_cast<int64_t>(id) * d);
   const uint2* p2 = reinterpret_cast<const uint2*>(Pm + static_cast<int64_t>(p) * d);
   const uint2* g2 = reinterpret_cast<const uint2*>(g);
@@ -678,9 +736,9 @@ extern "C" int rlhf_adamw(float* master, float* m, float* v, const float* grad, 
   return cuda_status();
 }
 
-extern "C" int rlhf_embed_ln(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev, const void* tok_emb,
-                             const void* pos_emb, int d, float* x, const void* ln_g, const void* ln_b, void* y,
-                             rlhf_stream_t s) {
+static int embed_ln_launch(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev, const void* tok_emb,
+                           const void* pos_emb, int d, float* x, const void* ln_g, const void* ln_b, void* y,
+                           rlhf_stream_t s, const float4* t2, int tiles, int32_t* dst, float* margin) {
   if (d % 4 || d > 4096 || !pos_dev) return 2;
   const dim3 grid((B + 7) / 8), blk(256);
   const auto* E = static_cast<const uint16_t*>(tok_emb);
@@ -688,20 +746,50 @@ extern "C" int rlhf_embed_ln(const int32_t* tokens, int64_t tok_stride, int B, c
   const auto* g = static_cast<const uint16_t*>(ln_g);
   const auto* b = static_cast<const uint16_t*>(ln_b);
   auto* yp = static_cast<uint16_t*>(y);
-  if (d <= 1024) return launch_k(embed_ln_kernel<8, false>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
-  if (d <= 2048) return launch_k(embed_ln_kernel<16, false>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
-  return launch_k(embed_ln_kernel<32, false>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B);
+  if (d <= 1024) return launch_k(embed_ln_kernel<8, false>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B, t2, tiles, dst, margin);
+  if (d <= 2048) return launch_k(embed_ln_kernel<16, false>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B, t2, tiles, dst, margin);
+  return launch_k(embed_ln_kernel<32, false>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, Pm, d, x, g, b, yp, B, t2, tiles, dst, margin);
 }
 
-extern "C" int rlhf_embed_rmsnorm(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev,
-                                  const void* tok_emb, int d, float* x, const void* g, void* y, rlhf_stream_t s) {
+static int embed_rmsnorm_launch(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev,
+                                const void* tok_emb, int d, float* x, const void* g, void* y, rlhf_stream_t s,
+                                const float4* t2, int tiles, int32_t* dst, float* margin) {
   if (d % 4 || d > 4096 || !pos_dev) return 2;
   const dim3 grid((B + 7) / 8), blk(256);
   const auto* E = static_cast<const uint16_t*>(tok_emb);
   const auto* gp = static_cast<const uint16_t*>(g);
   const uint16_t* nil = nullptr;
   auto* yp = static_cast<uint16_t*>(y);
-  if (d <= 1024) return launch_k(embed_ln_kernel<8, true>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, nil, d, x, gp, nil, yp, B);
-  if (d <= 2048) return launch_k(embed_ln_kernel<16, true>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, nil, d, x, gp, nil, yp, B);
-  return launch_k(embed_ln_kernel<32, true>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, nil, d, x, gp, nil, yp, B);
+  if (d <= 1024) return launch_k(embed_ln_kernel<8, true>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, nil, d, x, gp, nil, yp, B, t2, tiles, dst, margin);
+  if (d <= 2048) return launch_k(embed_ln_kernel<16, true>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, nil, d, x, gp, nil, yp, B, t2, tiles, dst, margin);
+  return launch_k(embed_ln_kernel<32, true>, grid, blk, 0, S(s), tokens, tok_stride, pos_dev, E, nil, d, x, gp, nil, yp, B, t2, tiles, dst, margin);
+}
+
+extern "C" int rlhf_embed_ln(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev, const void* tok_emb,
+                             const void* pos_emb, int d, float* x, const void* ln_g, const void* ln_b, void* y,
+                             rlhf_stream_t s) {
+  return embed_ln_launch(tokens, tok_stride, B, pos_dev, tok_emb, pos_emb, d, x, ln_g, ln_b, y, s, nullptr, 0, nullptr,
+                         nullptr);
+}
+
+extern "C" int rlhf_embed_rmsnorm(const int32_t* tokens, int64_t tok_stride, int B, const int* pos_dev,
+                                  const void* tok_emb, int d, float* x, const void* g, void* y, rlhf_stream_t s) {
+  return embed_rmsnorm_launch(tokens, tok_stride, B, pos_dev, tok_emb, d, x, g, y, s, nullptr, 0, nullptr, nullptr);
+}
+
+extern "C" int rlhf_argmax_embed_ln(const float* top2, int tiles, int32_t* dst, float* margin, const int32_t* tokens,
+                                    int64_t tok_stride, int B, int* pos_dev, const void* tok_emb, const void* pos_emb,
+                                    int d, float* x, const void* ln_g, const void* ln_b, void* y, rlhf_stream_t s) {
+  if (!top2 || tiles < 1 || !dst) return 2;
+  return embed_ln_launch(tokens, tok_stride, B, pos_dev, tok_emb, pos_emb, d, x, ln_g, ln_b, y, s,
+                         reinterpret_cast<const float4*>(top2), tiles, dst, margin);
+}
+
+extern "C" int rlhf_argmax_embed_rmsnorm(const float* top2, int tiles, int32_t* dst, float* margin,
+                                         const int32_t* tokens, int64_t tok_stride, int B, int* pos_dev,
+                                         const void* tok_emb, int d, float* x, const void* g, void* y,
+                                         rlhf_stream_t s) {
+  if (!top2 || tiles < 1 || !dst) return 2;
+  return embed_rmsnorm_launch(tokens, tok_stride, B, pos_dev, tok_emb, d, x, g, y, s,
+                              reinterpret_cast<const float4*>(top2), tiles, dst, margin);
 }
