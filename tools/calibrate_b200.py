@@ -35,9 +35,9 @@ def params(name, scalar_head):
 
 # workload family -> (actor arch, critic arch, bench-line glob, per-GPU batch at 8 GPUs, zero level, train micro-batch)
 FAMILIES = {
-    "c2 (OPT-125m x4, 256+256)": ("opt-125m", "opt-125m", "r2_bench_c2_n*.json", 32, 0),
+    "c2 (OPT-125m x4, 256+256)": ("opt-125m", "opt-125m", "r2b_bench_c2_n*.json|r2b_n4_c2_*.json", 32, 0),
     "c3 / c5 (OPT-1.3B / OPT-350m, prompt 256, response 128..1024)":
-        ("opt-1.3b", "opt-350m", "r2_bench_c3_n*.json|r2_sweeps/r2_sweep_c*.json", 8, 0),
+        ("opt-1.3b", "opt-350m", "r2b_bench_c3_n*.json|r2b_n4_c3_*.json|r2_sweeps/r2_sweep_c*.json", 8, 0),
     "c4 (LLaMA-7B x4, 256+256)": ("llama-7b", "llama-7b", "r1_bench_c4_llama7b_n4_colocated_*.json|r2_bench_c4_*.json", 32, 1),
 }
 
