@@ -2,7 +2,9 @@
 two launches it replaces (rlhf_argmax_tiles with the position advance, then rlhf_embed_ln /
 rlhf_embed_rmsnorm): token, margin, position, residual row x and normalised row y must be
 bit-identical, free-running (the merged token is embedded) and teacher-forced (predictions
-to a separate buffer, the given token embedded).  GPU only."""
+to a separate buffer, the given token embedded).  GPU only.  Every tensor's dtype is explicit:
+tests/golden/make_golden.py switches torch's default dtype to float64 when an earlier test
+imports it."""
 import ctypes as C
 
 import pytest
@@ -27,11 +29,11 @@ def _top2_partials(logits):
     """[B, V] fp32 -> [tiles, B, 4] (max, row id bits, second max, 0) per 128-row tile."""
     B, V = logits.shape
     tiles = (V + 127) // 128
-    pad = torch.full((B, tiles * 128), -float("inf"), device=logits.device)
+    pad = torch.full((B, tiles * 128), -float("inf"), device=logits.device, dtype=torch.float32)
     pad[:, :V] = logits
     v, i = pad.view(B, tiles, 128).topk(2, dim=2)
     ids = (i[..., 0] + torch.arange(tiles, device=logits.device).view(1, -1) * 128).int()
-    out = torch.zeros(tiles, B, 4, device=logits.device)
+    out = torch.zeros(tiles, B, 4, device=logits.device, dtype=torch.float32)
     out[..., 0] = v[..., 0].t()
     out[..., 1] = ids.t().contiguous().view(torch.float32)
     out[..., 2] = v[..., 1].t()
@@ -46,11 +48,11 @@ def test_argmax_embed_matches_two_launches(rms, teacher, B, d, V):
     L = _lib()
     S = 24
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    E = (torch.randn(V, d, device="cuda") * 0.1).bfloat16()
-    Pm = (torch.randn(S, d, device="cuda") * 0.1).bfloat16()
-    g = (1 + 0.1 * torch.randn(d, device="cuda")).bfloat16()
-    b = (0.1 * torch.randn(d, device="cuda")).bfloat16()
-    t2, tiles = _top2_partials(torch.randn(B, V, device="cuda"))
+    E = (torch.randn(V, d, device="cuda", dtype=torch.float32) * 0.1).bfloat16()
+    Pm = (torch.randn(S, d, device="cuda", dtype=torch.float32) * 0.1).bfloat16()
+    g = (1 + 0.1 * torch.randn(d, device="cuda", dtype=torch.float32)).bfloat16()
+    b = (0.1 * torch.randn(d, device="cuda", dtype=torch.float32)).bfloat16()
+    t2, tiles = _top2_partials(torch.randn(B, V, device="cuda", dtype=torch.float32))
     tok0 = torch.randint(0, V, (B, S), device="cuda", dtype=torch.int32)
     p0 = 9
     outs = []
@@ -58,9 +60,9 @@ def test_argmax_embed_matches_two_launches(rms, teacher, B, d, V):
         tok = tok0.clone()
         pred = torch.full((B, S), -1, device="cuda", dtype=torch.int32)
         dst = pred if teacher else tok
-        margin = torch.zeros(B, S, device="cuda")
+        margin = torch.zeros(B, S, device="cuda", dtype=torch.float32)
         pos = torch.tensor([p0, 0], device="cuda", dtype=torch.int32)
-        x = torch.zeros(B, d, device="cuda")
+        x = torch.zeros(B, d, device="cuda", dtype=torch.float32)
         y = torch.zeros(B, d, device="cuda", dtype=torch.bfloat16)
         if fused:
             if rms:

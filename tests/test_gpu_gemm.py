@@ -328,20 +328,20 @@ def test_gemm_lm_head_top2_and_tile_merge(V, N):
     L.rlhf_argmax_tiles.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                     C.c_int, C.c_void_p]
     d = 768
-    W = (torch.randn(V, d, device="cuda") * 0.05).bfloat16()
-    hf = torch.randn(N, d, device="cuda").bfloat16()
+    W = (torch.randn(V, d, device="cuda", dtype=torch.float32) * 0.05).bfloat16()
+    hf = torch.randn(N, d, device="cuda", dtype=torch.float32).bfloat16()
     tiles = (V + 127) // 128
-    top2 = torch.full((tiles, N, 4), float("nan"), device="cuda")
+    top2 = torch.full((tiles, N, 4), float("nan"), device="cuda", dtype=torch.float32)
     p = GemmParams()
     p.M, p.N, p.K, p.batch, p.batch_h = V, N, d, 1, 1
     p.A, p.lda, p.B, p.ldb = W.data_ptr(), d, hf.data_ptr(), d
-    sink = torch.empty(N, V, device="cuda")  # the top-2 epilogue never stores logits
+    sink = torch.empty(N, V, device="cuda", dtype=torch.float32)  # the top-2 epilogue never stores logits
     p.C, p.c_f32, p.c_rs, p.c_cs, p.alpha = sink.data_ptr(), 1, 1, V, 1.0
     p.top2 = top2.data_ptr()
     s = torch.cuda.current_stream().cuda_stream
     assert L.rlhf_gemm(C.byref(p), C.c_void_p(s)) == 0
     logits = hf.float() @ W.float().t()  # [N, V]
-    pad = torch.full((N, tiles * 128), -float("inf"), device="cuda")
+    pad = torch.full((N, tiles * 128), -float("inf"), device="cuda", dtype=torch.float32)
     pad[:, :V] = logits
     t = pad.view(N, tiles, 128)
     v2, i2 = t.topk(2, dim=2)
@@ -356,7 +356,7 @@ def test_gemm_lm_head_top2_and_tile_merge(V, N):
     # merge: token at tok[b*S + pos + 1], margin likewise
     S = 8
     tok = torch.full((N, S), -1, device="cuda", dtype=torch.int32)
-    margin = torch.zeros(N, S, device="cuda")
+    margin = torch.zeros(N, S, device="cuda", dtype=torch.float32)
     pos = torch.tensor([2, 0], device="cuda", dtype=torch.int32)
     assert L.rlhf_argmax_tiles(top2.data_ptr(), tiles, N, tok.data_ptr(), S, pos.data_ptr(), margin.data_ptr(), 1,
                                C.c_void_p(s)) == 0
