@@ -110,9 +110,17 @@ __global__ void embed_ln_kernel(const int32_t* __restrict__ tokens, int64_t tok_
   if (t2) {
     float v1 = -FLT_MAX, v2 = -FLT_MAX;
     int i1 = 0x7fffffff;
-    for (int i = lane; i < tiles; i += 32) {
-      const float4 o = t2[static_cast<int64_t>(i) * B + row];
-      top2_fold(v1, i1, v2, o.x, __float_as_int(o.y), o.z);
+    // 8 partial loads in flight per lane, folded in ascending tile order (the same order as
+    // one load per iteration; out-of-range slots are neutral (-FLT_MAX, INT_MAX, -FLT_MAX))
+    for (int i0 = lane; i0 < tiles; i0 += 32 * 8) {
+      float4 o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + 32 * j;
+        o[j] = i < tiles ? t2[static_cast<int64_t>(i) * B + row] : make_float4(-FLT_MAX, __int_as_float(0x7fffffff), -FLT_MAX, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) top2_fold(v1, i1, v2, o[j].x, __float_as_int(o[j].y), o[j].z);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
